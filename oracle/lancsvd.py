@@ -1,0 +1,82 @@
+"""LancSVD: block Golub-Kahan-Lanczos truncated SVD with full
+reorthogonalisation and basic restart.  Alg. 2.
+
+ORACLE / TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+Notation: the paper's Krylov dimension "r" is d here (k = d/b
+block steps per cycle); the paper's restart count "p" is maxit (with an early
+exit on tol, reading R12); r is the number of wanted triplets.
+
+Readings applied: both sides are orthogonalised (R15);
+B_k[i,i] = L_i = R^T of the S3 factorisation, B_k[i+1,i] = Rbar_i (Eq. 8,
+R17, R1); Qbar_{k+1} is kept to supply Rbar_k (R18); the restart block is the
+first b left Ritz vectors (R19) re-orthonormalised with CholQR2 (R11);
+V_r = P_k Vbar (Eq. 12, R2); convergence rho_i = ||Rbar_k Vbar[last b, i]||
+<= tol * sigma_1 (from Eq. 10, R12).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .core import DrawCtx, cholqr2, cgs_cqr2, small_svd, sign_normalize
+from .philox import gaussian_block
+
+
+@dataclass
+class LancResult:
+    U: np.ndarray
+    S: np.ndarray
+    V: np.ndarray
+    rho: np.ndarray
+    cycles: int
+    nconv: int
+    converged: bool
+    debug: dict = field(default_factory=dict)
+
+
+def lancsvd(op, r: int, b: int, d: int, tol: float, maxit: int, seed: int,
+            start=None, debug: bool = False) -> LancResult:
+    m, n = op.m, op.n
+    assert m >= n and 1 <= r <= d <= n and d % b == 0 and maxit >= 1
+    k = d // b
+    ctx = DrawCtx(seed)
+    G = gaussian_block(m, b, seed, draw=0) if start is None else np.array(start, dtype=np.float64)
+    Qbar, _ = cholqr2(G, ctx)                                   # S1
+    for cycle in range(1, maxit + 1):                            # j = 1..p
+        Pbar = np.zeros((m, d + b))
+        P = np.zeros((n, d))
+        B = np.zeros((d, d))
+        Pbar[:, 0:b] = Qbar
+        Rb = None
+        for i in range(k):                                       # i = 1..k
+            lo, hi = i * b, (i + 1) * b
+            Y = op.rmatmul(Pbar[:, lo:hi])                       # S2
+            if i == 0:
+                Q, R = cholqr2(Y, ctx)                           # S3a
+            else:
+                Q, _, R = cgs_cqr2(Y, P[:, :lo], ctx)            # S3b
+            P[:, lo:hi] = Q
+            B[lo:hi, lo:hi] = R.T                                # L_i
+            Z = op.matmul(Q)                                     # S4
+            Qb, _, Rb = cgs_cqr2(Z, Pbar[:, :hi], ctx)           # S5
+            Pbar[:, hi:hi + b] = Qb
+            if i < k - 1:
+                B[hi:hi + b, lo:hi] = Rb                         # Rbar_i
+        Ub, S, Vb = small_svd(B)                                 # SVD(B_k)
+        rho = np.linalg.norm(Rb @ Vb[(k - 1) * b:k * b, :], axis=0)
+        ok = rho[:r] <= tol * S[0]
+        converged = bool(np.all(ok))
+        if converged or cycle == maxit:
+            break
+        Qbar, _ = cholqr2(Pbar[:, :d] @ Ub[:, :b], ctx)          # S7 (+R11)
+    U = Pbar[:, :d] @ Ub[:, :r]                                  # S9
+    V = P @ Vb[:, :r]                                            # S8 (Eq. 12)
+    U, V = sign_normalize(U, V)
+    dbg = {}
+    if debug:
+        dbg = dict(B=B, P=P, Pbar=Pbar[:, :d], Qnext=Pbar[:, d:d + b], Rbar=Rb,
+                   Ub=Ub, Vb=Vb, S_all=S)
+    return LancResult(U=U, S=S[:r].copy(), V=V, rho=rho[:r].copy(), cycles=cycle,
+                      nconv=int(np.sum(ok)), converged=converged, debug=dbg)
