@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""Benchmark: truncated-SVD time-to-solution on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A "step" is one complete tsvd_block_lanczos solve (all SURVEY 8(a) rows:
+Philox start block + CholQR2, per block step A^T.Qbar (CSR(A^T) SpMM),
+CGS-CQR2 against P, A.Q (CSR SpMM), CGS-CQR2 against Pbar, B_k assembly,
+one-sided Jacobi SVD of B_k, rho test, restart, outputs U, V, sign) on the
+synthetic config's CSR matrix, with A already resident in HBM.  value = the
+time-to-solution in seconds (lower is better), max over ranks.
+
+N > 1: every rank solves its own replica of the workload (different seed);
+"scaling": "weak" (replicas - the row-partitioned NCCL path is the next
+SURVEY 8(e) row).
+
+--impl reference: the CPU oracle (oracle/, numpy/scipy fp64) on the host
+cores, on a bounded sample of the same workload (the first block steps of
+cycle 1, extrapolated linearly in the block index to the GPU run's cycle
+count); rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "truncated-SVD time-to-solution (s) at fixed residual; SpMM/QR HBM GB/s vs peak"
+CONFIG_TEXT = {
+    "C1": "dense 200x100 FP64 with prescribed geometric spectrum, r=10, block Lanczos b=4",
+    "C2": "synthetic sparse square CSR, m=n=1e6, nnz~1e7, power-law row lengths, r=50, "
+          "block Lanczos b=16 on 1 B200",
+    "C3": "synthetic sparse rectangular CSR, m=4e6, n=5e5, nnz~5e7, r=100, block Lanczos b=32",
+    "C4": "synthetic dense 40000x20000 FP64 with slowly decaying spectrum, r=200, "
+          "block Lanczos b=32",
+}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# --------------------------------------------------------------- workload --
+def make_workload(cfg_name: str, rank: int):
+    from tsvd_inputs import CONFIGS, SEEDS, dense_prescribed, powerlaw_csr, spectrum_eq16
+    cfg = dict(CONFIGS[cfg_name])
+    seed = SEEDS[cfg_name] + 1000 * rank
+    if cfg["kind"] == "csr":
+        csr = powerlaw_csr(cfg["m"], cfg["n"], cfg["nnz"], cfg["alpha"], seed)
+        return cfg, seed, dict(csr=csr, shape=(cfg["m"], cfg["n"]))
+    s = spectrum_eq16(cfg["n"])
+    refl = None if cfg["m"] * cfg["n"] <= 4_000_000 else 4
+    A = dense_prescribed(cfg["m"], cfg["n"], s, seed, n_reflectors=refl)
+    return cfg, seed, dict(A=A)
+
+
+def _to_device(work):
+    import numpy as np
+    import torch
+    if "csr" in work:
+        rp, ci, va = work["csr"]
+        return dict(csr=tuple(torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (rp, ci, va)),
+                    shape=work["shape"])
+    return dict(A=torch.from_numpy(work["A"]).cuda())
+
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = max(smax, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------- cpu baseline --
+def oracle_sample(cfg_name: str, budget_s: float, cycles: int, seed: int):
+    """Time the oracle's LancSVD block steps (Alg. 2 S2-S5, calling only
+    oracle/) for ~budget_s on the host, fit t_i = a + c*i and extrapolate to
+    `cycles` full cycles of k = d/b steps plus the small SVD."""
+    import numpy as np
+    from threadpoolctl import threadpool_info
+    import oracle
+    from oracle.core import DrawCtx, cholqr2, cgs_cqr2, small_svd
+    cfg, seed_, work = make_workload(cfg_name, 0)
+    op = oracle.Operator(dense=work["A"]) if "A" in work else oracle.Operator(csr=work["csr"], shape=work["shape"])
+    m, n, b, d = cfg["m"], cfg["n"], cfg["b"], cfg["d"]
+    k = d // b
+    ctx = DrawCtx(seed)
+    t0 = time.perf_counter()
+    Qbar, _ = cholqr2(oracle.gaussian_block(m, b, seed, draw=0), ctx)
+    t_start = time.perf_counter() - t0
+    Pbar = np.zeros((m, d + b))
+    P = np.zeros((n, d))
+    Pbar[:, :b] = Qbar
+    times = []
+    t_begin = time.perf_counter()
+    for i in range(k):
+        ts = time.perf_counter()
+        lo, hi = i * b, (i + 1) * b
+        Y = op.rmatmul(Pbar[:, lo:hi])
+        Q = cholqr2(Y, ctx)[0] if i == 0 else cgs_cqr2(Y, P[:, :lo], ctx)[0]
+        P[:, lo:hi] = Q
+        Z = op.matmul(Q)
+        Pbar[:, hi:hi + b] = cgs_cqr2(Z, Pbar[:, :hi], ctx)[0]
+        times.append(time.perf_counter() - ts)
+        if time.perf_counter() - t_begin > budget_s and len(times) >= 3:
+            break
+    ts = time.perf_counter()
+    small_svd(np.random.default_rng(0).standard_normal((d, d)))
+    t_svd = time.perf_counter() - ts
+    idx = np.arange(len(times))
+    c, a = np.polyfit(idx, np.array(times), 1) if len(times) > 1 else (0.0, times[0])
+    per_cycle = float(sum(max(a + c * i, times[0] * 0.5) for i in range(k))) + t_svd
+    est = t_start + cycles * per_cycle
+    threads = max((x.get("num_threads", 1) for x in threadpool_info()), default=1)
+    sample = (f"{cfg_name} LancSVD block steps i=0..{len(times)-1} of k={k} of cycle 1 "
+              f"({sum(times):.1f} s measured) + SVD({d}) ({t_svd:.2f} s); t_i fitted "
+              f"linearly in i and extrapolated to {cycles} cycle(s) x {k} steps")
+    return dict(value=est, unit="s", cores=int(threads), kind="oracle", sample=sample,
+                measured_s=sum(times) + t_svd + t_start)
+
+
+# ------------------------------------------------------------------- main --
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg_name = args.config
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        from tsvd_inputs import CONFIGS, SEEDS
+        cfg = CONFIGS[cfg_name]
+        budget = max(5.0, 150.0 / max(1, args.steps + args.warmup))
+        vals, last = [], None
+        for it in range(args.warmup + args.steps):
+            last = oracle_sample(cfg_name, budget, cycles=1, seed=SEEDS[cfg_name])
+            if it >= args.warmup:
+                vals.append(last["value"])
+        v = statistics.median(vals)
+        out = {"impl": "reference", "metric": METRIC, "value": v, "unit": "s",
+               "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
+               "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": {"workload": f"{cfg_name}: {CONFIG_TEXT.get(cfg_name, '')}",
+                          "m": cfg["m"], "n": cfg["n"], "r": cfg["r"], "b": cfg["b"],
+                          "d": cfg["d"], "tol": cfg["tol"]},
+               "cpu_baseline": {"value": v, "unit": "s", "cores": last["cores"],
+                                "kind": "oracle", "sample": last["sample"]},
+               "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0}}
+        print(json.dumps(out), flush=True)
+        return 0
+
+    import numpy as np
+    import torch
+    import paper_2403_06218_b200 as T
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    T.lib()
+
+    cfg, seed, work = make_workload(cfg_name, rank)
+    dwork = _to_device(work)
+    r, b, d, tol, maxit = cfg["r"], cfg["b"], cfg["d"], cfg["tol"], cfg["maxit"]
+    stream = torch.cuda.current_stream()
+    h = T.TruncatedSVD(**dwork)
+    h.set_seed(seed)
+    h.set_krylov_dim(d)
+    for _ in range(args.warmup):
+        h.block_lanczos(r, b, tol, maxit)
+    h.set_profiling(True)
+    h.reset_profile()
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    gpu_idx = int(vis.split(",")[local]) if vis and vis.split(",")[local].isdigit() else local
+    clocks = ClockSampler(gpu_idx)
+    launches = 0
+    infos = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        h.block_lanczos(r, b, tol, maxit)
+        inf = h.info()
+        infos.append(inf)
+        launches += int(inf["launches"])
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if dist:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    prof = h.profile()
+    h.set_profiling(False)
+    U, S, V = h.get()
+    h.close()
+
+    # roofline of the dominant phase
+    peak, peak_kind = _peaks()
+    hbm_phases = {k: v for k, v in prof.items() if v["calls"] > 0 and v["bytes"] > 0}
+    dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    roof = None
+    if dom[1]["bytes"] > 0:
+        ach = dom[1]["bytes"] / (dom[1]["ms"] * 1e-3) / 1e9
+        traffic = None
+        tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tfile):
+            try:
+                tr = json.load(open(tfile)).get(dom[0])
+                if tr:
+                    traffic = tr["dram_over_alg"] * dom[1]["bytes"] / max(1, dom[1]["calls"])
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "kernel": dom[0], "achieved": round(ach, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": traffic,
+                "alg_bytes_per_launch": dom[1]["bytes"] / max(1, dom[1]["calls"]),
+                "avg_launch_ms": dom[1]["ms"] / max(1, dom[1]["calls"]),
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
+    else:
+        roof = {"bound": "alu", "kernel": dom[0], "achieved": None, "peak": None,
+                "unit": "GFLOP/s", "frac": None, "traffic": None}
+    total_ms = sum(v["ms"] for v in prof.values()) or 1.0
+    phases = {k: {"ms_per_step": round(v["ms"] / args.steps, 3),
+                  "share": round(v["ms"] / total_ms, 4),
+                  "GBps": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] > 0 and v["bytes"] > 0 else None,
+                  "calls_per_step": v["calls"] / args.steps}
+              for k, v in prof.items() if v["calls"] > 0}
+
+    # end-to-end through the public API with host buffers
+    e2e = None
+    if args.e2e_steps > 0:
+        torch.cuda.synchronize()
+        times = []
+        h2d = d2h = 0
+        for _ in range(args.e2e_steps):
+            t0 = time.perf_counter()
+            if "csr" in work:
+                h2 = T.TruncatedSVD(csr=work["csr"], shape=work["shape"])
+                h2d = sum(x.nbytes for x in work["csr"])
+            else:
+                h2 = T.TruncatedSVD(work["A"])
+                h2d = work["A"].nbytes
+            h2.set_seed(seed)
+            h2.set_krylov_dim(d)
+            h2.block_lanczos(r, b, tol, maxit)
+            U2, S2, V2 = h2.get()
+            h2.close()
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+            d2h = U2.nbytes + S2.nbytes + V2.nbytes
+        ev = statistics.median(times)
+        if dist:
+            t = torch.tensor([ev], device="cuda", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ev = float(t.item())
+        e2e = {"value": round(ev, 6), "unit": "s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = oracle_sample(cfg_name, args.cpu_budget, cycles=infos[-1]["cycles"], seed=seed)
+            cpu.pop("measured_s", None)
+        except Exception as ex:  # report, never fake
+            cpu = {"value": None, "error": repr(ex)}
+
+    last = infos[-1]
+    out = {
+        "metric": METRIC, "value": round(ms / 1e3, 6), "unit": "s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{cfg_name}: {CONFIG_TEXT.get(cfg_name, '')}",
+                   "m": cfg["m"], "n": cfg["n"], "nnz": int(len(work["csr"][1])) if "csr" in work else None,
+                   "r": r, "b": b, "d": d, "tol": tol, "maxit": maxit,
+                   "l2": "no flush: working set (A, A^T, bases) >> 126 MB L2",
+                   "parallelism": "replicas" if world > 1 else "single"},
+        "solver": {"cycles": last["cycles"], "nconv": last["nconv"], "rho_max": last["rho_max"],
+                   "breakdowns": last["breakdowns"], "sigma1": last["sigma1"]},
+        "roofline": roof,
+        "phases": phases,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,207 @@
+/*
+ * tsvd.h - C ABI of the B200-native truncated SVD hot path.
+ *
+ * Implements the block iteration shared by RandSVD (Alg. 1)
+ * and LancSVD (Alg. 2) of Tomas, Quintana-Orti, Anzt,
+ * "Fast Truncated SVD of Sparse and Dense Matrices on Graphics Processors"
+ * (arXiv 2403.06218).  Citations "P:<line>" refer to PAPER.md.
+ *
+ * Problem (Sec. 2): A in R^{m x n}, m >= n, given as CSR or
+ * dense; compute U_r (m x r), Sigma_r = diag(sigma_1..sigma_r) descending,
+ * V_r (n x r) with A ~ U_r Sigma_r V_r^T (Eq. 2).
+ *
+ * Conventions
+ *  - FP64 only (IEEE binary64).  Integers: int64 row pointers, int32
+ *    column indices (n < 2^31).
+ *  - Every dense block crossing this ABI is ROW-MAJOR with an explicit
+ *    leading dimension (elements).  U is m x r (ldu >= r), V is n x r.
+ *  - mem_kind: TSVD_HOST (pageable or pinned host memory) or TSVD_DEVICE
+ *    (device memory on the current CUDA device).
+ *  - Ownership: create* COPIES A into library-owned device memory; the caller
+ *    keeps its buffers.  get copies into caller buffers.  destroy frees all.
+ *  - Errors: every call returns a tsvd_status; nothing is thrown, nothing
+ *    aborts.  After a negative status the handle stays valid for destroy.
+ *    Non-convergence is the positive warning TSVD_WARN_NOTCONV (results of
+ *    the last cycle are retrievable).  A Cholesky breakdown is not an error:
+ *    the CGS2 fallback of P:275 handles it.
+ *  - Threading: a handle is not thread-safe; distinct handles may run
+ *    concurrently on distinct streams.  All work is ordered on the handle's
+ *    stream (tsvd_set_stream); calls return after the stream work they
+ *    enqueue has completed unless documented otherwise.
+ *  - There is no CPU fallback: if no CUDA device is usable every entry point
+ *    that needs one returns TSVD_ECUDA.
+ */
+#ifndef TSVD_H
+#define TSVD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct tsvd_ctx* tsvd_t;
+typedef int tsvd_status;
+
+enum {
+  TSVD_OK = 0,
+  TSVD_WARN_NOTCONV = 1, /* maxit reached before max_{i<=r} rho_i <= tol*sigma_1 */
+  TSVD_EINVAL = -1,      /* bad argument (NULL, non-canonical CSR, tol <= 0 ...) */
+  TSVD_ESHAPE = -2,      /* m < n, r > n, d % b != 0, r > d, r + p > n ...     */
+  TSVD_ENOMEM = -3,      /* device allocation failed                            */
+  TSVD_ECUDA = -4,       /* CUDA runtime error / no usable device               */
+  TSVD_ESTATE = -6       /* e.g. tsvd_get before a successful solve             */
+};
+
+enum { TSVD_HOST = 0, TSVD_DEVICE = 1 };
+enum { TSVD_ROW_MAJOR = 0, TSVD_COL_MAJOR = 1 };
+
+/* ---- creation ----------------------------------------------------------
+ * tsvd_create_csr: A as CSR.  rowptr[m+1] (rowptr[0] = 0,
+ * non-decreasing, rowptr[m] = nnz), colidx[nnz] in [0, n) strictly increasing
+ * within each row (canonical: sorted, no duplicates), vals[nnz].  The library
+ * builds CSR(A^T) on the device (counting sort by column, stable) so that
+ * A^T.X needs no atomics (north_star; P:460 discusses the transposed product).
+ * Returns TSVD_ESHAPE if m < n ("otherwise target the transpose"),
+ * TSVD_EINVAL if the CSR is not canonical. */
+tsvd_status tsvd_create_csr(tsvd_t* h, int64_t m, int64_t n, int64_t nnz,
+                            const int64_t* rowptr, const int32_t* colidx,
+                            const double* vals, int mem_kind);
+
+/* tsvd_create_dense: dense A (Table 1 caption P:327: the products become
+ * GEMMs).  layout TSVD_ROW_MAJOR (lda >= n) or TSVD_COL_MAJOR (lda >= m);
+ * stored row-major on the device. */
+tsvd_status tsvd_create_dense(tsvd_t* h, int64_t m, int64_t n, const double* A,
+                              int64_t lda, int layout, int mem_kind);
+
+/* ---- options ----------------------------------------------------------- */
+/* cudaStream_t to order all work on (e.g. torch.cuda.current_stream()).
+ * NULL => the legacy default stream.  Until this is called a handle uses a
+ * library-owned non-blocking stream. */
+tsvd_status tsvd_set_stream(tsvd_t h, void* cuda_stream);
+/* Philox4x32-10 seed for the start block (draw 0) and for breakdown
+ * replacement columns (draws 1, 2, ...).  P:406, reading R9. */
+tsvd_status tsvd_set_seed(tsvd_t h, uint64_t seed);
+/* Krylov dimension d of LancSVD (the paper's "r"); must be a
+ * multiple of b with r <= d <= n.  0 => default min(n, max(4r, 2b)) rounded
+ * down to a multiple of b. */
+tsvd_status tsvd_set_krylov_dim(tsvd_t h, int d);
+/* Panel width of CGS-QR (Alg. 3) inside RandSVD; default 16. */
+tsvd_status tsvd_set_qr_block(tsvd_t h, int b_qr);
+/* Optional exact start block instead of the Philox one: for LancSVD the
+ * m x b block G that S1 orthonormalises; for RandSVD the n x l block Q_0.
+ * Row-major, leading dimension ld.  The block is copied; it is used by every
+ * later solve on this handle until tsvd_set_start(h, NULL, 0, 0). */
+tsvd_status tsvd_set_start(tsvd_t h, const double* block, int64_t rows,
+                           int64_t cols, int64_t ld, int mem_kind);
+
+/* ---- solvers ------------------------------------------------------------
+ * tsvd_block_lanczos: Alg. 2 with both-side full reorthogonalisation
+ * (CGS-CQR2, Alg. 5) and the basic restart of [9], restart block
+ * re-orthonormalised (reading R11).  Cycles until
+ * max_{i<=r} ||Rbar_k Vbar[last b rows, i]||_2 <= tol * sigma_1 (from Eq. 10,
+ * reading R12) or maxit cycles.  r >= 1 wanted triplets, b >= 1 block size,
+ * tol > 0, maxit >= 1. */
+tsvd_status tsvd_block_lanczos(tsvd_t h, int r, int b, double tol, int maxit);
+/* tsvd_rsvd: Alg. 1 with l = r + p columns (p = oversampling) and q power
+ * iterations, i.e. q + 1 passes of S1-S4 (paper p = q + 1, reading R6); QR by
+ * CGS-QR (Alg. 3) with panels of b_qr columns. */
+tsvd_status tsvd_rsvd(tsvd_t h, int r, int p, int q);
+
+/* ---- results ------------------------------------------------------------
+ * Copies U_r (m x r, row-major, ldu >= r), S (r), V_r (n x r, ldv >= r) of
+ * the last solve.  Any pointer may be NULL to skip it.  Sign convention: the
+ * largest-|.| entry of each v_i is positive (lowest index on ties). */
+tsvd_status tsvd_get(tsvd_t h, double* U, int64_t ldu, double* S, double* V,
+                     int64_t ldv, int mem_kind);
+
+typedef struct {
+  int cycles;       /* LancSVD restart cycles run (RandSVD: q + 1)        */
+  int nconv;        /* i < r with rho_i <= tol*sigma_1 (LancSVD)          */
+  int r, d, b;      /* parameters of the last solve (RandSVD: d = l)      */
+  int breakdowns;   /* Cholesky breakdowns handled by the CGS2 fallback   */
+  double rho_max;   /* max_{i<r} rho_i / sigma_1 (LancSVD)                */
+  double sigma1;
+  double ms_total;  /* device time of the last solve (CUDA events)        */
+  int64_t launches; /* kernels launched by the last solve                 */
+} tsvd_info;
+tsvd_status tsvd_get_info(tsvd_t h, tsvd_info* out);
+/* rho_i / sigma_1 for i < r of the last LancSVD cycle (host buffer). */
+tsvd_status tsvd_get_rho(tsvd_t h, double* rho);
+
+/* Per-phase device-time instrumentation (CUDA events on the handle's stream
+ * around each phase call).  Phases (index: name): 0 apply_A (A.X, Alg. 2
+ * S4 / Alg. 1 S1), 1 apply_AT (A^T.X, S2 / S3), 2 ortho_tn (gemm_tn passes
+ * of Alg. 4/5), 3 ortho_nn (gemm_nn passes of Alg. 4/5, incl. TRSM-only
+ * passes), 4 ortho_small (b x b Cholesky / reductions), 5 small_svd,
+ * 6 restart_out (restart product, outputs, sign), 7 other.  bytes/flops are
+ * ALGORITHMIC (compulsory) counts per DESIGN.md "Roofline", not measured
+ * traffic.  Aggregates accumulate over solves until reset. */
+typedef struct {
+  const char* name;   /* static string */
+  int64_t calls;      /* phase calls */
+  int64_t launches;   /* kernels launched inside them */
+  double ms;          /* summed event time */
+  double bytes;       /* summed algorithmic bytes */
+  double flops;       /* summed algorithmic flops */
+} tsvd_prof_entry;
+enum { TSVD_NPROF = 8 };
+tsvd_status tsvd_set_profiling(tsvd_t h, int on);
+tsvd_status tsvd_get_profile(tsvd_t h, tsvd_prof_entry* out /* TSVD_NPROF */);
+tsvd_status tsvd_reset_profile(tsvd_t h);
+
+tsvd_status tsvd_destroy(tsvd_t h);
+const char* tsvd_strerror(tsvd_status s);
+/* Message of the last failing call on this thread ("" if none). */
+const char* tsvd_last_error(void);
+
+/* ---- single-kernel entry points for parity tests (same library) ---------
+ * All pointers are DEVICE pointers, row-major with the given leading
+ * dimensions, work is enqueued on `stream` (NULL = legacy default) and the
+ * call synchronises that stream before returning. */
+
+/* Philox normal block (reading R9): out[i*ld + j] = G(row0+i, j) of a
+ * q_total x w block, seed, draw. */
+tsvd_status tsvd_dbg_philox(double* out, int64_t q, int w, int64_t ld,
+                            uint64_t seed, uint64_t draw, int64_t row0,
+                            int64_t q_total, void* stream);
+/* Raw Philox4x32-10 words for (ctr, key) pairs: ctr[4*i..], key[2*i..] ->
+ * out[4*i..] (uint32).  count pairs.  Pointers are device pointers. */
+tsvd_status tsvd_dbg_philox_words(const uint32_t* ctr, const uint32_t* key,
+                                  uint32_t* out, int64_t count, void* stream);
+/* Y (rows x w) = op(A) X: trans = 0 -> A X (Alg. 2 S4), 1 -> A^T X (S2),
+ * with the handle's CSR or dense A.  w >= 1 (any width). */
+tsvd_status tsvd_dbg_apply(tsvd_t h, int trans, const double* X, int64_t ldx,
+                           double* Y, int64_t ldy, int w);
+/* CholeskyQR2 in place (Alg. 4): Y (q x w, ld) -> Q, R (w x w row-major). */
+tsvd_status tsvd_dbg_cholqr2(double* Y, int64_t q, int w, int64_t ld,
+                             double* R, uint64_t seed, void* stream);
+/* CGS-CQR2 (Alg. 5): Y (q x w) against P (q x s); both inside ONE row-major
+ * buffer `basis` with leading dimension ld: P = columns [0, s), Y = columns
+ * [s, s+w).  Outputs H (s x w), R (w x w) row-major. */
+tsvd_status tsvd_dbg_cgs_cqr2(double* basis, int64_t q, int s, int w,
+                              int64_t ld, double* H, double* R, uint64_t seed,
+                              void* stream);
+/* CGS-QR (Alg. 3) in place on Y (q x l, ld) with panels of bq -> R (l x l). */
+tsvd_status tsvd_dbg_cgs_qr(double* Y, int64_t q, int l, int64_t ld, int bq,
+                            double* R, uint64_t seed, void* stream);
+/* Small SVD by one-sided Jacobi on the device (reading R20): B (d x d,
+ * row-major) -> Ub (d x d), S (d, descending), Vb (d x d), B = Ub S Vb^T. */
+tsvd_status tsvd_dbg_small_svd(const double* B, int d, double* Ub, double* S,
+                               double* Vb, void* stream);
+/* Tall-skinny products used by the passes: C (s x w) = X^T Y with X (q x s,
+ * ldx), Y (q x w, ldy) (Alg. 5 S1/S6); and Z (q x w) = beta*Z + alpha*X H
+ * with H (s x w, ldh) (Alg. 5 S2/S7, restart, outputs). */
+tsvd_status tsvd_dbg_gemm_tn(const double* X, int64_t ldx, const double* Y,
+                             int64_t ldy, int64_t q, int s, int w, double* C,
+                             void* stream);
+tsvd_status tsvd_dbg_gemm_nn(const double* X, int64_t ldx, const double* H,
+                             int64_t ldh, double* Z, int64_t ldz, int64_t q,
+                             int s, int w, double alpha, double beta,
+                             void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSVD_H */

@@ -1,0 +1,309 @@
+// Building blocks of Sec. 3 on the device, composed from the
+// kernels of ts.cu / spmm.cu:
+//   cholqr2   Alg. 4  readings R3, R4
+//   cgs_cqr2  Alg. 5  readings R4, R5
+//   cgs2      P:275 fallback        reading R16
+//   cgs_qr    Alg. 3  reading R8
+//   apply     A.X / A^T.X (Alg. 1 S1/S3, Alg. 2 S2/S4; dense: Table 1 "*")
+//
+// Pass structure of CGS-CQR2 on q x w against q x s (each pass reads P once):
+//   1 gemm_tn : H     = P^T Y                         (S1)
+//   2 gemm_nn : S     = Y - P H,  W = S^T S            (S2, S3)      -> L = chol(W)     (S4)
+//   3 gemm_tn : Hbar  = P^T (S L^{-T})                 (S5 fused into S6)
+//   4 gemm_nn : S     = S L^{-T} - P Hbar, Wbar = S^T S (S5, S7, S8)  -> Lbar, R, H (S9, S11, S12)
+//   5 gemm_nn : Y     = S Lbar^{-T}                    (S10)
+// Y itself is only overwritten by pass 5, after the host has seen both
+// breakdown flags, so the CGS2 fallback always restarts from the original Y
+// exactly as in the oracle (one stream sync per orthogonalisation).
+#include "ctx.h"
+
+namespace tsvd {
+
+void* buf(Ctx& c, const std::string& name, size_t bytes) {
+  if (bytes == 0) bytes = 8;
+  auto it = c.bufs.find(name);
+  if (it != c.bufs.end() && it->second.second >= bytes) return it->second.first;
+  if (it != c.bufs.end()) {
+    TSVD_CUDA(cudaStreamSynchronize(c.st));
+    cudaFree(it->second.first);
+    c.bufs.erase(it);
+  }
+  void* p = nullptr;
+  TSVD_CUDA(cudaMalloc(&p, bytes));
+  c.bufs[name] = {p, bytes};
+  return p;
+}
+
+void free_bufs(Ctx& c) {
+  for (auto& kv : c.bufs) cudaFree(kv.second.first);
+  c.bufs.clear();
+}
+
+static const char* kProfNames[TSVD_NPROF] = {"apply_A", "apply_AT", "ortho_tn", "ortho_nn",
+                                             "ortho_small", "small_svd", "restart_out", "other"};
+
+static cudaEvent_t pool_get(Ctx& c) {
+  if (!c.ev_pool.empty()) {
+    cudaEvent_t e = c.ev_pool.back();
+    c.ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  TSVD_CUDA(cudaEventCreate(&e));
+  return e;
+}
+
+Prof::Prof(Ctx& c_, int cat_, double bytes_, double flops_)
+    : c(c_), cat(cat_), bytes(bytes_), flops(flops_) {
+  if (!c.prof_on) return;
+  a = pool_get(c);
+  TSVD_CUDA(cudaEventRecord(a, c.st));
+  l0 = g_launches.load();
+}
+
+Prof::~Prof() {
+  if (!c.prof_on || !a) return;
+  cudaEvent_t b = pool_get(c);
+  cudaEventRecord(b, c.st);
+  c.prof_open.push_back(ProfRec{cat, a, b, g_launches.load() - l0, bytes, flops});
+}
+
+void prof_harvest(Ctx& c) {
+  for (auto& r : c.prof_open) {
+    float ms = 0.f;
+    cudaEventSynchronize(r.b);
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    tsvd_prof_entry& e = c.prof[r.cat];
+    e.name = kProfNames[r.cat];
+    e.calls += 1;
+    e.launches += r.launches;
+    e.ms += ms;
+    e.bytes += r.bytes;
+    e.flops += r.flops;
+    c.ev_pool.push_back(r.a);
+    c.ev_pool.push_back(r.b);
+  }
+  c.prof_open.clear();
+  for (int i = 0; i < TSVD_NPROF; ++i) c.prof[i].name = kProfNames[i];
+}
+
+void prof_release(Ctx& c) {
+  for (auto& r : c.prof_open) {
+    c.ev_pool.push_back(r.a);
+    c.ev_pool.push_back(r.b);
+  }
+  c.prof_open.clear();
+  for (auto e : c.ev_pool) cudaEventDestroy(e);
+  c.ev_pool.clear();
+}
+
+// algorithmic traffic of the pass kernels
+static double tn_bytes(int64_t q, int s, int w) { return 8.0 * q * (s + w); }
+static double nn_bytes(int64_t q, int s, int w, bool readY, bool writeZ) {
+  return 8.0 * q * (s + (readY ? w : 0) + (writeZ ? w : 0));
+}
+
+static double* part_tn(Ctx& c, int64_t q, int s, int w) {
+  const TnGeom g = tn_geom(q, s);
+  return dbuf(c, "part_tn", (size_t)(g.splits + 1) * (size_t)std::max(s, 1) * 32);
+  (void)w;
+}
+
+static double* gram_buf(Ctx& c, int64_t q) {
+  return dbuf(c, "gram", (size_t)nn_ctas(q) * 32 * 32);
+}
+
+static double* scratch(Ctx& c, int64_t q) { return dbuf(c, "scratch", (size_t)q * 32); }
+
+static int read_flags(Ctx& c) {
+  TSVD_CUDA(cudaMemcpyAsync(c.hflags, c.dflags, 4 * sizeof(int), cudaMemcpyDeviceToHost, c.st));
+  TSVD_CUDA(cudaStreamSynchronize(c.st));
+  return c.hflags[0] | c.hflags[1];
+}
+
+static void clear_flags(Ctx& c) {
+  TSVD_CUDA(cudaMemsetAsync(c.dflags, 0, 4 * sizeof(int), c.st));
+}
+
+int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
+  if (w > 32) throw Error{TSVD_EINVAL, "cholqr2: block wider than 32"};
+  double* S = scratch(c, q);
+  double* gram = gram_buf(c, q);
+  double* L1 = dbuf(c, "L1", 32 * 32);
+  double* L2 = dbuf(c, "L2", 32 * 32);
+  const int np = nn_ctas(q);
+  clear_flags(c);
+  {  // S1: W = Y^T Y
+    Prof p(c, P_NN, nn_bytes(q, 0, w, true, false), 2.0 * q * w * w);
+    gemm_nn(nullptr, 0, nullptr, 0, Y, ld, nullptr, nullptr, 0, q, 0, w, 0.0, 1.0, gram, c.st);
+  }
+  {
+    Prof p(c, P_SMALL, 0, 0);
+    chol_finalize(gram, np, w, L1, c.dflags + 0, c.st);                         // S2
+  }
+  {  // S3 + S4: S = Y L^{-T}, Wbar = S^T S
+    Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 3.0 * q * w * w);
+    gemm_nn(nullptr, 0, nullptr, 0, Y, ld, L1, S, w, q, 0, w, 0.0, 1.0, gram, c.st);
+  }
+  {
+    Prof p(c, P_SMALL, 0, 0);
+    chol2_finalize(gram, np, w, L1, L2, R, nullptr, nullptr, 0, c.dflags + 1, c.st);  // S5, S7
+  }
+  if (read_flags(c)) {
+    Prof p(c, P_OTHER, 0, 0);
+    cgs2(c, Y, q, 0, w, ld, nullptr, R);
+    return 1;
+  }
+  {  // S6: Q = S Lbar^{-T}
+    Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 1.0 * q * w * w);
+    gemm_nn(nullptr, 0, nullptr, 0, S, w, L2, Y, ld, q, 0, w, 0.0, 1.0, nullptr, c.st);
+  }
+  return 0;
+}
+
+int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H,
+             double* R) {
+  if (s == 0) return cholqr2(c, basis, q, w, ld, R);
+  if (w > 32) throw Error{TSVD_EINVAL, "cgs_cqr2: block wider than 32"};
+  double* Y = basis + s;
+  double* S = scratch(c, q);
+  double* gram = gram_buf(c, q);
+  double* part = part_tn(c, q, s, w);
+  double* L1 = dbuf(c, "L1", 32 * 32);
+  double* L2 = dbuf(c, "L2", 32 * 32);
+  double* Hbar = dbuf(c, "Hbar", (size_t)s * w);
+  const int np = nn_ctas(q);
+  clear_flags(c);
+  const double fl = 2.0 * q * s * w;
+  {
+    Prof p(c, P_TN, tn_bytes(q, s, w), fl);
+    gemm_tn(basis, ld, Y, ld, nullptr, q, s, w, H, w, part, c.st);                   // S1
+  }
+  {
+    Prof p(c, P_NN, nn_bytes(q, s, w, true, true), fl + 2.0 * q * w * w);
+    gemm_nn(basis, ld, H, w, Y, ld, nullptr, S, w, q, s, w, -1.0, 1.0, gram, c.st);  // S2,S3
+  }
+  {
+    Prof p(c, P_SMALL, 0, 0);
+    chol_finalize(gram, np, w, L1, c.dflags + 0, c.st);                              // S4
+  }
+  {
+    Prof p(c, P_TN, tn_bytes(q, s, w), fl + 1.0 * q * w * w);
+    gemm_tn(basis, ld, S, w, L1, q, s, w, Hbar, w, part, c.st);                      // S5,S6
+  }
+  {
+    Prof p(c, P_NN, nn_bytes(q, s, w, true, true), fl + 3.0 * q * w * w);
+    gemm_nn(basis, ld, Hbar, w, S, w, L1, S, w, q, s, w, -1.0, 1.0, gram, c.st);     // S5,S7,S8
+  }
+  {
+    Prof p(c, P_SMALL, 0, 0);
+    chol2_finalize(gram, np, w, L1, L2, R, H, Hbar, s, c.dflags + 1, c.st);          // S9,S11,S12
+  }
+  if (read_flags(c)) {
+    Prof p(c, P_OTHER, 0, 0);
+    cgs2(c, basis, q, s, w, ld, H, R);
+    return 1;
+  }
+  {
+    Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 1.0 * q * w * w);
+    gemm_nn(nullptr, 0, nullptr, 0, S, w, L2, Y, ld, q, 0, w, 0.0, 1.0, nullptr, c.st);  // S10
+  }
+  return 0;
+}
+
+// Column-wise CGS with reorthogonalisation against [P, Q_<j] (
+// reading R16).  Y = columns [s, s+w) of basis is processed in place; H (s x w)
+// and R (w x w) receive the coefficients.
+void cgs2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H, double* R) {
+  const double tau = 1e-13;
+  double* S = dbuf(c, "cgs2_col", (size_t)q);
+  double* gram = gram_buf(c, q);
+  const int np = nn_ctas(q);
+  double* c1 = dbuf(c, "cgs2_c1", (size_t)(s + w));
+  double* c2 = dbuf(c, "cgs2_c2", (size_t)(s + w));
+  double* coef = dbuf(c, "cgs2_coef", (size_t)(s + w));
+  double* sc = dbuf(c, "cgs2_sc", 8);  // [0] |y_orig|^2, [1] |y''|^2, [2] nrm
+  double* part = part_tn(c, q, s + w, 1);
+  int* dep = c.dflags + 2;
+  fill_zero(R, (int64_t)w * w, c.st);
+  for (int j = 0; j < w; ++j) {
+    const int nb = s + j;
+    double* col = basis + s + j;
+    // ||y_orig||^2
+    gemm_nn(nullptr, 0, nullptr, 0, col, ld, nullptr, nullptr, 0, q, 0, 1, 0.0, 1.0, gram, c.st);
+    reduce_partials(gram, np, 1, sc + 0, c.st);
+    if (nb > 0) {
+      gemm_tn(basis, ld, col, ld, nullptr, q, nb, 1, c1, 1, part, c.st);
+      gemm_nn(basis, ld, c1, 1, col, ld, nullptr, S, 1, q, nb, 1, -1.0, 1.0, nullptr, c.st);
+      gemm_tn(basis, ld, S, 1, nullptr, q, nb, 1, c2, 1, part, c.st);
+      gemm_nn(basis, ld, c2, 1, S, 1, nullptr, S, 1, q, nb, 1, -1.0, 1.0, gram, c.st);
+    } else {
+      gemm_nn(nullptr, 0, nullptr, 0, col, ld, nullptr, S, 1, q, 0, 1, 0.0, 1.0, gram, c.st);
+    }
+    reduce_partials(gram, np, 1, sc + 1, c.st);
+    cgs2_col_finalize(c1, c2, nb, sc + 1, sc + 0, tau, coef, sc + 2, dep, c.st);
+    int hdep = 0;
+    TSVD_CUDA(cudaMemcpyAsync(&hdep, dep, sizeof(int), cudaMemcpyDeviceToHost, c.st));
+    TSVD_CUDA(cudaStreamSynchronize(c.st));
+    if (hdep) {
+      // replacement column: next Philox draw, orthogonalised twice
+      launch_philox_normal(S, q, 1, 1, c.seed, c.draw_next++, 0, q, c.st);
+      for (int it = 0; it < 2 && nb > 0; ++it) {
+        gemm_tn(basis, ld, S, 1, nullptr, q, nb, 1, c2, 1, part, c.st);
+        gemm_nn(basis, ld, c2, 1, S, 1, nullptr, S, 1, q, nb, 1, -1.0, 1.0, nullptr, c.st);
+      }
+      gemm_nn(nullptr, 0, nullptr, 0, S, 1, nullptr, nullptr, 0, q, 0, 1, 0.0, 1.0, gram, c.st);
+      reduce_partials(gram, np, 1, sc + 1, c.st);
+      cgs2_col_finalize(c1, c1, 0, sc + 1, sc + 1, 0.0, coef + nb, sc + 2, dep, c.st);
+      ++c.breakdowns;
+    } else {
+      TSVD_CUDA(cudaMemcpyAsync(R + (int64_t)j * w + j, sc + 2, sizeof(double),
+                                cudaMemcpyDeviceToDevice, c.st));
+    }
+    // Q_j = S / nrm
+    copy_block(S, 1, col, ld, q, 1, false, c.st);
+    scale_column(col, q, ld, sc + 2, c.st);
+    if (s > 0 && H) copy_block(coef, 1, H + j, w, s, 1, false, c.st);
+    if (j > 0) copy_block(coef + s, 1, R + j, w, j, 1, false, c.st);
+  }
+}
+
+int cgs_qr(Ctx& c, double* Y, int64_t q, int l, int64_t ld, int bq, double* R) {
+  int bd = 0;
+  fill_zero(R, (int64_t)l * l, c.st);
+  double* Hj = dbuf(c, "cgsqr_H", (size_t)l * 32);
+  double* Rj = dbuf(c, "cgsqr_R", 32 * 32);
+  for (int s0 = 0; s0 < l; s0 += bq) {
+    const int w = std::min(bq, l - s0);
+    if (s0 == 0) {
+      bd += cholqr2(c, Y, q, w, ld, Rj);                       // Alg. 3 S1
+    } else {
+      bd += cgs_cqr2(c, Y, q, s0, w, ld, Hj, Rj);              // Alg. 3 S2
+      copy_block(Hj, w, R + s0, l, s0, w, false, c.st);        // [H_j; R_j]
+    }
+    copy_block(Rj, w, R + (int64_t)s0 * l + s0, l, w, w, false, c.st);
+  }
+  return bd;
+}
+
+void apply(Ctx& c, bool trans, const double* X, int64_t ldx, double* Y, int64_t ldy, int w) {
+  const double rows = trans ? (double)c.n : (double)c.m, cols = trans ? (double)c.m : (double)c.n;
+  const double bytes = c.dense ? 8.0 * ((double)c.m * c.n + w * (rows + cols))
+                               : 12.0 * c.A.nnz + 8.0 * (rows + 1) + 8.0 * w * (rows + cols);
+  const double flops = c.dense ? 2.0 * c.m * c.n * w : 2.0 * c.A.nnz * w;
+  Prof p(c, trans ? P_APPLY_AT : P_APPLY_A, bytes, flops);
+  if (c.dense) {
+    if (!trans)   // Y (m x w) = A X
+      gemm_nn(c.Ad, c.lda, X, ldx, nullptr, 0, nullptr, Y, ldy, c.m, (int)c.n, w, 1.0, 0.0,
+              nullptr, c.st);
+    else          // Y (n x w) = A^T X
+      gemm_tn(c.Ad, c.lda, X, ldx, nullptr, c.m, (int)c.n, w, Y, ldy,
+              part_tn(c, c.m, (int)c.n, std::min(w, 32)), c.st);
+  } else {
+    const Csr& A = trans ? c.AT : c.A;
+    double* part = dbuf(c, trans ? "spmm_part_t" : "spmm_part", (size_t)std::max<int64_t>(1, A.nslots) * 32);
+    launch_spmm_wide(A, X, ldx, Y, ldy, w, part, c.st);
+  }
+}
+
+}  // namespace tsvd

@@ -1,0 +1,461 @@
+// extern "C" entry points of include/tsvd.h.  Argument validation, copies
+// across the host/device boundary, and exception -> status translation.
+#include <algorithm>
+#include <cstring>
+
+#include "ctx.h"
+
+namespace tsvd {
+std::atomic<int64_t> g_launches{0};
+static thread_local std::string g_last_error;
+}  // namespace tsvd
+
+using namespace tsvd;
+
+#define TSVD_API_BEGIN try {
+#define TSVD_API_END                                   \
+  }                                                    \
+  catch (const tsvd::Error& e) {                       \
+    tsvd::g_last_error = e.msg;                        \
+    return e.code;                                     \
+  }                                                    \
+  catch (const std::bad_alloc&) {                      \
+    return TSVD_ENOMEM;                                \
+  }                                                    \
+  catch (...) {                                        \
+    return TSVD_ECUDA;                                 \
+  }
+
+static tsvd_status init_ctx(tsvd_ctx* c) {
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return TSVD_ECUDA;
+  }
+  TSVD_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+  c->own_stream = true;
+  TSVD_CUDA(cudaMalloc(&c->dflags, 4 * sizeof(int)));
+  TSVD_CUDA(cudaMallocHost(&c->hflags, 4 * sizeof(int)));
+  return TSVD_OK;
+}
+
+static void destroy_ctx(tsvd_ctx* c) {
+  if (!c) return;
+  if (c->st) cudaStreamSynchronize(c->st);
+  csr_free(c->A);
+  csr_free(c->AT);
+  cudaFree(c->Ad);
+  free_bufs(*c);
+  prof_release(*c);
+  cudaFree(c->dflags);
+  if (c->hflags) cudaFreeHost(c->hflags);
+  if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+  delete c;
+}
+
+extern "C" {
+
+const char* tsvd_strerror(tsvd_status s) {
+  switch (s) {
+    case TSVD_OK: return "ok";
+    case TSVD_WARN_NOTCONV: return "not converged within maxit (results retrievable)";
+    case TSVD_EINVAL: return "invalid argument";
+    case TSVD_ESHAPE: return "invalid shape";
+    case TSVD_ENOMEM: return "device out of memory";
+    case TSVD_ECUDA: return "CUDA error or no usable device";
+    case TSVD_ESTATE: return "invalid state (no results yet)";
+    default: return "unknown status";
+  }
+}
+
+const char* tsvd_last_error(void) { return tsvd::g_last_error.c_str(); }
+
+tsvd_status tsvd_create_csr(tsvd_t* h, int64_t m, int64_t n, int64_t nnz,
+                            const int64_t* rowptr, const int32_t* colidx, const double* vals,
+                            int mem_kind) {
+  if (!h || !rowptr || (nnz > 0 && (!colidx || !vals)) || m < 0 || n < 1 || nnz < 0)
+    return TSVD_EINVAL;
+  if (m < n) return TSVD_ESHAPE;
+  if (n >= (int64_t)INT32_MAX || m >= (int64_t)INT32_MAX) return TSVD_ESHAPE;
+  *h = nullptr;
+  tsvd_ctx* c = new tsvd_ctx();
+  TSVD_API_BEGIN
+  tsvd_status s = init_ctx(c);
+  if (s != TSVD_OK) {
+    destroy_ctx(c);
+    return s;
+  }
+  c->m = m;
+  c->n = n;
+  c->dense = false;
+  Csr& A = c->A;
+  A.rows = m;
+  A.cols = n;
+  A.nnz = nnz;
+  const cudaMemcpyKind kind = mem_kind == TSVD_DEVICE ? cudaMemcpyDeviceToDevice
+                                                      : cudaMemcpyHostToDevice;
+  std::vector<int64_t> hrp(m + 1);
+  if (mem_kind == TSVD_DEVICE) {
+    TSVD_CUDA(cudaMemcpy(hrp.data(), rowptr, (m + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  } else {
+    std::memcpy(hrp.data(), rowptr, (m + 1) * sizeof(int64_t));
+    // host-side validation (cheap, exact)
+    if (hrp[0] != 0 || hrp[m] != nnz) {
+      destroy_ctx(c);
+      return TSVD_EINVAL;
+    }
+    for (int64_t i = 0; i < m; ++i) {
+      if (hrp[i + 1] < hrp[i]) {
+        destroy_ctx(c);
+        return TSVD_EINVAL;
+      }
+      int64_t prev = -1;
+      for (int64_t k = hrp[i]; k < hrp[i + 1]; ++k) {
+        const int64_t cj = colidx[k];
+        if (cj <= prev || cj >= n) {
+          destroy_ctx(c);
+          return TSVD_EINVAL;
+        }
+        prev = cj;
+      }
+    }
+  }
+  TSVD_CUDA(cudaMalloc(&A.rowptr, (m + 1) * sizeof(int64_t)));
+  TSVD_CUDA(cudaMalloc(&A.colidx, std::max<int64_t>(1, nnz) * sizeof(int32_t)));
+  TSVD_CUDA(cudaMalloc(&A.vals, std::max<int64_t>(1, nnz) * sizeof(double)));
+  TSVD_CUDA(cudaMemcpyAsync(A.rowptr, rowptr, (m + 1) * sizeof(int64_t), kind, c->st));
+  if (nnz > 0) {
+    TSVD_CUDA(cudaMemcpyAsync(A.colidx, colidx, nnz * sizeof(int32_t), kind, c->st));
+    TSVD_CUDA(cudaMemcpyAsync(A.vals, vals, nnz * sizeof(double), kind, c->st));
+  }
+  TSVD_CUDA(cudaStreamSynchronize(c->st));
+  if (mem_kind == TSVD_DEVICE && csr_validate_device(A, c->st) != 0) {
+    destroy_ctx(c);
+    return TSVD_EINVAL;
+  }
+  csr_transpose(A, c->AT, c->st);
+  csr_build_plan(A, hrp.data(), c->st);
+  std::vector<int64_t> hrpt(n + 1);
+  TSVD_CUDA(cudaMemcpy(hrpt.data(), c->AT.rowptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  csr_build_plan(c->AT, hrpt.data(), c->st);
+  *h = c;
+  return TSVD_OK;
+  }
+  catch (const tsvd::Error& e) {
+    tsvd::g_last_error = e.msg;
+    destroy_ctx(c);
+    return e.code;
+  }
+  catch (...) {
+    destroy_ctx(c);
+    return TSVD_ECUDA;
+  }
+}
+
+tsvd_status tsvd_create_dense(tsvd_t* h, int64_t m, int64_t n, const double* Ain, int64_t lda,
+                              int layout, int mem_kind) {
+  if (!h || !Ain || m < 1 || n < 1) return TSVD_EINVAL;
+  if (m < n) return TSVD_ESHAPE;
+  if (layout == TSVD_ROW_MAJOR ? lda < n : lda < m) return TSVD_EINVAL;
+  if (n >= (int64_t)INT32_MAX) return TSVD_ESHAPE;
+  *h = nullptr;
+  tsvd_ctx* c = new tsvd_ctx();
+  TSVD_API_BEGIN
+  tsvd_status s = init_ctx(c);
+  if (s != TSVD_OK) {
+    destroy_ctx(c);
+    return s;
+  }
+  c->m = m;
+  c->n = n;
+  c->dense = true;
+  c->lda = n;
+  TSVD_CUDA(cudaMalloc(&c->Ad, (size_t)m * n * sizeof(double)));
+  if (layout == TSVD_ROW_MAJOR) {
+    TSVD_CUDA(cudaMemcpy2DAsync(c->Ad, n * sizeof(double), Ain, lda * sizeof(double),
+                                n * sizeof(double), m,
+                                mem_kind == TSVD_DEVICE ? cudaMemcpyDeviceToDevice
+                                                        : cudaMemcpyHostToDevice,
+                                c->st));
+  } else {
+    // column-major input: upload as an n x m row-major block, transpose on device
+    double* tmp;
+    TSVD_CUDA(cudaMalloc(&tmp, (size_t)m * n * sizeof(double)));
+    TSVD_CUDA(cudaMemcpy2DAsync(tmp, m * sizeof(double), Ain, lda * sizeof(double),
+                                m * sizeof(double), n,
+                                mem_kind == TSVD_DEVICE ? cudaMemcpyDeviceToDevice
+                                                        : cudaMemcpyHostToDevice,
+                                c->st));
+    copy_block(tmp, m, c->Ad, n, m, (int)n, true, c->st);
+    TSVD_CUDA(cudaStreamSynchronize(c->st));
+    cudaFree(tmp);
+  }
+  TSVD_CUDA(cudaStreamSynchronize(c->st));
+  *h = c;
+  return TSVD_OK;
+  }
+  catch (const tsvd::Error& e) {
+    tsvd::g_last_error = e.msg;
+    destroy_ctx(c);
+    return e.code;
+  }
+  catch (...) {
+    destroy_ctx(c);
+    return TSVD_ECUDA;
+  }
+}
+
+tsvd_status tsvd_set_stream(tsvd_t h, void* stream) {
+  if (!h) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  TSVD_CUDA(cudaStreamSynchronize(h->st));
+  if (h->own_stream) cudaStreamDestroy(h->st);
+  h->st = (cudaStream_t)stream;  // NULL = legacy default stream
+  h->own_stream = false;
+  return TSVD_OK;
+  TSVD_API_END
+}
+
+tsvd_status tsvd_set_seed(tsvd_t h, uint64_t seed) {
+  if (!h) return TSVD_EINVAL;
+  h->seed = seed;
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_set_krylov_dim(tsvd_t h, int d) {
+  if (!h || d < 0) return TSVD_EINVAL;
+  h->krylov_d = d;
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_set_qr_block(tsvd_t h, int b_qr) {
+  if (!h || b_qr < 1 || b_qr > 32) return TSVD_EINVAL;
+  h->b_qr = b_qr;
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_set_start(tsvd_t h, const double* block, int64_t rows, int64_t cols,
+                           int64_t ld, int mem_kind) {
+  if (!h) return TSVD_EINVAL;
+  if (!block) {
+    h->start.clear();
+    h->start_rows = h->start_cols = 0;
+    return TSVD_OK;
+  }
+  if (rows < 1 || cols < 1 || ld < cols) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  h->start.resize((size_t)rows * cols);
+  TSVD_CUDA(cudaMemcpy2D(h->start.data(), cols * sizeof(double), block, ld * sizeof(double),
+                         cols * sizeof(double), rows,
+                         mem_kind == TSVD_DEVICE ? cudaMemcpyDeviceToHost
+                                                 : cudaMemcpyHostToHost));
+  h->start_rows = rows;
+  h->start_cols = cols;
+  return TSVD_OK;
+  TSVD_API_END
+}
+
+tsvd_status tsvd_block_lanczos(tsvd_t h, int r, int b, double tol, int maxit) {
+  if (!h) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  return lanczos_solve(*h, r, b, tol, maxit);
+  TSVD_API_END
+}
+
+tsvd_status tsvd_rsvd(tsvd_t h, int r, int p, int q) {
+  if (!h) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  return rsvd_solve(*h, r, p, q);
+  TSVD_API_END
+}
+
+tsvd_status tsvd_get(tsvd_t h, double* U, int64_t ldu, double* S, double* V, int64_t ldv,
+                     int mem_kind) {
+  if (!h) return TSVD_EINVAL;
+  if (!h->have) return TSVD_ESTATE;
+  const int r = h->r;
+  if ((U && ldu < r) || (V && ldv < r)) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  const cudaMemcpyKind k = mem_kind == TSVD_DEVICE ? cudaMemcpyDeviceToDevice
+                                                   : cudaMemcpyDeviceToHost;
+  if (U)
+    TSVD_CUDA(cudaMemcpy2DAsync(U, ldu * sizeof(double), h->U, r * sizeof(double),
+                                r * sizeof(double), h->m, k, h->st));
+  if (V)
+    TSVD_CUDA(cudaMemcpy2DAsync(V, ldv * sizeof(double), h->V, r * sizeof(double),
+                                r * sizeof(double), h->n, k, h->st));
+  if (S) TSVD_CUDA(cudaMemcpyAsync(S, h->S, r * sizeof(double), k, h->st));
+  TSVD_CUDA(cudaStreamSynchronize(h->st));
+  return TSVD_OK;
+  TSVD_API_END
+}
+
+tsvd_status tsvd_get_info(tsvd_t h, tsvd_info* out) {
+  if (!h || !out) return TSVD_EINVAL;
+  *out = h->info;
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_get_rho(tsvd_t h, double* rho) {
+  if (!h || !rho) return TSVD_EINVAL;
+  if (!h->have || h->rho.empty()) return TSVD_ESTATE;
+  std::copy(h->rho.begin(), h->rho.end(), rho);
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_set_profiling(tsvd_t h, int on) {
+  if (!h) return TSVD_EINVAL;
+  h->prof_on = on != 0;
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_get_profile(tsvd_t h, tsvd_prof_entry* out) {
+  if (!h || !out) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  TSVD_CUDA(cudaStreamSynchronize(h->st));
+  prof_harvest(*h);
+  for (int i = 0; i < TSVD_NPROF; ++i) out[i] = h->prof[i];
+  return TSVD_OK;
+  TSVD_API_END
+}
+
+tsvd_status tsvd_reset_profile(tsvd_t h) {
+  if (!h) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  TSVD_CUDA(cudaStreamSynchronize(h->st));
+  prof_harvest(*h);
+  for (int i = 0; i < TSVD_NPROF; ++i) {
+    const char* nm = h->prof[i].name;
+    h->prof[i] = tsvd_prof_entry{};
+    h->prof[i].name = nm;
+  }
+  return TSVD_OK;
+  TSVD_API_END
+}
+
+tsvd_status tsvd_destroy(tsvd_t h) {
+  if (!h) return TSVD_EINVAL;
+  destroy_ctx(h);
+  return TSVD_OK;
+}
+
+// ------------------------------------------------------------------ debug --
+static tsvd_ctx* dbg_ctx(void* stream) {
+  static thread_local tsvd_ctx* c = nullptr;
+  if (!c) {
+    c = new tsvd_ctx();
+    TSVD_CUDA(cudaMalloc(&c->dflags, 4 * sizeof(int)));
+    TSVD_CUDA(cudaMallocHost(&c->hflags, 4 * sizeof(int)));
+  }
+  c->st = (cudaStream_t)stream;
+  c->own_stream = false;
+  return c;
+}
+
+tsvd_status tsvd_dbg_philox(double* out, int64_t q, int w, int64_t ld, uint64_t seed,
+                            uint64_t draw, int64_t row0, int64_t q_total, void* stream) {
+  if (!out || q < 0 || w < 1 || ld < w) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  launch_philox_normal(out, q, w, ld, seed, draw, row0, q_total, (cudaStream_t)stream);
+  TSVD_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return TSVD_OK;
+  TSVD_API_END
+}
+
+tsvd_status tsvd_dbg_philox_words(const uint32_t* ctr, const uint32_t* key, uint32_t* out,
+                                  int64_t count, void* stream) {
+  if (!ctr || !key || !out || count < 0) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  launch_philox_words(ctr, key, out, count, (cudaStream_t)stream);
+  TSVD_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return TSVD_OK;
+  TSVD_API_END
+}
+
+tsvd_status tsvd_dbg_apply(tsvd_t h, int trans, const double* X, int64_t ldx, double* Y,
+                           int64_t ldy, int w) {
+  if (!h || !X || !Y || w < 1 || ldx < w || ldy < w) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  apply(*h, trans != 0, X, ldx, Y, ldy, w);
+  TSVD_CUDA(cudaStreamSynchronize(h->st));
+  return TSVD_OK;
+  TSVD_API_END
+}
+
+tsvd_status tsvd_dbg_cholqr2(double* Y, int64_t q, int w, int64_t ld, double* R, uint64_t seed,
+                             void* stream) {
+  if (!Y || !R || q < 1 || w < 1 || w > 32 || ld < w) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  tsvd_ctx* c = dbg_ctx(stream);
+  c->seed = seed;
+  c->draw_next = 1;
+  cholqr2(*c, Y, q, w, ld, R);
+  TSVD_CUDA(cudaStreamSynchronize(c->st));
+  return TSVD_OK;
+  TSVD_API_END
+}
+
+tsvd_status tsvd_dbg_cgs_cqr2(double* basis, int64_t q, int s, int w, int64_t ld, double* H,
+                              double* R, uint64_t seed, void* stream) {
+  if (!basis || !R || (s > 0 && !H) || q < 1 || s < 0 || w < 1 || w > 32 || ld < s + w)
+    return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  tsvd_ctx* c = dbg_ctx(stream);
+  c->seed = seed;
+  c->draw_next = 1;
+  cgs_cqr2(*c, basis, q, s, w, ld, H, R);
+  TSVD_CUDA(cudaStreamSynchronize(c->st));
+  return TSVD_OK;
+  TSVD_API_END
+}
+
+tsvd_status tsvd_dbg_cgs_qr(double* Y, int64_t q, int l, int64_t ld, int bq, double* R,
+                            uint64_t seed, void* stream) {
+  if (!Y || !R || q < 1 || l < 1 || bq < 1 || bq > 32 || ld < l) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  tsvd_ctx* c = dbg_ctx(stream);
+  c->seed = seed;
+  c->draw_next = 1;
+  cgs_qr(*c, Y, q, l, ld, bq, R);
+  TSVD_CUDA(cudaStreamSynchronize(c->st));
+  return TSVD_OK;
+  TSVD_API_END
+}
+
+tsvd_status tsvd_dbg_small_svd(const double* B, int d, double* Ub, double* S, double* Vb,
+                               void* stream) {
+  if (!B || !Ub || !S || !Vb || d < 1) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  tsvd_ctx* c = dbg_ctx(stream);
+  small_svd(B, d, Ub, S, Vb, dbuf(*c, "jacobi_work", small_svd_work(d)), c->st);
+  TSVD_CUDA(cudaStreamSynchronize(c->st));
+  return TSVD_OK;
+  TSVD_API_END
+}
+
+tsvd_status tsvd_dbg_gemm_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy,
+                             int64_t q, int s, int w, double* C, void* stream) {
+  if (!X || !Y || !C || q < 0 || s < 1 || w < 1) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  tsvd_ctx* c = dbg_ctx(stream);
+  const TnGeom g = tn_geom(q, s);
+  double* part = dbuf(*c, "part_tn", (size_t)(g.splits + 1) * s * 32);
+  gemm_tn(X, ldx, Y, ldy, nullptr, q, s, w, C, w, part, c->st);
+  TSVD_CUDA(cudaStreamSynchronize(c->st));
+  return TSVD_OK;
+  TSVD_API_END
+}
+
+tsvd_status tsvd_dbg_gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh,
+                             double* Z, int64_t ldz, int64_t q, int s, int w, double alpha,
+                             double beta, void* stream) {
+  if (!Z || q < 0 || s < 0 || w < 1 || (s > 0 && (!X || !H))) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  gemm_nn(X, ldx, H, ldh, Z, ldz, nullptr, Z, ldz, q, s, w, alpha, beta, nullptr,
+          (cudaStream_t)stream);
+  TSVD_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  return TSVD_OK;
+  TSVD_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,87 @@
+// Handle state of libtsvd (behind the opaque tsvd_t of include/tsvd.h).
+#pragma once
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace tsvd {
+enum ProfCat { P_APPLY_A = 0, P_APPLY_AT, P_TN, P_NN, P_SMALL, P_SVD, P_RESTART, P_OTHER };
+struct ProfRec {
+  int cat;
+  cudaEvent_t a, b;
+  int64_t launches;
+  double bytes, flops;
+};
+}  // namespace tsvd
+
+struct tsvd_ctx {
+  int64_t m = 0, n = 0;
+  bool dense = false;
+  tsvd::Csr A, AT;           // CSR(A), CSR(A^T)
+  double* Ad = nullptr;      // dense A, row-major m x n
+  int64_t lda = 0;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  uint64_t seed = 0x2403062180ULL;
+  uint64_t draw_next = 1;    // Philox draw id of the next breakdown replacement
+  int krylov_d = 0;
+  int b_qr = 16;
+  std::vector<double> start;  // optional exact start block (row-major, dense)
+  int64_t start_rows = 0, start_cols = 0;
+  // device workspace: named buffers grown on demand, kept across solves
+  std::map<std::string, std::pair<void*, size_t>> bufs;
+  int* dflags = nullptr;      // device flags
+  int* hflags = nullptr;      // pinned host mirror
+  // results of the last solve
+  double *U = nullptr, *S = nullptr, *V = nullptr;
+  int r = 0;
+  bool have = false;
+  std::vector<double> rho;    // rho_i / sigma_1, i < r (LancSVD)
+  tsvd_info info{};
+  int breakdowns = 0;
+  // instrumentation (tsvd_set_profiling)
+  bool prof_on = false;
+  std::vector<tsvd::ProfRec> prof_open;   // recorded, not yet harvested
+  std::vector<cudaEvent_t> ev_pool;
+  tsvd_prof_entry prof[TSVD_NPROF]{};
+};
+
+namespace tsvd {
+using Ctx = tsvd_ctx;
+// named device buffer of at least `bytes`, contents undefined
+void* buf(Ctx& c, const std::string& name, size_t bytes);
+inline double* dbuf(Ctx& c, const std::string& name, size_t n) {
+  return (double*)buf(c, name, n * sizeof(double));
+}
+void free_bufs(Ctx& c);
+
+// RAII phase scope: events around everything enqueued while alive.
+struct Prof {
+  Ctx& c;
+  int cat;
+  double bytes, flops;
+  cudaEvent_t a = nullptr;
+  int64_t l0 = 0;
+  Prof(Ctx& c_, int cat_, double bytes_, double flops_);
+  ~Prof();
+};
+void prof_harvest(Ctx& c);   // after a stream sync: fold records into c.prof
+void prof_release(Ctx& c);
+
+// building blocks (blocks.cu).  All blocks are row-major with leading
+// dimension ld; "basis" holds P in columns [0, s) and the block Y being
+// orthogonalised in columns [s, s+w).
+int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R);
+int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H,
+             double* R);
+void cgs2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H, double* R);
+int cgs_qr(Ctx& c, double* Y, int64_t q, int l, int64_t ld, int bq, double* R);
+void apply(Ctx& c, bool trans, const double* X, int64_t ldx, double* Y, int64_t ldy, int w);
+
+// solvers (solvers.cu)
+tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit);
+tsvd_status rsvd_solve(Ctx& c, int r, int p, int q);
+}  // namespace tsvd

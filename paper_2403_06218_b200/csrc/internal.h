@@ -1,0 +1,146 @@
+// Internal declarations shared by the CUDA translation units of libtsvd.
+// Nothing here crosses the C ABI (include/tsvd.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+#include <vector>
+
+#include "tsvd.h"
+
+namespace tsvd {
+
+// ---------------------------------------------------------------- errors --
+struct Error {
+  tsvd_status code;
+  std::string msg;
+};
+
+#define TSVD_CUDA(call)                                                     \
+  do {                                                                      \
+    cudaError_t e_ = (call);                                                \
+    if (e_ != cudaSuccess)                                                  \
+      throw ::tsvd::Error{e_ == cudaErrorMemoryAllocation ? TSVD_ENOMEM     \
+                                                          : TSVD_ECUDA,     \
+                          std::string(#call) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+// every kernel launch site ends with TSVD_CHECK_LAUNCH(): it also counts
+// launches for tsvd_info.launches / bench.py's gpu_launches.
+extern std::atomic<int64_t> g_launches;
+#define TSVD_CHECK_LAUNCH()                                                 \
+  do {                                                                      \
+    ::tsvd::g_launches.fetch_add(1, std::memory_order_relaxed);             \
+    TSVD_CUDA(cudaGetLastError());                                          \
+  } while (0)
+
+// ------------------------------------------------------------ data views --
+// Row-major view: element (i, j) at p[i*ld + j].  Row offsets are 64-bit.
+struct DMat {
+  double* p;
+  int64_t rows;
+  int cols;
+  int64_t ld;
+  DMat col(int c0, int w) const { return DMat{p + c0, rows, w, ld}; }
+};
+
+struct Csr {  // device CSR (canonical)
+  int64_t rows = 0, cols = 0, nnz = 0;
+  int64_t* rowptr = nullptr;
+  int32_t* colidx = nullptr;
+  double* vals = nullptr;
+  // load-balancing plan (SpMM): rows longer than kLongRow go to segments
+  int64_t nseg = 0;           // number of long-row segments
+  int64_t* seg_row = nullptr; // row of each segment
+  int64_t* seg_beg = nullptr; // [beg, end) nonzero range of each segment
+  int64_t* seg_end = nullptr;
+  int32_t* seg_slot = nullptr;   // partial slot (-1: segment covers the whole row)
+  int64_t nsplit = 0;            // long rows split into > 1 segment
+  int64_t* split_row = nullptr;  // row of each split row
+  int32_t* split_first = nullptr;// first partial slot of that row
+  int32_t* split_count = nullptr;// number of slots
+  int64_t nslots = 0;            // partial slots
+};
+
+
+
+// ---------------------------------------------------------- kernel entry --
+// All launchers enqueue on ctx-independent stream `st`.
+void launch_philox_normal(double* out, int64_t q, int w, int64_t ld, uint64_t seed,
+                          uint64_t draw, int64_t row0, int64_t q_total, cudaStream_t st);
+void launch_philox_words(const uint32_t* ctr, const uint32_t* key, uint32_t* out,
+                         int64_t count, cudaStream_t st);
+
+// SpMM: Y (A.rows x w) = A X, w <= 32 per call (callers chunk wider blocks).
+void launch_spmm(const Csr& A, const double* X, int64_t ldx, double* Y, int64_t ldy, int w,
+                 double* part, cudaStream_t st);
+void launch_spmm_wide(const Csr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                      int w, double* part, cudaStream_t st);
+
+// CSR transpose on the device (stable: rows of A^T list original rows in
+// increasing order).  Allocates T's arrays.
+void csr_transpose(const Csr& A, Csr& T, cudaStream_t st);
+void csr_build_plan(Csr& A, const int64_t* host_rowptr, cudaStream_t st);
+void csr_free(Csr& A);
+// device validation of a CSR: returns 0 if canonical
+int csr_validate_device(const Csr& A, cudaStream_t st);
+
+// -------------------------------------------------- tall-skinny products --
+// Partial-sum geometry of gemm_tn for (q, s): grid (s_tiles, splits).
+struct TnGeom {
+  int s_tiles, splits;
+};
+TnGeom tn_geom(int64_t q, int s);
+// C (s x w, ldc) = X^T Y', Y' = Y L^{-T} if L != null (L: w x w row-major,
+// lower).  part: workspace >= splits*s*w doubles (unused when splits == 1).
+void gemm_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, const double* L,
+             int64_t q, int s, int w, double* C, int64_t ldc, double* part, cudaStream_t st);
+// Z (q x w) = beta * (Y L^{-T}) + alpha * X H   (L optional, Y optional when
+// beta == 0); gram != null: per-CTA partial Gram Z^T Z written to
+// gram[cta*w*w], number of CTAs returned through *nparts.
+int nn_ctas(int64_t q);
+void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const double* Y,
+             int64_t ldy, const double* L, double* Z, int64_t ldz, int64_t q, int s, int w,
+             double alpha, double beta, double* gram, cudaStream_t st);
+
+// small (single-CTA) finalizers
+// W = sum of nparts partial (w x w) Grams; L = chol(W); flag[0] |= breakdown.
+// mode 1: also R = L^T (first CholQR pass result kept in Rprev)
+// mode 2: L2 = chol(W); R = L2^T Lprev^T; H (s x w) += Hbar Lprev^T
+void chol_finalize(const double* gram, int nparts, int w, double* L, int* flag,
+                   cudaStream_t st);
+void chol2_finalize(const double* gram, int nparts, int w, const double* Lprev, double* L2,
+                    double* R, double* H, const double* Hbar, int s, int* flag,
+                    cudaStream_t st);
+// out[i] = sum_p part[p*count + i], fixed order
+void reduce_partials(const double* part, int nparts, int64_t count, double* out,
+                     cudaStream_t st);
+
+// small helpers
+void copy_block(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
+                int cols, bool transpose, cudaStream_t st);
+void fill_zero(double* p, int64_t n, cudaStream_t st);
+
+// CGS2 column finalize (fallback path): see blocks.cu
+void cgs2_col_finalize(const double* c1, const double* c2, int nb, const double* gram_y,
+                       const double* gram_orig, double tau, double* coef_out, double* nrm_out,
+                       int* dependent, cudaStream_t st);
+void scale_column(double* col, int64_t q, int64_t ld, const double* nrm, cudaStream_t st);
+
+// one-sided Jacobi SVD of a d x d row-major B -> Ub, S (desc), Vb (row-major)
+void small_svd(const double* B, int d, double* Ub, double* S, double* Vb, double* work,
+               cudaStream_t st);
+size_t small_svd_work(int d);
+
+// rho_i = || Rbar * Vb[(k-1)b:kb, i] || / S[0] for i < cnt
+void lanczos_rho(const double* Rbar, int b, const double* Vb, int d, const double* S, int cnt,
+                 double* rho, cudaStream_t st);
+
+// sign normalisation: flip U[:,i], V[:,i] so that max |V[:,i]| entry > 0
+void sign_normalize(double* U, int64_t m, int64_t ldu, double* V, int64_t n, int64_t ldv,
+                    int r, double* work, cudaStream_t st);
+
+}  // namespace tsvd

@@ -1,0 +1,243 @@
+// Solver drivers: LancSVD (Alg. 2) and RandSVD (Alg. 1,
+// P:66-92).  Host loops that enqueue the device building blocks on the
+// handle's stream; the host reads one flag per orthogonalisation (breakdown,
+// P:275) and rho/sigma once per restart cycle.
+//
+// Layout in HBM: the Lanczos bases are row-major
+// panels Pbar (m x (d+b)) and P (n x d); block i lives in columns
+// [i b, (i+1) b), so one row of [P_{i-1} | Q_i] is one contiguous segment and
+// the orthogonalisation kernels read each basis row once per pass.  Column
+// block k of Pbar holds Qbar_{k+1} (reading R18), later reused as the slot
+// for the restart product.
+#include <algorithm>
+#include <cmath>
+
+#include "ctx.h"
+
+namespace tsvd {
+
+static void upload_start(Ctx& c, double* dst, int64_t rows, int cols, int64_t ld) {
+  TSVD_CUDA(cudaMemcpy2DAsync(dst, ld * sizeof(double), c.start.data(), cols * sizeof(double),
+                              cols * sizeof(double), rows, cudaMemcpyHostToDevice, c.st));
+}
+
+static void alloc_results(Ctx& c, int r) {
+  c.U = dbuf(c, "res_U", (size_t)c.m * r);
+  c.V = dbuf(c, "res_V", (size_t)c.n * r);
+  c.S = dbuf(c, "res_S", (size_t)r);
+  c.r = r;
+}
+
+struct EventTimer {
+  cudaEvent_t a, b;
+  cudaStream_t st;
+  explicit EventTimer(cudaStream_t s) : st(s) {
+    TSVD_CUDA(cudaEventCreate(&a));
+    TSVD_CUDA(cudaEventCreate(&b));
+    TSVD_CUDA(cudaEventRecord(a, st));
+  }
+  double stop() {
+    TSVD_CUDA(cudaEventRecord(b, st));
+    TSVD_CUDA(cudaEventSynchronize(b));
+    float ms = 0.f;
+    TSVD_CUDA(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+  }
+  ~EventTimer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+};
+
+tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
+  const int64_t m = c.m, n = c.n;
+  if (r < 1 || b < 1 || !(tol > 0.0) || maxit < 1) return TSVD_EINVAL;
+  if (b > 32) return TSVD_EINVAL;  // kernel tile limit
+  if (r > n) return TSVD_ESHAPE;
+  int d = c.krylov_d;
+  if (d == 0) {
+    d = std::max(4 * r, 2 * b);
+    d = (int)std::min<int64_t>(d, n);
+    d -= d % b;
+  }
+  if (d % b != 0 || d < r || d > n || d < b) return TSVD_ESHAPE;
+  if (!c.start.empty() && (c.start_rows != m || c.start_cols != b)) return TSVD_ESHAPE;
+  const int k = d / b;
+  const int64_t ldb = d + b, ldp = d;
+  c.have = false;
+  c.breakdowns = 0;
+  c.draw_next = 1;
+  const int64_t launches0 = g_launches.load();
+  EventTimer timer(c.st);
+
+  double* Pb = dbuf(c, "Pbar", (size_t)m * ldb);
+  double* P = dbuf(c, "P", (size_t)n * ldp);
+  double* B = dbuf(c, "B", (size_t)d * d);
+  double* Ub = dbuf(c, "Ub", (size_t)d * d);
+  double* Vb = dbuf(c, "Vb", (size_t)d * d);
+  double* Sg = dbuf(c, "Sg", (size_t)d);
+  double* jw = dbuf(c, "jacobi_work", small_svd_work(d));
+  double* H = dbuf(c, "H", (size_t)d * 32);
+  double* R = dbuf(c, "R", 32 * 32);
+  double* Rb = dbuf(c, "Rb", 32 * 32);
+  double* rho = dbuf(c, "rho", (size_t)d);
+  // pre-size the pass workspaces for the largest q and s of this solve
+  (void)dbuf(c, "scratch", (size_t)std::max(m, n) * 32);
+  (void)dbuf(c, "gram", (size_t)nn_ctas(std::max(m, n)) * 32 * 32);
+  (void)dbuf(c, "Hbar", (size_t)(d + b) * 32);
+  {
+    const TnGeom g1 = tn_geom(m, d + b), g2 = tn_geom(n, d);
+    const size_t need = (size_t)std::max((g1.splits + 1) * (d + b), (g2.splits + 1) * d) * 32;
+    (void)dbuf(c, "part_tn", need);
+  }
+
+  // S1: random orthonormal Qbar_1 (m x b)
+  if (!c.start.empty())
+    upload_start(c, Pb, m, b, ldb);
+  else
+    launch_philox_normal(Pb, m, b, ldb, c.seed, 0, 0, m, c.st);
+  cholqr2(c, Pb, m, b, ldb, R);
+
+  std::vector<double> hrho(r), hs(1);
+  int cycle = 0, nconv = 0;
+  bool conv = false;
+  double rho_max = 0.0;
+  for (cycle = 1; cycle <= maxit; ++cycle) {
+    fill_zero(B, (int64_t)d * d, c.st);
+    for (int i = 0; i < k; ++i) {
+      const int lo = i * b;
+      apply(c, true, Pb + lo, ldb, P + lo, ldp, b);                    // S2: A^T Qbar_i
+      if (i == 0)
+        cholqr2(c, P, n, b, ldp, R);                                   // S3a
+      else
+        cgs_cqr2(c, P, n, lo, b, ldp, H, R);                           // S3b
+      copy_block(R, b, B + (int64_t)lo * d + lo, d, b, b, true, c.st); // L_i = R^T
+      apply(c, false, P + lo, ldp, Pb + lo + b, ldb, b);               // S4: A Q_i
+      cgs_cqr2(c, Pb, m, lo + b, b, ldb, H, Rb);                       // S5
+      if (i < k - 1)
+        copy_block(Rb, b, B + (int64_t)(lo + b) * d + lo, d, b, b, false, c.st);  // Rbar_i
+    }
+    {
+      Prof p(c, P_SVD, 16.0 * d * d, 0);
+      small_svd(B, d, Ub, Sg, Vb, jw, c.st);                           // B_k = Ub S Vb^T
+    }
+    {
+      Prof p(c, P_OTHER, 0, 0);
+      lanczos_rho(Rb, b, Vb, d, Sg, r, rho, c.st);
+    }
+    TSVD_CUDA(cudaMemcpyAsync(hrho.data(), rho, r * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    TSVD_CUDA(cudaMemcpyAsync(hs.data(), Sg, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    TSVD_CUDA(cudaStreamSynchronize(c.st));
+    nconv = 0;
+    rho_max = 0.0;
+    for (int i = 0; i < r; ++i) {
+      if (hrho[i] <= tol) ++nconv;
+      rho_max = std::max(rho_max, hrho[i]);
+    }
+    conv = (nconv == r);
+    if (conv || cycle == maxit) break;
+    // S7: Qbar_1 = Pbar_k Ubar_1 (first b left Ritz vectors, reading R19),
+    // re-orthonormalised (reading R11); computed into the spare slot.
+    {
+      Prof p(c, P_RESTART, 8.0 * m * (d + b), 2.0 * m * d * b);
+      gemm_nn(Pb, ldb, Ub, d, nullptr, 0, nullptr, Pb + d, ldb, m, d, b, 1.0, 0.0, nullptr, c.st);
+    }
+    cholqr2(c, Pb + d, m, b, ldb, R);
+    {
+      Prof p(c, P_RESTART, 16.0 * m * b, 0);
+      copy_block(Pb + d, ldb, Pb, ldb, m, b, false, c.st);
+    }
+  }
+  if (cycle > maxit) cycle = maxit;
+  alloc_results(c, r);
+  {
+    Prof p(c, P_RESTART, 8.0 * (m + n) * (d + r), 2.0 * (m + n) * d * r);
+    // S9: U = Pbar_k Ubar[:, :r] ; S8 (Eq. 12): V = P_k Vbar[:, :r]
+    gemm_nn(Pb, ldb, Ub, d, nullptr, 0, nullptr, c.U, r, m, d, r, 1.0, 0.0, nullptr, c.st);
+    gemm_nn(P, ldp, Vb, d, nullptr, 0, nullptr, c.V, r, n, d, r, 1.0, 0.0, nullptr, c.st);
+    TSVD_CUDA(cudaMemcpyAsync(c.S, Sg, r * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+    sign_normalize(c.U, m, r, c.V, n, r, r, dbuf(c, "sign_work", (size_t)r), c.st);
+  }
+  const double ms = timer.stop();
+  prof_harvest(c);
+  c.rho = hrho;
+  c.have = true;
+  c.info = tsvd_info{};
+  c.info.cycles = cycle;
+  c.info.nconv = nconv;
+  c.info.r = r;
+  c.info.d = d;
+  c.info.b = b;
+  c.info.breakdowns = c.breakdowns;
+  c.info.rho_max = rho_max;
+  c.info.sigma1 = hs[0];
+  c.info.ms_total = ms;
+  c.info.launches = g_launches.load() - launches0;
+  return conv ? TSVD_OK : TSVD_WARN_NOTCONV;
+}
+
+tsvd_status rsvd_solve(Ctx& c, int r, int p, int q) {
+  const int64_t m = c.m, n = c.n;
+  if (r < 1 || p < 0 || q < 0) return TSVD_EINVAL;
+  const int l = r + p;
+  if (l > n) return TSVD_ESHAPE;
+  if (!c.start.empty() && (c.start_rows != n || c.start_cols != l)) return TSVD_ESHAPE;
+  const int bq = std::min(std::max(1, c.b_qr), 32);
+  c.have = false;
+  c.breakdowns = 0;
+  c.draw_next = 1;
+  const int64_t launches0 = g_launches.load();
+  EventTimer timer(c.st);
+
+  double* Qb = dbuf(c, "Qbar", (size_t)m * l);
+  double* Q = dbuf(c, "Q", (size_t)n * l);
+  double* R = dbuf(c, "Rp", (size_t)l * l);
+  double* Rb = dbuf(c, "Rbarp", (size_t)l * l);
+  double* Ub = dbuf(c, "Ub", (size_t)l * l);
+  double* Vb = dbuf(c, "Vb", (size_t)l * l);
+  double* Sg = dbuf(c, "Sg", (size_t)l);
+  double* jw = dbuf(c, "jacobi_work", small_svd_work(l));
+  (void)dbuf(c, "scratch", (size_t)std::max(m, n) * 32);
+  (void)dbuf(c, "gram", (size_t)nn_ctas(std::max(m, n)) * 32 * 32);
+
+  if (!c.start.empty())
+    upload_start(c, Q, n, l, l);
+  else
+    launch_philox_normal(Q, n, l, l, c.seed, 0, 0, n, c.st);         // Q_0 (not orthonormal)
+  for (int j = 0; j <= q; ++j) {
+    apply(c, false, Q, l, Qb, l, l);                                   // S1
+    cgs_qr(c, Qb, m, l, l, bq, Rb);                                    // S2
+    apply(c, true, Qb, l, Q, l, l);                                    // S3
+    cgs_qr(c, Q, n, l, l, bq, R);                                      // S4
+  }
+  {
+    Prof p(c, P_SVD, 16.0 * l * l, 0);
+    small_svd(R, l, Ub, Sg, Vb, jw, c.st);                             // S5
+  }
+  alloc_results(c, r);
+  {
+    Prof p(c, P_RESTART, 8.0 * (m + n) * (l + r), 2.0 * (m + n) * l * r);
+    gemm_nn(Qb, l, Vb, l, nullptr, 0, nullptr, c.U, r, m, l, r, 1.0, 0.0, nullptr, c.st);  // S6
+    gemm_nn(Q, l, Ub, l, nullptr, 0, nullptr, c.V, r, n, l, r, 1.0, 0.0, nullptr, c.st);   // S7
+    TSVD_CUDA(cudaMemcpyAsync(c.S, Sg, r * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+    sign_normalize(c.U, m, r, c.V, n, r, r, dbuf(c, "sign_work", (size_t)r), c.st);
+  }
+  double s1 = 0.0;
+  TSVD_CUDA(cudaMemcpyAsync(&s1, Sg, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+  const double ms = timer.stop();
+  prof_harvest(c);
+  c.rho.clear();
+  c.have = true;
+  c.info = tsvd_info{};
+  c.info.cycles = q + 1;
+  c.info.r = r;
+  c.info.d = l;
+  c.info.b = bq;
+  c.info.breakdowns = c.breakdowns;
+  c.info.sigma1 = s1;
+  c.info.ms_total = ms;
+  c.info.launches = g_launches.load() - launches0;
+  return TSVD_OK;
+}
+
+}  // namespace tsvd

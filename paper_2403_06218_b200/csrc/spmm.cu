@@ -1,0 +1,361 @@
+// CSR SpMM Y = A X on a tall-skinny row-major block (Alg. 1 S1/S3,
+// Alg. 2 S2/S4; P:416 stores A as CSR).  A^T X uses the same kernels on the
+// precomputed CSR(A^T) (built here by a stable counting sort), so the
+// transposed product needs no atomics (north_star; P:460/P:498 note that
+// cuSPARSE's implicitly transposed SpMM is the paper's bottleneck).
+//
+// Load balance for power-law rows:
+//  * short rows (<= kLongRow nonzeros): a group of L = pow2 >= w lanes per
+//    row, lane c owns output column c; nonzeros unrolled by 8 so eight
+//    independent row gathers of X are in flight per lane;
+//  * long rows: split into segments of <= kSeg nonzeros, one CTA per segment
+//    (256/L groups strided over the segment, fixed-order smem reduction);
+//    rows with several segments write partials that a fix-up kernel sums in
+//    segment order.  Deterministic: no floating-point atomics anywhere.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "internal.h"
+
+namespace tsvd {
+
+constexpr int kLongRow = 64;
+constexpr int kSeg = 2048;
+
+template <int L>
+__global__ void __launch_bounds__(256) spmm_short_kernel(
+    const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
+    const double* __restrict__ vals, const double* __restrict__ X, int64_t ldx,
+    double* __restrict__ Y, int64_t ldy, int64_t rows, int w) {
+  constexpr int RPW = 32 / L;  // rows per warp
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t row = warp * RPW + lane / L;
+  const int c = lane % L;
+  if (row >= rows) return;
+  const int64_t beg = __ldg(rowptr + row), end = __ldg(rowptr + row + 1);
+  if (end - beg > kLongRow) return;  // handled by the long-row kernels
+  const bool active = c < w;
+  const double* Xc = X + c;
+  double acc0 = 0.0, acc1 = 0.0;
+  int64_t k = beg;
+  for (; k + 8 <= end; k += 8) {
+    int32_t col[8];
+    double v[8], x[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      col[u] = __ldg(colidx + k + u);
+      v[u] = __ldg(vals + k + u);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) x[u] = active ? __ldg(Xc + (int64_t)col[u] * ldx) : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; u += 2) {
+      acc0 = fma(v[u], x[u], acc0);
+      acc1 = fma(v[u + 1], x[u + 1], acc1);
+    }
+  }
+  for (; k < end; ++k) {
+    const int32_t col = __ldg(colidx + k);
+    const double v = __ldg(vals + k);
+    const double x = active ? __ldg(Xc + (int64_t)col * ldx) : 0.0;
+    acc0 = fma(v, x, acc0);
+  }
+  if (active) Y[row * ldy + c] = acc0 + acc1;
+}
+
+template <int L>
+__global__ void __launch_bounds__(256) spmm_long_kernel(
+    const int64_t* __restrict__ seg_row, const int64_t* __restrict__ seg_beg,
+    const int64_t* __restrict__ seg_end, const int32_t* __restrict__ seg_slot,
+    const int32_t* __restrict__ colidx, const double* __restrict__ vals,
+    const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy, int w,
+    double* __restrict__ part) {
+  constexpr int G = 256 / L;
+  __shared__ double red[G][33];
+  const int g = threadIdx.x / L, c = threadIdx.x % L;
+  const int64_t s = blockIdx.x;
+  const int64_t beg = seg_beg[s], end = seg_end[s];
+  const bool active = c < w;
+  const double* Xc = X + c;
+  double acc0 = 0.0, acc1 = 0.0;
+  int64_t k = beg + g;
+  for (; k + 3 * G < end; k += 4 * G) {
+    const int32_t c0 = __ldg(colidx + k), c1 = __ldg(colidx + k + G);
+    const int32_t c2 = __ldg(colidx + k + 2 * G), c3 = __ldg(colidx + k + 3 * G);
+    const double v0 = __ldg(vals + k), v1 = __ldg(vals + k + G);
+    const double v2 = __ldg(vals + k + 2 * G), v3 = __ldg(vals + k + 3 * G);
+    double x0 = 0, x1 = 0, x2 = 0, x3 = 0;
+    if (active) {
+      x0 = __ldg(Xc + (int64_t)c0 * ldx);
+      x1 = __ldg(Xc + (int64_t)c1 * ldx);
+      x2 = __ldg(Xc + (int64_t)c2 * ldx);
+      x3 = __ldg(Xc + (int64_t)c3 * ldx);
+    }
+    acc0 = fma(v0, x0, acc0);
+    acc1 = fma(v1, x1, acc1);
+    acc0 = fma(v2, x2, acc0);
+    acc1 = fma(v3, x3, acc1);
+  }
+  for (; k < end; k += G) {
+    const int32_t c0 = __ldg(colidx + k);
+    const double v0 = __ldg(vals + k);
+    const double x0 = active ? __ldg(Xc + (int64_t)c0 * ldx) : 0.0;
+    acc0 = fma(v0, x0, acc0);
+  }
+  red[g][c] = acc0 + acc1;
+  __syncthreads();
+  if (threadIdx.x < w) {
+    double sum = 0.0;
+    for (int gg = 0; gg < G; ++gg) sum += red[gg][threadIdx.x];
+    const int slot = seg_slot[s];
+    if (slot < 0)
+      Y[seg_row[s] * ldy + threadIdx.x] = sum;
+    else
+      part[(int64_t)slot * 32 + threadIdx.x] = sum;
+  }
+}
+
+__global__ void spmm_fixup_kernel(const int64_t* __restrict__ split_row,
+                                  const int32_t* __restrict__ split_first,
+                                  const int32_t* __restrict__ split_count,
+                                  const double* __restrict__ part, double* __restrict__ Y,
+                                  int64_t ldy, int w, int64_t nsplit) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t r = t / 32;
+  const int c = (int)(t % 32);
+  if (r >= nsplit || c >= w) return;
+  const int first = split_first[r], cnt = split_count[r];
+  double sum = 0.0;
+  for (int j = 0; j < cnt; ++j) sum += part[(int64_t)(first + j) * 32 + c];
+  Y[split_row[r] * ldy + c] = sum;
+}
+
+template <int L>
+static void spmm_dispatch(const Csr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                          int w, double* part, cudaStream_t st) {
+  constexpr int RPW = 32 / L;
+  const int64_t rows_per_block = 8 * RPW;
+  const int64_t blocks = (A.rows + rows_per_block - 1) / rows_per_block;
+  if (blocks > 0) {
+    spmm_short_kernel<L><<<(unsigned)blocks, 256, 0, st>>>(A.rowptr, A.colidx, A.vals, X, ldx,
+                                                            Y, ldy, A.rows, w);
+    TSVD_CHECK_LAUNCH();
+  }
+  if (A.nseg > 0) {
+    spmm_long_kernel<L><<<(unsigned)A.nseg, 256, 0, st>>>(A.seg_row, A.seg_beg, A.seg_end,
+                                                           A.seg_slot, A.colidx, A.vals, X,
+                                                           ldx, Y, ldy, w, part);
+    TSVD_CHECK_LAUNCH();
+  }
+  if (A.nsplit > 0) {
+    const int64_t thr = A.nsplit * 32;
+    spmm_fixup_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(
+        A.split_row, A.split_first, A.split_count, part, Y, ldy, w, A.nsplit);
+    TSVD_CHECK_LAUNCH();
+  }
+}
+
+void launch_spmm(const Csr& A, const double* X, int64_t ldx, double* Y, int64_t ldy, int w,
+                 double* part, cudaStream_t st) {
+  if (w <= 4)
+    spmm_dispatch<4>(A, X, ldx, Y, ldy, w, part, st);
+  else if (w <= 8)
+    spmm_dispatch<8>(A, X, ldx, Y, ldy, w, part, st);
+  else if (w <= 16)
+    spmm_dispatch<16>(A, X, ldx, Y, ldy, w, part, st);
+  else
+    spmm_dispatch<32>(A, X, ldx, Y, ldy, w, part, st);
+}
+
+void launch_spmm_wide(const Csr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                      int w, double* part, cudaStream_t st) {
+  for (int c0 = 0; c0 < w; c0 += 32) {
+    const int wc = w - c0 < 32 ? w - c0 : 32;
+    launch_spmm(A, X + c0, ldx, Y + c0, ldy, wc, part, st);
+  }
+}
+
+// ------------------------------------------------------- plan / transpose --
+void csr_build_plan(Csr& A, const int64_t* hrp, cudaStream_t st) {
+  std::vector<int64_t> srow, sbeg, send, sprow;
+  std::vector<int32_t> sslot, spfirst, spcnt;
+  int32_t slots = 0;
+  for (int64_t i = 0; i < A.rows; ++i) {
+    const int64_t len = hrp[i + 1] - hrp[i];
+    if (len <= kLongRow) continue;
+    const int64_t nseg = (len + kSeg - 1) / kSeg;
+    if (nseg > 1) {
+      sprow.push_back(i);
+      spfirst.push_back(slots);
+      spcnt.push_back((int32_t)nseg);
+    }
+    for (int64_t s = 0; s < nseg; ++s) {
+      srow.push_back(i);
+      sbeg.push_back(hrp[i] + s * kSeg);
+      send.push_back(std::min(hrp[i + 1], hrp[i] + (s + 1) * kSeg));
+      sslot.push_back(nseg > 1 ? slots++ : -1);
+    }
+  }
+  A.nseg = (int64_t)srow.size();
+  A.nsplit = (int64_t)sprow.size();
+  A.nslots = slots;
+  auto up64 = [&](std::vector<int64_t>& v, int64_t** d) {
+    if (v.empty()) return;
+    TSVD_CUDA(cudaMalloc(d, v.size() * sizeof(int64_t)));
+    TSVD_CUDA(cudaMemcpyAsync(*d, v.data(), v.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  };
+  auto up32 = [&](std::vector<int32_t>& v, int32_t** d) {
+    if (v.empty()) return;
+    TSVD_CUDA(cudaMalloc(d, v.size() * sizeof(int32_t)));
+    TSVD_CUDA(cudaMemcpyAsync(*d, v.data(), v.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  };
+  up64(srow, &A.seg_row);
+  up64(sbeg, &A.seg_beg);
+  up64(send, &A.seg_end);
+  up32(sslot, &A.seg_slot);
+  up64(sprow, &A.split_row);
+  up32(spfirst, &A.split_first);
+  up32(spcnt, &A.split_count);
+  TSVD_CUDA(cudaStreamSynchronize(st));
+}
+
+void csr_free(Csr& A) {
+  cudaFree(A.rowptr);
+  cudaFree(A.colidx);
+  cudaFree(A.vals);
+  cudaFree(A.seg_row);
+  cudaFree(A.seg_beg);
+  cudaFree(A.seg_end);
+  cudaFree(A.seg_slot);
+  cudaFree(A.split_row);
+  cudaFree(A.split_first);
+  cudaFree(A.split_count);
+  A = Csr{};
+}
+
+__global__ void row_of_nz_kernel(const int64_t* __restrict__ rowptr, int64_t rows, int64_t nnz,
+                                 int32_t* __restrict__ row_of) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = rows;  // largest i with rowptr[i] <= k
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (rowptr[mid] <= k) lo = mid; else hi = mid;
+    }
+    row_of[k] = (int32_t)lo;
+  }
+}
+
+__global__ void iota_kernel(int32_t* p, int64_t n) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    p[k] = (int32_t)k;
+}
+
+__global__ void gather_t_kernel(const int32_t* __restrict__ perm,
+                                const int32_t* __restrict__ row_of,
+                                const double* __restrict__ vals, int32_t* __restrict__ tcol,
+                                double* __restrict__ tval, int64_t nnz) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = perm[k];
+    tcol[k] = row_of[p];
+    tval[k] = vals[p];
+  }
+}
+
+__global__ void t_rowptr_kernel(const int32_t* __restrict__ sorted_cols, int64_t nnz,
+                                int64_t ncols, int64_t* __restrict__ trowptr) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j <= ncols;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = nnz;  // first k with sorted_cols[k] >= j
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (sorted_cols[mid] < j) lo = mid + 1; else hi = mid;
+    }
+    trowptr[j] = lo;
+  }
+}
+
+void csr_transpose(const Csr& A, Csr& T, cudaStream_t st) {
+  T.rows = A.cols;
+  T.cols = A.rows;
+  T.nnz = A.nnz;
+  if (A.nnz >= (int64_t)INT32_MAX) throw Error{TSVD_EINVAL, "nnz >= 2^31 per shard"};
+  const int nnz = (int)A.nnz;
+  TSVD_CUDA(cudaMalloc(&T.rowptr, (T.rows + 1) * sizeof(int64_t)));
+  TSVD_CUDA(cudaMalloc(&T.colidx, std::max<int64_t>(1, T.nnz) * sizeof(int32_t)));
+  TSVD_CUDA(cudaMalloc(&T.vals, std::max<int64_t>(1, T.nnz) * sizeof(double)));
+  if (nnz == 0) {
+    TSVD_CUDA(cudaMemsetAsync(T.rowptr, 0, (T.rows + 1) * sizeof(int64_t), st));
+    TSVD_CUDA(cudaStreamSynchronize(st));
+    return;
+  }
+  int32_t *row_of, *perm_in, *perm_out, *keys_out;
+  TSVD_CUDA(cudaMalloc(&row_of, nnz * sizeof(int32_t)));
+  TSVD_CUDA(cudaMalloc(&perm_in, nnz * sizeof(int32_t)));
+  TSVD_CUDA(cudaMalloc(&perm_out, nnz * sizeof(int32_t)));
+  TSVD_CUDA(cudaMalloc(&keys_out, nnz * sizeof(int32_t)));
+  const unsigned grid = 148 * 8;
+  row_of_nz_kernel<<<grid, 256, 0, st>>>(A.rowptr, A.rows, A.nnz, row_of);
+  iota_kernel<<<grid, 256, 0, st>>>(perm_in, A.nnz);
+  TSVD_CHECK_LAUNCH();
+  int end_bit = 1;
+  while (end_bit < 31 && (int64_t(1) << end_bit) < A.cols) ++end_bit;
+  size_t tmp_bytes = 0;
+  TSVD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, A.colidx, keys_out, perm_in,
+                                            perm_out, nnz, 0, end_bit, st));
+  void* tmp;
+  TSVD_CUDA(cudaMalloc(&tmp, tmp_bytes));
+  TSVD_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, A.colidx, keys_out, perm_in,
+                                            perm_out, nnz, 0, end_bit, st));
+  gather_t_kernel<<<grid, 256, 0, st>>>(perm_out, row_of, A.vals, T.colidx, T.vals, A.nnz);
+  t_rowptr_kernel<<<grid, 256, 0, st>>>(keys_out, A.nnz, T.rows, T.rowptr);
+  TSVD_CHECK_LAUNCH();
+  TSVD_CUDA(cudaStreamSynchronize(st));
+  cudaFree(tmp);
+  cudaFree(row_of);
+  cudaFree(perm_in);
+  cudaFree(perm_out);
+  cudaFree(keys_out);
+}
+
+__global__ void csr_validate_kernel(const int64_t* __restrict__ rowptr,
+                                    const int32_t* __restrict__ colidx, int64_t rows,
+                                    int64_t cols, int64_t nnz, int* __restrict__ bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = rowptr[i], e = rowptr[i + 1];
+    if (b > e || b < 0 || e > nnz) {
+      atomicOr(bad, 1);
+      continue;
+    }
+    int64_t prev = -1;
+    for (int64_t k = b; k < e; ++k) {
+      const int64_t c = colidx[k];
+      if (c <= prev || c >= cols) {
+        atomicOr(bad, 2);
+        break;
+      }
+      prev = c;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (rowptr[0] != 0 || rowptr[rows] != nnz) atomicOr(bad, 4);
+  }
+}
+
+int csr_validate_device(const Csr& A, cudaStream_t st) {
+  int* d;
+  TSVD_CUDA(cudaMalloc(&d, sizeof(int)));
+  TSVD_CUDA(cudaMemsetAsync(d, 0, sizeof(int), st));
+  csr_validate_kernel<<<148 * 4, 256, 0, st>>>(A.rowptr, A.colidx, A.rows, A.cols, A.nnz, d);
+  TSVD_CHECK_LAUNCH();
+  int h = 0;
+  TSVD_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st));
+  TSVD_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d);
+  return h;
+}
+
+}  // namespace tsvd
