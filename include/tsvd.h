@@ -189,7 +189,8 @@ tsvd_status tsvd_dbg_cgs_qr(double* Y, int64_t q, int l, int64_t ld, int bq,
 /* Small SVD by one-sided Jacobi on the device (reading R20): B (d x d,
  * row-major) -> Ub (d x d), S (d, descending), Vb (d x d), B = Ub S Vb^T. */
 tsvd_status tsvd_dbg_small_svd(const double* B, int d, double* Ub, double* S,
-                               double* Vb, void* stream);
+                               double* Vb, int* sweeps /* host, may be NULL */,
+                               void* stream);
 /* Tall-skinny products used by the passes: C (s x w) = X^T Y with X (q x s,
  * ldx), Y (q x w, ldy) (Alg. 5 S1/S6); and Z (q x w) = beta*Z + alpha*X H
  * with H (s x w, ldh) (Alg. 5 S2/S7, restart, outputs). */

@@ -82,7 +82,7 @@ _SIGS = {
     "tsvd_dbg_cholqr2": [vp, i64, i32, i64, vp, u64, vp],
     "tsvd_dbg_cgs_cqr2": [vp, i64, i32, i32, i64, vp, vp, u64, vp],
     "tsvd_dbg_cgs_qr": [vp, i64, i32, i64, i32, vp, u64, vp],
-    "tsvd_dbg_small_svd": [vp, i32, vp, vp, vp, vp],
+    "tsvd_dbg_small_svd": [vp, i32, vp, vp, vp, C.POINTER(C.c_int), vp],
     "tsvd_dbg_gemm_tn": [vp, i64, vp, i64, i64, i32, i32, vp, vp],
     "tsvd_dbg_gemm_nn": [vp, i64, vp, i64, vp, i64, i64, i32, i32, dbl, dbl, vp],
     "tsvd_set_profiling": [vp, i32],
@@ -351,10 +351,13 @@ def dbg_cgs_qr(Y, bq: int, R, seed: int = 0, stream=None):
                                  _stream_ptr(stream)), "tsvd_dbg_cgs_qr")
 
 
-def dbg_small_svd(B, Ub, S, Vb, stream=None):
+def dbg_small_svd(B, Ub, S, Vb, stream=None) -> int:
+    """Returns the number of Jacobi sweeps used."""
     d = B.shape[0]
-    _check(lib().tsvd_dbg_small_svd(_dp(B), d, _dp(Ub), _dp(S), _dp(Vb), _stream_ptr(stream)),
-           "tsvd_dbg_small_svd")
+    sw = C.c_int(0)
+    _check(lib().tsvd_dbg_small_svd(_dp(B), d, _dp(Ub), _dp(S), _dp(Vb), C.byref(sw),
+                                    _stream_ptr(stream)), "tsvd_dbg_small_svd")
+    return sw.value
 
 
 def dbg_gemm_tn(X, Y, Cout, stream=None):

@@ -423,12 +423,14 @@ tsvd_status tsvd_dbg_cgs_qr(double* Y, int64_t q, int l, int64_t ld, int bq, dou
 }
 
 tsvd_status tsvd_dbg_small_svd(const double* B, int d, double* Ub, double* S, double* Vb,
-                               void* stream) {
+                               int* sweeps, void* stream) {
   if (!B || !Ub || !S || !Vb || d < 1) return TSVD_EINVAL;
   TSVD_API_BEGIN
   tsvd_ctx* c = dbg_ctx(stream);
-  small_svd(B, d, Ub, S, Vb, dbuf(*c, "jacobi_work", small_svd_work(d)), c->st);
+  double* work = dbuf(*c, "jacobi_work", small_svd_work(d));
+  small_svd(B, d, Ub, S, Vb, work, c->st);
   TSVD_CUDA(cudaStreamSynchronize(c->st));
+  if (sweeps) *sweeps = small_svd_sweeps(work, d);
   return TSVD_OK;
   TSVD_API_END
 }

@@ -134,6 +134,7 @@ void scale_column(double* col, int64_t q, int64_t ld, const double* nrm, cudaStr
 void small_svd(const double* B, int d, double* Ub, double* S, double* Vb, double* work,
                cudaStream_t st);
 size_t small_svd_work(int d);
+int small_svd_sweeps(const double* work, int d);  // sweeps of the last small_svd (syncs)
 
 // rho_i = || Rbar * Vb[(k-1)b:kb, i] || / S[0] for i < cnt
 void lanczos_rho(const double* Rbar, int b, const double* Vb, int d, const double* S, int cnt,

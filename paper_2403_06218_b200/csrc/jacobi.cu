@@ -1,133 +1,294 @@
-// Small projected SVD on the device: one-sided (Hestenes) Jacobi.
+// Small projected SVD on the device: block one-sided (Hestenes) Jacobi.
 // Alg. 1 S5 (SVD of R_p) and Alg. 2 (SVD of B_k, Eq. 9).  The paper runs
 // LAPACK GESVD on the host (Table 1); any backward-stable SVD
 // gives the same triplets up to signs (reading R20), and keeping it on the
 // device removes the PCIe round trip (north_star (4)).
 //
-// Columns g_p, g_q of G (initially B) are rotated until all pairs are
-// orthogonal to |g_p^T g_q| <= sqrt(d) u ||g_p|| ||g_q||; V accumulates the
-// rotations.  Then sigma_j = ||g_j||, ubar_j = g_j / sigma_j; sorted
-// descending.  Parallel ordering: round-robin tournament, d/2 disjoint pairs
-// per round, one warp per pair; rotation of Rutishauser form
-//   zeta = (b - a) / (2c), t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)),
-//   cs = 1/sqrt(1+t^2), sn = cs t,  [g_p g_q] <- [g_p g_q] [[cs, sn], [-sn, cs]].
+// G (initially B, column-major in global memory / L2) is orthogonalised by
+// plane rotations applied from the right, V accumulates them; at convergence
+// sigma_j = ||g_j||, ubar_j = g_j / sigma_j, vbar_j = v_j, sorted descending.
+//
+// Parallel block ordering (one cooperative launch, one CTA per block pair):
+// the d columns are cut into nb blocks of JC columns; in each round of the
+// round-robin tournament CTA p owns a disjoint pair of blocks (I, J) and
+//   1. loads the 2*JC columns [G_I G_J] into shared memory,
+//   2. runs one-sided Jacobi sweeps on those 2*JC columns in shared memory
+//      (JC disjoint column pairs per inner round, one warp per pair), each
+//      rotation computed from the current columns' dot products, and
+//      accumulates the 2JC x 2JC orthogonal J of the applied rotations,
+//   3. writes the rotated columns back and updates [V_I V_J] <- [V_I V_J] J,
+// then all CTAs meet at a grid barrier.  A sweep = nb-1 rounds; sweeps repeat
+// until no rotation with |g_p^T g_q| > tol ||g_p|| ||g_q|| (tol = d u) was needed.
+// Rotation (Rutishauser): zeta = (M_qq - M_pp) / (2 M_pq),
+//   t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), cs = 1/sqrt(1+t^2), sn = cs t,
+//   [g_p g_q] <- [g_p g_q] [[cs, sn], [-sn, cs]].
+#include <cooperative_groups.h>
+
 #include "internal.h"
 
 namespace tsvd {
 
-size_t small_svd_work(int d) { return 2 * (size_t)d * d + 2 * (size_t)d + 64; }
+constexpr int JC = 8;        // columns per block
+constexpr int JW = 2 * JC;   // columns per block pair
+constexpr int JP = JW + 1;   // padded smem row
+constexpr int kMaxSweeps = 30;
+constexpr int kInnerSweeps = 1;
+constexpr int kJacobiMaxD = 1536;
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
+static int jac_nb(int d) {
+  int nb = (d + JC - 1) / JC;
+  if (nb < 2) nb = 2;
+  if (nb & 1) ++nb;
+  return nb;
 }
 
-__global__ void __launch_bounds__(1024) jacobi_svd_kernel(const double* __restrict__ B, int d,
-                                                          double* __restrict__ Ub,
-                                                          double* __restrict__ S,
-                                                          double* __restrict__ Vb,
-                                                          double* __restrict__ work) {
-  double* G = work;                    // column-major d x d
-  double* V = work + (size_t)d * d;    // column-major d x d
-  double* nrm = V + (size_t)d * d;     // d
-  __shared__ int rotated;
-  __shared__ int sweeps_done;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nw = blockDim.x >> 5;
-  for (int64_t i = tid; i < (int64_t)d * d; i += blockDim.x) {
-    const int r = (int)(i / d), c = (int)(i % d);
-    G[(size_t)c * d + r] = B[i];
-    V[(size_t)c * d + r] = (r == c) ? 1.0 : 0.0;
-  }
-  if (tid == 0) sweeps_done = 0;
+size_t small_svd_work(int d) {
+  const size_t nb = (size_t)jac_nb(d), dp = nb * JC;
+  return (size_t)d * dp + dp * dp + dp + 64;
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
   __syncthreads();
-  const int ne = d + (d & 1);  // even number of players
-  const double tol = sqrt((double)d) * 0x1.0p-53;
-  for (int sweep = 0; sweep < 40; ++sweep) {
-    if (tid == 0) rotated = 0;
-    __syncthreads();
-    for (int round = 0; round < ne - 1; ++round) {
-      for (int t = warp; t < ne / 2; t += nw) {
-        // circle method: position 0 fixed, others rotate
-        int p = (t == 0) ? 0 : ((t - 1 + round) % (ne - 1)) + 1;
-        int q = ((ne - 2 - t + round) % (ne - 1)) + 1;
-        if (p >= d || q >= d) continue;
-        if (p > q) {
-          const int tmp = p;
-          p = q;
-          q = tmp;
+  if (threadIdx.x == 0) {
+    volatile unsigned* vgen = bar + 1;
+    const unsigned gen = *vgen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == nblocks - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*vgen == gen) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void circle_pair(int t, int round, int ne, int& p, int& q) {
+  p = (t == 0) ? 0 : ((t - 1 + round) % (ne - 1)) + 1;
+  q = ((ne - 2 - t + round) % (ne - 1)) + 1;
+  if (p > q) {
+    const int x = p;
+    p = q;
+    q = x;
+  }
+}
+
+__global__ void jacobi_init_kernel(const double* __restrict__ B, int d, int dp,
+                                   double* __restrict__ G, double* __restrict__ V,
+                                   unsigned* __restrict__ ctl) {
+  const int64_t total = (int64_t)d * dp + (int64_t)dp * dp;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < (int64_t)d * dp) {
+      const int c = (int)(i / d), r = (int)(i % d);
+      G[i] = c < d ? B[(int64_t)r * d + c] : 0.0;  // G column-major
+    } else {
+      const int64_t k = i - (int64_t)d * dp;
+      const int c = (int)(k / dp), r = (int)(k % dp);
+      V[k] = (r == c) ? 1.0 : 0.0;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < 8) ctl[threadIdx.x] = 0u;
+}
+
+__global__ void __launch_bounds__(256) jacobi_block_kernel(double* __restrict__ G,
+                                                           double* __restrict__ V, int d, int nb,
+                                                           double* __restrict__ nrm,
+                                                           double* __restrict__ Ub,
+                                                           double* __restrict__ S,
+                                                           double* __restrict__ Vb,
+                                                           unsigned* __restrict__ ctl) {
+  extern __shared__ double sm[];
+  double* Gs = sm;                   // d x JP (row r, col k) ; reused for V chunks
+  double* Js = Gs + (size_t)d * JP;  // JW x JP
+  __shared__ int any_rot, inner_rot;
+  unsigned* bar = ctl;          // [0] count, [1] generation
+  unsigned* rot = ctl + 2;      // [2], [3] sweep flags (double-buffered)
+  const int tid = threadIdx.x;
+  const int dp = nb * JC;
+  const unsigned nblk = gridDim.x;
+  const double tol = (double)d * 0x1.0p-53;
+  const int warp = tid >> 5, lane = tid & 31;
+
+  int sweep = 0;
+  for (; sweep < kMaxSweeps; ++sweep) {
+    for (int round = 0; round < nb - 1; ++round) {
+      int bi, bj;
+      circle_pair(blockIdx.x, round, nb, bi, bj);
+      // 1. load the pair's columns
+      for (int base = 0; base < d * JW; base += 256 * 8) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = base + tid + 256 * u;
+          const int k = idx / d, r = idx % d;
+          const int col = k < JC ? bi * JC + k : bj * JC + (k - JC);
+          v[u] = idx < d * JW ? G[(size_t)col * d + r] : 0.0;
         }
-        double* gp = G + (size_t)p * d;
-        double* gq = G + (size_t)q * d;
-        double a = 0.0, b = 0.0, c = 0.0;
-        for (int i = lane; i < d; i += 32) {
-          const double x = gp[i], y = gq[i];
-          a = fma(x, x, a);
-          b = fma(y, y, b);
-          c = fma(x, y, c);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int idx = base + tid + 256 * u;
+          if (idx < d * JW) Gs[(idx % d) * JP + idx / d] = v[u];
         }
-        a = warp_sum(a);
-        b = warp_sum(b);
-        c = warp_sum(c);
-        if (a == 0.0 || b == 0.0 || !(fabs(c) > tol * sqrt(a) * sqrt(b))) continue;
-        const double zeta = (b - a) / (2.0 * c);
-        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-        const double cs = 1.0 / sqrt(1.0 + tt * tt);
-        const double sn = cs * tt;
-        for (int i = lane; i < d; i += 32) {
-          const double x = gp[i], y = gq[i];
-          gp[i] = cs * x - sn * y;
-          gq[i] = sn * x + cs * y;
-        }
-        double* vp = V + (size_t)p * d;
-        double* vq = V + (size_t)q * d;
-        for (int i = lane; i < d; i += 32) {
-          const double x = vp[i], y = vq[i];
-          vp[i] = cs * x - sn * y;
-          vq[i] = sn * x + cs * y;
-        }
-        if (lane == 0) rotated = 1;
+      }
+      if (tid == 0) any_rot = 0;
+      __syncthreads();
+      // 2. J = I
+      {
+        const int i = tid / JW, j = tid % JW;
+        Js[i * JP + j] = (i == j) ? 1.0 : 0.0;
       }
       __syncthreads();
+      // 3. one-sided Jacobi inside the pair: JC disjoint column pairs per
+      //    inner round, one warp per pair, dot products from the current
+      //    columns (no Gram matrix: keeps the relative accuracy of Hestenes
+      //    rotations); J accumulates the rotations for V.
+      for (int is = 0; is < kInnerSweeps; ++is) {
+        if (tid == 0) inner_rot = 0;
+        __syncthreads();
+        for (int ir = 0; ir < JW - 1; ++ir) {
+          int p, q;
+          circle_pair(warp, ir, JW, p, q);
+          double a = 0.0, b = 0.0, c = 0.0;
+          for (int r = lane; r < d; r += 32) {
+            const double x = Gs[r * JP + p], y = Gs[r * JP + q];
+            a = fma(x, x, a);
+            b = fma(y, y, b);
+            c = fma(x, y, c);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            a += __shfl_xor_sync(0xffffffffu, a, o);
+            b += __shfl_xor_sync(0xffffffffu, b, o);
+            c += __shfl_xor_sync(0xffffffffu, c, o);
+          }
+          if (a > 0.0 && b > 0.0 && fabs(c) > tol * sqrt(a * b)) {
+            // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = h / c, h = (b - a)/2,
+            // rewritten as sign(h) c / (|h| + sqrt(h^2 + c^2)) (one division)
+            const double h = 0.5 * (b - a);
+            const double t = (h >= 0.0 ? c : -c) / (fabs(h) + sqrt(fma(h, h, c * c)));
+            const double cs = rsqrt(fma(t, t, 1.0));
+            const double sn = cs * t;
+            for (int r = lane; r < d; r += 32) {
+              const double x = Gs[r * JP + p], y = Gs[r * JP + q];
+              Gs[r * JP + p] = cs * x - sn * y;
+              Gs[r * JP + q] = sn * x + cs * y;
+            }
+            if (lane < JW) {
+              const double x = Js[lane * JP + p], y = Js[lane * JP + q];
+              Js[lane * JP + p] = cs * x - sn * y;
+              Js[lane * JP + q] = sn * x + cs * y;
+            }
+            if (lane == 0) inner_rot = 1;
+          }
+          __syncthreads();
+        }
+        const int ir_any = inner_rot;
+        if (ir_any && tid == 0) any_rot = 1;
+        __syncthreads();
+        if (!ir_any) break;
+      }
+      // 4. write the rotated pair back; V pair <- V pair J
+      if (any_rot) {
+        for (int idx = tid; idx < d * JW; idx += 256) {
+          const int k = idx / d, r = idx % d;
+          const int col = k < JC ? bi * JC + k : bj * JC + (k - JC);
+          G[(size_t)col * d + r] = Gs[r * JP + k];
+        }
+        const int chunk = min(256, d);  // Gs holds d rows
+        for (int r0 = 0; r0 < dp; r0 += chunk) {
+          const int rows = min(chunk, dp - r0);
+          __syncthreads();
+#pragma unroll 4
+          for (int idx = tid; idx < rows * JW; idx += 256) {
+            const int k = idx / rows, r = idx % rows;
+            const int col = k < JC ? bi * JC + k : bj * JC + (k - JC);
+            Gs[r * JP + k] = V[(size_t)col * dp + r0 + r];
+          }
+          __syncthreads();
+          for (int idx = tid; idx < rows * JW; idx += 256) {
+            const int k = idx / rows, r = idx % rows;
+            double acc = 0.0;
+#pragma unroll
+            for (int l = 0; l < JW; ++l) acc = fma(Gs[r * JP + l], Js[l * JP + k], acc);
+            const int col = k < JC ? bi * JC + k : bj * JC + (k - JC);
+            V[(size_t)col * dp + r0 + r] = acc;
+          }
+        }
+        if (tid == 0) atomicOr(rot + (sweep & 1), 1u);
+      }
+      grid_barrier(bar, nblk);
+      if (round == 0 && blockIdx.x == 0 && tid == 0) atomicExch(rot + ((sweep + 1) & 1), 0u);
     }
-    const int any = rotated;
-    __syncthreads();
+    // every CTA passed the last barrier of the sweep: the flag is final
+    const unsigned any = *((volatile unsigned*)(rot + (sweep & 1)));
     if (!any) break;
   }
-  // norms
-  for (int j = warp; j < d; j += nw) {
-    const double* gj = G + (size_t)j * d;
+  if (blockIdx.x == 0 && tid == 0) ctl[4] = (unsigned)sweep;
+  // norms of the d genuine columns (padded columns are zero)
+  for (int j = blockIdx.x * 8 + warp; j < dp; j += nblk * 8) {
     double a = 0.0;
-    for (int i = lane; i < d; i += 32) a = fma(gj[i], gj[i], a);
-    a = warp_sum(a);
+    for (int i = lane; i < d; i += 32) {
+      const double g = G[(size_t)j * d + i];
+      a = fma(g, g, a);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
     if (lane == 0) nrm[j] = sqrt(a);
   }
-  __syncthreads();
-  // rank = position in descending order (ties: lower index first)
-  for (int j = warp; j < d; j += nw) {
+  grid_barrier(bar, nblk);
+  // rank (descending, ties -> lower index) and outputs
+  for (int j = blockIdx.x * 8 + warp; j < dp; j += nblk * 8) {
     const double sj = nrm[j];
     int cnt = 0;
-    for (int k = lane; k < d; k += 32) {
+    for (int k = lane; k < dp; k += 32) {
       const double sk = nrm[k];
       cnt += (sk > sj || (sk == sj && k < j)) ? 1 : 0;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    const int rank = cnt;
+    if (cnt >= d) continue;
     const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
-    if (lane == 0) S[rank] = sj;
-    const double* gj = G + (size_t)j * d;
-    const double* vj = V + (size_t)j * d;
+    if (lane == 0) S[cnt] = sj;
     for (int i = lane; i < d; i += 32) {
-      Ub[(size_t)i * d + rank] = gj[i] * inv;
-      Vb[(size_t)i * d + rank] = vj[i];
+      Ub[(size_t)i * d + cnt] = G[(size_t)j * d + i] * inv;
+      Vb[(size_t)i * d + cnt] = V[(size_t)j * dp + i];
     }
   }
 }
 
+int small_svd_sweeps(const double* work, int d) {
+  const int nb = jac_nb(d), dp = nb * JC;
+  const unsigned* ctl = (const unsigned*)(work + (size_t)d * dp + (size_t)dp * dp + dp);
+  unsigned h = 0;
+  TSVD_CUDA(cudaMemcpy(&h, ctl + 4, sizeof(unsigned), cudaMemcpyDeviceToHost));
+  return (int)h;
+}
+
 void small_svd(const double* B, int d, double* Ub, double* S, double* Vb, double* work,
                cudaStream_t st) {
-  jacobi_svd_kernel<<<1, 1024, 0, st>>>(B, d, Ub, S, Vb, work);
+  if (d > kJacobiMaxD) throw Error{TSVD_ESHAPE, "small_svd: d > 1536"};
+  const int nb = jac_nb(d), dp = nb * JC;
+  double* G = work;
+  double* V = G + (size_t)d * dp;
+  double* nrm = V + (size_t)dp * dp;
+  unsigned* ctl = (unsigned*)(nrm + dp);
+  jacobi_init_kernel<<<148 * 4, 256, 0, st>>>(B, d, dp, G, V, ctl);
+  TSVD_CHECK_LAUNCH();
+  const size_t smem = sizeof(double) * ((size_t)d * JP + 2 * JW * JP);
+  static int attr_for = -1;
+  if (attr_for < (int)smem) {
+    TSVD_CUDA(cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    attr_for = (int)smem;
+  }
+  int nblocks = nb / 2;
+  int nbv = nb;
+  void* args[] = {&G, &V, &d, &nbv, &nrm, &Ub, &S, &Vb, &ctl};
+  TSVD_CUDA(cudaLaunchCooperativeKernel((void*)jacobi_block_kernel, dim3(nblocks), dim3(256), args,
+                                        smem, st));
   TSVD_CHECK_LAUNCH();
 }
 

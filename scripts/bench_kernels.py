@@ -1,0 +1,116 @@
+"""Micro-benchmarks of single building blocks through the tsvd_dbg_* entry
+points (CUDA-event timed, after warm-up).  Development tool, not the bench.
+
+    python scripts/bench_kernels.py [svd] [tn] [nn] [spmm] [cqr]
+"""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2403_06218_b200 as T  # noqa: E402
+
+HBM = 6540.8
+
+
+def timeit(fn, reps=5, warm=2):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def svd_bench():
+    for d in (28, 128, 384, 704):
+        rng = np.random.default_rng(d)
+        B = torch.from_numpy(np.tril(rng.standard_normal((d, d))) * (0.97 ** np.arange(d))).cuda()
+        Ub = torch.empty((d, d), dtype=torch.float64, device="cuda")
+        Vb = torch.empty_like(Ub)
+        S = torch.empty(d, dtype=torch.float64, device="cuda")
+        ms = timeit(lambda: T.dbg_small_svd(B, Ub, S, Vb), reps=3, warm=1)
+        sweeps = T.dbg_small_svd(B, Ub, S, Vb)
+        Bn = B.cpu().numpy()
+        sv = np.linalg.svd(Bn, compute_uv=False)
+        err = np.abs(S.cpu().numpy() - sv).max() / sv[0]
+        Vn, Un, Sn = Vb.cpu().numpy(), Ub.cpu().numpy(), S.cpu().numpy()
+        orth = np.abs(Vn.T @ Vn - np.eye(d)).max()
+        rec = np.abs(Un @ np.diag(Sn) @ Vn.T - Bn).max() / sv[0]
+        print(f"small_svd d={d}: {ms:.3f} ms  sweeps {sweeps}  sigma err {err:.1e}  "
+              f"V orth {orth:.1e}  recon {rec:.1e}", flush=True)
+
+
+def tn_bench():
+    for q, s, w in ((1_000_000, 384, 16), (1_000_000, 128, 16), (1_000_000, 16, 16),
+                    (1_000_000, 704, 32), (1_000_000, 384, 32)):
+        X = torch.randn((q, s + w), dtype=torch.float64, device="cuda")
+        C = torch.empty((s, w), dtype=torch.float64, device="cuda")
+        Xv, Yv = X[:, :s], X[:, s:]
+        ms = timeit(lambda: T.lib().tsvd_dbg_gemm_tn(Xv.data_ptr(), X.stride(0), Yv.data_ptr(),
+                                                     X.stride(0), q, s, w, C.data_ptr(), None))
+        gb = 8.0 * q * (s + w) / (ms * 1e-3) / 1e9
+        print(f"gemm_tn q={q} s={s} w={w}: {ms:.3f} ms  {gb:.0f} GB/s ({gb / HBM:.2f} of HBM)",
+              flush=True)
+
+
+def nn_bench():
+    for q, s, w in ((1_000_000, 384, 16), (1_000_000, 128, 16), (1_000_000, 0, 16),
+                    (1_000_000, 704, 32), (1_000_000, 384, 32)):
+        X = torch.randn((q, max(s, 1) + w), dtype=torch.float64, device="cuda")
+        H = torch.randn((max(s, 1), w), dtype=torch.float64, device="cuda")
+        Z = torch.empty((q, w), dtype=torch.float64, device="cuda")
+        Y = X[:, max(s, 1):]
+        ms = timeit(lambda: T.lib().tsvd_dbg_gemm_nn(X.data_ptr(), X.stride(0), H.data_ptr(), w,
+                                                     Z.data_ptr(), w, q, s, w, -1.0, 1.0, None))
+        gb = 8.0 * q * (s + 2 * w) / (ms * 1e-3) / 1e9
+        print(f"gemm_nn q={q} s={s} w={w}: {ms:.3f} ms  {gb:.0f} GB/s ({gb / HBM:.2f} of HBM)",
+              flush=True)
+
+
+def spmm_bench():
+    from tsvd_inputs import powerlaw_csr
+    m = n = 1_000_000
+    csr = powerlaw_csr(m, n, 10_000_000, 2.5, seed=0x2403062182)
+    h = T.TruncatedSVD(csr=csr, shape=(m, n))
+    nnz = len(csr[1])
+    for w in (16, 32):
+        X = torch.randn((n, w), dtype=torch.float64, device="cuda")
+        Y = torch.empty((m, w), dtype=torch.float64, device="cuda")
+        for tr in (False, True):
+            ms = timeit(lambda: T.dbg_apply(h, tr, X, Y))
+            gb = (12.0 * nnz + 8 * (m + 1) + 8.0 * w * (m + n)) / (ms * 1e-3) / 1e9
+            print(f"spmm w={w} trans={tr}: {ms:.3f} ms  {gb:.0f} GB/s compulsory "
+                  f"({gb / HBM:.2f} of HBM)", flush=True)
+
+
+def cqr_bench():
+    q = 1_000_000
+    for s, w in ((0, 16), (192, 16), (384, 16), (640, 32)):
+        basis = torch.randn((q, s + w), dtype=torch.float64, device="cuda")
+        if s:
+            Qp, _ = torch.linalg.qr(basis[:, :s])
+            basis[:, :s] = Qp
+        H = torch.empty((max(s, 1), w), dtype=torch.float64, device="cuda")
+        R = torch.empty((w, w), dtype=torch.float64, device="cuda")
+        Y0 = basis[:, s:].clone()
+
+        def run():
+            basis[:, s:] = Y0
+            T.dbg_cgs_cqr2(basis, s, w, H, R)
+        ms = timeit(run, reps=3, warm=1)
+        print(f"cgs_cqr2 q={q} s={s} w={w}: {ms:.3f} ms (incl. copy)", flush=True)
+
+
+if __name__ == "__main__":
+    T.lib()
+    what = sys.argv[1:] or ["svd", "tn", "nn", "spmm", "cqr"]
+    for w in what:
+        globals()[f"{w}_bench"]()
