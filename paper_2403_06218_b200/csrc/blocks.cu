@@ -103,14 +103,12 @@ static double nn_bytes(int64_t q, int s, int w, bool readY, bool writeZ) {
   return 8.0 * q * (s + (readY ? w : 0) + (writeZ ? w : 0));
 }
 
-static double* part_tn(Ctx& c, int64_t q, int s, int w) {
-  const TnGeom g = tn_geom(q, s);
-  return dbuf(c, "part_tn", (size_t)(g.splits + 1) * (size_t)std::max(s, 1) * 32);
-  (void)w;
+static double* part_tn(Ctx& c, int64_t q, int s) {
+  return dbuf(c, "part_tn", tn_part_size(q, s));
 }
 
 static double* gram_buf(Ctx& c, int64_t q) {
-  return dbuf(c, "gram", (size_t)nn_ctas(q) * 32 * 32);
+  return dbuf(c, "gram", (size_t)nn_ctas(q, 1) * 32 * 32);
 }
 
 static double* scratch(Ctx& c, int64_t q) { return dbuf(c, "scratch", (size_t)q * 32); }
@@ -125,13 +123,17 @@ static void clear_flags(Ctx& c) {
   TSVD_CUDA(cudaMemsetAsync(c.dflags, 0, 4 * sizeof(int), c.st));
 }
 
+// TRSM Q = Y L^{-T} (Alg. 4 S3/S6, Alg. 5 S5/S10) is applied as the product
+// Y T with T = L^{-T} formed by the Cholesky finaliser (reading R30).
 int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
   if (w > 32) throw Error{TSVD_EINVAL, "cholqr2: block wider than 32"};
   double* S = scratch(c, q);
   double* gram = gram_buf(c, q);
   double* L1 = dbuf(c, "L1", 32 * 32);
+  double* T1 = dbuf(c, "T1", 32 * 32);
   double* L2 = dbuf(c, "L2", 32 * 32);
-  const int np = nn_ctas(q);
+  double* T2 = dbuf(c, "T2", 32 * 32);
+  const int np = nn_ctas(q, w);
   clear_flags(c);
   {  // S1: W = Y^T Y
     Prof p(c, P_NN, nn_bytes(q, 0, w, true, false), 2.0 * q * w * w);
@@ -139,15 +141,15 @@ int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
   }
   {
     Prof p(c, P_SMALL, 0, 0);
-    chol_finalize(gram, np, w, L1, c.dflags + 0, c.st);                         // S2
+    chol_finalize(gram, np, w, L1, T1, c.dflags + 0, c.st);                     // S2
   }
   {  // S3 + S4: S = Y L^{-T}, Wbar = S^T S
     Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 3.0 * q * w * w);
-    gemm_nn(nullptr, 0, nullptr, 0, Y, ld, L1, S, w, q, 0, w, 0.0, 1.0, gram, c.st);
+    gemm_nn(nullptr, 0, nullptr, 0, Y, ld, T1, S, w, q, 0, w, 0.0, 1.0, gram, c.st);
   }
   {
     Prof p(c, P_SMALL, 0, 0);
-    chol2_finalize(gram, np, w, L1, L2, R, nullptr, nullptr, 0, c.dflags + 1, c.st);  // S5, S7
+    chol2_finalize(gram, np, w, L1, L2, T2, R, nullptr, nullptr, 0, c.dflags + 1, c.st);  // S5, S7
   }
   if (read_flags(c)) {
     Prof p(c, P_OTHER, 0, 0);
@@ -156,7 +158,7 @@ int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
   }
   {  // S6: Q = S Lbar^{-T}
     Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 1.0 * q * w * w);
-    gemm_nn(nullptr, 0, nullptr, 0, S, w, L2, Y, ld, q, 0, w, 0.0, 1.0, nullptr, c.st);
+    gemm_nn(nullptr, 0, nullptr, 0, S, w, T2, Y, ld, q, 0, w, 0.0, 1.0, nullptr, c.st);
   }
   return 0;
 }
@@ -168,36 +170,42 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
   double* Y = basis + s;
   double* S = scratch(c, q);
   double* gram = gram_buf(c, q);
-  double* part = part_tn(c, q, s, w);
+  double* part = part_tn(c, q, s);
   double* L1 = dbuf(c, "L1", 32 * 32);
+  double* T1 = dbuf(c, "T1", 32 * 32);
   double* L2 = dbuf(c, "L2", 32 * 32);
+  double* T2 = dbuf(c, "T2", 32 * 32);
   double* Hbar = dbuf(c, "Hbar", (size_t)s * w);
-  const int np = nn_ctas(q);
+  const int np = nn_ctas(q, w);
   clear_flags(c);
   const double fl = 2.0 * q * s * w;
   {
     Prof p(c, P_TN, tn_bytes(q, s, w), fl);
-    gemm_tn(basis, ld, Y, ld, nullptr, q, s, w, H, w, part, c.st);                   // S1
+    gemm_tn(basis, ld, Y, ld, q, s, w, H, w, part, c.st);                             // S1
   }
   {
     Prof p(c, P_NN, nn_bytes(q, s, w, true, true), fl + 2.0 * q * w * w);
-    gemm_nn(basis, ld, H, w, Y, ld, nullptr, S, w, q, s, w, -1.0, 1.0, gram, c.st);  // S2,S3
+    gemm_nn(basis, ld, H, w, Y, ld, nullptr, S, w, q, s, w, -1.0, 1.0, gram, c.st);   // S2,S3
   }
   {
     Prof p(c, P_SMALL, 0, 0);
-    chol_finalize(gram, np, w, L1, c.dflags + 0, c.st);                              // S4
+    chol_finalize(gram, np, w, L1, T1, c.dflags + 0, c.st);                           // S4
   }
   {
-    Prof p(c, P_TN, tn_bytes(q, s, w), fl + 1.0 * q * w * w);
-    gemm_tn(basis, ld, S, w, L1, q, s, w, Hbar, w, part, c.st);                      // S5,S6
+    Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 1.0 * q * w * w);
+    gemm_nn(nullptr, 0, nullptr, 0, S, w, T1, S, w, q, 0, w, 0.0, 1.0, nullptr, c.st);  // S5
   }
   {
-    Prof p(c, P_NN, nn_bytes(q, s, w, true, true), fl + 3.0 * q * w * w);
-    gemm_nn(basis, ld, Hbar, w, S, w, L1, S, w, q, s, w, -1.0, 1.0, gram, c.st);     // S5,S7,S8
+    Prof p(c, P_TN, tn_bytes(q, s, w), fl);
+    gemm_tn(basis, ld, S, w, q, s, w, Hbar, w, part, c.st);                           // S6
+  }
+  {
+    Prof p(c, P_NN, nn_bytes(q, s, w, true, true), fl + 2.0 * q * w * w);
+    gemm_nn(basis, ld, Hbar, w, S, w, nullptr, S, w, q, s, w, -1.0, 1.0, gram, c.st);  // S7,S8
   }
   {
     Prof p(c, P_SMALL, 0, 0);
-    chol2_finalize(gram, np, w, L1, L2, R, H, Hbar, s, c.dflags + 1, c.st);          // S9,S11,S12
+    chol2_finalize(gram, np, w, L1, L2, T2, R, H, Hbar, s, c.dflags + 1, c.st);       // S9,S11,S12
   }
   if (read_flags(c)) {
     Prof p(c, P_OTHER, 0, 0);
@@ -206,7 +214,7 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
   }
   {
     Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 1.0 * q * w * w);
-    gemm_nn(nullptr, 0, nullptr, 0, S, w, L2, Y, ld, q, 0, w, 0.0, 1.0, nullptr, c.st);  // S10
+    gemm_nn(nullptr, 0, nullptr, 0, S, w, T2, Y, ld, q, 0, w, 0.0, 1.0, nullptr, c.st);  // S10
   }
   return 0;
 }
@@ -218,12 +226,12 @@ void cgs2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H,
   const double tau = 1e-13;
   double* S = dbuf(c, "cgs2_col", (size_t)q);
   double* gram = gram_buf(c, q);
-  const int np = nn_ctas(q);
+  const int np = nn_ctas(q, 1);
   double* c1 = dbuf(c, "cgs2_c1", (size_t)(s + w));
   double* c2 = dbuf(c, "cgs2_c2", (size_t)(s + w));
   double* coef = dbuf(c, "cgs2_coef", (size_t)(s + w));
   double* sc = dbuf(c, "cgs2_sc", 8);  // [0] |y_orig|^2, [1] |y''|^2, [2] nrm
-  double* part = part_tn(c, q, s + w, 1);
+  double* part = part_tn(c, q, s + w);
   int* dep = c.dflags + 2;
   fill_zero(R, (int64_t)w * w, c.st);
   for (int j = 0; j < w; ++j) {
@@ -233,9 +241,9 @@ void cgs2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H,
     gemm_nn(nullptr, 0, nullptr, 0, col, ld, nullptr, nullptr, 0, q, 0, 1, 0.0, 1.0, gram, c.st);
     reduce_partials(gram, np, 1, sc + 0, c.st);
     if (nb > 0) {
-      gemm_tn(basis, ld, col, ld, nullptr, q, nb, 1, c1, 1, part, c.st);
+      gemm_tn(basis, ld, col, ld, q, nb, 1, c1, 1, part, c.st);
       gemm_nn(basis, ld, c1, 1, col, ld, nullptr, S, 1, q, nb, 1, -1.0, 1.0, nullptr, c.st);
-      gemm_tn(basis, ld, S, 1, nullptr, q, nb, 1, c2, 1, part, c.st);
+      gemm_tn(basis, ld, S, 1, q, nb, 1, c2, 1, part, c.st);
       gemm_nn(basis, ld, c2, 1, S, 1, nullptr, S, 1, q, nb, 1, -1.0, 1.0, gram, c.st);
     } else {
       gemm_nn(nullptr, 0, nullptr, 0, col, ld, nullptr, S, 1, q, 0, 1, 0.0, 1.0, gram, c.st);
@@ -249,7 +257,7 @@ void cgs2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H,
       // replacement column: next Philox draw, orthogonalised twice
       launch_philox_normal(S, q, 1, 1, c.seed, c.draw_next++, 0, q, c.st);
       for (int it = 0; it < 2 && nb > 0; ++it) {
-        gemm_tn(basis, ld, S, 1, nullptr, q, nb, 1, c2, 1, part, c.st);
+        gemm_tn(basis, ld, S, 1, q, nb, 1, c2, 1, part, c.st);
         gemm_nn(basis, ld, c2, 1, S, 1, nullptr, S, 1, q, nb, 1, -1.0, 1.0, nullptr, c.st);
       }
       gemm_nn(nullptr, 0, nullptr, 0, S, 1, nullptr, nullptr, 0, q, 0, 1, 0.0, 1.0, gram, c.st);
@@ -297,8 +305,7 @@ void apply(Ctx& c, bool trans, const double* X, int64_t ldx, double* Y, int64_t 
       gemm_nn(c.Ad, c.lda, X, ldx, nullptr, 0, nullptr, Y, ldy, c.m, (int)c.n, w, 1.0, 0.0,
               nullptr, c.st);
     else          // Y (n x w) = A^T X
-      gemm_tn(c.Ad, c.lda, X, ldx, nullptr, c.m, (int)c.n, w, Y, ldy,
-              part_tn(c, c.m, (int)c.n, std::min(w, 32)), c.st);
+      gemm_tn(c.Ad, c.lda, X, ldx, c.m, (int)c.n, w, Y, ldy, part_tn(c, c.m, (int)c.n), c.st);
   } else {
     const Csr& A = trans ? c.AT : c.A;
     double* part = dbuf(c, trans ? "spmm_part_t" : "spmm_part", (size_t)std::max<int64_t>(1, A.nslots) * 32);

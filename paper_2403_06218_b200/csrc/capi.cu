@@ -440,9 +440,8 @@ tsvd_status tsvd_dbg_gemm_tn(const double* X, int64_t ldx, const double* Y, int6
   if (!X || !Y || !C || q < 0 || s < 1 || w < 1) return TSVD_EINVAL;
   TSVD_API_BEGIN
   tsvd_ctx* c = dbg_ctx(stream);
-  const TnGeom g = tn_geom(q, s);
-  double* part = dbuf(*c, "part_tn", (size_t)(g.splits + 1) * s * 32);
-  gemm_tn(X, ldx, Y, ldy, nullptr, q, s, w, C, w, part, c->st);
+  double* part = dbuf(*c, "part_tn", tn_part_size(q, s));
+  gemm_tn(X, ldx, Y, ldy, q, s, w, C, w, part, c->st);
   TSVD_CUDA(cudaStreamSynchronize(c->st));
   return TSVD_OK;
   TSVD_API_END

@@ -89,31 +89,28 @@ void csr_free(Csr& A);
 int csr_validate_device(const Csr& A, cudaStream_t st);
 
 // -------------------------------------------------- tall-skinny products --
-// Partial-sum geometry of gemm_tn for (q, s): grid (s_tiles, splits).
-struct TnGeom {
-  int s_tiles, splits;
-};
-TnGeom tn_geom(int64_t q, int s);
-// C (s x w, ldc) = X^T Y', Y' = Y L^{-T} if L != null (L: w x w row-major,
-// lower).  part: workspace >= splits*s*w doubles (unused when splits == 1).
-void gemm_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, const double* L,
-             int64_t q, int s, int w, double* C, int64_t ldc, double* part, cudaStream_t st);
-// Z (q x w) = beta * (Y L^{-T}) + alpha * X H   (L optional, Y optional when
-// beta == 0); gram != null: per-CTA partial Gram Z^T Z written to
-// gram[cta*w*w], number of CTAs returned through *nparts.
-int nn_ctas(int64_t q);
+// gemm_tn: C (s x w, ldc) = X^T Y  (X: q x s, Y: q x w, both row-major).
+// Split over rows into partial sums reduced in a fixed order; part: workspace
+// of tn_part_size(q, s) doubles.
+size_t tn_part_size(int64_t q, int s);
+void gemm_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t q, int s,
+             int w, double* C, int64_t ldc, double* part, cudaStream_t st);
+// gemm_nn: Z (q x w) = alpha X H + beta Y T   (H: s x w; T: w x w upper
+// triangular, optional = identity; Y optional when beta == 0; Z may alias Y).
+// gram != null: per-CTA partial Gram Z^T Z (w x w) at gram[cta*w*w] for
+// nn_ctas(q, w) CTAs.
+int nn_ctas(int64_t q, int w);
 void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const double* Y,
-             int64_t ldy, const double* L, double* Z, int64_t ldz, int64_t q, int s, int w,
+             int64_t ldy, const double* T, double* Z, int64_t ldz, int64_t q, int s, int w,
              double alpha, double beta, double* gram, cudaStream_t st);
 
-// small (single-CTA) finalizers
-// W = sum of nparts partial (w x w) Grams; L = chol(W); flag[0] |= breakdown.
-// mode 1: also R = L^T (first CholQR pass result kept in Rprev)
-// mode 2: L2 = chol(W); R = L2^T Lprev^T; H (s x w) += Hbar Lprev^T
-void chol_finalize(const double* gram, int nparts, int w, double* L, int* flag,
+// small (single-CTA) finalisers (small.cu)
+// W = sum of nparts partial (w x w) Grams; L = chol(W), T = L^{-T}; flag |= breakdown.
+void chol_finalize(const double* gram, int nparts, int w, double* L, double* T, int* flag,
                    cudaStream_t st);
+// Lbar = chol(Wbar), Tbar = Lbar^{-T}; R = Lbar^T Lprev^T; H (s x w) += Hbar Lprev^T.
 void chol2_finalize(const double* gram, int nparts, int w, const double* Lprev, double* L2,
-                    double* R, double* H, const double* Hbar, int s, int* flag,
+                    double* T2, double* R, double* H, const double* Hbar, int s, int* flag,
                     cudaStream_t st);
 // out[i] = sum_p part[p*count + i], fixed order
 void reduce_partials(const double* part, int nparts, int64_t count, double* out,

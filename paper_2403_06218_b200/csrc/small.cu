@@ -1,0 +1,274 @@
+// Small single-CTA finalisers and helpers of the orthogonalisation passes:
+// fixed-order partial sums, b x b Cholesky with the breakdown test of P:275,
+// T = L^{-T} for the TRSM-as-multiply passes, R = Lbar^T L^T (reading R4),
+// H += Hbar L^T (reading R5), block copies, CGS2 column bookkeeping, the
+// Lanczos rho test and sign normalisation.
+#include "internal.h"
+
+namespace tsvd {
+
+// ----------------------------------------------------------- finalisers ---
+// One warp Cholesky of W (w x w, w <= 32) held in shared memory, row-major.
+// Breakdown: a pivot <= 0 or non-finite -> *bad = 1; the pivot is
+// then replaced by 1 so the (discarded) result stays finite.
+__device__ void warp_cholesky(double* Ws, double* Lo, int w, int* bad) {
+  const int lane = threadIdx.x & 31;
+  for (int j = 0; j < w; ++j) {
+    double d = 0.0;
+    if (lane == 0) {
+      d = Ws[j * w + j];
+      for (int k = 0; k < j; ++k) d = fma(-Lo[j * 32 + k], Lo[j * 32 + k], d);
+      if (!(d > 0.0) || !isfinite(d)) {
+        *bad = 1;
+        d = 1.0;
+      }
+      Lo[j * 32 + j] = sqrt(d);
+    }
+    __syncwarp();
+    const double ljj = Lo[j * 32 + j];
+    for (int i = j + 1 + lane; i < w; i += 32) {
+      double v = Ws[i * w + j];
+      for (int k = 0; k < j; ++k) v = fma(-Lo[i * 32 + k], Lo[j * 32 + k], v);
+      Lo[i * 32 + j] = v / ljj;
+    }
+    __syncwarp();
+  }
+}
+
+// T = L^{-T} (upper triangular) from the lower triangular L held in Lo (ld 32):
+// lane j computes column j of L^{-1} by forward substitution; T[j][i] = Linv[i][j].
+__device__ void warp_tri_inverse_t(const double* Lo, double* Tout, int w) {
+  const int j = threadIdx.x & 31;
+  if (j >= w) return;
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    x[i] = 0.0;
+    if (i < w && i >= j) {
+      double v = (i == j) ? 1.0 : 0.0;
+      for (int k = j; k < i; ++k) v = fma(-Lo[i * 32 + k], x[k], v);
+      x[i] = v / Lo[i * 32 + i];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (i < w) Tout[j * w + i] = x[i];  // T[j][i] = Linv[i][j]
+}
+
+__global__ void chol_finalize_kernel(const double* __restrict__ gram, int nparts, int w,
+                                     double* __restrict__ L, double* __restrict__ T,
+                                     int* __restrict__ flag) {
+  __shared__ double Ws[32 * 32];
+  __shared__ double Lo[32 * 32];
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  if (tid == 0) bad = 0;
+  for (int i = tid; i < w * w; i += blockDim.x) {
+    double s = 0.0;
+    for (int p = 0; p < nparts; ++p) s += gram[(int64_t)p * w * w + i];
+    Ws[i] = s;
+  }
+  for (int i = tid; i < 32 * 32; i += blockDim.x) Lo[i] = 0.0;
+  __syncthreads();
+  if (tid < 32) warp_cholesky(Ws, Lo, w, &bad);
+  __syncthreads();
+  for (int i = tid; i < w * w; i += blockDim.x) L[i] = Lo[(i / w) * 32 + (i % w)];
+  if (tid < 32) warp_tri_inverse_t(Lo, T, w);
+  if (tid == 0 && bad) *flag = 1;
+}
+
+void chol_finalize(const double* gram, int nparts, int w, double* L, double* T, int* flag,
+                   cudaStream_t st) {
+  chol_finalize_kernel<<<1, 256, 0, st>>>(gram, nparts, w, L, T, flag);
+  TSVD_CHECK_LAUNCH();
+}
+
+// Second pass: Lbar = chol(Wbar), Tbar = Lbar^{-T}; R = Lbar^T Lprev^T (Alg. 4 S7 /
+// Alg. 5 S11, reading R4); H (s x w) += Hbar Lprev^T (Alg. 5 S12, reading R5).
+__global__ void chol2_finalize_kernel(const double* __restrict__ gram, int nparts, int w,
+                                      const double* __restrict__ Lprev, double* __restrict__ L2,
+                                      double* __restrict__ T2, double* __restrict__ R,
+                                      double* __restrict__ H, const double* __restrict__ Hbar,
+                                      int s, int* __restrict__ flag) {
+  __shared__ double Ws[32 * 32];
+  __shared__ double Lo[32 * 32];
+  __shared__ double Lp[32 * 32];
+  __shared__ int bad;
+  const int tid = threadIdx.x;
+  if (tid == 0) bad = 0;
+  for (int i = tid; i < w * w; i += blockDim.x) {
+    double sum = 0.0;
+    for (int p = 0; p < nparts; ++p) sum += gram[(int64_t)p * w * w + i];
+    Ws[i] = sum;
+    Lp[i] = Lprev[i];
+  }
+  for (int i = tid; i < 32 * 32; i += blockDim.x) Lo[i] = 0.0;
+  __syncthreads();
+  if (tid < 32) warp_cholesky(Ws, Lo, w, &bad);
+  __syncthreads();
+  if (tid < 32) warp_tri_inverse_t(Lo, T2, w);
+  for (int i = tid; i < w * w; i += blockDim.x) {
+    const int r = i / w, c = i % w;
+    L2[i] = Lo[r * 32 + c];
+    // R[r][c] = sum_k Lbar[k][r] * Lprev[c][k]
+    double sum = 0.0;
+    for (int k = 0; k < w; ++k) sum = fma(Lo[k * 32 + r], Lp[c * w + k], sum);
+    R[i] = sum;
+  }
+  if (H) {
+    for (int64_t i = tid; i < (int64_t)s * w; i += blockDim.x) {
+      const int64_t r = i / w;
+      const int c = (int)(i % w);
+      double sum = 0.0;
+      for (int k = 0; k < w; ++k) sum = fma(Hbar[r * w + k], Lp[c * w + k], sum);
+      H[i] += sum;
+    }
+  }
+  if (tid == 0 && bad) *flag = 1;
+}
+
+void chol2_finalize(const double* gram, int nparts, int w, const double* Lprev, double* L2,
+                    double* T2, double* R, double* H, const double* Hbar, int s, int* flag,
+                    cudaStream_t st) {
+  chol2_finalize_kernel<<<1, 256, 0, st>>>(gram, nparts, w, Lprev, L2, T2, R, H, Hbar, s, flag);
+  TSVD_CHECK_LAUNCH();
+}
+
+// --------------------------------------------------------------- helpers ---
+__global__ void copy_block_kernel(const double* __restrict__ src, int64_t lds,
+                                  double* __restrict__ dst, int64_t ldd, int64_t rows, int cols,
+                                  int transpose) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols;
+    const int c = (int)(i % cols);
+    dst[r * ldd + c] = transpose ? src[(int64_t)c * lds + r] : src[r * lds + c];
+  }
+}
+
+void copy_block(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
+                int cols, bool transpose, cudaStream_t st) {
+  const int64_t n = rows * cols;
+  if (n <= 0) return;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  copy_block_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, lds, dst, ldd, rows, cols,
+                                                       transpose ? 1 : 0);
+  TSVD_CHECK_LAUNCH();
+}
+
+void fill_zero(double* p, int64_t n, cudaStream_t st) {
+  if (n > 0) TSVD_CUDA(cudaMemsetAsync(p, 0, n * sizeof(double), st));
+}
+
+// CGS2 per-column decision (P:275 fallback, reading R16):
+// coef = c1 + c2 ; nrm = ||y''|| ; dependent = nrm <= tau ||y_orig||
+__global__ void cgs2_col_finalize_kernel(const double* c1, const double* c2, int nb,
+                                         const double* gram_y, const double* gram_orig,
+                                         double tau, double* coef, double* nrm, int* dep) {
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) coef[i] = c1[i] + c2[i];
+  if (threadIdx.x == 0) {
+    const double ny = sqrt(gram_y[0]);
+    const double no = sqrt(gram_orig[0]);
+    nrm[0] = ny;
+    dep[0] = (ny <= tau * no) ? 1 : 0;
+  }
+}
+
+void cgs2_col_finalize(const double* c1, const double* c2, int nb, const double* gram_y,
+                       const double* gram_orig, double tau, double* coef_out, double* nrm_out,
+                       int* dependent, cudaStream_t st) {
+  cgs2_col_finalize_kernel<<<1, 256, 0, st>>>(c1, c2, nb, gram_y, gram_orig, tau, coef_out,
+                                              nrm_out, dependent);
+  TSVD_CHECK_LAUNCH();
+}
+
+__global__ void scale_column_kernel(double* col, int64_t q, int64_t ld, const double* nrm) {
+  const double inv = 1.0 / nrm[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < q;
+       i += (int64_t)gridDim.x * blockDim.x)
+    col[i * ld] = col[i * ld] * inv;
+}
+
+void scale_column(double* col, int64_t q, int64_t ld, const double* nrm, cudaStream_t st) {
+  scale_column_kernel<<<148 * 4, 256, 0, st>>>(col, q, ld, nrm);
+  TSVD_CHECK_LAUNCH();
+}
+
+// rho_i = ||Rbar Vb[(k-1)b : kb, i]||_2 / S[0]  (from Eq. 10; reading R12)
+__global__ void lanczos_rho_kernel(const double* __restrict__ Rbar, int b,
+                                   const double* __restrict__ Vb, int d,
+                                   const double* __restrict__ S, int cnt,
+                                   double* __restrict__ rho) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= cnt) return;
+  double ss = 0.0;
+  for (int j = 0; j < b; ++j) {
+    double t = 0.0;
+    for (int l = 0; l < b; ++l) t = fma(Rbar[j * b + l], Vb[(int64_t)(d - b + l) * d + i], t);
+    ss = fma(t, t, ss);
+  }
+  rho[i] = sqrt(ss) / S[0];
+}
+
+void lanczos_rho(const double* Rbar, int b, const double* Vb, int d, const double* S, int cnt,
+                 double* rho, cudaStream_t st) {
+  lanczos_rho_kernel<<<(cnt + 127) / 128, 128, 0, st>>>(Rbar, b, Vb, d, S, cnt, rho);
+  TSVD_CHECK_LAUNCH();
+}
+
+// sign normalisation (reading R28): per column i of V, the largest-|.| entry
+// (lowest index on ties) is made positive; U's column flips with it.
+__global__ void colmax_kernel(const double* __restrict__ V, int64_t n, int64_t ldv,
+                              double* __restrict__ sgn) {
+  __shared__ double bv[256];
+  __shared__ int64_t bi[256];
+  const int i = blockIdx.x;
+  double best = -1.0;
+  int64_t bidx = 0;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    const double a = fabs(V[j * ldv + i]);
+    if (a > best) {  // strictly greater keeps the lowest index of this thread
+      best = a;
+      bidx = j;
+    }
+  }
+  bv[threadIdx.x] = best;
+  bi[threadIdx.x] = bidx;
+  __syncthreads();
+  for (int off = 128; off > 0; off >>= 1) {
+    if (threadIdx.x < off) {
+      const double o = bv[threadIdx.x + off];
+      const int64_t oi = bi[threadIdx.x + off];
+      if (o > bv[threadIdx.x] || (o == bv[threadIdx.x] && oi < bi[threadIdx.x])) {
+        bv[threadIdx.x] = o;
+        bi[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) sgn[i] = (V[bi[0] * ldv + i] < 0.0) ? -1.0 : 1.0;
+}
+
+__global__ void flip_kernel(double* __restrict__ M, int64_t rows, int64_t ld, int r,
+                            const double* __restrict__ sgn) {
+  const int64_t n = rows * r;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = t / r;
+    const int i = (int)(t % r);
+    if (sgn[i] < 0.0) M[j * ld + i] = -M[j * ld + i];
+  }
+}
+
+void sign_normalize(double* U, int64_t m, int64_t ldu, double* V, int64_t n, int64_t ldv,
+                    int r, double* work, cudaStream_t st) {
+  if (r <= 0) return;
+  colmax_kernel<<<r, 256, 0, st>>>(V, n, ldv, work);
+  flip_kernel<<<148 * 4, 256, 0, st>>>(U, m, ldu, r, work);
+  flip_kernel<<<148 * 4, 256, 0, st>>>(V, n, ldv, r, work);
+  TSVD_CHECK_LAUNCH();
+}
+
+}  // namespace tsvd

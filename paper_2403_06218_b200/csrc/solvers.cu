@@ -83,13 +83,9 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   double* rho = dbuf(c, "rho", (size_t)d);
   // pre-size the pass workspaces for the largest q and s of this solve
   (void)dbuf(c, "scratch", (size_t)std::max(m, n) * 32);
-  (void)dbuf(c, "gram", (size_t)nn_ctas(std::max(m, n)) * 32 * 32);
+  (void)dbuf(c, "gram", (size_t)nn_ctas(std::max(m, n), 1) * 32 * 32);
   (void)dbuf(c, "Hbar", (size_t)(d + b) * 32);
-  {
-    const TnGeom g1 = tn_geom(m, d + b), g2 = tn_geom(n, d);
-    const size_t need = (size_t)std::max((g1.splits + 1) * (d + b), (g2.splits + 1) * d) * 32;
-    (void)dbuf(c, "part_tn", need);
-  }
+  (void)dbuf(c, "part_tn", std::max(tn_part_size(m, d + b), tn_part_size(n, d)));
 
   // S1: random orthonormal Qbar_1 (m x b)
   if (!c.start.empty())
@@ -198,7 +194,7 @@ tsvd_status rsvd_solve(Ctx& c, int r, int p, int q) {
   double* Sg = dbuf(c, "Sg", (size_t)l);
   double* jw = dbuf(c, "jacobi_work", small_svd_work(l));
   (void)dbuf(c, "scratch", (size_t)std::max(m, n) * 32);
-  (void)dbuf(c, "gram", (size_t)nn_ctas(std::max(m, n)) * 32 * 32);
+  (void)dbuf(c, "gram", (size_t)nn_ctas(std::max(m, n), 1) * 32 * 32);
 
   if (!c.start.empty())
     upload_start(c, Q, n, l, l);
