@@ -84,12 +84,14 @@ struct TnGeom {
   int s_tiles, splits;
 };
 
-static TnGeom tn_geom(int64_t q, int s) {
+static TnGeom tn_geom(int64_t q, int s, int w) {
   TnGeom g;
+  const int per_sm = (w > 16) ? 1 : 2;  // matches __launch_bounds__ of gemm_tn_kernel
   g.s_tiles = (s + TN_ST - 1) / TN_ST;
   if (g.s_tiles < 1) g.s_tiles = 1;
   const int64_t chunks = (q + TN_RB - 1) / TN_RB;
-  int64_t splits = (2 * 148 + g.s_tiles - 1) / g.s_tiles;
+  // one wave: at most (CTAs per SM x 148) CTAs in total
+  int64_t splits = (int64_t)(per_sm * 148) / g.s_tiles;
   const int64_t min_chunks = 8;  // keep the pipeline busy
   if (splits > chunks / min_chunks) splits = chunks / min_chunks;
   if (splits < 1) splits = 1;
@@ -98,7 +100,7 @@ static TnGeom tn_geom(int64_t q, int s) {
 }
 
 size_t tn_part_size(int64_t q, int s) {
-  const TnGeom g = tn_geom(q, s);
+  const TnGeom g = tn_geom(q, s, 1);  // the most splits any width uses
   return (size_t)(g.splits + 1) * (size_t)std::max(s, 1) * 32;
 }
 
@@ -249,7 +251,7 @@ void gemm_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t
       TSVD_CUDA(cudaMemsetAsync(C + (int64_t)i * ldc, 0, w * sizeof(double), st));
     return;
   }
-  const TnGeom g = tn_geom(q, s);
+  const TnGeom g = tn_geom(q, s, w);
   dim3 grid(g.s_tiles, g.splits);
   const bool v2 = aligned16(X, ldx) && aligned16(Y, ldy);
 #define TN_CASE(WPV)                                                              \
@@ -276,162 +278,159 @@ void gemm_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t
 
 // ------------------------------------------------------------------ NN ---
 // Persistent CTAs over row tiles of NN_R rows; the K dimension (s) streams
-// in chunks of NN_KC through an NN_S-stage cp.async ring whose steps run
-// across tile boundaries.  Each warp owns 16 rows (2 DMMA M-tiles) x WP.
-// The Y tile of a row tile travels with its first K chunk (own ring of NN_S
-// slots); the epilogue forms beta*Y*T (DMMA, T = L^{-T} upper triangular,
-// i.e. the TRSM of Alg. 4/5 as a multiply) + alpha*acc, stores Z and
-// accumulates the Gram Z^T Z of the tile (DMMA).
+// in chunks of NN_KC through an S-stage cp.async ring whose steps run across
+// tile boundaries.  Each warp owns 16 rows (2 DMMA M-tiles) x WP columns and
+// keeps two accumulator sets (even / odd k-steps) so 4*NT independent DMMA
+// chains are in flight per warp.  The epilogue of a tile loads its Y rows
+// straight into DMMA A-fragments (issued before the tile's last K chunk so
+// the latency overlaps), forms beta*Y*T (T = L^{-T} upper triangular: the
+// TRSM of Alg. 4/5 as a multiply; identity if T is null) + alpha*acc, stores
+// Z through a shared out-tile (coalesced) and accumulates the Gram Z^T Z of
+// the tile (DMMA).
 constexpr int NN_R = 128;
 constexpr int NN_KC = 32;
 
 template <int WP>
 struct NnCfg {
-  static constexpr int S = (WP == 32) ? 2 : 3;
-  static constexpr int XP = NN_KC + 4, HP = WP + 4, YP = WP + 4, NT = WP / 8;
+  static constexpr int S = (WP == 32) ? 3 : 2;
+  static constexpr int PER_SM = (WP == 32) ? 1 : 2;
+  static constexpr int XP = NN_KC + 4, HP = WP + 4, OP = WP + 4, NT = WP / 8;
   static constexpr size_t stage = (size_t)NN_R * XP + (size_t)NN_KC * HP;
-  static constexpr size_t yslot = (size_t)NN_R * YP;
   static constexpr size_t bytes =
-      sizeof(double) * (S * stage + S * yslot + (size_t)WP * WP);
+      sizeof(double) * (S * stage + (size_t)NN_R * OP + (size_t)WP * WP);
 };
 
-static int nn_ctas_wp(int64_t q, int wp) {
+static int wp_of(int w) { return w <= 8 ? 8 : (w <= 16 ? 16 : 32); }
+
+int nn_ctas(int64_t q, int w) {
+  const int wp = wp_of(w);
   int64_t tiles = (q + NN_R - 1) / NN_R;
-  const int per_sm = (wp == 8) ? 2 : 1;
-  const int64_t cap = 148 * per_sm;
+  const int64_t cap = 148 * (wp == 32 ? NnCfg<32>::PER_SM : NnCfg<16>::PER_SM);
   if (tiles > cap) tiles = cap;
   if (tiles < 1) tiles = 1;
   return (int)tiles;
 }
 
-static int wp_of(int w) { return w <= 8 ? 8 : (w <= 16 ? 16 : 32); }
-
-int nn_ctas(int64_t q, int w) { return nn_ctas_wp(q, wp_of(w)); }
-
 template <int WP, int VEC>
-__global__ void __launch_bounds__(256, 1) gemm_nn_kernel(
+__global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
     const double* __restrict__ X, int64_t ldx, const double* __restrict__ H, int64_t ldh,
     const double* Y, int64_t ldy, const double* __restrict__ T, double* Z, int64_t ldz,
     int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram) {
   using CF = NnCfg<WP>;
-  constexpr int S = CF::S, XP = CF::XP, HP = CF::HP, YP = CF::YP, NT = CF::NT;
-  constexpr int NPAIR = NT * NT, PPW = (NPAIR + 7) / 8;
+  constexpr int S = CF::S, XP = CF::XP, HP = CF::HP, OP = CF::OP, NT = CF::NT;
+  constexpr int NPAIR = NT * NT, PPW = (NPAIR + 7) / 8, KY = WP / 4;
   extern __shared__ __align__(16) double sm[];
-  double* Ts = sm + S * CF::stage + S * CF::yslot;
+  double* Os = sm + S * CF::stage;
+  double* Ts = Os + NN_R * OP;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
-  const double* dummy = Y ? Y : (X ? X : H);
+  const double* dummy = X ? X : (H ? H : Y);
   for (int i = tid; i < WP * WP; i += 256) {
     const int r = i / WP, c = i % WP;
     Ts[i] = (r < w && c < w) ? (T ? T[r * w + c] : (r == c ? 1.0 : 0.0)) : 0.0;
   }
   const int64_t ntiles = (q + NN_R - 1) / NN_R;
-  const int64_t my_tiles = (ntiles > blockIdx.x) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t my_tiles =
+      (ntiles > (int64_t)blockIdx.x) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int nk = s > 0 ? (s + NN_KC - 1) / NN_KC : 1;
   const int64_t nsteps = my_tiles * nk;
   auto Xs = [&](int st) { return sm + (size_t)st * CF::stage; };
   auto Hs = [&](int st) { return sm + (size_t)st * CF::stage + NN_R * XP; };
-  auto Ys = [&](int slot) { return sm + (size_t)S * CF::stage + (size_t)slot * CF::yslot; };
   auto issue = [&](int64_t j) {
-    if (j < nsteps) {
+    if (j < nsteps && s > 0) {
       const int st = (int)(j % S);
       const int64_t lt = j / nk;
       const int kc = (int)(j % nk);
       const int64_t r0 = (blockIdx.x + lt * gridDim.x) * NN_R;
-      if (s > 0) {
-        load_tile<NN_R, NN_KC, XP, VEC, 256>(Xs(st), X, ldx, r0, q, kc * NN_KC, s, dummy);
-        load_tile<NN_KC, WP, HP, VEC, 256>(Hs(st), H, ldh, kc * NN_KC, s, 0, w, dummy);
-      }
-      if (kc == 0)
-        load_tile<NN_R, WP, YP, VEC, 256>(Ys((int)(lt % S)), beta != 0.0 ? Y : nullptr, ldy,
-                                          r0, q, 0, w, dummy);
+      load_tile<NN_R, NN_KC, XP, VEC, 256>(Xs(st), X, ldx, r0, q, kc * NN_KC, s, dummy);
+      load_tile<NN_KC, WP, HP, VEC, 256>(Hs(st), H, ldh, kc * NN_KC, s, 0, w, dummy);
     }
     cp_commit();
   };
   double g[PPW][2];
 #pragma unroll
   for (int p = 0; p < PPW; ++p) g[p][0] = g[p][1] = 0.0;
-  double acc[2][NT][2];
+  double acc[2][2][NT][2];
+  double ya[2][KY];
 #pragma unroll
   for (int j = 0; j < S - 1; ++j) issue(j);
   for (int64_t j = 0; j < nsteps; ++j) {
     issue(j + S - 1);
-    cp_wait<S - 1>();
-    __syncthreads();
     const int st = (int)(j % S);
     const int kc = (int)(j % nk);
     const int64_t lt = j / nk;
+    const int64_t r0 = (blockIdx.x + lt * gridDim.x) * NN_R;
     if (kc == 0) {
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
+      for (int h = 0; h < 2; ++h)
 #pragma unroll
-        for (int ni = 0; ni < NT; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) acc[h][mi][ni][0] = acc[h][mi][ni][1] = 0.0;
     }
+    if (kc == nk - 1) {  // prefetch this tile's Y rows as A-fragments
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        const int64_t row = r0 + warp * 16 + mi * 8 + gid;
+#pragma unroll
+        for (int kk = 0; kk < KY; ++kk) {
+          const int col = kk * 4 + tig;
+          ya[mi][kk] = (beta != 0.0 && Y && row < q && col < w) ? Y[row * ldy + col] : 0.0;
+        }
+      }
+    }
+    cp_wait<S - 1>();
+    __syncthreads();
     if (s > 0) {
       const double* xs = Xs(st);
       const double* hs = Hs(st);
 #pragma unroll
       for (int kk = 0; kk < NN_KC / 4; ++kk) {
+        const int h = kk & 1;
         const double a0 = xs[(warp * 16 + gid) * XP + kk * 4 + tig];
         const double a1 = xs[(warp * 16 + 8 + gid) * XP + kk * 4 + tig];
 #pragma unroll
         for (int ni = 0; ni < NT; ++ni) {
           const double b = hs[(kk * 4 + tig) * HP + ni * 8 + gid];
-          dmma884(acc[0][ni][0], acc[0][ni][1], a0, b);
-          dmma884(acc[1][ni][0], acc[1][ni][1], a1, b);
+          dmma884(acc[h][0][ni][0], acc[h][0][ni][1], a0, b);
+          dmma884(acc[h][1][ni][0], acc[h][1][ni][1], a1, b);
         }
       }
     }
     if (kc == nk - 1) {
-      // epilogue of local tile lt: Z = alpha*acc + beta*(Y T)
-      double* ys = Ys((int)(lt % S));
-      const int64_t r0 = (blockIdx.x + lt * gridDim.x) * NN_R;
+      // epilogue: Z = alpha*acc + beta*(Y T)
+      double yt[2][NT][2];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni) yt[mi][ni][0] = yt[mi][ni][1] = 0.0;
       if (beta != 0.0) {
-        double yt[2][NT][2];
 #pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < NT; ++ni) yt[mi][ni][0] = yt[mi][ni][1] = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < WP / 4; ++kk) {
-          const double a0 = ys[(warp * 16 + gid) * YP + kk * 4 + tig];
-          const double a1 = ys[(warp * 16 + 8 + gid) * YP + kk * 4 + tig];
+        for (int kk = 0; kk < KY; ++kk)
 #pragma unroll
           for (int ni = 0; ni < NT; ++ni) {
             const double b = Ts[(kk * 4 + tig) * WP + ni * 8 + gid];
-            dmma884(yt[0][ni][0], yt[0][ni][1], a0, b);
-            dmma884(yt[1][ni][0], yt[1][ni][1], a1, b);
+            dmma884(yt[0][ni][0], yt[0][ni][1], ya[0][kk], b);
+            dmma884(yt[1][ni][0], yt[1][ni][1], ya[1][kk], b);
           }
-        }
-        __syncwarp();  // each warp only touches its own 16 rows of ys
-#pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < NT; ++ni)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int r = warp * 16 + mi * 8 + gid, c = ni * 8 + 2 * tig + e;
-              const double z = alpha * acc[mi][ni][e] + beta * yt[mi][ni][e];
-              ys[r * YP + c] = (c < w && r0 + r < q) ? z : 0.0;
-            }
-      } else {
-#pragma unroll
-        for (int mi = 0; mi < 2; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < NT; ++ni)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int r = warp * 16 + mi * 8 + gid, c = ni * 8 + 2 * tig + e;
-              const double z = alpha * acc[mi][ni][e];
-              ys[r * YP + c] = (c < w && r0 + r < q) ? z : 0.0;
-            }
       }
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = warp * 16 + mi * 8 + gid, c = ni * 8 + 2 * tig + e;
+            const double z =
+                alpha * (acc[0][mi][ni][e] + acc[1][mi][ni][e]) + beta * yt[mi][ni][e];
+            Os[r * OP + c] = (c < w && r0 + r < q) ? z : 0.0;
+          }
       __syncthreads();
       if (Z) {
         for (int idx = tid; idx < NN_R * WP; idx += 256) {
           const int r = idx / WP, c = idx % WP;
           const int64_t row = r0 + r;
-          if (row < q && c < w) Z[row * ldz + c] = ys[r * YP + c];
+          if (row < q && c < w) Z[row * ldz + c] = Os[r * OP + c];
         }
       }
       if (gram) {
@@ -442,8 +441,8 @@ __global__ void __launch_bounds__(256, 1) gemm_nn_kernel(
             const int mi = pair / NT, ni = pair % NT;
 #pragma unroll 8
             for (int kk = 0; kk < NN_R / 4; ++kk) {
-              const double a = ys[(kk * 4 + tig) * YP + mi * 8 + gid];  // (Z^T)[i][k]
-              const double b = ys[(kk * 4 + tig) * YP + ni * 8 + gid];
+              const double a = Os[(kk * 4 + tig) * OP + mi * 8 + gid];  // (Z^T)[i][k]
+              const double b = Os[(kk * 4 + tig) * OP + ni * 8 + gid];
               dmma884(g[p][0], g[p][1], a, b);
             }
           }
@@ -481,9 +480,8 @@ static void nn_launch(const double* X, int64_t ldx, const double* H, int64_t ldh
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     attr = true;
   }
-  gemm_nn_kernel<WP, VEC><<<nn_ctas_wp(q, WP), 256, bytes, st>>>(X, ldx, H, ldh, Y, ldy, T, Z,
-                                                                  ldz, q, s, w, alpha, beta,
-                                                                  gram);
+  gemm_nn_kernel<WP, VEC><<<nn_ctas(q, WP), 256, bytes, st>>>(X, ldx, H, ldh, Y, ldy, T, Z,
+                                                               ldz, q, s, w, alpha, beta, gram);
   TSVD_CHECK_LAUNCH();
 }
 
@@ -498,8 +496,7 @@ void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const d
               std::min(32, w - c0), alpha, beta, nullptr, st);
     return;
   }
-  const bool v2 = (s == 0 || (aligned16(X, ldx) && aligned16(H, ldh))) &&
-                  (beta == 0.0 || !Y || aligned16(Y, ldy));
+  const bool v2 = s == 0 || (aligned16(X, ldx) && aligned16(H, ldh));
 #define NN_CASE(WPV)                                                                      \
   if (v2)                                                                                 \
     nn_launch<WPV, 2>(X, ldx, H, ldh, Y, ldy, T, Z, ldz, q, s, w, alpha, beta, gram, st); \
