@@ -5,9 +5,9 @@
 // cuSPARSE's implicitly transposed SpMM is the paper's bottleneck).
 //
 // Load balance for power-law rows:
-//  * short rows (<= kLongRow nonzeros): a group of L = pow2 >= w lanes per
-//    row, lane c owns output column c; nonzeros unrolled by 8 so eight
-//    independent row gathers of X are in flight per lane;
+//  * short rows (<= kLongRow nonzeros): a group of L lanes per row, each
+//    lane owns VEC (2 when aligned) output columns; nonzeros in masked
+//    batches of 8 so eight independent row gathers of X are in flight;
 //  * long rows: split into segments of <= kSeg nonzeros, one CTA per segment
 //    (256/L groups strided over the segment, fixed-order smem reduction);
 //    rows with several segments write partials that a fix-up kernel sums in
@@ -21,7 +21,23 @@ namespace tsvd {
 constexpr int kLongRow = 64;
 constexpr int kSeg = 2048;
 
-template <int L>
+template <int VEC>
+__device__ __forceinline__ void ldx_vec(const double* p, double (&x)[VEC]) {
+  if constexpr (VEC == 2) {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    x[0] = t.x;
+    x[1] = t.y;
+  } else {
+    x[0] = __ldg(p);
+  }
+}
+
+// Short rows: a group of L lanes per row, lane owns VEC consecutive output
+// columns (double2 gathers when the block width and ld are even).  Nonzeros
+// are consumed in batches of 8 with masked loads, so a row of <= 8 nonzeros
+// costs one index-load + one gather round trip and 8 independent row
+// gathers per lane are in flight.
+template <int L, int VEC>
 __global__ void __launch_bounds__(256) spmm_short_kernel(
     const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
     const double* __restrict__ vals, const double* __restrict__ X, int64_t ldx,
@@ -30,79 +46,100 @@ __global__ void __launch_bounds__(256) spmm_short_kernel(
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t row = warp * RPW + lane / L;
-  const int c = lane % L;
+  const int c = (lane % L) * VEC;
   if (row >= rows) return;
   const int64_t beg = __ldg(rowptr + row), end = __ldg(rowptr + row + 1);
   if (end - beg > kLongRow) return;  // handled by the long-row kernels
   const bool active = c < w;
   const double* Xc = X + c;
-  double acc0 = 0.0, acc1 = 0.0;
-  int64_t k = beg;
-  for (; k + 8 <= end; k += 8) {
+  double acc0[VEC], acc1[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) acc0[e] = acc1[e] = 0.0;
+  for (int64_t k = beg; k < end; k += 8) {
     int32_t col[8];
-    double v[8], x[8];
+    double v[8];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      col[u] = __ldg(colidx + k + u);
-      v[u] = __ldg(vals + k + u);
+      const bool ok = k + u < end;
+      col[u] = ok ? __ldg(colidx + k + u) : 0;
+      v[u] = ok ? __ldg(vals + k + u) : 0.0;
+    }
+    double x[8][VEC];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (active && k + u < end)
+        ldx_vec<VEC>(Xc + (int64_t)col[u] * ldx, x[u]);
+      else
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) x[u][e] = 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) x[u] = active ? __ldg(Xc + (int64_t)col[u] * ldx) : 0.0;
+    for (int u = 0; u < 8; u += 2)
 #pragma unroll
-    for (int u = 0; u < 8; u += 2) {
-      acc0 = fma(v[u], x[u], acc0);
-      acc1 = fma(v[u + 1], x[u + 1], acc1);
+      for (int e = 0; e < VEC; ++e) {
+        acc0[e] = fma(v[u], x[u][e], acc0[e]);
+        acc1[e] = fma(v[u + 1], x[u + 1][e], acc1[e]);
+      }
+  }
+  if (active) {
+    if constexpr (VEC == 2) {
+      *reinterpret_cast<double2*>(Y + row * ldy + c) = make_double2(acc0[0] + acc1[0], acc0[1] + acc1[1]);
+    } else {
+      Y[row * ldy + c] = acc0[0] + acc1[0];
     }
   }
-  for (; k < end; ++k) {
-    const int32_t col = __ldg(colidx + k);
-    const double v = __ldg(vals + k);
-    const double x = active ? __ldg(Xc + (int64_t)col * ldx) : 0.0;
-    acc0 = fma(v, x, acc0);
-  }
-  if (active) Y[row * ldy + c] = acc0 + acc1;
 }
 
-template <int L>
+// Long rows: one CTA per segment of <= kSeg nonzeros; 256/L groups strided
+// over the segment (adjacent groups read adjacent nonzeros), fixed-order
+// shared-memory reduction of the groups; a row split into several segments
+// writes one partial per segment, summed in segment order by the fix-up.
+template <int L, int VEC>
 __global__ void __launch_bounds__(256) spmm_long_kernel(
     const int64_t* __restrict__ seg_row, const int64_t* __restrict__ seg_beg,
     const int64_t* __restrict__ seg_end, const int32_t* __restrict__ seg_slot,
     const int32_t* __restrict__ colidx, const double* __restrict__ vals,
     const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy, int w,
     double* __restrict__ part) {
-  constexpr int G = 256 / L;
-  __shared__ double red[G][33];
-  const int g = threadIdx.x / L, c = threadIdx.x % L;
+  constexpr int G = 256 / L, CW = L * VEC;
+  __shared__ double red[G][CW + 1];
+  const int g = threadIdx.x / L, c = (threadIdx.x % L) * VEC;
   const int64_t s = blockIdx.x;
   const int64_t beg = seg_beg[s], end = seg_end[s];
   const bool active = c < w;
   const double* Xc = X + c;
-  double acc0 = 0.0, acc1 = 0.0;
-  int64_t k = beg + g;
-  for (; k + 3 * G < end; k += 4 * G) {
-    const int32_t c0 = __ldg(colidx + k), c1 = __ldg(colidx + k + G);
-    const int32_t c2 = __ldg(colidx + k + 2 * G), c3 = __ldg(colidx + k + 3 * G);
-    const double v0 = __ldg(vals + k), v1 = __ldg(vals + k + G);
-    const double v2 = __ldg(vals + k + 2 * G), v3 = __ldg(vals + k + 3 * G);
-    double x0 = 0, x1 = 0, x2 = 0, x3 = 0;
-    if (active) {
-      x0 = __ldg(Xc + (int64_t)c0 * ldx);
-      x1 = __ldg(Xc + (int64_t)c1 * ldx);
-      x2 = __ldg(Xc + (int64_t)c2 * ldx);
-      x3 = __ldg(Xc + (int64_t)c3 * ldx);
+  double acc0[VEC], acc1[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) acc0[e] = acc1[e] = 0.0;
+  for (int64_t k = beg + g; k < end; k += 4 * G) {
+    int32_t col[4];
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool ok = k + u * G < end;
+      col[u] = ok ? __ldg(colidx + k + u * G) : 0;
+      v[u] = ok ? __ldg(vals + k + u * G) : 0.0;
     }
-    acc0 = fma(v0, x0, acc0);
-    acc1 = fma(v1, x1, acc1);
-    acc0 = fma(v2, x2, acc0);
-    acc1 = fma(v3, x3, acc1);
+    double x[4][VEC];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (active && k + u * G < end)
+        ldx_vec<VEC>(Xc + (int64_t)col[u] * ldx, x[u]);
+      else
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) x[u][e] = 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; u += 2)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        acc0[e] = fma(v[u], x[u][e], acc0[e]);
+        acc1[e] = fma(v[u + 1], x[u + 1][e], acc1[e]);
+      }
   }
-  for (; k < end; k += G) {
-    const int32_t c0 = __ldg(colidx + k);
-    const double v0 = __ldg(vals + k);
-    const double x0 = active ? __ldg(Xc + (int64_t)c0 * ldx) : 0.0;
-    acc0 = fma(v0, x0, acc0);
-  }
-  red[g][c] = acc0 + acc1;
+#pragma unroll
+  for (int e = 0; e < VEC; ++e)
+    red[g][c + e] = acc0[e] + acc1[e];
   __syncthreads();
   if (threadIdx.x < w) {
     double sum = 0.0;
@@ -130,21 +167,20 @@ __global__ void spmm_fixup_kernel(const int64_t* __restrict__ split_row,
   Y[split_row[r] * ldy + c] = sum;
 }
 
-template <int L>
+template <int L, int VEC>
 static void spmm_dispatch(const Csr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
                           int w, double* part, cudaStream_t st) {
   constexpr int RPW = 32 / L;
   const int64_t rows_per_block = 8 * RPW;
   const int64_t blocks = (A.rows + rows_per_block - 1) / rows_per_block;
   if (blocks > 0) {
-    spmm_short_kernel<L><<<(unsigned)blocks, 256, 0, st>>>(A.rowptr, A.colidx, A.vals, X, ldx,
-                                                            Y, ldy, A.rows, w);
+    spmm_short_kernel<L, VEC><<<(unsigned)blocks, 256, 0, st>>>(A.rowptr, A.colidx, A.vals, X,
+                                                                 ldx, Y, ldy, A.rows, w);
     TSVD_CHECK_LAUNCH();
   }
   if (A.nseg > 0) {
-    spmm_long_kernel<L><<<(unsigned)A.nseg, 256, 0, st>>>(A.seg_row, A.seg_beg, A.seg_end,
-                                                           A.seg_slot, A.colidx, A.vals, X,
-                                                           ldx, Y, ldy, w, part);
+    spmm_long_kernel<L, VEC><<<(unsigned)A.nseg, 256, 0, st>>>(
+        A.seg_row, A.seg_beg, A.seg_end, A.seg_slot, A.colidx, A.vals, X, ldx, Y, ldy, w, part);
     TSVD_CHECK_LAUNCH();
   }
   if (A.nsplit > 0) {
@@ -157,14 +193,29 @@ static void spmm_dispatch(const Csr& A, const double* X, int64_t ldx, double* Y,
 
 void launch_spmm(const Csr& A, const double* X, int64_t ldx, double* Y, int64_t ldy, int w,
                  double* part, cudaStream_t st) {
-  if (w <= 4)
-    spmm_dispatch<4>(A, X, ldx, Y, ldy, w, part, st);
-  else if (w <= 8)
-    spmm_dispatch<8>(A, X, ldx, Y, ldy, w, part, st);
-  else if (w <= 16)
-    spmm_dispatch<16>(A, X, ldx, Y, ldy, w, part, st);
-  else
-    spmm_dispatch<32>(A, X, ldx, Y, ldy, w, part, st);
+  const bool v2 = (w % 2 == 0) && (ldx % 2 == 0) && (ldy % 2 == 0) &&
+                  ((uintptr_t)X % 16 == 0) && ((uintptr_t)Y % 16 == 0);
+  if (v2) {
+    if (w <= 2)
+      spmm_dispatch<1, 2>(A, X, ldx, Y, ldy, w, part, st);
+    else if (w <= 4)
+      spmm_dispatch<2, 2>(A, X, ldx, Y, ldy, w, part, st);
+    else if (w <= 8)
+      spmm_dispatch<4, 2>(A, X, ldx, Y, ldy, w, part, st);
+    else if (w <= 16)
+      spmm_dispatch<8, 2>(A, X, ldx, Y, ldy, w, part, st);
+    else
+      spmm_dispatch<16, 2>(A, X, ldx, Y, ldy, w, part, st);
+  } else {
+    if (w <= 4)
+      spmm_dispatch<4, 1>(A, X, ldx, Y, ldy, w, part, st);
+    else if (w <= 8)
+      spmm_dispatch<8, 1>(A, X, ldx, Y, ldy, w, part, st);
+    else if (w <= 16)
+      spmm_dispatch<16, 1>(A, X, ldx, Y, ldy, w, part, st);
+    else
+      spmm_dispatch<32, 1>(A, X, ldx, Y, ldy, w, part, st);
+  }
 }
 
 void launch_spmm_wide(const Csr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
