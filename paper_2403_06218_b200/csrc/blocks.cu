@@ -141,7 +141,7 @@ int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
   }
   {
     Prof p(c, P_SMALL, 0, 0);
-    chol_finalize(gram, np, w, L1, T1, c.dflags + 0, c.st);                     // S2
+    chol_finalize(gram, np, w, dbuf(c, "Wred", 32 * 32), L1, T1, c.dflags + 0, c.st);                     // S2
   }
   {  // S3 + S4: S = Y L^{-T}, Wbar = S^T S
     Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 3.0 * q * w * w);
@@ -149,7 +149,7 @@ int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
   }
   {
     Prof p(c, P_SMALL, 0, 0);
-    chol2_finalize(gram, np, w, L1, L2, T2, R, nullptr, nullptr, 0, c.dflags + 1, c.st);  // S5, S7
+    chol2_finalize(gram, np, w, dbuf(c, "Wred", 32 * 32), L1, L2, T2, R, nullptr, nullptr, 0, c.dflags + 1, c.st);  // S5, S7
   }
   if (read_flags(c)) {
     Prof p(c, P_OTHER, 0, 0);
@@ -189,7 +189,7 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
   }
   {
     Prof p(c, P_SMALL, 0, 0);
-    chol_finalize(gram, np, w, L1, T1, c.dflags + 0, c.st);                           // S4
+    chol_finalize(gram, np, w, dbuf(c, "Wred", 32 * 32), L1, T1, c.dflags + 0, c.st);                           // S4
   }
   {
     Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 1.0 * q * w * w);
@@ -205,7 +205,7 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
   }
   {
     Prof p(c, P_SMALL, 0, 0);
-    chol2_finalize(gram, np, w, L1, L2, T2, R, H, Hbar, s, c.dflags + 1, c.st);       // S9,S11,S12
+    chol2_finalize(gram, np, w, dbuf(c, "Wred", 32 * 32), L1, L2, T2, R, H, Hbar, s, c.dflags + 1, c.st);       // S9,S11,S12
   }
   if (read_flags(c)) {
     Prof p(c, P_OTHER, 0, 0);

@@ -106,12 +106,13 @@ void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const d
 
 // small (single-CTA) finalisers (small.cu)
 // W = sum of nparts partial (w x w) Grams; L = chol(W), T = L^{-T}; flag |= breakdown.
-void chol_finalize(const double* gram, int nparts, int w, double* L, double* T, int* flag,
-                   cudaStream_t st);
+// Wred: w*w workspace for the reduced Gram.
+void chol_finalize(const double* gram, int nparts, int w, double* Wred, double* L, double* T,
+                   int* flag, cudaStream_t st);
 // Lbar = chol(Wbar), Tbar = Lbar^{-T}; R = Lbar^T Lprev^T; H (s x w) += Hbar Lprev^T.
-void chol2_finalize(const double* gram, int nparts, int w, const double* Lprev, double* L2,
-                    double* T2, double* R, double* H, const double* Hbar, int s, int* flag,
-                    cudaStream_t st);
+void chol2_finalize(const double* gram, int nparts, int w, double* Wred, const double* Lprev,
+                    double* L2, double* T2, double* R, double* H, const double* Hbar, int s,
+                    int* flag, cudaStream_t st);
 // out[i] = sum_p part[p*count + i], fixed order
 void reduce_partials(const double* part, int nparts, int64_t count, double* out,
                      cudaStream_t st);

@@ -259,6 +259,217 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(double* __restrict__ 
   }
 }
 
+// Register-resident variant (d <= 1024): during a round the pair's 2*JC
+// columns of G are held in registers (rows tid + JR_T*k, k < RG), so a
+// rotation touches no shared memory.  Per inner round every thread adds its
+// rows' contributions to the 3*JC dot products, the CTA reduces them (warp
+// recursive-halving butterfly, then a fixed-order sum over warps), JC
+// threads form the rotations, every thread applies them to its rows and 128
+// threads accumulate them into the 2JC x 2JC orthogonal J (shared memory).
+// After the inner sweep the V rows are streamed through registers and
+// multiplied by J.
+constexpr int JR_T = 256;
+
+__host__ __device__ constexpr int cpair_lo(int t, int r) {
+  const int p = (t == 0) ? 0 : ((t - 1 + r) % (JW - 1)) + 1;
+  const int q = ((JW - 2 - t + r) % (JW - 1)) + 1;
+  return p < q ? p : q;
+}
+__host__ __device__ constexpr int cpair_hi(int t, int r) {
+  const int p = (t == 0) ? 0 : ((t - 1 + r) % (JW - 1)) + 1;
+  const int q = ((JW - 2 - t + r) % (JW - 1)) + 1;
+  return p < q ? q : p;
+}
+
+template <int RG>
+__global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict__ G,
+                                                            double* __restrict__ V, int d, int nb,
+                                                            double* __restrict__ nrm,
+                                                            double* __restrict__ Ub,
+                                                            double* __restrict__ S,
+                                                            double* __restrict__ Vb,
+                                                            unsigned* __restrict__ ctl) {
+  constexpr int NW = JR_T / 32;
+  constexpr int NV = 3 * JC;  // 24 partial sums per inner round
+  __shared__ double red[NW][NV + 1];
+  __shared__ double rot_cs[JC], rot_sn[JC];
+  __shared__ double Js[JW][JW + 1];
+  __shared__ int any_rot;
+  unsigned* bar = ctl;
+  unsigned* rot = ctl + 2;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int dp = nb * JC;
+  const unsigned nblk = gridDim.x;
+  const double tol = (double)d * 0x1.0p-53;
+  double x[RG][JW];
+  int sweep = 0;
+  for (; sweep < kMaxSweeps; ++sweep) {
+    for (int round = 0; round < nb - 1; ++round) {
+      int bi, bj;
+      circle_pair(blockIdx.x, round, nb, bi, bj);
+#pragma unroll
+      for (int k = 0; k < RG; ++k) {
+        const int row = tid + JR_T * k;
+#pragma unroll
+        for (int c = 0; c < JW; ++c) {
+          const int col = c < JC ? bi * JC + c : bj * JC + (c - JC);
+          x[k][c] = row < d ? G[(size_t)col * d + row] : 0.0;
+        }
+      }
+      if (tid < JW * JW) Js[tid / JW][tid % JW] = (tid / JW == tid % JW) ? 1.0 : 0.0;
+      if (tid == 0) any_rot = 0;
+#pragma unroll
+      for (int ir = 0; ir < JW - 1; ++ir) {
+        double v[32];
+#pragma unroll
+        for (int i = NV; i < 32; ++i) v[i] = 0.0;
+#pragma unroll
+        for (int t = 0; t < JC; ++t) {
+          const int p = cpair_lo(t, ir), q = cpair_hi(t, ir);
+          double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+          for (int k = 0; k < RG; ++k) {
+            a = fma(x[k][p], x[k][p], a);
+            b = fma(x[k][q], x[k][q], b);
+            c = fma(x[k][p], x[k][q], c);
+          }
+          v[3 * t] = a;
+          v[3 * t + 1] = b;
+          v[3 * t + 2] = c;
+        }
+        // recursive-halving butterfly over 32 lanes on 24 (zero-padded to 32)
+        // values: afterwards lane l holds the warp sum of value l
+        {
+          const bool up = (lane & 16) != 0;
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const double lo = v[i], hi = v[i + 16];
+            const double send = up ? lo : hi, keep = up ? hi : lo;
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+          }
+        }
+#pragma unroll
+        for (int o = 8; o >= 1; o >>= 1) {
+          const bool up = (lane & o) != 0;
+#pragma unroll
+          for (int i = 0; i < o; ++i) {
+            const double send = up ? v[i] : v[i + o], keep = up ? v[i + o] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+          }
+        }
+        if (lane < NV) red[warp][lane] = v[0];
+        __syncthreads();
+        if (tid < JC) {
+          double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+          for (int w2 = 0; w2 < NW; ++w2) {
+            a += red[w2][3 * tid];
+            b += red[w2][3 * tid + 1];
+            c += red[w2][3 * tid + 2];
+          }
+          double cs = 1.0, sn = 0.0;
+          if (a > 0.0 && b > 0.0 && fabs(c) > tol * sqrt(a * b)) {
+            const double h = 0.5 * (b - a);
+            const double t = (h >= 0.0 ? c : -c) / (fabs(h) + sqrt(fma(h, h, c * c)));
+            cs = rsqrt(fma(t, t, 1.0));
+            sn = cs * t;
+            any_rot = 1;
+          }
+          rot_cs[tid] = cs;
+          rot_sn[tid] = sn;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int t = 0; t < JC; ++t) {
+          const int p = cpair_lo(t, ir), q = cpair_hi(t, ir);
+          const double cs = rot_cs[t], sn = rot_sn[t];
+#pragma unroll
+          for (int k = 0; k < RG; ++k) {
+            const double xp = x[k][p], xq = x[k][q];
+            x[k][p] = cs * xp - sn * xq;
+            x[k][q] = sn * xp + cs * xq;
+          }
+        }
+        if (tid < JC * JW) {
+          const int t = tid / JW, i = tid % JW;
+          const int p = cpair_lo(t, ir), q = cpair_hi(t, ir);
+          const double cs = rot_cs[t], sn = rot_sn[t];
+          const double jp = Js[i][p], jq = Js[i][q];
+          Js[i][p] = cs * jp - sn * jq;
+          Js[i][q] = sn * jp + cs * jq;
+        }
+      }
+      __syncthreads();
+      if (any_rot) {
+#pragma unroll
+        for (int k = 0; k < RG; ++k) {
+          const int row = tid + JR_T * k;
+          if (row < d) {
+#pragma unroll
+            for (int c = 0; c < JW; ++c) {
+              const int col = c < JC ? bi * JC + c : bj * JC + (c - JC);
+              G[(size_t)col * d + row] = x[k][c];
+            }
+          }
+        }
+        // V pair <- V pair J, rows streamed through registers
+#pragma unroll 1
+        for (int row = tid; row < dp; row += JR_T) {
+          double acc[JW];
+#pragma unroll
+          for (int c = 0; c < JW; ++c) acc[c] = 0.0;
+#pragma unroll 4
+          for (int l = 0; l < JW; ++l) {
+            const int coll = l < JC ? bi * JC + l : bj * JC + (l - JC);
+            const double yl = V[(size_t)coll * dp + row];
+#pragma unroll
+            for (int c = 0; c < JW; ++c) acc[c] = fma(yl, Js[l][c], acc[c]);
+          }
+#pragma unroll
+          for (int c = 0; c < JW; ++c) {
+            const int col = c < JC ? bi * JC + c : bj * JC + (c - JC);
+            V[(size_t)col * dp + row] = acc[c];
+          }
+        }
+        if (tid == 0) atomicOr(rot + (sweep & 1), 1u);
+      }
+      grid_barrier(bar, nblk);
+      if (round == 0 && blockIdx.x == 0 && tid == 0) atomicExch(rot + ((sweep + 1) & 1), 0u);
+    }
+    const unsigned any = *((volatile unsigned*)(rot + (sweep & 1)));
+    if (!any) break;
+  }
+  if (blockIdx.x == 0 && tid == 0) ctl[4] = (unsigned)sweep;
+  for (int j = blockIdx.x * NW + warp; j < dp; j += nblk * NW) {
+    double a = 0.0;
+    for (int i = lane; i < d; i += 32) {
+      const double g = G[(size_t)j * d + i];
+      a = fma(g, g, a);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) nrm[j] = sqrt(a);
+  }
+  grid_barrier(bar, nblk);
+  for (int j = blockIdx.x * NW + warp; j < dp; j += nblk * NW) {
+    const double sj = nrm[j];
+    int cnt = 0;
+    for (int k = lane; k < dp; k += 32) {
+      const double sk = nrm[k];
+      cnt += (sk > sj || (sk == sj && k < j)) ? 1 : 0;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (cnt >= d) continue;
+    const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
+    if (lane == 0) S[cnt] = sj;
+    for (int i = lane; i < d; i += 32) {
+      Ub[(size_t)i * d + cnt] = G[(size_t)j * d + i] * inv;
+      Vb[(size_t)i * d + cnt] = V[(size_t)j * dp + i];
+    }
+  }
+}
+
 int small_svd_sweeps(const double* work, int d) {
   const int nb = jac_nb(d), dp = nb * JC;
   const unsigned* ctl = (const unsigned*)(work + (size_t)d * dp + (size_t)dp * dp + dp);
@@ -277,6 +488,21 @@ void small_svd(const double* B, int d, double* Ub, double* S, double* Vb, double
   unsigned* ctl = (unsigned*)(nrm + dp);
   jacobi_init_kernel<<<148 * 4, 256, 0, st>>>(B, d, dp, G, V, ctl);
   TSVD_CHECK_LAUNCH();
+  {
+    int nblocks = nb / 2, nbv = nb;
+    void* args[] = {&G, &V, &d, &nbv, &nrm, &Ub, &S, &Vb, &ctl};
+    const int RG = (d + JR_T - 1) / JR_T;
+    void* fn = nullptr;
+    if (RG <= 1) fn = (void*)jacobi_reg_kernel<1>;
+    else if (RG == 2) fn = (void*)jacobi_reg_kernel<2>;
+    else if (RG == 3) fn = (void*)jacobi_reg_kernel<3>;
+    else if (RG == 4) fn = (void*)jacobi_reg_kernel<4>;
+    if (fn) {
+      TSVD_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(JR_T), args, 0, st));
+      TSVD_CHECK_LAUNCH();
+      return;
+    }
+  }
   const size_t smem = sizeof(double) * ((size_t)d * JP + 2 * JW * JP);
   static int attr_for = -1;
   if (attr_for < (int)smem) {

@@ -77,9 +77,10 @@ __global__ void chol_finalize_kernel(const double* __restrict__ gram, int nparts
   if (tid == 0 && bad) *flag = 1;
 }
 
-void chol_finalize(const double* gram, int nparts, int w, double* L, double* T, int* flag,
-                   cudaStream_t st) {
-  chol_finalize_kernel<<<1, 256, 0, st>>>(gram, nparts, w, L, T, flag);
+void chol_finalize(const double* gram, int nparts, int w, double* Wred, double* L, double* T,
+                   int* flag, cudaStream_t st) {
+  reduce_partials(gram, nparts, (int64_t)w * w, Wred, st);
+  chol_finalize_kernel<<<1, 256, 0, st>>>(Wred, 1, w, L, T, flag);
   TSVD_CHECK_LAUNCH();
 }
 
@@ -127,10 +128,11 @@ __global__ void chol2_finalize_kernel(const double* __restrict__ gram, int npart
   if (tid == 0 && bad) *flag = 1;
 }
 
-void chol2_finalize(const double* gram, int nparts, int w, const double* Lprev, double* L2,
-                    double* T2, double* R, double* H, const double* Hbar, int s, int* flag,
-                    cudaStream_t st) {
-  chol2_finalize_kernel<<<1, 256, 0, st>>>(gram, nparts, w, Lprev, L2, T2, R, H, Hbar, s, flag);
+void chol2_finalize(const double* gram, int nparts, int w, double* Wred, const double* Lprev,
+                    double* L2, double* T2, double* R, double* H, const double* Hbar, int s,
+                    int* flag, cudaStream_t st) {
+  reduce_partials(gram, nparts, (int64_t)w * w, Wred, st);
+  chol2_finalize_kernel<<<1, 256, 0, st>>>(Wred, 1, w, Lprev, L2, T2, R, H, Hbar, s, flag);
   TSVD_CHECK_LAUNCH();
 }
 

@@ -189,34 +189,52 @@ __global__ void __launch_bounds__(256, (WP == 32) ? 1 : 2) gemm_tn_kernel(const 
   }
 }
 
+// Fixed-order split-K reduction: lanes own 32 consecutive outputs, warp k of
+// the CTA sums partials k, k+8, k+16, ... (two interleaved accumulators), the
+// 8 warp sums are added in warp order.  Deterministic for a given nparts.
 __global__ void reduce_partials_kernel(const double* __restrict__ part, int nparts,
-                                       int64_t count, double* __restrict__ out) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int p = 0; p < nparts; ++p) s += part[(int64_t)p * count + i];
-    out[i] = s;
+                                       int64_t count, double* __restrict__ out, int w,
+                                       int64_t ldc) {
+  __shared__ double red[8][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int64_t base = (int64_t)blockIdx.x * 32; base < count; base += (int64_t)gridDim.x * 32) {
+    const int64_t i = base + lane;
+    double a0 = 0.0, a1 = 0.0;
+    if (i < count) {
+      int p = warp;
+      for (; p + 8 < nparts; p += 16) {
+        a0 += part[(int64_t)p * count + i];
+        a1 += part[(int64_t)(p + 8) * count + i];
+      }
+      if (p < nparts) a0 += part[(int64_t)p * count + i];
+    }
+    red[warp][lane] = a0 + a1;
+    __syncthreads();
+    if (warp == 0 && i < count) {
+      double sum = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum += red[k][lane];
+      if (ldc)
+        out[(i / w) * ldc + (i % w)] = sum;
+      else
+        out[i] = sum;
+    }
+    __syncthreads();
   }
 }
 
-__global__ void reduce_partials_ld_kernel(const double* __restrict__ part, int nparts, int s,
-                                          int w, double* __restrict__ C, int64_t ldc) {
-  const int64_t count = (int64_t)s * w;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    double acc = 0.0;
-    for (int p = 0; p < nparts; ++p) acc += part[(int64_t)p * count + i];
-    C[(i / w) * ldc + (i % w)] = acc;
-  }
+static void reduce_launch(const double* part, int nparts, int64_t count, double* out, int w,
+                          int64_t ldc, cudaStream_t st) {
+  if (count <= 0) return;
+  int64_t blocks = (count + 31) / 32;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  reduce_partials_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, nparts, count, out, w, ldc);
+  TSVD_CHECK_LAUNCH();
 }
 
 void reduce_partials(const double* part, int nparts, int64_t count, double* out,
                      cudaStream_t st) {
-  if (count <= 0) return;
-  int64_t blocks = (count + 255) / 256;
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  reduce_partials_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, nparts, count, out);
-  TSVD_CHECK_LAUNCH();
+  reduce_launch(part, nparts, count, out, 1, 0, st);
 }
 
 static bool aligned16(const void* p, int64_t ld) {
@@ -267,13 +285,7 @@ void gemm_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t
     TN_CASE(32)
   }
 #undef TN_CASE
-  if (g.splits > 1) {
-    const int64_t count = (int64_t)s * w;
-    int64_t blocks = (count + 255) / 256;
-    if (blocks > 148 * 8) blocks = 148 * 8;
-    reduce_partials_ld_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, g.splits, s, w, C, ldc);
-    TSVD_CHECK_LAUNCH();
-  }
+  if (g.splits > 1) reduce_launch(part, g.splits, (int64_t)s * w, C, w, ldc == w ? 0 : ldc, st);
 }
 
 // ------------------------------------------------------------------ NN ---
