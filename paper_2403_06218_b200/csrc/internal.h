@@ -138,8 +138,12 @@ int small_svd_sweeps(const double* work, int d);  // sweeps of the last small_sv
 void lanczos_rho(const double* Rbar, int b, const double* Vb, int d, const double* S, int cnt,
                  double* rho, cudaStream_t st);
 
-// sign normalisation: flip U[:,i], V[:,i] so that max |V[:,i]| entry > 0
-void sign_normalize(double* U, int64_t m, int64_t ldu, double* V, int64_t n, int64_t ldv,
-                    int r, double* work, cudaStream_t st);
+// sign normalisation (reading R28): sgn[i] = sign of the largest-|.| entry of
+// V[:, i] (lowest index on ties); flip_columns multiplies columns by sgn.
+size_t col_signs_work(int r);
+void col_signs(const double* V, int64_t n, int64_t ldv, int r, double* sgn, double* work,
+               cudaStream_t st);
+void flip_columns(double* M, int64_t rows, int64_t ld, int r, const double* sgn,
+                  cudaStream_t st);
 
 }  // namespace tsvd

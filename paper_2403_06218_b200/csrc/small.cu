@@ -36,29 +36,30 @@ __device__ void warp_cholesky(double* Ws, double* Lo, int w, int* bad) {
 }
 
 // T = L^{-T} (upper triangular) from the lower triangular L held in Lo (ld 32):
-// lane j computes column j of L^{-1} by forward substitution; T[j][i] = Linv[i][j].
-__device__ void warp_tri_inverse_t(const double* Lo, double* Tout, int w) {
+// lane j computes column j of L^{-1} by forward substitution into the shared
+// scratch Xs (ld 33); T[j][i] = Linv[i][j].
+__device__ void warp_tri_inverse_t(const double* Lo, double* Xs, double* Tout, int w) {
   const int j = threadIdx.x & 31;
-  if (j >= w) return;
-  double x[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    x[i] = 0.0;
-    if (i < w && i >= j) {
-      double v = (i == j) ? 1.0 : 0.0;
-      for (int k = j; k < i; ++k) v = fma(-Lo[i * 32 + k], x[k], v);
-      x[i] = v / Lo[i * 32 + i];
+  if (j < w) {
+    for (int i = 0; i < w; ++i) {
+      double v = 0.0;
+      if (i >= j) {
+        v = (i == j) ? 1.0 : 0.0;
+        for (int k = j; k < i; ++k) v = fma(-Lo[i * 32 + k], Xs[k * 33 + j], v);
+        v = v / Lo[i * 32 + i];
+      }
+      Xs[i * 33 + j] = v;
     }
   }
-#pragma unroll
-  for (int i = 0; i < 32; ++i)
-    if (i < w) Tout[j * w + i] = x[i];  // T[j][i] = Linv[i][j]
+  __syncwarp();
+  if (j < w)
+    for (int i = 0; i < w; ++i) Tout[j * w + i] = Xs[i * 33 + j];  // T[j][i] = Linv[i][j]
 }
 
 __global__ void chol_finalize_kernel(const double* __restrict__ gram, int nparts, int w,
                                      double* __restrict__ L, double* __restrict__ T,
                                      int* __restrict__ flag) {
-  __shared__ double Ws[32 * 32];
+  __shared__ double Ws[32 * 33];
   __shared__ double Lo[32 * 32];
   __shared__ int bad;
   const int tid = threadIdx.x;
@@ -73,7 +74,7 @@ __global__ void chol_finalize_kernel(const double* __restrict__ gram, int nparts
   if (tid < 32) warp_cholesky(Ws, Lo, w, &bad);
   __syncthreads();
   for (int i = tid; i < w * w; i += blockDim.x) L[i] = Lo[(i / w) * 32 + (i % w)];
-  if (tid < 32) warp_tri_inverse_t(Lo, T, w);
+  if (tid < 32) warp_tri_inverse_t(Lo, Ws, T, w);
   if (tid == 0 && bad) *flag = 1;
 }
 
@@ -91,7 +92,7 @@ __global__ void chol2_finalize_kernel(const double* __restrict__ gram, int npart
                                       double* __restrict__ T2, double* __restrict__ R,
                                       double* __restrict__ H, const double* __restrict__ Hbar,
                                       int s, int* __restrict__ flag) {
-  __shared__ double Ws[32 * 32];
+  __shared__ double Ws[32 * 33];
   __shared__ double Lo[32 * 32];
   __shared__ double Lp[32 * 32];
   __shared__ int bad;
@@ -107,7 +108,7 @@ __global__ void chol2_finalize_kernel(const double* __restrict__ gram, int npart
   __syncthreads();
   if (tid < 32) warp_cholesky(Ws, Lo, w, &bad);
   __syncthreads();
-  if (tid < 32) warp_tri_inverse_t(Lo, T2, w);
+  if (tid < 32) warp_tri_inverse_t(Lo, Ws, T2, w);
   for (int i = tid; i < w * w; i += blockDim.x) {
     const int r = i / w, c = i % w;
     L2[i] = Lo[r * 32 + c];
@@ -117,12 +118,18 @@ __global__ void chol2_finalize_kernel(const double* __restrict__ gram, int npart
     R[i] = sum;
   }
   if (H) {
-    for (int64_t i = tid; i < (int64_t)s * w; i += blockDim.x) {
-      const int64_t r = i / w;
-      const int c = (int)(i % w);
-      double sum = 0.0;
-      for (int k = 0; k < w; ++k) sum = fma(Hbar[r * w + k], Lp[c * w + k], sum);
-      H[i] += sum;
+    // one H row per thread: its w Hbar entries are loaded together
+    for (int r = tid; r < s; r += blockDim.x) {
+      double hb[32];
+#pragma unroll
+      for (int k = 0; k < 32; ++k) hb[k] = k < w ? Hbar[(int64_t)r * w + k] : 0.0;
+      for (int c = 0; c < w; ++c) {
+        double sum = 0.0;
+#pragma unroll
+        for (int k = 0; k < 32; ++k)
+          if (k < w) sum = fma(hb[k], Lp[c * w + k], sum);
+        H[(int64_t)r * w + c] += sum;
+      }
     }
   }
   if (tid == 0 && bad) *flag = 1;
@@ -221,36 +228,64 @@ void lanczos_rho(const double* Rbar, int b, const double* Vb, int d, const doubl
 }
 
 // sign normalisation (reading R28): per column i of V, the largest-|.| entry
-// (lowest index on ties) is made positive; U's column flips with it.
-__global__ void colmax_kernel(const double* __restrict__ V, int64_t n, int64_t ldv,
-                              double* __restrict__ sgn) {
-  __shared__ double bv[256];
-  __shared__ int64_t bi[256];
-  const int i = blockIdx.x;
+// (lowest index on ties) is made positive; the column of U flips with it.
+// Pass 1: CTAs own row ranges, lanes own 32 consecutive columns (coalesced
+// row reads), per-CTA (max, argmin-index) partials; pass 2: fixed-order scan
+// of the partials per column -> sign.
+constexpr int kSignCtas = 296;
+
+__global__ void colmax_partial_kernel(const double* __restrict__ V, int64_t n, int64_t ldv,
+                                      int r, double* __restrict__ pval,
+                                      int64_t* __restrict__ pidx) {
+  __shared__ double bv[8][32];
+  __shared__ int64_t bi[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int c = blockIdx.y * 32 + lane;
   double best = -1.0;
   int64_t bidx = 0;
-  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
-    const double a = fabs(V[j * ldv + i]);
-    if (a > best) {  // strictly greater keeps the lowest index of this thread
-      best = a;
-      bidx = j;
-    }
-  }
-  bv[threadIdx.x] = best;
-  bi[threadIdx.x] = bidx;
-  __syncthreads();
-  for (int off = 128; off > 0; off >>= 1) {
-    if (threadIdx.x < off) {
-      const double o = bv[threadIdx.x + off];
-      const int64_t oi = bi[threadIdx.x + off];
-      if (o > bv[threadIdx.x] || (o == bv[threadIdx.x] && oi < bi[threadIdx.x])) {
-        bv[threadIdx.x] = o;
-        bi[threadIdx.x] = oi;
+  if (c < r) {
+    for (int64_t j = (int64_t)blockIdx.x * 8 + warp; j < n; j += (int64_t)gridDim.x * 8) {
+      const double a = fabs(V[j * ldv + c]);
+      if (a > best) {  // rows visited in increasing order: keeps the lowest index
+        best = a;
+        bidx = j;
       }
     }
-    __syncthreads();
   }
-  if (threadIdx.x == 0) sgn[i] = (V[bi[0] * ldv + i] < 0.0) ? -1.0 : 1.0;
+  bv[warp][lane] = best;
+  bi[warp][lane] = bidx;
+  __syncthreads();
+  if (warp == 0 && c < r) {
+    for (int k = 1; k < 8; ++k) {
+      const double o = bv[k][lane];
+      const int64_t oi = bi[k][lane];
+      if (o > best || (o == best && oi < bidx)) {
+        best = o;
+        bidx = oi;
+      }
+    }
+    pval[(int64_t)blockIdx.x * r + c] = best;
+    pidx[(int64_t)blockIdx.x * r + c] = bidx;
+  }
+}
+
+__global__ void colsign_final_kernel(const double* __restrict__ V, int64_t ldv, int r,
+                                     const double* __restrict__ pval,
+                                     const int64_t* __restrict__ pidx, int nparts,
+                                     double* __restrict__ sgn) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= r) return;
+  double best = -1.0;
+  int64_t bidx = 0;
+  for (int p = 0; p < nparts; ++p) {
+    const double o = pval[(int64_t)p * r + c];
+    const int64_t oi = pidx[(int64_t)p * r + c];
+    if (o > best || (o == best && oi < bidx)) {
+      best = o;
+      bidx = oi;
+    }
+  }
+  sgn[c] = (V[bidx * ldv + c] < 0.0) ? -1.0 : 1.0;
 }
 
 __global__ void flip_kernel(double* __restrict__ M, int64_t rows, int64_t ld, int r,
@@ -264,12 +299,26 @@ __global__ void flip_kernel(double* __restrict__ M, int64_t rows, int64_t ld, in
   }
 }
 
-void sign_normalize(double* U, int64_t m, int64_t ldu, double* V, int64_t n, int64_t ldv,
-                    int r, double* work, cudaStream_t st) {
+size_t col_signs_work(int r) { return (size_t)kSignCtas * r * 2 + r + 8; }
+
+void col_signs(const double* V, int64_t n, int64_t ldv, int r, double* sgn, double* work,
+               cudaStream_t st) {
   if (r <= 0) return;
-  colmax_kernel<<<r, 256, 0, st>>>(V, n, ldv, work);
-  flip_kernel<<<148 * 4, 256, 0, st>>>(U, m, ldu, r, work);
-  flip_kernel<<<148 * 4, 256, 0, st>>>(V, n, ldv, r, work);
+  double* pval = work;
+  int64_t* pidx = (int64_t*)(work + (size_t)kSignCtas * r);
+  dim3 grid(kSignCtas, (r + 31) / 32);
+  colmax_partial_kernel<<<grid, 256, 0, st>>>(V, n, ldv, r, pval, pidx);
+  TSVD_CHECK_LAUNCH();
+  colsign_final_kernel<<<(r + 127) / 128, 128, 0, st>>>(V, ldv, r, pval, pidx, kSignCtas, sgn);
+  TSVD_CHECK_LAUNCH();
+}
+
+void flip_columns(double* M, int64_t rows, int64_t ld, int r, const double* sgn,
+                  cudaStream_t st) {
+  if (r <= 0 || rows <= 0) return;
+  int64_t blocks = (rows * r + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  flip_kernel<<<(unsigned)blocks, 256, 0, st>>>(M, rows, ld, r, sgn);
   TSVD_CHECK_LAUNCH();
 }
 

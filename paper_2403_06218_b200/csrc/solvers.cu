@@ -148,11 +148,15 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   alloc_results(c, r);
   {
     Prof p(c, P_RESTART, 8.0 * (m + n) * (d + r), 2.0 * (m + n) * d * r);
-    // S9: U = Pbar_k Ubar[:, :r] ; S8 (Eq. 12): V = P_k Vbar[:, :r]
-    gemm_nn(Pb, ldb, Ub, d, nullptr, 0, nullptr, c.U, r, m, d, r, 1.0, 0.0, nullptr, c.st);
+    // S8 (Eq. 12): V = P_k Vbar[:, :r]; signs (R28) from V, folded into
+    // Ubar's columns before S9: U = Pbar_k Ubar[:, :r]
     gemm_nn(P, ldp, Vb, d, nullptr, 0, nullptr, c.V, r, n, d, r, 1.0, 0.0, nullptr, c.st);
+    double* sgn = dbuf(c, "sign", (size_t)r);
+    col_signs(c.V, n, r, r, sgn, dbuf(c, "sign_work", col_signs_work(r)), c.st);
+    flip_columns(c.V, n, r, r, sgn, c.st);
+    flip_columns(Ub, d, d, r, sgn, c.st);
+    gemm_nn(Pb, ldb, Ub, d, nullptr, 0, nullptr, c.U, r, m, d, r, 1.0, 0.0, nullptr, c.st);
     TSVD_CUDA(cudaMemcpyAsync(c.S, Sg, r * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
-    sign_normalize(c.U, m, r, c.V, n, r, r, dbuf(c, "sign_work", (size_t)r), c.st);
   }
   const double ms = timer.stop();
   prof_harvest(c);
@@ -213,10 +217,13 @@ tsvd_status rsvd_solve(Ctx& c, int r, int p, int q) {
   alloc_results(c, r);
   {
     Prof p(c, P_RESTART, 8.0 * (m + n) * (l + r), 2.0 * (m + n) * l * r);
-    gemm_nn(Qb, l, Vb, l, nullptr, 0, nullptr, c.U, r, m, l, r, 1.0, 0.0, nullptr, c.st);  // S6
     gemm_nn(Q, l, Ub, l, nullptr, 0, nullptr, c.V, r, n, l, r, 1.0, 0.0, nullptr, c.st);   // S7
+    double* sgn = dbuf(c, "sign", (size_t)r);
+    col_signs(c.V, n, r, r, sgn, dbuf(c, "sign_work", col_signs_work(r)), c.st);
+    flip_columns(c.V, n, r, r, sgn, c.st);
+    flip_columns(Vb, l, l, r, sgn, c.st);
+    gemm_nn(Qb, l, Vb, l, nullptr, 0, nullptr, c.U, r, m, l, r, 1.0, 0.0, nullptr, c.st);  // S6
     TSVD_CUDA(cudaMemcpyAsync(c.S, Sg, r * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
-    sign_normalize(c.U, m, r, c.V, n, r, r, dbuf(c, "sign_work", (size_t)r), c.st);
   }
   double s1 = 0.0;
   TSVD_CUDA(cudaMemcpyAsync(&s1, Sg, sizeof(double), cudaMemcpyDeviceToHost, c.st));

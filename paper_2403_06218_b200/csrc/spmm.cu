@@ -371,25 +371,25 @@ void csr_transpose(const Csr& A, Csr& T, cudaStream_t st) {
   cudaFree(keys_out);
 }
 
+// one warp per row: bounds, monotone row pointer, strictly increasing
+// in-range column indices (canonical CSR, include/tsvd.h)
 __global__ void csr_validate_kernel(const int64_t* __restrict__ rowptr,
                                     const int32_t* __restrict__ colidx, int64_t rows,
                                     int64_t cols, int64_t nnz, int* __restrict__ bad) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < rows;
+       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t b = rowptr[i], e = rowptr[i + 1];
     if (b > e || b < 0 || e > nnz) {
-      atomicOr(bad, 1);
+      if (lane == 0) atomicOr(bad, 1);
       continue;
     }
-    int64_t prev = -1;
-    for (int64_t k = b; k < e; ++k) {
+    bool ok = true;
+    for (int64_t k = b + lane; k < e; k += 32) {
       const int64_t c = colidx[k];
-      if (c <= prev || c >= cols) {
-        atomicOr(bad, 2);
-        break;
-      }
-      prev = c;
+      if (c < 0 || c >= cols || (k > b && colidx[k - 1] >= c)) ok = false;
     }
+    if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicOr(bad, 2);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (rowptr[0] != 0 || rowptr[rows] != nnz) atomicOr(bad, 4);

@@ -305,19 +305,20 @@ constexpr int NN_KC = 32;
 template <int WP>
 struct NnCfg {
   static constexpr int S = (WP == 32) ? 3 : 2;
-  static constexpr int PER_SM = (WP == 32) ? 1 : 2;
+  static constexpr int PER_SM = (WP >= 32) ? 1 : 2;
+  static constexpr int NACC = (WP == 64) ? 1 : 2;  // even/odd accumulator sets
   static constexpr int XP = NN_KC + 4, HP = WP + 4, OP = WP + 4, NT = WP / 8;
   static constexpr size_t stage = (size_t)NN_R * XP + (size_t)NN_KC * HP;
   static constexpr size_t bytes =
       sizeof(double) * (S * stage + (size_t)NN_R * OP + (size_t)WP * WP);
 };
 
-static int wp_of(int w) { return w <= 8 ? 8 : (w <= 16 ? 16 : 32); }
+static int wp_of(int w) { return w <= 8 ? 8 : (w <= 16 ? 16 : (w <= 32 ? 32 : 64)); }
 
 int nn_ctas(int64_t q, int w) {
   const int wp = wp_of(w);
   int64_t tiles = (q + NN_R - 1) / NN_R;
-  const int64_t cap = 148 * (wp == 32 ? NnCfg<32>::PER_SM : NnCfg<16>::PER_SM);
+  const int64_t cap = 148 * (wp >= 32 ? 1 : 2);
   if (tiles > cap) tiles = cap;
   if (tiles < 1) tiles = 1;
   return (int)tiles;
@@ -330,7 +331,8 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
     int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram) {
   using CF = NnCfg<WP>;
   constexpr int S = CF::S, XP = CF::XP, HP = CF::HP, OP = CF::OP, NT = CF::NT;
-  constexpr int NPAIR = NT * NT, PPW = (NPAIR + 7) / 8, KY = WP / 4;
+  constexpr int NPAIR = NT * NT, PPW = (NPAIR + 7) / 8, KY = WP / 4, NACC = CF::NACC;
+  constexpr bool kEpiY = WP != 64;  // the WP = 64 variant serves beta = 0 products only
   extern __shared__ __align__(16) double sm[];
   double* Os = sm + S * CF::stage;
   double* Ts = Os + NN_R * OP;
@@ -362,8 +364,8 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
   double g[PPW][2];
 #pragma unroll
   for (int p = 0; p < PPW; ++p) g[p][0] = g[p][1] = 0.0;
-  double acc[2][2][NT][2];
-  double ya[2][KY];
+  double acc[NACC][2][NT][2];
+  double ya[kEpiY ? 2 : 1][kEpiY ? KY : 1];
 #pragma unroll
   for (int j = 0; j < S - 1; ++j) issue(j);
   for (int64_t j = 0; j < nsteps; ++j) {
@@ -374,20 +376,21 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
     const int64_t r0 = (blockIdx.x + lt * gridDim.x) * NN_R;
     if (kc == 0) {
 #pragma unroll
-      for (int h = 0; h < 2; ++h)
+      for (int h = 0; h < NACC; ++h)
 #pragma unroll
         for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
           for (int ni = 0; ni < NT; ++ni) acc[h][mi][ni][0] = acc[h][mi][ni][1] = 0.0;
     }
-    if (kc == nk - 1) {  // prefetch this tile's Y rows as A-fragments
+    if (kEpiY && kc == nk - 1) {  // prefetch this tile's Y rows as A-fragments
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi) {
         const int64_t row = r0 + warp * 16 + mi * 8 + gid;
 #pragma unroll
         for (int kk = 0; kk < KY; ++kk) {
           const int col = kk * 4 + tig;
-          ya[mi][kk] = (beta != 0.0 && Y && row < q && col < w) ? Y[row * ldy + col] : 0.0;
+          if constexpr (kEpiY)
+            ya[mi][kk] = (beta != 0.0 && Y && row < q && col < w) ? Y[row * ldy + col] : 0.0;
         }
       }
     }
@@ -398,7 +401,7 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
       const double* hs = Hs(st);
 #pragma unroll
       for (int kk = 0; kk < NN_KC / 4; ++kk) {
-        const int h = kk & 1;
+        const int h = (NACC == 2) ? (kk & 1) : 0;
         const double a0 = xs[(warp * 16 + gid) * XP + kk * 4 + tig];
         const double a1 = xs[(warp * 16 + 8 + gid) * XP + kk * 4 + tig];
 #pragma unroll
@@ -411,12 +414,12 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
     }
     if (kc == nk - 1) {
       // epilogue: Z = alpha*acc + beta*(Y T)
-      double yt[2][NT][2];
+      double yt[kEpiY ? 2 : 1][kEpiY ? NT : 1][2];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
+      for (int mi = 0; mi < (kEpiY ? 2 : 1); ++mi)
 #pragma unroll
-        for (int ni = 0; ni < NT; ++ni) yt[mi][ni][0] = yt[mi][ni][1] = 0.0;
-      if (beta != 0.0) {
+        for (int ni = 0; ni < (kEpiY ? NT : 1); ++ni) yt[mi][ni][0] = yt[mi][ni][1] = 0.0;
+      if constexpr (kEpiY) if (beta != 0.0) {
 #pragma unroll
         for (int kk = 0; kk < KY; ++kk)
 #pragma unroll
@@ -433,8 +436,9 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int r = warp * 16 + mi * 8 + gid, c = ni * 8 + 2 * tig + e;
-            const double z =
-                alpha * (acc[0][mi][ni][e] + acc[1][mi][ni][e]) + beta * yt[mi][ni][e];
+            double z = alpha * (NACC == 2 ? acc[0][mi][ni][e] + acc[NACC - 1][mi][ni][e]
+                                          : acc[0][mi][ni][e]);
+            if constexpr (kEpiY) z += beta * yt[mi][ni][e];
             Os[r * OP + c] = (c < w && r0 + r < q) ? z : 0.0;
           }
       __syncthreads();
@@ -503,10 +507,19 @@ void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const d
   if (w <= 0 || q <= 0) return;
   if (w > 32) {
     if (T || gram) throw Error{TSVD_EINVAL, "gemm_nn: T/gram need w <= 32"};
-    for (int c0 = 0; c0 < w; c0 += 32)
-      gemm_nn(X, ldx, H + c0, ldh, Y ? Y + c0 : nullptr, ldy, nullptr, Z + c0, ldz, q, s,
-              std::min(32, w - c0), alpha, beta, nullptr, st);
-    return;
+    const int cw = (beta == 0.0) ? 64 : 32;  // wide products (outputs) in one pass per 64 cols
+    if (w > cw) {
+      for (int c0 = 0; c0 < w; c0 += cw)
+        gemm_nn(X, ldx, H + c0, ldh, Y ? Y + c0 : nullptr, ldy, nullptr, Z + c0, ldz, q, s,
+                std::min(cw, w - c0), alpha, beta, nullptr, st);
+      return;
+    }
+    if (cw == 32) {
+      for (int c0 = 0; c0 < w; c0 += 32)
+        gemm_nn(X, ldx, H + c0, ldh, Y ? Y + c0 : nullptr, ldy, nullptr, Z + c0, ldz, q, s,
+                std::min(32, w - c0), alpha, beta, nullptr, st);
+      return;
+    }
   }
   const bool v2 = s == 0 || (aligned16(X, ldx) && aligned16(H, ldh));
 #define NN_CASE(WPV)                                                                      \
@@ -518,8 +531,10 @@ void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const d
     NN_CASE(8)
   } else if (w <= 16) {
     NN_CASE(16)
-  } else {
+  } else if (w <= 32) {
     NN_CASE(32)
+  } else {
+    NN_CASE(64)
   }
 #undef NN_CASE
 }

@@ -75,6 +75,25 @@ def nn_bench():
               flush=True)
 
 
+def sweep_bench():
+    q, w = 1_000_000, 16
+    X = torch.randn((q, 400), dtype=torch.float64, device="cuda")
+    H = torch.randn((400, w), dtype=torch.float64, device="cuda")
+    Z = torch.empty((q, w), dtype=torch.float64, device="cuda")
+    C = torch.empty((400, w), dtype=torch.float64, device="cuda")
+    L = T.lib()
+    for s in (16, 32, 64, 96, 128, 192, 256, 320, 384):
+        Y = X[:, s:]
+        ms_tn = timeit(lambda: L.tsvd_dbg_gemm_tn(X.data_ptr(), 400, Y.data_ptr(), 400, q, s, w,
+                                                  C.data_ptr(), None))
+        ms_nn = timeit(lambda: L.tsvd_dbg_gemm_nn(X.data_ptr(), 400, H.data_ptr(), w, Z.data_ptr(),
+                                                  w, q, s, w, -1.0, 1.0, None))
+        gtn = 8.0 * q * (s + w) / (ms_tn * 1e-3) / 1e9
+        gnn = 8.0 * q * (s + 2 * w) / (ms_nn * 1e-3) / 1e9
+        print(f"s={s:4d}  tn {ms_tn:.3f} ms {gtn:5.0f} GB/s ({gtn / HBM:.2f})   "
+              f"nn {ms_nn:.3f} ms {gnn:5.0f} GB/s ({gnn / HBM:.2f})", flush=True)
+
+
 def spmm_bench():
     from tsvd_inputs import powerlaw_csr
     m = n = 1_000_000
