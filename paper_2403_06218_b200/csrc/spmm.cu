@@ -12,14 +12,17 @@
 //    (256/L groups strided over the segment, fixed-order smem reduction);
 //    rows with several segments write partials that a fix-up kernel sums in
 //    segment order.  Deterministic: no floating-point atomics anywhere.
+#include <algorithm>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "internal.h"
 
 namespace tsvd {
 
-constexpr int kLongRow = 64;
-constexpr int kSeg = 2048;
+constexpr int kLongRow = 64;   // rows up to this length: sub-warp groups (sorted)
+constexpr int kMedRow = 512;   // rows up to this length: one warp each (sorted)
+constexpr int kSeg = 2048;     // longer rows: CTA segments of this many nonzeros
 
 template <int VEC>
 __device__ __forceinline__ void ldx_vec(const double* p, double (&x)[VEC]) {
@@ -38,18 +41,20 @@ __device__ __forceinline__ void ldx_vec(const double* p, double (&x)[VEC]) {
 // costs one index-load + one gather round trip and 8 independent row
 // gathers per lane are in flight.
 template <int L, int VEC>
-__global__ void __launch_bounds__(256) spmm_short_kernel(
+__device__ __forceinline__ void spmm_short_dev(
     const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
     const double* __restrict__ vals, const double* __restrict__ X, int64_t ldx,
-    double* __restrict__ Y, int64_t ldy, int64_t rows, int w) {
+    double* __restrict__ Y, int64_t ldy, const int32_t* __restrict__ order, int64_t nrows,
+    int w, int64_t bidx) {
   constexpr int RPW = 32 / L;  // rows per warp
   const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t row = warp * RPW + lane / L;
+  const int64_t warp = (bidx * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t idx = warp * RPW + lane / L;
   const int c = (lane % L) * VEC;
-  if (row >= rows) return;
+  if (idx >= nrows) return;
+  // rows of similar length share a warp (order = short rows by decreasing length)
+  const int64_t row = __ldg(order + idx);
   const int64_t beg = __ldg(rowptr + row), end = __ldg(rowptr + row + 1);
-  if (end - beg > kLongRow) return;  // handled by the long-row kernels
   const bool active = c < w;
   const double* Xc = X + c;
   double acc0[VEC], acc1[VEC];
@@ -90,21 +95,84 @@ __global__ void __launch_bounds__(256) spmm_short_kernel(
   }
 }
 
+// Medium rows (kLongRow < len <= kMedRow): one warp per row, 32/L lane groups
+// strided over the row's nonzeros (batches of 8 per group), combined by
+// xor-shuffles across groups (fixed order).
+template <int L, int VEC>
+__device__ __forceinline__ void spmm_medium_dev(
+    const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
+    const double* __restrict__ vals, const double* __restrict__ X, int64_t ldx,
+    double* __restrict__ Y, int64_t ldy, const int32_t* __restrict__ order, int64_t nrows,
+    int w, int64_t bidx) {
+  constexpr int G = 32 / L;
+  const int lane = threadIdx.x & 31;
+  const int64_t widx = (bidx * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (widx >= nrows) return;
+  const int g = lane / L, c = (lane % L) * VEC;
+  const bool active = c < w;
+  const double* Xc = X + c;
+  const int64_t row = __ldg(order + widx);
+  const int64_t beg = __ldg(rowptr + row), end = __ldg(rowptr + row + 1);
+  double acc0[VEC], acc1[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) acc0[e] = acc1[e] = 0.0;
+  for (int64_t k = beg + g; k < end; k += 8 * G) {
+    int32_t col[8];
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const bool ok = k + u * G < end;
+      col[u] = ok ? __ldg(colidx + k + u * G) : 0;
+      v[u] = ok ? __ldg(vals + k + u * G) : 0.0;
+    }
+    double x[8][VEC];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      if (active && k + u * G < end)
+        ldx_vec<VEC>(Xc + (int64_t)col[u] * ldx, x[u]);
+      else
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) x[u][e] = 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; u += 2)
+#pragma unroll
+      for (int e = 0; e < VEC; ++e) {
+        acc0[e] = fma(v[u], x[u][e], acc0[e]);
+        acc1[e] = fma(v[u + 1], x[u + 1][e], acc1[e]);
+      }
+  }
+  double r[VEC];
+#pragma unroll
+  for (int e = 0; e < VEC; ++e) {
+    r[e] = acc0[e] + acc1[e];
+#pragma unroll
+    for (int o = L; o < 32; o <<= 1) r[e] += __shfl_xor_sync(0xffffffffu, r[e], o);
+  }
+  if (g == 0 && active) {
+    if constexpr (VEC == 2) {
+      *reinterpret_cast<double2*>(Y + row * ldy + c) = make_double2(r[0], r[1]);
+    } else {
+      Y[row * ldy + c] = r[0];
+    }
+  }
+}
+
 // Long rows: one CTA per segment of <= kSeg nonzeros; 256/L groups strided
 // over the segment (adjacent groups read adjacent nonzeros), fixed-order
 // shared-memory reduction of the groups; a row split into several segments
 // writes one partial per segment, summed in segment order by the fix-up.
 template <int L, int VEC>
-__global__ void __launch_bounds__(256) spmm_long_kernel(
+__device__ __forceinline__ void spmm_long_dev(
     const int64_t* __restrict__ seg_row, const int64_t* __restrict__ seg_beg,
     const int64_t* __restrict__ seg_end, const int32_t* __restrict__ seg_slot,
     const int32_t* __restrict__ colidx, const double* __restrict__ vals,
     const double* __restrict__ X, int64_t ldx, double* __restrict__ Y, int64_t ldy, int w,
-    double* __restrict__ part) {
+    double* __restrict__ part, int64_t bidx) {
   constexpr int G = 256 / L, CW = L * VEC;
   __shared__ double red[G][CW + 1];
   const int g = threadIdx.x / L, c = (threadIdx.x % L) * VEC;
-  const int64_t s = blockIdx.x;
+  const int64_t s = bidx;
   const int64_t beg = seg_beg[s], end = seg_end[s];
   const bool active = c < w;
   const double* Xc = X + c;
@@ -152,6 +220,27 @@ __global__ void __launch_bounds__(256) spmm_long_kernel(
   }
 }
 
+// One launch for all three row classes so their tails overlap: the heaviest
+// units (long-row segments) are scheduled first, then medium rows (one warp
+// each), then short rows (sub-warp groups).
+template <int L, int VEC>
+__global__ void __launch_bounds__(256) spmm_kernel(Csr A, const double* __restrict__ X,
+                                                   int64_t ldx, double* __restrict__ Y,
+                                                   int64_t ldy, int w, double* __restrict__ part,
+                                                   int64_t nb_long, int64_t nb_med) {
+  const int64_t b = blockIdx.x;
+  if (b < nb_long) {
+    spmm_long_dev<L, VEC>(A.seg_row, A.seg_beg, A.seg_end, A.seg_slot, A.colidx, A.vals, X, ldx,
+                          Y, ldy, w, part, b);
+  } else if (b < nb_long + nb_med) {
+    spmm_medium_dev<L, VEC>(A.rowptr, A.colidx, A.vals, X, ldx, Y, ldy, A.med_rows, A.nmed, w,
+                            b - nb_long);
+  } else {
+    spmm_short_dev<L, VEC>(A.rowptr, A.colidx, A.vals, X, ldx, Y, ldy, A.short_rows, A.nshort,
+                           w, b - nb_long - nb_med);
+  }
+}
+
 __global__ void spmm_fixup_kernel(const int64_t* __restrict__ split_row,
                                   const int32_t* __restrict__ split_first,
                                   const int32_t* __restrict__ split_count,
@@ -172,15 +261,13 @@ static void spmm_dispatch(const Csr& A, const double* X, int64_t ldx, double* Y,
                           int w, double* part, cudaStream_t st) {
   constexpr int RPW = 32 / L;
   const int64_t rows_per_block = 8 * RPW;
-  const int64_t blocks = (A.rows + rows_per_block - 1) / rows_per_block;
+  const int64_t nb_short = (A.nshort + rows_per_block - 1) / rows_per_block;
+  const int64_t nb_med = (A.nmed + 7) / 8;
+  const int64_t nb_long = A.nseg;
+  const int64_t blocks = nb_short + nb_med + nb_long;
   if (blocks > 0) {
-    spmm_short_kernel<L, VEC><<<(unsigned)blocks, 256, 0, st>>>(A.rowptr, A.colidx, A.vals, X,
-                                                                 ldx, Y, ldy, A.rows, w);
-    TSVD_CHECK_LAUNCH();
-  }
-  if (A.nseg > 0) {
-    spmm_long_kernel<L, VEC><<<(unsigned)A.nseg, 256, 0, st>>>(
-        A.seg_row, A.seg_beg, A.seg_end, A.seg_slot, A.colidx, A.vals, X, ldx, Y, ldy, w, part);
+    spmm_kernel<L, VEC><<<(unsigned)blocks, 256, 0, st>>>(A, X, ldx, Y, ldy, w, part, nb_long,
+                                                           nb_med);
     TSVD_CHECK_LAUNCH();
   }
   if (A.nsplit > 0) {
@@ -233,7 +320,7 @@ void csr_build_plan(Csr& A, const int64_t* hrp, cudaStream_t st) {
   int32_t slots = 0;
   for (int64_t i = 0; i < A.rows; ++i) {
     const int64_t len = hrp[i + 1] - hrp[i];
-    if (len <= kLongRow) continue;
+    if (len <= kMedRow) continue;
     const int64_t nseg = (len + kSeg - 1) / kSeg;
     if (nseg > 1) {
       sprow.push_back(i);
@@ -250,6 +337,30 @@ void csr_build_plan(Csr& A, const int64_t* hrp, cudaStream_t st) {
   A.nseg = (int64_t)srow.size();
   A.nsplit = (int64_t)sprow.size();
   A.nslots = slots;
+  // short rows, counting-sorted by decreasing length (stable in the row index)
+  std::vector<int64_t> cnt(kLongRow + 2, 0);
+  for (int64_t i = 0; i < A.rows; ++i) {
+    const int64_t len = hrp[i + 1] - hrp[i];
+    if (len <= kLongRow) ++cnt[kLongRow - len + 1];
+  }
+  for (int k = 1; k <= kLongRow + 1; ++k) cnt[k] += cnt[k - 1];
+  std::vector<int32_t> order(cnt[kLongRow + 1]);
+  for (int64_t i = 0; i < A.rows; ++i) {
+    const int64_t len = hrp[i + 1] - hrp[i];
+    if (len <= kLongRow) order[cnt[kLongRow - len]++] = (int32_t)i;
+  }
+  A.nshort = (int64_t)order.size();
+  // medium rows by decreasing length
+  std::vector<std::pair<int64_t, int32_t>> med;
+  for (int64_t i = 0; i < A.rows; ++i) {
+    const int64_t len = hrp[i + 1] - hrp[i];
+    if (len > kLongRow && len <= kMedRow) med.push_back({-len, (int32_t)i});
+  }
+  std::stable_sort(med.begin(), med.end(),
+                   [](const auto& a, const auto& b) { return a.first < b.first; });
+  std::vector<int32_t> morder(med.size());
+  for (size_t k = 0; k < med.size(); ++k) morder[k] = med[k].second;
+  A.nmed = (int64_t)morder.size();
   auto up64 = [&](std::vector<int64_t>& v, int64_t** d) {
     if (v.empty()) return;
     TSVD_CUDA(cudaMalloc(d, v.size() * sizeof(int64_t)));
@@ -267,6 +378,8 @@ void csr_build_plan(Csr& A, const int64_t* hrp, cudaStream_t st) {
   up64(sprow, &A.split_row);
   up32(spfirst, &A.split_first);
   up32(spcnt, &A.split_count);
+  up32(order, &A.short_rows);
+  up32(morder, &A.med_rows);
   TSVD_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -281,6 +394,8 @@ void csr_free(Csr& A) {
   cudaFree(A.split_row);
   cudaFree(A.split_first);
   cudaFree(A.split_count);
+  cudaFree(A.short_rows);
+  cudaFree(A.med_rows);
   A = Csr{};
 }
 

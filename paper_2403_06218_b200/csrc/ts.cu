@@ -304,11 +304,12 @@ constexpr int NN_KC = 32;
 
 template <int WP>
 struct NnCfg {
+  static constexpr int KC = NN_KC;  // K chunk per stage
   static constexpr int S = (WP == 32) ? 3 : 2;
   static constexpr int PER_SM = (WP >= 32) ? 1 : 2;
   static constexpr int NACC = (WP == 64) ? 1 : 2;  // even/odd accumulator sets
-  static constexpr int XP = NN_KC + 4, HP = WP + 4, OP = WP + 4, NT = WP / 8;
-  static constexpr size_t stage = (size_t)NN_R * XP + (size_t)NN_KC * HP;
+  static constexpr int XP = KC + 4, HP = WP + 4, OP = WP + 4, NT = WP / 8;
+  static constexpr size_t stage = (size_t)NN_R * XP + (size_t)KC * HP;
   static constexpr size_t bytes =
       sizeof(double) * (S * stage + (size_t)NN_R * OP + (size_t)WP * WP);
 };
@@ -346,7 +347,8 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
   const int64_t ntiles = (q + NN_R - 1) / NN_R;
   const int64_t my_tiles =
       (ntiles > (int64_t)blockIdx.x) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int nk = s > 0 ? (s + NN_KC - 1) / NN_KC : 1;
+  constexpr int KC = CF::KC;
+  const int nk = s > 0 ? (s + KC - 1) / KC : 1;
   const int64_t nsteps = my_tiles * nk;
   auto Xs = [&](int st) { return sm + (size_t)st * CF::stage; };
   auto Hs = [&](int st) { return sm + (size_t)st * CF::stage + NN_R * XP; };
@@ -356,8 +358,8 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
       const int64_t lt = j / nk;
       const int kc = (int)(j % nk);
       const int64_t r0 = (blockIdx.x + lt * gridDim.x) * NN_R;
-      load_tile<NN_R, NN_KC, XP, VEC, 256>(Xs(st), X, ldx, r0, q, kc * NN_KC, s, dummy);
-      load_tile<NN_KC, WP, HP, VEC, 256>(Hs(st), H, ldh, kc * NN_KC, s, 0, w, dummy);
+      load_tile<NN_R, KC, XP, VEC, 256>(Xs(st), X, ldx, r0, q, kc * KC, s, dummy);
+      load_tile<KC, WP, HP, VEC, 256>(Hs(st), H, ldh, kc * KC, s, 0, w, dummy);
     }
     cp_commit();
   };
@@ -365,7 +367,7 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
 #pragma unroll
   for (int p = 0; p < PPW; ++p) g[p][0] = g[p][1] = 0.0;
   double acc[NACC][2][NT][2];
-  double ya[kEpiY ? 2 : 1][kEpiY ? KY : 1];
+  double ya[kEpiY ? 2 : 1][kEpiY ? KY : 1], yn[kEpiY ? 2 : 1][kEpiY ? KY : 1];
 #pragma unroll
   for (int j = 0; j < S - 1; ++j) issue(j);
   for (int64_t j = 0; j < nsteps; ++j) {
@@ -382,16 +384,33 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
 #pragma unroll
           for (int ni = 0; ni < NT; ++ni) acc[h][mi][ni][0] = acc[h][mi][ni][1] = 0.0;
     }
-    if (kEpiY && kc == nk - 1) {  // prefetch this tile's Y rows as A-fragments
+    // this tile's Y rows as DMMA A-fragments: loaded before the tile's last K
+    // chunk (nk > 1), or one tile ahead into yn when every step is a tile (nk == 1)
+    auto load_ya = [&](double (&dst)[kEpiY ? 2 : 1][kEpiY ? KY : 1], int64_t rbase) {
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi) {
-        const int64_t row = r0 + warp * 16 + mi * 8 + gid;
+        const int64_t row = rbase + warp * 16 + mi * 8 + gid;
 #pragma unroll
         for (int kk = 0; kk < KY; ++kk) {
           const int col = kk * 4 + tig;
           if constexpr (kEpiY)
-            ya[mi][kk] = (beta != 0.0 && Y && row < q && col < w) ? Y[row * ldy + col] : 0.0;
+            dst[mi][kk] = (beta != 0.0 && Y && row < q && col < w) ? Y[row * ldy + col] : 0.0;
         }
+      }
+    };
+    if (kEpiY && kc == nk - 1) {
+      if (nk > 1) {
+        load_ya(ya, r0);
+      } else {
+        if (j == 0) load_ya(ya, r0);
+        else {
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+            for (int kk = 0; kk < KY; ++kk)
+              if constexpr (kEpiY) ya[mi][kk] = yn[mi][kk];
+        }
+        if (j + 1 < nsteps) load_ya(yn, r0 + (int64_t)gridDim.x * NN_R);
       }
     }
     cp_wait<S - 1>();
@@ -400,7 +419,7 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
       const double* xs = Xs(st);
       const double* hs = Hs(st);
 #pragma unroll
-      for (int kk = 0; kk < NN_KC / 4; ++kk) {
+      for (int kk = 0; kk < KC / 4; ++kk) {
         const int h = (NACC == 2) ? (kk & 1) : 0;
         const double a0 = xs[(warp * 16 + gid) * XP + kk * 4 + tig];
         const double a1 = xs[(warp * 16 + 8 + gid) * XP + kk * 4 + tig];

@@ -94,6 +94,20 @@ def sweep_bench():
               f"nn {ms_nn:.3f} ms {gnn:5.0f} GB/s ({gnn / HBM:.2f})", flush=True)
 
 
+def nn0_bench():
+    """single s=0 and s=384 gemm_nn launches (for ncu)"""
+    q, w = 1_000_000, 16
+    X = torch.randn((q, 400), dtype=torch.float64, device="cuda")
+    H = torch.randn((400, w), dtype=torch.float64, device="cuda")
+    Z = torch.randn((q, w), dtype=torch.float64, device="cuda")
+    Tm = torch.triu(torch.randn((w, w), dtype=torch.float64, device="cuda"))
+    G = torch.empty((148 * 2, w, w), dtype=torch.float64, device="cuda")
+    L = T.lib()
+    for s in (0, 384):
+        L.tsvd_dbg_gemm_nn(X.data_ptr(), 400, H.data_ptr(), w, Z.data_ptr(), w, q, s, w, -1.0, 1.0, None)
+    torch.cuda.synchronize()
+
+
 def spmm_bench():
     from tsvd_inputs import powerlaw_csr
     m = n = 1_000_000

@@ -116,6 +116,17 @@ int main() {
     const double fl = 2.0 * 256.0 * 8.0 * iters * (256.0 / 32.0) * blocks;
     printf("{\"dmma_tflops\": %.2f}\n", fl / (ms * 1e-3) / 1e12);
   }
+  for (int bps : {1, 2, 4}) {  // DMMA throughput vs resident warps per SM
+    const int iters = 20000, blocks = sms * bps;
+    dmma_loop<<<blocks, 256>>>(out, 100);
+    cudaEventRecord(a);
+    dmma_loop<<<blocks, 256>>>(out, iters);
+    cudaEventRecord(b);
+    CK(cudaEventSynchronize(b));
+    cudaEventElapsedTime(&ms, a, b);
+    const double fl = 2.0 * 256.0 * 8.0 * iters * (256.0 / 32.0) * blocks;
+    printf("{\"dmma_tflops_warps_per_sm_%d\": %.2f}\n", 8 * bps, fl / (ms * 1e-3) / 1e12);
+  }
   {
     const int iters = 20000, blocks = sms * 8;
     mixed_loop<<<blocks, 256>>>(out, 100);
