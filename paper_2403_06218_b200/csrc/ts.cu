@@ -304,14 +304,16 @@ constexpr int NN_KC = 32;
 
 template <int WP>
 struct NnCfg {
-  static constexpr int KC = NN_KC;  // K chunk per stage
+  static constexpr int KC = NN_KC;
   static constexpr int S = (WP == 32) ? 3 : 2;
   static constexpr int PER_SM = (WP >= 32) ? 1 : 2;
+  static constexpr bool OS_ALIAS = false;  // out tile aliasing the consumed stage: slower
   static constexpr int NACC = (WP == 64) ? 1 : 2;  // even/odd accumulator sets
   static constexpr int XP = KC + 4, HP = WP + 4, OP = WP + 4, NT = WP / 8;
   static constexpr size_t stage = (size_t)NN_R * XP + (size_t)KC * HP;
   static constexpr size_t bytes =
-      sizeof(double) * (S * stage + (size_t)NN_R * OP + (size_t)WP * WP);
+      sizeof(double) * (S * stage + (OS_ALIAS ? 0 : (size_t)NN_R * OP) + (size_t)WP * WP);
+  static_assert(!OS_ALIAS || (size_t)NN_R * OP <= (size_t)NN_R * XP, "out tile must fit a stage");
 };
 
 static int wp_of(int w) { return w <= 8 ? 8 : (w <= 16 ? 16 : (w <= 32 ? 32 : 64)); }
@@ -333,10 +335,14 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
   using CF = NnCfg<WP>;
   constexpr int S = CF::S, XP = CF::XP, HP = CF::HP, OP = CF::OP, NT = CF::NT;
   constexpr int NPAIR = NT * NT, PPW = (NPAIR + 7) / 8, KY = WP / 4, NACC = CF::NACC;
+  // Gram schedule: with fewer 8x8 output pairs than warps, KSPLIT warps share a
+  // pair and each takes a contiguous K (row) range; two accumulators per chain
+  constexpr int KSPLIT = (NPAIR >= 8) ? 1 : 8 / NPAIR;
+  constexpr int KSTEPS = NN_R / 4 / KSPLIT;
   constexpr bool kEpiY = WP != 64;  // the WP = 64 variant serves beta = 0 products only
   extern __shared__ __align__(16) double sm[];
-  double* Os = sm + S * CF::stage;
-  double* Ts = Os + NN_R * OP;
+  double* Os = sm + S * CF::stage;  // (OS_ALIAS: re-pointed at the consumed stage)
+  double* Ts = CF::OS_ALIAS ? Os : Os + NN_R * OP;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const double* dummy = X ? X : (H ? H : Y);
@@ -363,9 +369,9 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
     }
     cp_commit();
   };
-  double g[PPW][2];
+  double g[PPW][2][2];
 #pragma unroll
-  for (int p = 0; p < PPW; ++p) g[p][0] = g[p][1] = 0.0;
+  for (int p = 0; p < PPW; ++p) g[p][0][0] = g[p][0][1] = g[p][1][0] = g[p][1][1] = 0.0;
   double acc[NACC][2][NT][2];
   double ya[kEpiY ? 2 : 1][kEpiY ? KY : 1], yn[kEpiY ? 2 : 1][kEpiY ? KY : 1];
 #pragma unroll
@@ -433,6 +439,10 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
     }
     if (kc == nk - 1) {
       // epilogue: Z = alpha*acc + beta*(Y T)
+      if constexpr (CF::OS_ALIAS) {
+        Os = Xs(st);
+        __syncthreads();  // every warp is done reading stage st
+      }
       double yt[kEpiY ? 2 : 1][kEpiY ? NT : 1][2];
 #pragma unroll
       for (int mi = 0; mi < (kEpiY ? 2 : 1); ++mi)
@@ -471,14 +481,16 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
       if (gram) {
 #pragma unroll
         for (int p = 0; p < PPW; ++p) {
-          const int pair = warp + 8 * p;
+          const int pair = (KSPLIT > 1) ? (warp % NPAIR) : (warp + 8 * p);
+          const int k0 = (KSPLIT > 1) ? (warp / NPAIR) * KSTEPS : 0;
           if (pair < NPAIR) {
             const int mi = pair / NT, ni = pair % NT;
 #pragma unroll 8
-            for (int kk = 0; kk < NN_R / 4; ++kk) {
-              const double a = Os[(kk * 4 + tig) * OP + mi * 8 + gid];  // (Z^T)[i][k]
-              const double b = Os[(kk * 4 + tig) * OP + ni * 8 + gid];
-              dmma884(g[p][0], g[p][1], a, b);
+            for (int kk = 0; kk < KSTEPS; ++kk) {
+              const int kr = (k0 + kk) * 4 + tig;
+              const double a = Os[kr * OP + mi * 8 + gid];  // (Z^T)[i][k]
+              const double b = Os[kr * OP + ni * 8 + gid];
+              dmma884(g[p][kk & 1][0], g[p][kk & 1][1], a, b);
             }
           }
         }
@@ -488,16 +500,34 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
   }
   cp_wait<0>();
   if (gram) {
+    if constexpr (KSPLIT == 1) {
 #pragma unroll
-    for (int p = 0; p < PPW; ++p) {
-      const int pair = warp + 8 * p;
-      if (pair < NPAIR) {
-        const int mi = pair / NT, ni = pair % NT;
+      for (int p = 0; p < PPW; ++p) {
+        const int pair = warp + 8 * p;
+        if (pair < NPAIR) {
+          const int mi = pair / NT, ni = pair % NT;
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int i = mi * 8 + gid, j = ni * 8 + 2 * tig + e;
-          if (i < w && j < w) gram[(int64_t)blockIdx.x * w * w + i * w + j] = g[p][e];
+          for (int e = 0; e < 2; ++e) {
+            const int i = mi * 8 + gid, j = ni * 8 + 2 * tig + e;
+            if (i < w && j < w)
+              gram[(int64_t)blockIdx.x * w * w + i * w + j] = g[p][0][e] + g[p][1][e];
+          }
         }
+      }
+    } else {
+      // the KSPLIT warps of a pair are summed in warp order (stage 0 is idle now)
+      double* red = sm;
+      __syncthreads();
+#pragma unroll
+      for (int e = 0; e < 2; ++e) red[warp * 64 + gid * 8 + 2 * tig + e] = g[0][0][e] + g[0][1][e];
+      __syncthreads();
+      for (int idx = tid; idx < NPAIR * 64; idx += 256) {
+        const int pair = idx / 64, ii = (idx % 64) / 8, jj = idx % 8;
+        double sum = 0.0;
+        for (int k = 0; k < KSPLIT; ++k) sum += red[(k * NPAIR + pair) * 64 + ii * 8 + jj];
+        const int mi = pair / NT, ni = pair % NT;
+        const int i = mi * 8 + ii, j = ni * 8 + jj;
+        if (i < w && j < w) gram[(int64_t)blockIdx.x * w * w + i * w + j] = sum;
       }
     }
   }
