@@ -51,6 +51,7 @@ enum {
   TSVD_ESHAPE = -2,      /* m < n, r > n, d % b != 0, r > d, r + p > n ...     */
   TSVD_ENOMEM = -3,      /* device allocation failed                            */
   TSVD_ECUDA = -4,       /* CUDA runtime error / no usable device               */
+  TSVD_ENCCL = -5,       /* NCCL missing or failed (multi-GPU handles)          */
   TSVD_ESTATE = -6       /* e.g. tsvd_get before a successful solve             */
 };
 
@@ -74,6 +75,37 @@ tsvd_status tsvd_create_csr(tsvd_t* h, int64_t m, int64_t n, int64_t nnz,
  * stored row-major on the device. */
 tsvd_status tsvd_create_dense(tsvd_t* h, int64_t m, int64_t n, const double* A,
                               int64_t lda, int layout, int mem_kind);
+
+/* ---- multi-GPU (row-partitioned) creation, SURVEY 8(e) ---------------------
+ * One process per GPU.  Rank g owns rows [row_begin, row_end) of A (the
+ * caller chooses them, e.g. balanced by nnz: tsvd_partition_rows) and the
+ * n-shard [g*ns, min(n, (g+1)*ns)) of every n-side vector, ns = ceil(n/world).
+ * The ranks share a 128-byte ncclUniqueId created by one of them with
+ * tsvd_nccl_unique_id and broadcast by the harness (torch.distributed).
+ * Per Lanczos block step the ranks exchange: a reduce-scatter of A_g^T Qbar_i,
+ * an all-gather of Q_i, and all-reduces of the b x b / s x b projections and
+ * Gram matrices; B_k, its SVD, rho and the restart are replicated.
+ * tsvd_get then returns this rank's rows of U (row_end-row_begin) and its
+ * n-shard of V.  All ranks must call every solver entry point collectively. */
+typedef struct {
+  int rank, world;
+  const void* nccl_id;        /* 128 bytes, identical on all ranks */
+  int64_t m_global, n_global; /* sizes of the whole A, m >= n */
+  int64_t row_begin, row_end; /* this rank's rows of A */
+} tsvd_dist;
+/* rowptr/colidx/vals: this rank's rows only (local rowptr starting at 0,
+ * GLOBAL column indices). */
+tsvd_status tsvd_create_csr_dist(tsvd_t* h, const tsvd_dist* dist, int64_t nnz_local,
+                                 const int64_t* rowptr, const int32_t* colidx,
+                                 const double* vals, int mem_kind);
+/* A: this rank's (row_end - row_begin) x n_global rows, row-major, lda >= n. */
+tsvd_status tsvd_create_dense_dist(tsvd_t* h, const tsvd_dist* dist, const double* A,
+                                   int64_t lda, int mem_kind);
+/* Fill out128 with a fresh ncclUniqueId (TSVD_ENCCL if NCCL is unavailable). */
+tsvd_status tsvd_nccl_unique_id(void* out128);
+/* Row split of a CSR row pointer (host) into `world` contiguous ranges with
+ * (nearly) equal nonzeros: bounds[0] = 0 ... bounds[world] = m. */
+tsvd_status tsvd_partition_rows(const int64_t* rowptr, int64_t m, int world, int64_t* bounds);
 
 /* ---- options ----------------------------------------------------------- */
 /* cudaStream_t to order all work on (e.g. torch.cuda.current_stream()).

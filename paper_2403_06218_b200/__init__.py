@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtsvd.so")
 
 TSVD_OK, TSVD_WARN_NOTCONV = 0, 1
-TSVD_EINVAL, TSVD_ESHAPE, TSVD_ENOMEM, TSVD_ECUDA, TSVD_ESTATE = -1, -2, -3, -4, -6
+TSVD_EINVAL, TSVD_ESHAPE, TSVD_ENOMEM, TSVD_ECUDA, TSVD_ENCCL, TSVD_ESTATE = -1, -2, -3, -4, -5, -6
 TSVD_HOST, TSVD_DEVICE = 0, 1
 TSVD_ROW_MAJOR, TSVD_COL_MAJOR = 0, 1
 
@@ -34,6 +34,8 @@ EXPORTS = [
     "tsvd_dbg_apply", "tsvd_dbg_cholqr2", "tsvd_dbg_cgs_cqr2", "tsvd_dbg_cgs_qr",
     "tsvd_dbg_small_svd", "tsvd_dbg_gemm_tn", "tsvd_dbg_gemm_nn",
     "tsvd_set_profiling", "tsvd_get_profile", "tsvd_reset_profile",
+    "tsvd_create_csr_dist", "tsvd_create_dense_dist", "tsvd_nccl_unique_id",
+    "tsvd_partition_rows",
 ]
 
 
@@ -41,6 +43,12 @@ class TsvdInfo(C.Structure):
     _fields_ = [("cycles", C.c_int), ("nconv", C.c_int), ("r", C.c_int), ("d", C.c_int),
                 ("b", C.c_int), ("breakdowns", C.c_int), ("rho_max", C.c_double),
                 ("sigma1", C.c_double), ("ms_total", C.c_double), ("launches", C.c_int64)]
+
+
+class TsvdDist(C.Structure):
+    _fields_ = [("rank", C.c_int), ("world", C.c_int), ("nccl_id", C.c_void_p),
+                ("m_global", C.c_int64), ("n_global", C.c_int64),
+                ("row_begin", C.c_int64), ("row_end", C.c_int64)]
 
 
 class TsvdProfEntry(C.Structure):
@@ -88,6 +96,10 @@ _SIGS = {
     "tsvd_set_profiling": [vp, i32],
     "tsvd_get_profile": [vp, C.POINTER(TsvdProfEntry)],
     "tsvd_reset_profile": [vp],
+    "tsvd_create_csr_dist": [C.POINTER(vp), C.POINTER(TsvdDist), i64, vp, vp, vp, i32],
+    "tsvd_create_dense_dist": [C.POINTER(vp), C.POINTER(TsvdDist), vp, i64, i32],
+    "tsvd_nccl_unique_id": [vp],
+    "tsvd_partition_rows": [vp, i64, i32, vp],
 }
 
 
@@ -166,9 +178,45 @@ class TruncatedSVD:
     into library-owned device memory.
     """
 
-    def __init__(self, A=None, *, csr=None, shape=None, stream="current"):
+    def __init__(self, A=None, *, csr=None, shape=None, stream="current", dist=None):
+        """dist (multi-GPU row partition, include/tsvd.h tsvd_dist): dict with
+        rank, world, nccl_id (128 bytes), m_global, n_global, row_begin,
+        row_end; A / csr then hold this rank's rows only (global columns)."""
         L = lib()
         h = vp()
+        if dist is not None:
+            self._id_buf = C.create_string_buffer(bytes(dist["nccl_id"]), 128)
+            dd = TsvdDist(int(dist["rank"]), int(dist["world"]),
+                          C.cast(self._id_buf, C.c_void_p).value, int(dist["m_global"]),
+                          int(dist["n_global"]), int(dist["row_begin"]), int(dist["row_end"]))
+            mloc = int(dist["row_end"]) - int(dist["row_begin"])
+            ng = int(dist["n_global"])
+            nsh = -(-ng // int(dist["world"]))
+            n0 = min(ng, int(dist["rank"]) * nsh)
+            if A is not None:
+                p, kind, keep = _ptr(A, np.float64)
+                _check(L.tsvd_create_dense_dist(C.byref(h), C.byref(dd), p, ng, kind),
+                       "tsvd_create_dense_dist")
+            else:
+                rowptr, colidx, vals = csr
+                prp, kind, k1 = _ptr(rowptr, np.int64)
+                pci, _, k2 = _ptr(colidx, np.int32)
+                pva, _, k3 = _ptr(vals, np.float64)
+                _check(L.tsvd_create_csr_dist(C.byref(h), C.byref(dd), int(vals.shape[0]), prp,
+                                              pci, pva, kind), "tsvd_create_csr_dist")
+            self._h = h
+            self.m, self.n = mloc, min(ng, n0 + nsh) - n0
+            self.r = None
+            if stream == "current":
+                try:
+                    import torch
+                    if torch.cuda.is_available():
+                        self.set_stream(torch.cuda.current_stream().cuda_stream)
+                except ImportError:
+                    pass
+            elif stream is not None:
+                self.set_stream(stream)
+            return
         if A is not None:
             if len(A.shape) != 2:
                 raise ValueError("A must be 2-D")
@@ -306,6 +354,22 @@ class TruncatedSVD:
 
     def __exit__(self, *a):
         self.close()
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (rank 0 creates it, the harness broadcasts it)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().tsvd_nccl_unique_id(buf), "tsvd_nccl_unique_id")
+    return buf.raw
+
+
+def partition_rows(rowptr, world: int) -> np.ndarray:
+    """nnz-balanced contiguous row split (tsvd_partition_rows): bounds[world+1]."""
+    rp = np.ascontiguousarray(rowptr, dtype=np.int64)
+    out = np.empty(world + 1, dtype=np.int64)
+    _check(lib().tsvd_partition_rows(rp.ctypes.data, len(rp) - 1, int(world), out.ctypes.data),
+           "tsvd_partition_rows")
+    return out
 
 
 # --------------------------------------------------- single-kernel entries --

@@ -123,12 +123,21 @@ static void clear_flags(Ctx& c) {
   TSVD_CUDA(cudaMemsetAsync(c.dflags, 0, 4 * sizeof(int), c.st));
 }
 
+// Row-sharded reductions: every X^T Y or Gram computed on this
+// rank's rows is a partial sum over the row partition; it is all-reduced
+// before use so all ranks continue with identical small matrices.
+static void reduce_gram(Ctx& c, const double* gram, int np, int w, double* Wred) {
+  reduce_partials(gram, np, (int64_t)w * w, Wred, c.st);
+  allreduce_sum(c, Wred, (size_t)w * w);
+}
+
 // TRSM Q = Y L^{-T} (Alg. 4 S3/S6, Alg. 5 S5/S10) is applied as the product
 // Y T with T = L^{-T} formed by the Cholesky finaliser (reading R30).
 int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
   if (w > 32) throw Error{TSVD_EINVAL, "cholqr2: block wider than 32"};
   double* S = scratch(c, q);
   double* gram = gram_buf(c, q);
+  double* Wred = dbuf(c, "Wred", 32 * 32);
   double* L1 = dbuf(c, "L1", 32 * 32);
   double* T1 = dbuf(c, "T1", 32 * 32);
   double* L2 = dbuf(c, "L2", 32 * 32);
@@ -141,7 +150,8 @@ int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
   }
   {
     Prof p(c, P_SMALL, 0, 0);
-    chol_finalize(gram, np, w, dbuf(c, "Wred", 32 * 32), L1, T1, c.dflags + 0, c.st);                     // S2
+    reduce_gram(c, gram, np, w, Wred);
+    chol_from_w(Wred, w, L1, T1, c.dflags + 0, c.st);                            // S2
   }
   {  // S3 + S4: S = Y L^{-T}, Wbar = S^T S
     Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 3.0 * q * w * w);
@@ -149,7 +159,8 @@ int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
   }
   {
     Prof p(c, P_SMALL, 0, 0);
-    chol2_finalize(gram, np, w, dbuf(c, "Wred", 32 * 32), L1, L2, T2, R, nullptr, nullptr, 0, c.dflags + 1, c.st);  // S5, S7
+    reduce_gram(c, gram, np, w, Wred);
+    chol2_from_w(Wred, w, L1, L2, T2, R, nullptr, nullptr, 0, c.dflags + 1, c.st);   // S5, S7
   }
   if (read_flags(c)) {
     Prof p(c, P_OTHER, 0, 0);
@@ -171,6 +182,7 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
   double* S = scratch(c, q);
   double* gram = gram_buf(c, q);
   double* part = part_tn(c, q, s);
+  double* Wred = dbuf(c, "Wred", 32 * 32);
   double* L1 = dbuf(c, "L1", 32 * 32);
   double* T1 = dbuf(c, "T1", 32 * 32);
   double* L2 = dbuf(c, "L2", 32 * 32);
@@ -182,6 +194,7 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
   {
     Prof p(c, P_TN, tn_bytes(q, s, w), fl);
     gemm_tn(basis, ld, Y, ld, q, s, w, H, w, part, c.st);                             // S1
+    allreduce_sum(c, H, (size_t)s * w);
   }
   {
     Prof p(c, P_NN, nn_bytes(q, s, w, true, true), fl + 2.0 * q * w * w);
@@ -189,7 +202,8 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
   }
   {
     Prof p(c, P_SMALL, 0, 0);
-    chol_finalize(gram, np, w, dbuf(c, "Wred", 32 * 32), L1, T1, c.dflags + 0, c.st);                           // S4
+    reduce_gram(c, gram, np, w, Wred);
+    chol_from_w(Wred, w, L1, T1, c.dflags + 0, c.st);                                 // S4
   }
   {
     Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 1.0 * q * w * w);
@@ -198,6 +212,7 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
   {
     Prof p(c, P_TN, tn_bytes(q, s, w), fl);
     gemm_tn(basis, ld, S, w, q, s, w, Hbar, w, part, c.st);                           // S6
+    allreduce_sum(c, Hbar, (size_t)s * w);
   }
   {
     Prof p(c, P_NN, nn_bytes(q, s, w, true, true), fl + 2.0 * q * w * w);
@@ -205,7 +220,8 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
   }
   {
     Prof p(c, P_SMALL, 0, 0);
-    chol2_finalize(gram, np, w, dbuf(c, "Wred", 32 * 32), L1, L2, T2, R, H, Hbar, s, c.dflags + 1, c.st);       // S9,S11,S12
+    reduce_gram(c, gram, np, w, Wred);
+    chol2_from_w(Wred, w, L1, L2, T2, R, H, Hbar, s, c.dflags + 1, c.st);            // S9,S11,S12
   }
   if (read_flags(c)) {
     Prof p(c, P_OTHER, 0, 0);
@@ -221,7 +237,9 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
 
 // Column-wise CGS with reorthogonalisation against [P, Q_<j] (
 // reading R16).  Y = columns [s, s+w) of basis is processed in place; H (s x w)
-// and R (w x w) receive the coefficients.
+// and R (w x w) receive the coefficients.  Replacement columns are rows
+// [cur_row0, cur_row0 + q) of a cur_qtot-row Philox column, so every rank of a
+// row partition draws its own rows of the same global vector.
 void cgs2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H, double* R) {
   const double tau = 1e-13;
   double* S = dbuf(c, "cgs2_col", (size_t)q);
@@ -233,35 +251,44 @@ void cgs2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H,
   double* sc = dbuf(c, "cgs2_sc", 8);  // [0] |y_orig|^2, [1] |y''|^2, [2] nrm
   double* part = part_tn(c, q, s + w);
   int* dep = c.dflags + 2;
+  const int64_t row0 = c.cur_row0, qtot = c.cur_qtot > 0 ? c.cur_qtot : q;
+  auto gram1 = [&](double* out) {
+    reduce_partials(gram, np, 1, out, c.st);
+    allreduce_sum(c, out, 1);
+  };
+  auto proj = [&](const double* x, int64_t ldx2, double* cc, int nb) {
+    gemm_tn(basis, ld, x, ldx2, q, nb, 1, cc, 1, part, c.st);
+    allreduce_sum(c, cc, (size_t)nb);
+  };
   fill_zero(R, (int64_t)w * w, c.st);
   for (int j = 0; j < w; ++j) {
     const int nb = s + j;
     double* col = basis + s + j;
     // ||y_orig||^2
     gemm_nn(nullptr, 0, nullptr, 0, col, ld, nullptr, nullptr, 0, q, 0, 1, 0.0, 1.0, gram, c.st);
-    reduce_partials(gram, np, 1, sc + 0, c.st);
+    gram1(sc + 0);
     if (nb > 0) {
-      gemm_tn(basis, ld, col, ld, q, nb, 1, c1, 1, part, c.st);
+      proj(col, ld, c1, nb);
       gemm_nn(basis, ld, c1, 1, col, ld, nullptr, S, 1, q, nb, 1, -1.0, 1.0, nullptr, c.st);
-      gemm_tn(basis, ld, S, 1, q, nb, 1, c2, 1, part, c.st);
+      proj(S, 1, c2, nb);
       gemm_nn(basis, ld, c2, 1, S, 1, nullptr, S, 1, q, nb, 1, -1.0, 1.0, gram, c.st);
     } else {
       gemm_nn(nullptr, 0, nullptr, 0, col, ld, nullptr, S, 1, q, 0, 1, 0.0, 1.0, gram, c.st);
     }
-    reduce_partials(gram, np, 1, sc + 1, c.st);
+    gram1(sc + 1);
     cgs2_col_finalize(c1, c2, nb, sc + 1, sc + 0, tau, coef, sc + 2, dep, c.st);
     int hdep = 0;
     TSVD_CUDA(cudaMemcpyAsync(&hdep, dep, sizeof(int), cudaMemcpyDeviceToHost, c.st));
     TSVD_CUDA(cudaStreamSynchronize(c.st));
     if (hdep) {
       // replacement column: next Philox draw, orthogonalised twice
-      launch_philox_normal(S, q, 1, 1, c.seed, c.draw_next++, 0, q, c.st);
+      launch_philox_normal(S, q, 1, 1, c.seed, c.draw_next++, row0, qtot, c.st);
       for (int it = 0; it < 2 && nb > 0; ++it) {
-        gemm_tn(basis, ld, S, 1, q, nb, 1, c2, 1, part, c.st);
+        proj(S, 1, c2, nb);
         gemm_nn(basis, ld, c2, 1, S, 1, nullptr, S, 1, q, nb, 1, -1.0, 1.0, nullptr, c.st);
       }
       gemm_nn(nullptr, 0, nullptr, 0, S, 1, nullptr, nullptr, 0, q, 0, 1, 0.0, 1.0, gram, c.st);
-      reduce_partials(gram, np, 1, sc + 1, c.st);
+      gram1(sc + 1);
       cgs2_col_finalize(c1, c1, 0, sc + 1, sc + 1, 0.0, coef + nb, sc + 2, dep, c.st);
       ++c.breakdowns;
     } else {
@@ -294,22 +321,57 @@ int cgs_qr(Ctx& c, double* Y, int64_t q, int l, int64_t ld, int bq, double* R) {
   return bd;
 }
 
-void apply(Ctx& c, bool trans, const double* X, int64_t ldx, double* Y, int64_t ldy, int w) {
-  const double rows = trans ? (double)c.n : (double)c.m, cols = trans ? (double)c.m : (double)c.n;
-  const double bytes = c.dense ? 8.0 * ((double)c.m * c.n + w * (rows + cols))
+// Products with A on this rank's rows (Alg. 1 S1/S3, Alg. 2 S2/S4).
+//  trans = 0: Y (m_loc x w) = A_g X, X = this rank's n-shard (n_loc x w);
+//             multi-GPU: the n-shards are all-gathered into the full X first.
+//  trans = 1: Y (n_loc x w) = (A^T X)[n-shard], X = this rank's rows (m_loc x w);
+//             multi-GPU: the full-n partial A_g^T X is reduce-scattered.
+static void apply_local(Ctx& c, bool trans, const double* X, int64_t ldx, double* Y,
+                        int64_t ldy, int w) {
+  const double rows = trans ? (double)c.ng : (double)c.m, cols = trans ? (double)c.m : (double)c.ng;
+  const double bytes = c.dense ? 8.0 * ((double)c.m * c.ng + w * (rows + cols))
                                : 12.0 * c.A.nnz + 8.0 * (rows + 1) + 8.0 * w * (rows + cols);
-  const double flops = c.dense ? 2.0 * c.m * c.n * w : 2.0 * c.A.nnz * w;
+  const double flops = c.dense ? 2.0 * c.m * c.ng * w : 2.0 * c.A.nnz * w;
   Prof p(c, trans ? P_APPLY_AT : P_APPLY_A, bytes, flops);
   if (c.dense) {
-    if (!trans)   // Y (m x w) = A X
-      gemm_nn(c.Ad, c.lda, X, ldx, nullptr, 0, nullptr, Y, ldy, c.m, (int)c.n, w, 1.0, 0.0,
+    if (!trans)
+      gemm_nn(c.Ad, c.lda, X, ldx, nullptr, 0, nullptr, Y, ldy, c.m, (int)c.ng, w, 1.0, 0.0,
               nullptr, c.st);
-    else          // Y (n x w) = A^T X
-      gemm_tn(c.Ad, c.lda, X, ldx, c.m, (int)c.n, w, Y, ldy, part_tn(c, c.m, (int)c.n), c.st);
+    else
+      gemm_tn(c.Ad, c.lda, X, ldx, c.m, (int)c.ng, w, Y, ldy, part_tn(c, c.m, (int)c.ng), c.st);
   } else {
     const Csr& A = trans ? c.AT : c.A;
-    double* part = dbuf(c, trans ? "spmm_part_t" : "spmm_part", (size_t)std::max<int64_t>(1, A.nslots) * 32);
+    double* part = dbuf(c, trans ? "spmm_part_t" : "spmm_part",
+                        (size_t)std::max<int64_t>(1, A.nslots) * 32);
     launch_spmm_wide(A, X, ldx, Y, ldy, w, part, c.st);
+  }
+}
+
+void apply(Ctx& c, bool trans, const double* X, int64_t ldx, double* Y, int64_t ldy, int w) {
+  if (!c.comm) {
+    apply_local(c, trans, X, ldx, Y, ldy, w);
+    return;
+  }
+  const int64_t npad = c.nsh * c.world;
+  double* full = dbuf(c, "dist_full", (size_t)npad * w);
+  double* shard = dbuf(c, "dist_shard", (size_t)c.nsh * w);
+  if (!trans) {
+    // all-gather the n-shards of X (zero-padded to nsh rows) into full n
+    fill_zero(shard, c.nsh * w, c.st);
+    copy_block(X, ldx, shard, w, c.n, w, false, c.st);
+    {
+      Prof p(c, P_OTHER, 8.0 * npad * w, 0);
+      all_gather(c, shard, full, (size_t)c.nsh * w);
+    }
+    apply_local(c, false, full, w, Y, ldy, w);
+  } else {
+    fill_zero(full, npad * w, c.st);
+    apply_local(c, true, X, ldx, full, w, w);
+    {
+      Prof p(c, P_OTHER, 8.0 * npad * w, 0);
+      reduce_scatter_sum(c, full, shard, (size_t)c.nsh * w);
+    }
+    copy_block(shard, w, Y, ldy, c.n, w, false, c.st);
   }
 }
 

@@ -47,6 +47,7 @@ static void destroy_ctx(tsvd_ctx* c) {
   cudaFree(c->Ad);
   free_bufs(*c);
   prof_release(*c);
+  comm_destroy(*c);
   cudaFree(c->dflags);
   if (c->hflags) cudaFreeHost(c->hflags);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
@@ -63,6 +64,7 @@ const char* tsvd_strerror(tsvd_status s) {
     case TSVD_ESHAPE: return "invalid shape";
     case TSVD_ENOMEM: return "device out of memory";
     case TSVD_ECUDA: return "CUDA error or no usable device";
+    case TSVD_ENCCL: return "NCCL unavailable or failed";
     case TSVD_ESTATE: return "invalid state (no results yet)";
     default: return "unknown status";
   }
@@ -70,24 +72,11 @@ const char* tsvd_strerror(tsvd_status s) {
 
 const char* tsvd_last_error(void) { return tsvd::g_last_error.c_str(); }
 
-tsvd_status tsvd_create_csr(tsvd_t* h, int64_t m, int64_t n, int64_t nnz,
-                            const int64_t* rowptr, const int32_t* colidx, const double* vals,
-                            int mem_kind) {
-  if (!h || !rowptr || (nnz > 0 && (!colidx || !vals)) || m < 0 || n < 1 || nnz < 0)
-    return TSVD_EINVAL;
-  if (m < n) return TSVD_ESHAPE;
-  if (n >= (int64_t)INT32_MAX || m >= (int64_t)INT32_MAX) return TSVD_ESHAPE;
-  *h = nullptr;
-  tsvd_ctx* c = new tsvd_ctx();
-  TSVD_API_BEGIN
-  tsvd_status s = init_ctx(c);
-  if (s != TSVD_OK) {
-    destroy_ctx(c);
-    return s;
-  }
-  c->m = m;
-  c->n = n;
-  c->dense = false;
+// Build the CSR part of a handle whose local/global geometry is already set:
+// c->m local rows, c->ng columns.  Validates, uploads, transposes, plans.
+static tsvd_status setup_csr(tsvd_ctx* c, int64_t nnz, const int64_t* rowptr,
+                             const int32_t* colidx, const double* vals, int mem_kind) {
+  const int64_t m = c->m, n = c->ng;
   Csr& A = c->A;
   A.rows = m;
   A.cols = n;
@@ -100,22 +89,13 @@ tsvd_status tsvd_create_csr(tsvd_t* h, int64_t m, int64_t n, int64_t nnz,
   } else {
     std::memcpy(hrp.data(), rowptr, (m + 1) * sizeof(int64_t));
     // host-side validation (cheap, exact)
-    if (hrp[0] != 0 || hrp[m] != nnz) {
-      destroy_ctx(c);
-      return TSVD_EINVAL;
-    }
+    if (hrp[0] != 0 || hrp[m] != nnz) return TSVD_EINVAL;
     for (int64_t i = 0; i < m; ++i) {
-      if (hrp[i + 1] < hrp[i]) {
-        destroy_ctx(c);
-        return TSVD_EINVAL;
-      }
+      if (hrp[i + 1] < hrp[i]) return TSVD_EINVAL;
       int64_t prev = -1;
       for (int64_t k = hrp[i]; k < hrp[i + 1]; ++k) {
         const int64_t cj = colidx[k];
-        if (cj <= prev || cj >= n) {
-          destroy_ctx(c);
-          return TSVD_EINVAL;
-        }
+        if (cj <= prev || cj >= n) return TSVD_EINVAL;
         prev = cj;
       }
     }
@@ -129,27 +109,102 @@ tsvd_status tsvd_create_csr(tsvd_t* h, int64_t m, int64_t n, int64_t nnz,
     TSVD_CUDA(cudaMemcpyAsync(A.vals, vals, nnz * sizeof(double), kind, c->st));
   }
   TSVD_CUDA(cudaStreamSynchronize(c->st));
-  if (mem_kind == TSVD_DEVICE && csr_validate_device(A, c->st) != 0) {
-    destroy_ctx(c);
-    return TSVD_EINVAL;
-  }
+  if (mem_kind == TSVD_DEVICE && csr_validate_device(A, c->st) != 0) return TSVD_EINVAL;
   csr_transpose(A, c->AT, c->st);
   csr_build_plan(A, hrp.data(), c->st);
   std::vector<int64_t> hrpt(n + 1);
   TSVD_CUDA(cudaMemcpy(hrpt.data(), c->AT.rowptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
   csr_build_plan(c->AT, hrpt.data(), c->st);
-  *h = c;
   return TSVD_OK;
+}
+
+// Dense rows (c->m x c->ng), row-major lda or (single GPU) column-major.
+static tsvd_status setup_dense(tsvd_ctx* c, const double* Ain, int64_t lda, int layout,
+                               int mem_kind) {
+  const int64_t m = c->m, n = c->ng;
+  c->dense = true;
+  c->lda = n;
+  TSVD_CUDA(cudaMalloc(&c->Ad, (size_t)std::max<int64_t>(1, m) * n * sizeof(double)));
+  const cudaMemcpyKind kind = mem_kind == TSVD_DEVICE ? cudaMemcpyDeviceToDevice
+                                                      : cudaMemcpyHostToDevice;
+  if (layout == TSVD_ROW_MAJOR) {
+    if (m > 0)
+      TSVD_CUDA(cudaMemcpy2DAsync(c->Ad, n * sizeof(double), Ain, lda * sizeof(double),
+                                  n * sizeof(double), m, kind, c->st));
+  } else {
+    // column-major input: upload as an n x m row-major block, transpose on device
+    double* tmp;
+    TSVD_CUDA(cudaMalloc(&tmp, (size_t)m * n * sizeof(double)));
+    TSVD_CUDA(cudaMemcpy2DAsync(tmp, m * sizeof(double), Ain, lda * sizeof(double),
+                                m * sizeof(double), n, kind, c->st));
+    copy_block(tmp, m, c->Ad, n, m, (int)n, true, c->st);
+    TSVD_CUDA(cudaStreamSynchronize(c->st));
+    cudaFree(tmp);
   }
-  catch (const tsvd::Error& e) {
-    tsvd::g_last_error = e.msg;
-    destroy_ctx(c);
-    return e.code;
+  TSVD_CUDA(cudaStreamSynchronize(c->st));
+  return TSVD_OK;
+}
+
+static void set_single(tsvd_ctx* c, int64_t m, int64_t n) {
+  c->m = c->mg = m;
+  c->n = c->ng = c->nsh = n;
+  c->m0 = c->n0 = 0;
+  c->world = 1;
+  c->rank = 0;
+}
+
+static tsvd_status set_dist(tsvd_ctx* c, const tsvd_dist* d) {
+  if (!d || d->world < 1 || d->rank < 0 || d->rank >= d->world || !d->nccl_id) return TSVD_EINVAL;
+  if (d->m_global < d->n_global) return TSVD_ESHAPE;
+  if (d->row_begin < 0 || d->row_end < d->row_begin || d->row_end > d->m_global)
+    return TSVD_EINVAL;
+  if (d->n_global < 1 || d->n_global >= (int64_t)INT32_MAX) return TSVD_ESHAPE;
+  c->world = d->world;
+  c->rank = d->rank;
+  c->mg = d->m_global;
+  c->ng = d->n_global;
+  c->m = d->row_end - d->row_begin;
+  c->m0 = d->row_begin;
+  c->nsh = (c->ng + c->world - 1) / c->world;
+  c->n0 = std::min<int64_t>(c->ng, (int64_t)c->rank * c->nsh);
+  c->n = std::min<int64_t>(c->ng, c->n0 + c->nsh) - c->n0;
+  return TSVD_OK;
+}
+
+#define TSVD_CREATE_CATCH                        \
+  catch (const tsvd::Error& e) {                 \
+    tsvd::g_last_error = e.msg;                  \
+    destroy_ctx(c);                              \
+    return e.code;                               \
+  }                                              \
+  catch (...) {                                  \
+    destroy_ctx(c);                              \
+    return TSVD_ECUDA;                           \
   }
-  catch (...) {
-    destroy_ctx(c);
-    return TSVD_ECUDA;
+
+tsvd_status tsvd_create_csr(tsvd_t* h, int64_t m, int64_t n, int64_t nnz,
+                            const int64_t* rowptr, const int32_t* colidx, const double* vals,
+                            int mem_kind) {
+  if (!h || !rowptr || (nnz > 0 && (!colidx || !vals)) || m < 0 || n < 1 || nnz < 0)
+    return TSVD_EINVAL;
+  if (m < n) return TSVD_ESHAPE;
+  if (n >= (int64_t)INT32_MAX || m >= (int64_t)INT32_MAX) return TSVD_ESHAPE;
+  *h = nullptr;
+  tsvd_ctx* c = new tsvd_ctx();
+  try {
+    tsvd_status s = init_ctx(c);
+    if (s == TSVD_OK) {
+      set_single(c, m, n);
+      s = setup_csr(c, nnz, rowptr, colidx, vals, mem_kind);
+    }
+    if (s != TSVD_OK) {
+      destroy_ctx(c);
+      return s;
+    }
+    *h = c;
+    return TSVD_OK;
   }
+  TSVD_CREATE_CATCH
 }
 
 tsvd_status tsvd_create_dense(tsvd_t* h, int64_t m, int64_t n, const double* Ain, int64_t lda,
@@ -160,49 +215,86 @@ tsvd_status tsvd_create_dense(tsvd_t* h, int64_t m, int64_t n, const double* Ain
   if (n >= (int64_t)INT32_MAX) return TSVD_ESHAPE;
   *h = nullptr;
   tsvd_ctx* c = new tsvd_ctx();
+  try {
+    tsvd_status s = init_ctx(c);
+    if (s == TSVD_OK) {
+      set_single(c, m, n);
+      s = setup_dense(c, Ain, lda, layout, mem_kind);
+    }
+    if (s != TSVD_OK) {
+      destroy_ctx(c);
+      return s;
+    }
+    *h = c;
+    return TSVD_OK;
+  }
+  TSVD_CREATE_CATCH
+}
+
+tsvd_status tsvd_create_csr_dist(tsvd_t* h, const tsvd_dist* dist, int64_t nnz,
+                                 const int64_t* rowptr, const int32_t* colidx,
+                                 const double* vals, int mem_kind) {
+  if (!h || !rowptr || (nnz > 0 && (!colidx || !vals)) || nnz < 0) return TSVD_EINVAL;
+  *h = nullptr;
+  tsvd_ctx* c = new tsvd_ctx();
+  try {
+    tsvd_status s = init_ctx(c);
+    if (s == TSVD_OK) s = set_dist(c, dist);
+    if (s == TSVD_OK) s = setup_csr(c, nnz, rowptr, colidx, vals, mem_kind);
+    if (s == TSVD_OK) comm_init(*c, dist->nccl_id, dist->rank, dist->world);
+    if (s != TSVD_OK) {
+      destroy_ctx(c);
+      return s;
+    }
+    *h = c;
+    return TSVD_OK;
+  }
+  TSVD_CREATE_CATCH
+}
+
+tsvd_status tsvd_create_dense_dist(tsvd_t* h, const tsvd_dist* dist, const double* Ain,
+                                   int64_t lda, int mem_kind) {
+  if (!h || !dist) return TSVD_EINVAL;
+  *h = nullptr;
+  tsvd_ctx* c = new tsvd_ctx();
+  try {
+    tsvd_status s = init_ctx(c);
+    if (s == TSVD_OK) s = set_dist(c, dist);
+    if (s == TSVD_OK && (c->m > 0 && (!Ain || lda < c->ng))) s = TSVD_EINVAL;
+    if (s == TSVD_OK) s = setup_dense(c, Ain, lda, TSVD_ROW_MAJOR, mem_kind);
+    if (s == TSVD_OK) comm_init(*c, dist->nccl_id, dist->rank, dist->world);
+    if (s != TSVD_OK) {
+      destroy_ctx(c);
+      return s;
+    }
+    *h = c;
+    return TSVD_OK;
+  }
+  TSVD_CREATE_CATCH
+}
+
+tsvd_status tsvd_nccl_unique_id(void* out128) {
+  if (!out128) return TSVD_EINVAL;
   TSVD_API_BEGIN
-  tsvd_status s = init_ctx(c);
-  if (s != TSVD_OK) {
-    destroy_ctx(c);
-    return s;
-  }
-  c->m = m;
-  c->n = n;
-  c->dense = true;
-  c->lda = n;
-  TSVD_CUDA(cudaMalloc(&c->Ad, (size_t)m * n * sizeof(double)));
-  if (layout == TSVD_ROW_MAJOR) {
-    TSVD_CUDA(cudaMemcpy2DAsync(c->Ad, n * sizeof(double), Ain, lda * sizeof(double),
-                                n * sizeof(double), m,
-                                mem_kind == TSVD_DEVICE ? cudaMemcpyDeviceToDevice
-                                                        : cudaMemcpyHostToDevice,
-                                c->st));
-  } else {
-    // column-major input: upload as an n x m row-major block, transpose on device
-    double* tmp;
-    TSVD_CUDA(cudaMalloc(&tmp, (size_t)m * n * sizeof(double)));
-    TSVD_CUDA(cudaMemcpy2DAsync(tmp, m * sizeof(double), Ain, lda * sizeof(double),
-                                m * sizeof(double), n,
-                                mem_kind == TSVD_DEVICE ? cudaMemcpyDeviceToDevice
-                                                        : cudaMemcpyHostToDevice,
-                                c->st));
-    copy_block(tmp, m, c->Ad, n, m, (int)n, true, c->st);
-    TSVD_CUDA(cudaStreamSynchronize(c->st));
-    cudaFree(tmp);
-  }
-  TSVD_CUDA(cudaStreamSynchronize(c->st));
-  *h = c;
+  nccl_unique_id(out128);
   return TSVD_OK;
+  TSVD_API_END
+}
+
+tsvd_status tsvd_partition_rows(const int64_t* rowptr, int64_t m, int world, int64_t* bounds) {
+  if (!rowptr || !bounds || m < 0 || world < 1) return TSVD_EINVAL;
+  const int64_t nnz = rowptr[m];
+  bounds[0] = 0;
+  int64_t r = 0;
+  for (int g = 1; g < world; ++g) {
+    const int64_t target = (nnz * g + world - 1) / world;  // first row whose prefix >= target
+    while (r < m && rowptr[r] < target) ++r;
+    int64_t b = r;  // nearest row boundary to the target prefix
+    if (r > bounds[g - 1] && target - rowptr[r - 1] < rowptr[r] - target) b = r - 1;
+    bounds[g] = std::max(bounds[g - 1], b);
   }
-  catch (const tsvd::Error& e) {
-    tsvd::g_last_error = e.msg;
-    destroy_ctx(c);
-    return e.code;
-  }
-  catch (...) {
-    destroy_ctx(c);
-    return TSVD_ECUDA;
-  }
+  bounds[world] = m;
+  return TSVD_OK;
 }
 
 tsvd_status tsvd_set_stream(tsvd_t h, void* stream) {

@@ -18,7 +18,16 @@ struct ProfRec {
 }  // namespace tsvd
 
 struct tsvd_ctx {
+  // Local sizes: m = rows of A (and of U, Pbar) on this rank, n = this rank's
+  // n-shard (rows of V, P).  Single GPU: the whole problem.
   int64_t m = 0, n = 0;
+  // multi-GPU; world == 1: mg = m, ng = n, offsets 0, nsh = n
+  int world = 1, rank = 0;
+  void* comm = nullptr;        // ncclComm_t
+  int64_t mg = 0, ng = 0;      // global sizes
+  int64_t m0 = 0, n0 = 0;      // global offsets of the local rows / n-shard
+  int64_t nsh = 0;             // uniform n-shard size (ceil(ng / world))
+  int64_t cur_row0 = 0, cur_qtot = 0;  // rows of the block being orthogonalised (Philox)
   bool dense = false;
   tsvd::Csr A, AT;           // CSR(A), CSR(A^T)
   double* Ad = nullptr;      // dense A, row-major m x n
@@ -80,6 +89,15 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
 void cgs2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H, double* R);
 int cgs_qr(Ctx& c, double* Y, int64_t q, int l, int64_t ld, int bq, double* R);
 void apply(Ctx& c, bool trans, const double* X, int64_t ldx, double* Y, int64_t ldy, int w);
+
+// collectives (comm.cu); no-ops / errors when world == 1 / NCCL missing
+bool nccl_available();
+void nccl_unique_id(void* out128);
+void comm_init(Ctx& c, const void* id128, int rank, int world);
+void comm_destroy(Ctx& c);
+void allreduce_sum(Ctx& c, double* buf, size_t count);
+void reduce_scatter_sum(Ctx& c, const double* send, double* recv, size_t recv_count);
+void all_gather(Ctx& c, const double* send, double* recv, size_t send_count);
 
 // solvers (solvers.cu)
 tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit);

@@ -117,6 +117,10 @@ void chol_finalize(const double* gram, int nparts, int w, double* Wred, double* 
 void chol2_finalize(const double* gram, int nparts, int w, double* Wred, const double* Lprev,
                     double* L2, double* T2, double* R, double* H, const double* Hbar, int s,
                     int* flag, cudaStream_t st);
+// the Cholesky finalisers on an already reduced (and all-reduced) Gram W
+void chol_from_w(const double* W, int w, double* L, double* T, int* flag, cudaStream_t st);
+void chol2_from_w(const double* W, int w, const double* Lprev, double* L2, double* T2,
+                  double* R, double* H, const double* Hbar, int s, int* flag, cudaStream_t st);
 // out[i] = sum_p part[p*count + i], fixed order
 void reduce_partials(const double* part, int nparts, int64_t count, double* out,
                      cudaStream_t st);
@@ -144,9 +148,10 @@ void lanczos_rho(const double* Rbar, int b, const double* Vb, int d, const doubl
 
 // sign normalisation (reading R28): sgn[i] = sign of the largest-|.| entry of
 // V[:, i] (lowest index on ties); flip_columns multiplies columns by sgn.
-size_t col_signs_work(int r);
-void col_signs(const double* V, int64_t n, int64_t ldv, int r, double* sgn, double* work,
-               cudaStream_t st);
+size_t col_signs_work(int r, int world);
+double* col_signs_local(const double* V, int64_t n, int64_t ldv, int r, int64_t row0,
+                        double* work, cudaStream_t st);
+void col_signs_final(const double* all, int world, int r, double* sgn, cudaStream_t st);
 void flip_columns(double* M, int64_t rows, int64_t ld, int r, const double* sgn,
                   cudaStream_t st);
 

@@ -78,6 +78,11 @@ __global__ void chol_finalize_kernel(const double* __restrict__ gram, int nparts
   if (tid == 0 && bad) *flag = 1;
 }
 
+void chol_from_w(const double* W, int w, double* L, double* T, int* flag, cudaStream_t st) {
+  chol_finalize_kernel<<<1, 256, 0, st>>>(W, 1, w, L, T, flag);
+  TSVD_CHECK_LAUNCH();
+}
+
 void chol_finalize(const double* gram, int nparts, int w, double* Wred, double* L, double* T,
                    int* flag, cudaStream_t st) {
   reduce_partials(gram, nparts, (int64_t)w * w, Wred, st);
@@ -133,6 +138,12 @@ __global__ void chol2_finalize_kernel(const double* __restrict__ gram, int npart
     }
   }
   if (tid == 0 && bad) *flag = 1;
+}
+
+void chol2_from_w(const double* W, int w, const double* Lprev, double* L2, double* T2,
+                  double* R, double* H, const double* Hbar, int s, int* flag, cudaStream_t st) {
+  chol2_finalize_kernel<<<1, 256, 0, st>>>(W, 1, w, Lprev, L2, T2, R, H, Hbar, s, flag);
+  TSVD_CHECK_LAUNCH();
 }
 
 void chol2_finalize(const double* gram, int nparts, int w, double* Wred, const double* Lprev,
@@ -269,10 +280,11 @@ __global__ void colmax_partial_kernel(const double* __restrict__ V, int64_t n, i
   }
 }
 
-__global__ void colsign_final_kernel(const double* __restrict__ V, int64_t ldv, int r,
+// per column: best (|v|, global row index, signed v) over the CTA partials
+__global__ void colsign_local_kernel(const double* __restrict__ V, int64_t ldv, int r,
                                      const double* __restrict__ pval,
-                                     const int64_t* __restrict__ pidx, int nparts,
-                                     double* __restrict__ sgn) {
+                                     const int64_t* __restrict__ pidx, int nparts, int64_t row0,
+                                     double* __restrict__ loc) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= r) return;
   double best = -1.0;
@@ -285,7 +297,26 @@ __global__ void colsign_final_kernel(const double* __restrict__ V, int64_t ldv, 
       bidx = oi;
     }
   }
-  sgn[c] = (V[bidx * ldv + c] < 0.0) ? -1.0 : 1.0;
+  loc[3 * c] = best;
+  loc[3 * c + 1] = (double)(bidx + row0);  // exact below 2^53
+  loc[3 * c + 2] = best >= 0.0 ? V[bidx * ldv + c] : 1.0;
+}
+
+// winner over ranks (rank order; ties -> lower global index) -> sign
+__global__ void colsign_final_kernel(const double* __restrict__ all, int world, int r,
+                                     double* __restrict__ sgn) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= r) return;
+  double best = -1.0, bidx = 0.0, bval = 1.0;
+  for (int g = 0; g < world; ++g) {
+    const double* e = all + ((size_t)g * r + c) * 3;
+    if (e[0] > best || (e[0] == best && e[1] < bidx)) {
+      best = e[0];
+      bidx = e[1];
+      bval = e[2];
+    }
+  }
+  sgn[c] = bval < 0.0 ? -1.0 : 1.0;
 }
 
 __global__ void flip_kernel(double* __restrict__ M, int64_t rows, int64_t ld, int r,
@@ -299,17 +330,28 @@ __global__ void flip_kernel(double* __restrict__ M, int64_t rows, int64_t ld, in
   }
 }
 
-size_t col_signs_work(int r) { return (size_t)kSignCtas * r * 2 + r + 8; }
+size_t col_signs_work(int r, int world) {
+  return (size_t)kSignCtas * r * 2 + (size_t)3 * r * (world + 1) + 8;
+}
 
-void col_signs(const double* V, int64_t n, int64_t ldv, int r, double* sgn, double* work,
-               cudaStream_t st) {
-  if (r <= 0) return;
+// Local pass: loc (3r doubles inside work) = per-column (|v|, global index,
+// v) of this rank's rows.  Returns the pointer to loc (for the all-gather).
+double* col_signs_local(const double* V, int64_t n, int64_t ldv, int r, int64_t row0,
+                        double* work, cudaStream_t st) {
   double* pval = work;
   int64_t* pidx = (int64_t*)(work + (size_t)kSignCtas * r);
+  double* loc = work + (size_t)kSignCtas * r * 2;
   dim3 grid(kSignCtas, (r + 31) / 32);
   colmax_partial_kernel<<<grid, 256, 0, st>>>(V, n, ldv, r, pval, pidx);
   TSVD_CHECK_LAUNCH();
-  colsign_final_kernel<<<(r + 127) / 128, 128, 0, st>>>(V, ldv, r, pval, pidx, kSignCtas, sgn);
+  colsign_local_kernel<<<(r + 127) / 128, 128, 0, st>>>(V, ldv, r, pval, pidx, kSignCtas, row0,
+                                                        loc);
+  TSVD_CHECK_LAUNCH();
+  return loc;
+}
+
+void col_signs_final(const double* all, int world, int r, double* sgn, cudaStream_t st) {
+  colsign_final_kernel<<<(r + 127) / 128, 128, 0, st>>>(all, world, r, sgn);
   TSVD_CHECK_LAUNCH();
 }
 

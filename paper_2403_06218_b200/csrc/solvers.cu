@@ -21,6 +21,21 @@ static void upload_start(Ctx& c, double* dst, int64_t rows, int cols, int64_t ld
                               cols * sizeof(double), rows, cudaMemcpyHostToDevice, c.st));
 }
 
+// sign of the largest-|.| entry of each column of the (row-sharded) V (R28)
+static double* signs_of(Ctx& c, const double* V, int64_t n, int r) {
+  double* work = dbuf(c, "sign_work", col_signs_work(r, c.world));
+  double* sgn = dbuf(c, "sign", (size_t)r);
+  double* loc = col_signs_local(V, n, r, r, c.n0, work, c.st);
+  if (c.comm) {
+    double* all = dbuf(c, "sign_all", (size_t)3 * r * c.world);
+    all_gather(c, loc, all, (size_t)3 * r);
+    col_signs_final(all, c.world, r, sgn, c.st);
+  } else {
+    col_signs_final(loc, 1, r, sgn, c.st);
+  }
+  return sgn;
+}
+
 static void alloc_results(Ctx& c, int r) {
   c.U = dbuf(c, "res_U", (size_t)c.m * r);
   c.V = dbuf(c, "res_V", (size_t)c.n * r);
@@ -50,17 +65,17 @@ struct EventTimer {
 };
 
 tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
-  const int64_t m = c.m, n = c.n;
+  const int64_t m = c.m, n = c.n;  // this rank's rows (single GPU: all)
   if (r < 1 || b < 1 || !(tol > 0.0) || maxit < 1) return TSVD_EINVAL;
   if (b > 32) return TSVD_EINVAL;  // kernel tile limit
-  if (r > n) return TSVD_ESHAPE;
+  if (r > c.ng) return TSVD_ESHAPE;
   int d = c.krylov_d;
   if (d == 0) {
     d = std::max(4 * r, 2 * b);
-    d = (int)std::min<int64_t>(d, n);
+    d = (int)std::min<int64_t>(d, c.ng);
     d -= d % b;
   }
-  if (d % b != 0 || d < r || d > n || d < b) return TSVD_ESHAPE;
+  if (d % b != 0 || d < r || d > c.ng || d < b) return TSVD_ESHAPE;
   if (!c.start.empty() && (c.start_rows != m || c.start_cols != b)) return TSVD_ESHAPE;
   const int k = d / b;
   const int64_t ldb = d + b, ldp = d;
@@ -87,11 +102,14 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   (void)dbuf(c, "Hbar", (size_t)(d + b) * 32);
   (void)dbuf(c, "part_tn", std::max(tn_part_size(m, d + b), tn_part_size(n, d)));
 
-  // S1: random orthonormal Qbar_1 (m x b)
+  // S1: random orthonormal Qbar_1 (m x b); rows [m0, m0+m) of the global block
+  auto m_side = [&]() { c.cur_row0 = c.m0; c.cur_qtot = c.mg; };
+  auto n_side = [&]() { c.cur_row0 = c.n0; c.cur_qtot = c.ng; };
   if (!c.start.empty())
     upload_start(c, Pb, m, b, ldb);
   else
-    launch_philox_normal(Pb, m, b, ldb, c.seed, 0, 0, m, c.st);
+    launch_philox_normal(Pb, m, b, ldb, c.seed, 0, c.m0, c.mg, c.st);
+  m_side();
   cholqr2(c, Pb, m, b, ldb, R);
 
   std::vector<double> hrho(r), hs(1);
@@ -103,12 +121,14 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
     for (int i = 0; i < k; ++i) {
       const int lo = i * b;
       apply(c, true, Pb + lo, ldb, P + lo, ldp, b);                    // S2: A^T Qbar_i
+      n_side();
       if (i == 0)
         cholqr2(c, P, n, b, ldp, R);                                   // S3a
       else
         cgs_cqr2(c, P, n, lo, b, ldp, H, R);                           // S3b
       copy_block(R, b, B + (int64_t)lo * d + lo, d, b, b, true, c.st); // L_i = R^T
       apply(c, false, P + lo, ldp, Pb + lo + b, ldb, b);               // S4: A Q_i
+      m_side();
       cgs_cqr2(c, Pb, m, lo + b, b, ldb, H, Rb);                       // S5
       if (i < k - 1)
         copy_block(Rb, b, B + (int64_t)(lo + b) * d + lo, d, b, b, false, c.st);  // Rbar_i
@@ -151,8 +171,7 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
     // S8 (Eq. 12): V = P_k Vbar[:, :r]; signs (R28) from V, folded into
     // Ubar's columns before S9: U = Pbar_k Ubar[:, :r]
     gemm_nn(P, ldp, Vb, d, nullptr, 0, nullptr, c.V, r, n, d, r, 1.0, 0.0, nullptr, c.st);
-    double* sgn = dbuf(c, "sign", (size_t)r);
-    col_signs(c.V, n, r, r, sgn, dbuf(c, "sign_work", col_signs_work(r)), c.st);
+    double* sgn = signs_of(c, c.V, n, r);
     flip_columns(c.V, n, r, r, sgn, c.st);
     flip_columns(Ub, d, d, r, sgn, c.st);
     gemm_nn(Pb, ldb, Ub, d, nullptr, 0, nullptr, c.U, r, m, d, r, 1.0, 0.0, nullptr, c.st);
@@ -177,10 +196,10 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
 }
 
 tsvd_status rsvd_solve(Ctx& c, int r, int p, int q) {
-  const int64_t m = c.m, n = c.n;
+  const int64_t m = c.m, n = c.n;  // this rank's rows (single GPU: all)
   if (r < 1 || p < 0 || q < 0) return TSVD_EINVAL;
   const int l = r + p;
-  if (l > n) return TSVD_ESHAPE;
+  if (l > c.ng) return TSVD_ESHAPE;
   if (!c.start.empty() && (c.start_rows != n || c.start_cols != l)) return TSVD_ESHAPE;
   const int bq = std::min(std::max(1, c.b_qr), 32);
   c.have = false;
@@ -203,11 +222,15 @@ tsvd_status rsvd_solve(Ctx& c, int r, int p, int q) {
   if (!c.start.empty())
     upload_start(c, Q, n, l, l);
   else
-    launch_philox_normal(Q, n, l, l, c.seed, 0, 0, n, c.st);         // Q_0 (not orthonormal)
+    launch_philox_normal(Q, n, l, l, c.seed, 0, c.n0, c.ng, c.st);   // Q_0 (not orthonormal)
   for (int j = 0; j <= q; ++j) {
     apply(c, false, Q, l, Qb, l, l);                                   // S1
+    c.cur_row0 = c.m0;
+    c.cur_qtot = c.mg;
     cgs_qr(c, Qb, m, l, l, bq, Rb);                                    // S2
     apply(c, true, Qb, l, Q, l, l);                                    // S3
+    c.cur_row0 = c.n0;
+    c.cur_qtot = c.ng;
     cgs_qr(c, Q, n, l, l, bq, R);                                      // S4
   }
   {
@@ -218,8 +241,7 @@ tsvd_status rsvd_solve(Ctx& c, int r, int p, int q) {
   {
     Prof p(c, P_RESTART, 8.0 * (m + n) * (l + r), 2.0 * (m + n) * l * r);
     gemm_nn(Q, l, Ub, l, nullptr, 0, nullptr, c.V, r, n, l, r, 1.0, 0.0, nullptr, c.st);   // S7
-    double* sgn = dbuf(c, "sign", (size_t)r);
-    col_signs(c.V, n, r, r, sgn, dbuf(c, "sign_work", col_signs_work(r)), c.st);
+    double* sgn = signs_of(c, c.V, n, r);
     flip_columns(c.V, n, r, r, sgn, c.st);
     flip_columns(Vb, l, l, r, sgn, c.st);
     gemm_nn(Qb, l, Vb, l, nullptr, 0, nullptr, c.U, r, m, l, r, 1.0, 0.0, nullptr, c.st);  // S6
