@@ -10,9 +10,10 @@ one-sided Jacobi SVD of B_k, rho test, restart, outputs U, V, sign) on the
 synthetic config's CSR matrix, with A already resident in HBM.  value = the
 time-to-solution in seconds (lower is better), max over ranks.
 
-N > 1: every rank solves its own replica of the workload (different seed);
-"scaling": "weak" (replicas - the row-partitioned NCCL path is the next
-SURVEY 8(e) row).
+N > 1 (torchrun, one process per GPU): the SAME workload is solved once,
+row-partitioned across the ranks (nnz-balanced row split,
+NCCL reduce-scatter of A^T Qbar, all-gather of Q_i, all-reduced projections
+and Grams); "scaling": "strong", value = max over ranks of the solve time.
 
 --impl reference: the CPU oracle (oracle/, numpy/scipy fp64) on the host
 cores, on a bounded sample of the same workload (the first block steps of
@@ -54,7 +55,7 @@ def _peaks():
 
 
 # --------------------------------------------------------------- workload --
-def make_workload(cfg_name: str, rank: int):
+def make_workload(cfg_name: str, rank: int = 0):
     from tsvd_inputs import CONFIGS, SEEDS, dense_prescribed, powerlaw_csr, spectrum_eq16
     cfg = dict(CONFIGS[cfg_name])
     seed = SEEDS[cfg_name] + 1000 * rank
@@ -67,14 +68,34 @@ def make_workload(cfg_name: str, rank: int):
     return cfg, seed, dict(A=A)
 
 
+def shard_workload(work, rank, world, T):
+    """This rank's rows (nnz-balanced split by the library's partitioner)."""
+    import numpy as np
+    if "csr" in work:
+        rp, ci, va = work["csr"]
+        m, n = work["shape"]
+        b = T.partition_rows(rp, world)
+        r0, r1 = int(b[rank]), int(b[rank + 1])
+        lo, hi = int(rp[r0]), int(rp[r1])
+        local = dict(csr=(np.ascontiguousarray(rp[r0:r1 + 1] - lo), ci[lo:hi], va[lo:hi]))
+    else:
+        A = work["A"]
+        m, n = A.shape
+        b = np.linspace(0, m, world + 1).astype(np.int64)
+        r0, r1 = int(b[rank]), int(b[rank + 1])
+        local = dict(A=np.ascontiguousarray(A[r0:r1]))
+    return local, dict(m_global=m, n_global=n, row_begin=r0, row_end=r1)
+
+
 def _to_device(work):
     import numpy as np
     import torch
+    out = dict(work)
     if "csr" in work:
-        rp, ci, va = work["csr"]
-        return dict(csr=tuple(torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (rp, ci, va)),
-                    shape=work["shape"])
-    return dict(A=torch.from_numpy(work["A"]).cuda())
+        out["csr"] = tuple(torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in work["csr"])
+    else:
+        out["A"] = torch.from_numpy(work["A"]).cuda()
+    return out
 
 
 # ----------------------------------------------------------------- clocks --
@@ -239,11 +260,30 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     T.lib()
 
-    cfg, seed, work = make_workload(cfg_name, rank)
-    dwork = _to_device(work)
+    cfg, seed, work = make_workload(cfg_name, 0)
+    dist_kw = None
+    # TSVD_BENCH_DIST=1 runs the row-partitioned NCCL path also with one rank
+    use_dist = world > 1 or os.environ.get("TSVD_BENCH_DIST") == "1"
+
+    def fresh_dist_kw(geo):
+        # every NCCL communicator needs its own unique id (rank 0 -> broadcast)
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(T.nccl_unique_id()), dtype=torch.uint8))
+        if dist:
+            dist.broadcast(idt, 0)
+        return dict(rank=rank, world=world, nccl_id=bytes(idt.cpu().numpy()), **geo)
+
+    if use_dist:
+        lwork, geo = shard_workload(work, rank, world, T)
+        dist_kw = fresh_dist_kw(geo)
+        hwork = lwork
+    else:
+        hwork = dict(work)
+    dwork = _to_device(hwork)
     r, b, d, tol, maxit = cfg["r"], cfg["b"], cfg["d"], cfg["tol"], cfg["maxit"]
     stream = torch.cuda.current_stream()
-    h = T.TruncatedSVD(**dwork)
+    h = T.TruncatedSVD(**dwork, dist=dist_kw) if dist_kw else T.TruncatedSVD(**dwork)
     h.set_seed(seed)
     h.set_krylov_dim(d)
     for _ in range(args.warmup):
@@ -320,12 +360,15 @@ def main():
         h2d = d2h = 0
         for _ in range(args.e2e_steps):
             t0 = time.perf_counter()
-            if "csr" in work:
-                h2 = T.TruncatedSVD(csr=work["csr"], shape=work["shape"])
-                h2d = sum(x.nbytes for x in work["csr"])
+            dkw2 = fresh_dist_kw(geo) if use_dist else None
+            if "csr" in hwork:
+                h2 = (T.TruncatedSVD(csr=hwork["csr"], dist=dkw2) if dkw2 else
+                      T.TruncatedSVD(csr=hwork["csr"], shape=hwork["shape"]))
+                h2d = sum(x.nbytes for x in hwork["csr"])
             else:
-                h2 = T.TruncatedSVD(work["A"])
-                h2d = work["A"].nbytes
+                h2 = (T.TruncatedSVD(hwork["A"], dist=dkw2) if dkw2 else
+                      T.TruncatedSVD(hwork["A"]))
+                h2d = hwork["A"].nbytes
             h2.set_seed(seed)
             h2.set_krylov_dim(d)
             h2.block_lanczos(r, b, tol, maxit)
@@ -354,13 +397,13 @@ def main():
     out = {
         "metric": METRIC, "value": round(ms / 1e3, 6), "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
+        "higher_is_better": False, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg_name}: {CONFIG_TEXT.get(cfg_name, '')}",
                    "m": cfg["m"], "n": cfg["n"], "nnz": int(len(work["csr"][1])) if "csr" in work else None,
                    "r": r, "b": b, "d": d, "tol": tol, "maxit": maxit,
                    "l2": "no flush: working set (A, A^T, bases) >> 126 MB L2",
-                   "parallelism": "replicas" if world > 1 else "single"},
+                   "parallelism": f"row-partitioned x{world} (NCCL)" if world > 1 else "single"},
         "solver": {"cycles": last["cycles"], "nconv": last["nconv"], "rho_max": last["rho_max"],
                    "breakdowns": last["breakdowns"], "sigma1": last["sigma1"]},
         "roofline": roof,
