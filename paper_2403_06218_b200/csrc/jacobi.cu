@@ -270,18 +270,18 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(double* __restrict__ 
 // multiplied by J.
 constexpr int JR_T = 256;
 
-__host__ __device__ constexpr int cpair_lo(int t, int r) {
-  const int p = (t == 0) ? 0 : ((t - 1 + r) % (JW - 1)) + 1;
-  const int q = ((JW - 2 - t + r) % (JW - 1)) + 1;
+__host__ __device__ constexpr int cpair_lo(int t, int r, int jw) {
+  const int p = (t == 0) ? 0 : ((t - 1 + r) % (jw - 1)) + 1;
+  const int q = ((jw - 2 - t + r) % (jw - 1)) + 1;
   return p < q ? p : q;
 }
-__host__ __device__ constexpr int cpair_hi(int t, int r) {
-  const int p = (t == 0) ? 0 : ((t - 1 + r) % (JW - 1)) + 1;
-  const int q = ((JW - 2 - t + r) % (JW - 1)) + 1;
+__host__ __device__ constexpr int cpair_hi(int t, int r, int jw) {
+  const int p = (t == 0) ? 0 : ((t - 1 + r) % (jw - 1)) + 1;
+  const int q = ((jw - 2 - t + r) % (jw - 1)) + 1;
   return p < q ? q : p;
 }
 
-template <int RG>
+template <int RG, int JC>
 __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict__ G,
                                                             double* __restrict__ V, int d, int nb,
                                                             double* __restrict__ nrm,
@@ -289,8 +289,10 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
                                                             double* __restrict__ S,
                                                             double* __restrict__ Vb,
                                                             unsigned* __restrict__ ctl) {
+  constexpr int JW = 2 * JC;   // columns of a block pair (shadows the file-scope JW)
   constexpr int NW = JR_T / 32;
-  constexpr int NV = 3 * JC;  // 24 partial sums per inner round
+  constexpr int NV = 3 * JC;  // partial sums per inner round
+  constexpr int NVP = NV > 16 ? 32 : 16;
   __shared__ double red[NW][NV + 1];
   __shared__ double rot_cs[JC], rot_sn[JC];
   __shared__ double Js[JW][JW + 1];
@@ -320,12 +322,12 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
       if (tid == 0) any_rot = 0;
 #pragma unroll
       for (int ir = 0; ir < JW - 1; ++ir) {
-        double v[32];
+        double v[NVP];
 #pragma unroll
-        for (int i = NV; i < 32; ++i) v[i] = 0.0;
+        for (int i = NV; i < NVP; ++i) v[i] = 0.0;
 #pragma unroll
         for (int t = 0; t < JC; ++t) {
-          const int p = cpair_lo(t, ir), q = cpair_hi(t, ir);
+          const int p = cpair_lo(t, ir, JW), q = cpair_hi(t, ir, JW);
           double a = 0.0, b = 0.0, c = 0.0;
 #pragma unroll
           for (int k = 0; k < RG; ++k) {
@@ -337,9 +339,9 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
           v[3 * t + 1] = b;
           v[3 * t + 2] = c;
         }
-        // recursive-halving butterfly over 32 lanes on 24 (zero-padded to 32)
-        // values: afterwards lane l holds the warp sum of value l
-        {
+        // recursive-halving butterfly over 32 lanes on NV (zero-padded to NVP)
+        // values: afterwards lane l holds the warp sum of value l % NVP
+        if constexpr (NVP == 32) {
           const bool up = (lane & 16) != 0;
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -347,6 +349,9 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
             const double send = up ? lo : hi, keep = up ? hi : lo;
             v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
           }
+        } else {
+#pragma unroll
+          for (int i = 0; i < NVP; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], 16);
         }
 #pragma unroll
         for (int o = 8; o >= 1; o >>= 1) {
@@ -381,7 +386,7 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
         __syncthreads();
 #pragma unroll
         for (int t = 0; t < JC; ++t) {
-          const int p = cpair_lo(t, ir), q = cpair_hi(t, ir);
+          const int p = cpair_lo(t, ir, JW), q = cpair_hi(t, ir, JW);
           const double cs = rot_cs[t], sn = rot_sn[t];
 #pragma unroll
           for (int k = 0; k < RG; ++k) {
@@ -392,7 +397,7 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
         }
         if (tid < JC * JW) {
           const int t = tid / JW, i = tid % JW;
-          const int p = cpair_lo(t, ir), q = cpair_hi(t, ir);
+          const int p = cpair_lo(t, ir, JW), q = cpair_hi(t, ir, JW);
           const double cs = rot_cs[t], sn = rot_sn[t];
           const double jp = Js[i][p], jq = Js[i][q];
           Js[i][p] = cs * jp - sn * jq;
@@ -486,23 +491,37 @@ void small_svd(const double* B, int d, double* Ub, double* S, double* Vb, double
   double* V = G + (size_t)d * dp;
   double* nrm = V + (size_t)dp * dp;
   unsigned* ctl = (unsigned*)(nrm + dp);
-  jacobi_init_kernel<<<148 * 4, 256, 0, st>>>(B, d, dp, G, V, ctl);
-  TSVD_CHECK_LAUNCH();
   {
-    int nblocks = nb / 2, nbv = nb;
-    void* args[] = {&G, &V, &d, &nbv, &nrm, &Ub, &S, &Vb, &ctl};
+    // register path: blocks of kRegJC columns (pairs of 2 kRegJC); the
+    // sequential chain is ~2d inner rounds per sweep whatever the block size,
+    // and narrower pairs make each inner round cheaper
+    constexpr int kRegJC = 4;
+    int nb4 = (d + kRegJC - 1) / kRegJC;
+    if (nb4 < 2) nb4 = 2;
+    if (nb4 & 1) ++nb4;
+    const int dp4 = nb4 * kRegJC;
     const int RG = (d + JR_T - 1) / JR_T;
     void* fn = nullptr;
-    if (RG <= 1) fn = (void*)jacobi_reg_kernel<1>;
-    else if (RG == 2) fn = (void*)jacobi_reg_kernel<2>;
-    else if (RG == 3) fn = (void*)jacobi_reg_kernel<3>;
-    else if (RG == 4) fn = (void*)jacobi_reg_kernel<4>;
-    if (fn) {
+    if (RG <= 1) fn = (void*)jacobi_reg_kernel<1, kRegJC>;
+    else if (RG == 2) fn = (void*)jacobi_reg_kernel<2, kRegJC>;
+    else if (RG == 3) fn = (void*)jacobi_reg_kernel<3, kRegJC>;
+    else if (RG == 4) fn = (void*)jacobi_reg_kernel<4, kRegJC>;
+    if (fn && nb4 / 2 <= 148) {
+      double* G4 = work;
+      double* V4 = G4 + (size_t)d * dp4;
+      double* nrm4 = V4 + (size_t)dp4 * dp4;
+      unsigned* ctl4 = (unsigned*)(nrm + dp);  // same control words as the JC path
+      jacobi_init_kernel<<<148 * 4, 256, 0, st>>>(B, d, dp4, G4, V4, ctl4);
+      TSVD_CHECK_LAUNCH();
+      int nblocks = nb4 / 2, nbv = nb4;
+      void* args[] = {&G4, &V4, &d, &nbv, &nrm4, &Ub, &S, &Vb, &ctl4};
       TSVD_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(JR_T), args, 0, st));
       TSVD_CHECK_LAUNCH();
       return;
     }
   }
+  jacobi_init_kernel<<<148 * 4, 256, 0, st>>>(B, d, dp, G, V, ctl);
+  TSVD_CHECK_LAUNCH();
   const size_t smem = sizeof(double) * ((size_t)d * JP + 2 * JW * JP);
   static int attr_for = -1;
   if (attr_for < (int)smem) {
