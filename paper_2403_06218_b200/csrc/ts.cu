@@ -533,6 +533,118 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
   }
 }
 
+// s = 0 passes (Gram only, TRSM-as-multiply Y T, scaling): pure streaming.
+// Warps are independent (no block barriers): each walks 8-row tiles, loads
+// the rows straight into DMMA A-fragments (next tile prefetched), multiplies
+// by T held in B-fragment registers, stores Z from the accumulator fragments
+// and accumulates the tile's Gram by DMMA through an 8-row warp-private
+// shared tile.  Per-CTA Gram partials are summed over warps in warp order.
+template <int WP>
+__global__ void __launch_bounds__(256) rowT_kernel(const double* Y, int64_t ldy,
+                                                   const double* __restrict__ T, double* Z,
+                                                   int64_t ldz, int64_t q, int w, double beta,
+                                                   double* __restrict__ gram) {
+  constexpr int NT = WP / 8, KY = WP / 4, NPAIR = NT * NT, ZP = WP + 4;
+  __shared__ double zs[8][8 * ZP];
+  __shared__ double gred[8][NPAIR * 64];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  double tb[KY][NT];
+#pragma unroll
+  for (int kk = 0; kk < KY; ++kk)
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      const int r = kk * 4 + tig, c = ni * 8 + gid;
+      tb[kk][ni] = (r < w && c < w) ? (T ? T[r * w + c] : (r == c ? 1.0 : 0.0)) : 0.0;
+    }
+  double g[NPAIR][2];
+#pragma unroll
+  for (int p = 0; p < NPAIR; ++p) g[p][0] = g[p][1] = 0.0;
+  const int64_t ntiles = (q + 7) / 8;
+  const int64_t gw = (int64_t)blockIdx.x * 8 + warp, nw = (int64_t)gridDim.x * 8;
+  // PF tiles of Y in flight per warp (register ring)
+  constexpr int PF = 4;
+  double yr[PF][KY];
+  auto load = [&](double (&dst)[KY], int64_t t) {
+    const int64_t row = t * 8 + gid;
+#pragma unroll
+    for (int kk = 0; kk < KY; ++kk) {
+      const int col = kk * 4 + tig;
+      dst[kk] = (t < ntiles && row < q && col < w) ? Y[row * ldy + col] : 0.0;
+    }
+  };
+#pragma unroll
+  for (int f = 0; f < PF - 1; ++f) load(yr[f], gw + f * nw);
+  double* zw = zs[warp];
+  int64_t it = 0;
+  for (int64_t t = gw; t < ntiles; t += nw, ++it) {
+    double ya[KY];
+    // rotate the ring: yr[0] is this tile, yr[PF-1] <- tile t + (PF-1) nw
+#pragma unroll
+    for (int kk = 0; kk < KY; ++kk) ya[kk] = yr[0][kk];
+#pragma unroll
+    for (int f = 0; f < PF - 1; ++f)
+#pragma unroll
+      for (int kk = 0; kk < KY; ++kk) yr[f][kk] = yr[f + 1][kk];
+    load(yr[PF - 2], t + (PF - 1) * nw);
+    double acc[NT][2];
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) acc[ni][0] = acc[ni][1] = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < KY; ++kk)
+#pragma unroll
+      for (int ni = 0; ni < NT; ++ni) dmma884(acc[ni][0], acc[ni][1], ya[kk], tb[kk][ni]);
+    const int64_t row = t * 8 + gid;
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) {
+      const int c = ni * 8 + 2 * tig;
+      const double z0 = (row < q && c < w) ? beta * acc[ni][0] : 0.0;
+      const double z1 = (row < q && c + 1 < w) ? beta * acc[ni][1] : 0.0;
+      if (Z && row < q) {
+        if (c + 1 < w && ((ldz | (uintptr_t)Z / 8 | c) & 1) == 0) {
+          *reinterpret_cast<double2*>(Z + row * ldz + c) = make_double2(z0, z1);
+        } else {
+          if (c < w) Z[row * ldz + c] = z0;
+          if (c + 1 < w) Z[row * ldz + c + 1] = z1;
+        }
+      }
+      zw[gid * ZP + c] = z0;
+      zw[gid * ZP + c + 1] = z1;
+    }
+    if (gram) {
+      __syncwarp();
+#pragma unroll
+      for (int k2 = 0; k2 < 2; ++k2)
+#pragma unroll
+        for (int mi = 0; mi < NT; ++mi) {
+          const double a = zw[(k2 * 4 + tig) * ZP + mi * 8 + gid];
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) {
+            const double b = zw[(k2 * 4 + tig) * ZP + ni * 8 + gid];
+            dmma884(g[mi * NT + ni][0], g[mi * NT + ni][1], a, b);
+          }
+        }
+      __syncwarp();
+    }
+  }
+  (void)it;
+  if (gram) {
+#pragma unroll
+    for (int p = 0; p < NPAIR; ++p)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) gred[warp][p * 64 + gid * 8 + 2 * tig + e] = g[p][e];
+    __syncthreads();
+    for (int idx = tid; idx < NPAIR * 64; idx += 256) {
+      double sum = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum += gred[k][idx];
+      const int p = idx / 64, ii = (idx % 64) / 8, jj = idx % 8;
+      const int i = (p / NT) * 8 + ii, j = (p % NT) * 8 + jj;
+      if (i < w && j < w) gram[(int64_t)blockIdx.x * w * w + i * w + j] = sum;
+    }
+  }
+}
+
 template <int WP, int VEC>
 static void nn_launch(const double* X, int64_t ldx, const double* H, int64_t ldh,
                       const double* Y, int64_t ldy, const double* T, double* Z, int64_t ldz,
@@ -569,6 +681,15 @@ void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const d
                 std::min(32, w - c0), alpha, beta, nullptr, st);
       return;
     }
+  }
+  if (s == 0 && w <= 16) {  // streaming row pass (WP = 32 keeps the tiled path: smem)
+    const int ctas = nn_ctas(q, w);
+    if (w <= 8)
+      rowT_kernel<8><<<ctas, 256, 0, st>>>(Y, ldy, T, Z, ldz, q, w, beta, gram);
+    else
+      rowT_kernel<16><<<ctas, 256, 0, st>>>(Y, ldy, T, Z, ldz, q, w, beta, gram);
+    TSVD_CHECK_LAUNCH();
+    return;
   }
   const bool v2 = s == 0 || (aligned16(X, ldx) && aligned16(H, ldh));
 #define NN_CASE(WPV)                                                                      \
