@@ -120,8 +120,16 @@ static int read_flags(Ctx& c) {
 }
 
 static void clear_flags(Ctx& c) {
-  TSVD_CUDA(cudaMemsetAsync(c.dflags, 0, 4 * sizeof(int), c.st));
+  if (!c.deferred) TSVD_CUDA(cudaMemsetAsync(c.dflags, 0, 4 * sizeof(int), c.st));
 }
+
+// where this call's two breakdown flags go (see tsvd_ctx::deferred)
+static int* ortho_flags(Ctx& c) {
+  return c.deferred ? c.flag_log + 2 * c.flag_slot : c.dflags;
+}
+
+// immediate mode: sync and read the flags; deferred mode: never breaks down here
+static int breakdown(Ctx& c) { return c.deferred ? 0 : read_flags(c); }
 
 // Row-sharded reductions: every X^T Y or Gram computed on this
 // rank's rows is a partial sum over the row partition; it is all-reduced
@@ -151,7 +159,7 @@ int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
   {
     Prof p(c, P_SMALL, 0, 0);
     reduce_gram(c, gram, np, w, Wred);
-    chol_from_w(Wred, w, L1, T1, c.dflags + 0, c.st);                            // S2
+    chol_from_w(Wred, w, L1, T1, ortho_flags(c) + 0, c.st);                      // S2
   }
   {  // S3 + S4: S = Y L^{-T}, Wbar = S^T S
     Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 3.0 * q * w * w);
@@ -160,9 +168,9 @@ int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
   {
     Prof p(c, P_SMALL, 0, 0);
     reduce_gram(c, gram, np, w, Wred);
-    chol2_from_w(Wred, w, L1, L2, T2, R, nullptr, nullptr, 0, c.dflags + 1, c.st);   // S5, S7
+    chol2_from_w(Wred, w, L1, L2, T2, R, nullptr, nullptr, 0, ortho_flags(c) + 1, c.st);  // S5, S7
   }
-  if (read_flags(c)) {
+  if (breakdown(c)) {
     Prof p(c, P_OTHER, 0, 0);
     cgs2(c, Y, q, 0, w, ld, nullptr, R);
     return 1;
@@ -203,7 +211,7 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
   {
     Prof p(c, P_SMALL, 0, 0);
     reduce_gram(c, gram, np, w, Wred);
-    chol_from_w(Wred, w, L1, T1, c.dflags + 0, c.st);                                 // S4
+    chol_from_w(Wred, w, L1, T1, ortho_flags(c) + 0, c.st);                           // S4
   }
   {
     Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 1.0 * q * w * w);
@@ -221,9 +229,9 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
   {
     Prof p(c, P_SMALL, 0, 0);
     reduce_gram(c, gram, np, w, Wred);
-    chol2_from_w(Wred, w, L1, L2, T2, R, H, Hbar, s, c.dflags + 1, c.st);            // S9,S11,S12
+    chol2_from_w(Wred, w, L1, L2, T2, R, H, Hbar, s, ortho_flags(c) + 1, c.st);      // S9,S11,S12
   }
-  if (read_flags(c)) {
+  if (breakdown(c)) {
     Prof p(c, P_OTHER, 0, 0);
     cgs2(c, basis, q, s, w, ld, H, R);
     return 1;

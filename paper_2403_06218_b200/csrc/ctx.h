@@ -43,6 +43,13 @@ struct tsvd_ctx {
   // device workspace: named buffers grown on demand, kept across solves
   std::map<std::string, std::pair<void*, size_t>> bufs;
   int* dflags = nullptr;      // device flags
+  // Deferred breakdown checks (Lanczos): each orthogonalisation writes its two
+  // Cholesky breakdown flags to flag_log[2*flag_slot + {0,1}] and the host
+  // reads the whole log once per cycle instead of syncing per call; on a
+  // breakdown the cycle is replayed from that call with immediate checks.
+  bool deferred = false;
+  int* flag_log = nullptr;
+  int flag_slot = 0;
   int* hflags = nullptr;      // pinned host mirror
   // results of the last solve
   double *U = nullptr, *S = nullptr, *V = nullptr;

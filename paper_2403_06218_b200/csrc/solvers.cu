@@ -116,23 +116,50 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   int cycle = 0, nconv = 0;
   bool conv = false;
   double rho_max = 0.0;
+  int* flog = (int*)buf(c, "flag_log", sizeof(int) * 4 * (size_t)k);
+  std::vector<int> hlog(4 * (size_t)k);
   for (cycle = 1; cycle <= maxit; ++cycle) {
     fill_zero(B, (int64_t)d * d, c.st);
-    for (int i = 0; i < k; ++i) {
-      const int lo = i * b;
-      apply(c, true, Pb + lo, ldb, P + lo, ldp, b);                    // S2: A^T Qbar_i
-      n_side();
-      if (i == 0)
-        cholqr2(c, P, n, b, ldp, R);                                   // S3a
-      else
-        cgs_cqr2(c, P, n, lo, b, ldp, H, R);                           // S3b
-      copy_block(R, b, B + (int64_t)lo * d + lo, d, b, b, true, c.st); // L_i = R^T
-      apply(c, false, P + lo, ldp, Pb + lo + b, ldb, b);               // S4: A Q_i
-      m_side();
-      cgs_cqr2(c, Pb, m, lo + b, b, ldb, H, Rb);                       // S5
-      if (i < k - 1)
-        copy_block(Rb, b, B + (int64_t)(lo + b) * d + lo, d, b, b, false, c.st);  // Rbar_i
+    // Block steps, first with deferred breakdown checks (no host sync per
+    // orthogonalisation); if the log shows a breakdown in call `slot`
+    // (2i: n side of step i, 2i+1: m side) the steps are replayed from there
+    // with immediate checks and the CGS2 fallback.
+    TSVD_CUDA(cudaMemsetAsync(flog, 0, sizeof(int) * 4 * (size_t)k, c.st));
+    c.flag_log = flog;
+    c.deferred = true;
+    int from_slot = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int i = from_slot / 2; i < k; ++i) {
+        const int lo = i * b;
+        if (!(i == from_slot / 2 && (from_slot & 1))) {
+          apply(c, true, Pb + lo, ldb, P + lo, ldp, b);                  // S2: A^T Qbar_i
+          n_side();
+          c.flag_slot = 2 * i;
+          if (i == 0)
+            cholqr2(c, P, n, b, ldp, R);                                 // S3a
+          else
+            cgs_cqr2(c, P, n, lo, b, ldp, H, R);                         // S3b
+          copy_block(R, b, B + (int64_t)lo * d + lo, d, b, b, true, c.st);  // L_i = R^T
+        }
+        apply(c, false, P + lo, ldp, Pb + lo + b, ldb, b);               // S4: A Q_i
+        m_side();
+        c.flag_slot = 2 * i + 1;
+        cgs_cqr2(c, Pb, m, lo + b, b, ldb, H, Rb);                       // S5
+        if (i < k - 1)
+          copy_block(Rb, b, B + (int64_t)(lo + b) * d + lo, d, b, b, false, c.st);  // Rbar_i
+      }
+      if (!c.deferred) break;
+      TSVD_CUDA(cudaMemcpyAsync(hlog.data(), flog, sizeof(int) * 4 * (size_t)k,
+                                cudaMemcpyDeviceToHost, c.st));
+      TSVD_CUDA(cudaStreamSynchronize(c.st));
+      c.deferred = false;
+      int bad = -1;
+      for (int sl = 0; sl < 2 * k && bad < 0; ++sl)
+        if (hlog[2 * sl] || hlog[2 * sl + 1]) bad = sl;
+      if (bad < 0) break;
+      from_slot = bad;
     }
+    c.deferred = false;
     {
       Prof p(c, P_SVD, 16.0 * d * d, 0);
       small_svd(B, d, Ub, Sg, Vb, jw, c.st);                           // B_k = Ub S Vb^T
