@@ -13,6 +13,10 @@
 // (LDGSTS) multi-stage pipelines so several tiles are in flight per SM, which
 // is what an HBM-bound pass needs.  Split-K partial sums are
 // reduced in a fixed order by a separate kernel; no floating-point atomics.
+#include <cuda.h>
+
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace tsvd {
@@ -645,6 +649,298 @@ __global__ void __launch_bounds__(256) rowT_kernel(const double* Y, int64_t ldy,
   }
 }
 
+// ---------------------------------------------------------- NN (TMA) ---
+// The w <= 16 main-pass variant of gemm_nn (the dominant kernel of C2):
+// warp-specialised, one producer warp issuing TMA tile loads
+// (cp.async.bulk.tensor, 128B-swizzled 16-column boxes, out-of-bounds rows /
+// columns zero-filled by the copy engine) into an S-stage mbarrier ring, and
+// eight consumer warps doing only LDS + DMMA.  The producer runs ahead across
+// tile boundaries, so the X stream continues through the epilogue.  Bank
+// conflicts of the swizzled layout are avoided by (i) pairing k-steps: lane
+// (gid, tig) takes k = 8*kk2 + 2*tig + h for the two DMMAs h = 0, 1, so its two
+// A values are one 16-byte LDS, and (ii) permuting the 8 rows of an M-tile,
+// lane gid -> row prow = 4*(gid&1) + gid/2, so every quarter-warp reads 8
+// distinct 16-byte chunks; the B (H) reads k = 8*kk2 + 2*tig + h are then
+// conflict-free as well.  Output rows follow the same permutation.
+constexpr int NT_R = 128;
+bool g_nn_tma = getenv("TSVD_NN_TMA") ? atoi(getenv("TSVD_NN_TMA")) != 0 : true;
+
+template <int KC, int S>
+struct NnTmaCfg {
+  static constexpr int NB = KC / 16;                       // 16-column boxes per stage
+  static constexpr size_t xbox = (size_t)NT_R * 16 * 8;    // 16 KB
+  static constexpr size_t hbox = (size_t)KC * 16 * 8;
+  static constexpr size_t stage = NB * xbox + hbox;        // multiple of 1024
+  static constexpr int OP = 16 + 4;
+  static constexpr size_t os_off = S * stage;
+  static constexpr size_t ts_off = os_off + (size_t)NT_R * OP * 8;
+  static constexpr size_t bar_off = ts_off + 16 * 16 * 8;
+  static constexpr size_t bytes = bar_off + 2 * S * 8 + 1024;  // + alignment slack
+  static constexpr unsigned tx = (unsigned)stage;
+};
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
+
+template <int KC, int S>
+__global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
+    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
+    const double* Y, int64_t ldy, const double* __restrict__ T, double* Z, int64_t ldz, int64_t q,
+    int s, int w, double alpha, double beta, double* __restrict__ gram) {
+  using CF = NnTmaCfg<KC, S>;
+  constexpr int WP = 16, NT = 2, OP = CF::OP, KY = WP / 4, NPAIR = NT * NT;
+  constexpr int KSPLIT = 8 / NPAIR, KSTEPS = NT_R / 4 / KSPLIT;
+  extern __shared__ unsigned char smraw[];
+  unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  double* Os = (double*)(sm + CF::os_off);
+  double* Ts = (double*)(sm + CF::ts_off);
+  uint64_t* full = (uint64_t*)(sm + CF::bar_off);
+  uint64_t* empty = full + S;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int prow = ((gid & 1) << 2) | (gid >> 1);
+  for (int i = tid; i < WP * WP; i += 288) {
+    const int r = i / WP, c = i % WP;
+    Ts[i] = (r < w && c < w) ? (T ? T[r * w + c] : (r == c ? 1.0 : 0.0)) : 0.0;
+  }
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t ntiles = (q + NT_R - 1) / NT_R;
+  const int64_t my_tiles =
+      (ntiles > (int64_t)blockIdx.x) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int nk = (s + KC - 1) / KC;
+  const int64_t nsteps = my_tiles * nk;
+  if (warp == 8) {  // producer
+    if (lane == 0) {
+      for (int64_t j = 0; j < nsteps; ++j) {
+        const int st = (int)(j % S);
+        const unsigned u = (unsigned)(j / S);
+        if (j >= S) mbar_wait(&empty[st], (u - 1) & 1);
+        const int64_t lt = j / nk;
+        const int kc = (int)(j % nk);
+        const int r0 = (int)((blockIdx.x + lt * gridDim.x) * NT_R);
+        unsigned char* base = sm + (size_t)st * CF::stage;
+        mbar_expect_tx(&full[st], CF::tx);
+#pragma unroll
+        for (int b = 0; b < CF::NB; ++b)
+          tma_load_2d(base + b * CF::xbox, &xmap, kc * KC + b * 16, r0, &full[st]);
+        tma_load_2d(base + CF::NB * CF::xbox, &hmap, 0, kc * KC, &full[st]);
+      }
+    }
+    return;
+  }
+  double g[2][2];
+  g[0][0] = g[0][1] = g[1][0] = g[1][1] = 0.0;
+  double acc[2][2][NT][2];
+  double ya[2][KY];
+  auto load_ya = [&](double (&dst)[2][KY], int64_t rbase) {
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi) {
+      const int64_t row = rbase + warp * 16 + mi * 8 + prow;
+#pragma unroll
+      for (int kk = 0; kk < KY; ++kk) {
+        const int col = kk * 4 + tig;
+        dst[mi][kk] = (beta != 0.0 && Y && row < q && col < w) ? Y[row * ldy + col] : 0.0;
+      }
+    }
+  };
+  for (int64_t j = 0; j < nsteps; ++j) {
+    const int st = (int)(j % S);
+    const unsigned u = (unsigned)(j / S);
+    const int kc = (int)(j % nk);
+    const int64_t lt = j / nk;
+    const int64_t r0 = (blockIdx.x + lt * gridDim.x) * NT_R;
+    if (kc == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) acc[h][mi][ni][0] = acc[h][mi][ni][1] = 0.0;
+    }
+    if (kc == nk - 1) load_ya(ya, r0);  // latency overlaps the chunk's DMMAs
+    mbar_wait(&full[st], u & 1);
+    {
+      const unsigned char* base = sm + (size_t)st * CF::stage;
+      const double* hs = (const double*)(base + CF::NB * CF::xbox);
+#pragma unroll
+      for (int kk2 = 0; kk2 < KC / 8; ++kk2) {
+        const double* xb = (const double*)(base + (kk2 >> 1) * CF::xbox);
+        const int chunk = (((kk2 & 1) << 2) | tig) ^ prow;
+        const double2 a0 =
+            *reinterpret_cast<const double2*>(xb + (warp * 16 + prow) * 16 + chunk * 2);
+        const double2 a1 =
+            *reinterpret_cast<const double2*>(xb + (warp * 16 + 8 + prow) * 16 + chunk * 2);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int hr = kk2 * 8 + 2 * tig + h;
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) {
+            const int c = ni * 8 + gid;
+            const double b = hs[hr * 16 + (((c >> 1) ^ (hr & 7)) << 1) + (c & 1)];
+            dmma884(acc[h][0][ni][0], acc[h][0][ni][1], h ? a0.y : a0.x, b);
+            dmma884(acc[h][1][ni][0], acc[h][1][ni][1], h ? a1.y : a1.x, b);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (kc == nk - 1) {
+      double yt[2][NT][2];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni) yt[mi][ni][0] = yt[mi][ni][1] = 0.0;
+      if (beta != 0.0) {
+#pragma unroll
+        for (int kk = 0; kk < KY; ++kk)
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) {
+            const double b = Ts[(kk * 4 + tig) * WP + ni * 8 + gid];
+            dmma884(yt[0][ni][0], yt[0][ni][1], ya[0][kk], b);
+            dmma884(yt[1][ni][0], yt[1][ni][1], ya[1][kk], b);
+          }
+      }
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int r = warp * 16 + mi * 8 + prow, c = ni * 8 + 2 * tig + e;
+            const double z = alpha * (acc[0][mi][ni][e] + acc[1][mi][ni][e]) + beta * yt[mi][ni][e];
+            Os[r * OP + c] = (c < w && r0 + r < q) ? z : 0.0;
+          }
+      bar_consumers();
+      if (Z) {
+        for (int idx = tid; idx < NT_R * WP; idx += 256) {
+          const int r = idx / WP, c = idx % WP;
+          const int64_t row = r0 + r;
+          if (row < q && c < w) Z[row * ldz + c] = Os[r * OP + c];
+        }
+      }
+      if (gram) {
+        const int pair = warp % NPAIR;
+        const int k0 = (warp / NPAIR) * KSTEPS;
+        const int mi = pair / NT, ni = pair % NT;
+#pragma unroll 8
+        for (int kk = 0; kk < KSTEPS; ++kk) {
+          const int kr = (k0 + kk) * 4 + tig;
+          const double a = Os[kr * OP + mi * 8 + gid];
+          const double b = Os[kr * OP + ni * 8 + gid];
+          dmma884(g[kk & 1][0], g[kk & 1][1], a, b);
+        }
+      }
+      bar_consumers();
+    }
+  }
+  if (gram) {
+    double* red = Os;  // free now: every consumer passed the last barrier
+#pragma unroll
+    for (int e = 0; e < 2; ++e) red[warp * 64 + gid * 8 + 2 * tig + e] = g[0][e] + g[1][e];
+    bar_consumers();
+    for (int idx = tid; idx < NPAIR * 64; idx += 256) {
+      const int pair = idx / 64, ii = (idx % 64) / 8, jj = idx % 8;
+      double sum = 0.0;
+      for (int k = 0; k < KSPLIT; ++k) sum += red[(k * NPAIR + pair) * 64 + ii * 8 + jj];
+      const int i = (pair / NT) * 8 + ii, jc = (pair % NT) * 8 + jj;
+      if (i < w && jc < w) gram[(int64_t)blockIdx.x * w * w + i * w + jc] = sum;
+    }
+  }
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) ==
+            cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// row-major rows x cols (ld) f64 matrix, box = 16 columns x box_rows, 128B swizzle
+static bool make_map(CUtensorMap* m, const double* base, int64_t rows, int64_t cols, int64_t ld,
+                     int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  const cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+constexpr int NNT_KC = 32, NNT_S = 2;
+
+static bool nn_tma_launch(const double* X, int64_t ldx, const double* H, int64_t ldh,
+                          const double* Y, int64_t ldy, const double* T, double* Z, int64_t ldz,
+                          int64_t q, int s, int w, double alpha, double beta, double* gram,
+                          cudaStream_t st) {
+  if (q >= (int64_t)1 << 31 || s >= (1 << 30)) return false;
+  CUtensorMap xm, hm;
+  if (!make_map(&xm, X, q, s, ldx, NT_R) || !make_map(&hm, H, s, w, ldh, NNT_KC)) return false;
+  using CF = NnTmaCfg<NNT_KC, NNT_S>;
+  static bool attr = false;
+  if (!attr) {
+    TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_tma_kernel<NNT_KC, NNT_S>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
+    attr = true;
+  }
+  gemm_nn_tma_kernel<NNT_KC, NNT_S><<<nn_ctas(q, 16), 288, CF::bytes, st>>>(
+      xm, hm, Y, ldy, T, Z, ldz, q, s, w, alpha, beta, gram);
+  TSVD_CHECK_LAUNCH();
+  return true;
+}
+
 template <int WP, int VEC>
 static void nn_launch(const double* X, int64_t ldx, const double* H, int64_t ldh,
                       const double* Y, int64_t ldy, const double* T, double* Z, int64_t ldz,
@@ -692,6 +988,9 @@ void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const d
     return;
   }
   const bool v2 = s == 0 || (aligned16(X, ldx) && aligned16(H, ldh));
+  if (w > 8 && w <= 16 && s > 0 && v2 && g_nn_tma &&
+      nn_tma_launch(X, ldx, H, ldh, Y, ldy, T, Z, ldz, q, s, w, alpha, beta, gram, st))
+    return;
 #define NN_CASE(WPV)                                                                      \
   if (v2)                                                                                 \
     nn_launch<WPV, 2>(X, ldx, H, ldh, Y, ldy, T, Z, ldz, q, s, w, alpha, beta, gram, st); \
