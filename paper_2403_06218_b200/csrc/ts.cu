@@ -69,6 +69,73 @@ __device__ __forceinline__ void load_tile(double* s, const double* g, int64_t ld
   }
 }
 
+// ------------------------------------------------------ TMA / mbarrier ---
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) ==
+            cudaSuccess &&
+        qr == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// row-major rows x cols (ld) f64 matrix, box = 16 columns x box_rows, 128B swizzle
+static bool make_map(CUtensorMap* m, const double* base, int64_t rows, int64_t cols, int64_t ld,
+                     int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
+  const cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // ------------------------------------------------------------------ TN ---
 // CTA = (s-tile of TN_ST columns of X) x (contiguous range of row chunks).
 // Each stage holds TN_RB rows of X's s-tile and of Y; each warp owns 4 rows
@@ -193,6 +260,133 @@ __global__ void __launch_bounds__(256, (WP == 32) ? 1 : 2) gemm_tn_kernel(const 
   }
 }
 
+// TMA variant of gemm_tn for 9 <= w <= 16 (the n- and m-side H = P^T Y
+// passes): one producer warp loads 64-row x 16-column 128B-swizzled boxes of
+// X (ST/16 of them) and Y into an mbarrier ring; consumer warp k takes rows
+// 8k..8k+7 of a stage as two paired DMMA k-steps (lane tig: rows 2 tig + h),
+// which makes both the X^T (A) and Y (B) fragment reads conflict-free under
+// the swizzle.  ST adapts to s (16..64) so small-s passes do no zero work.
+constexpr int TT_RB = 64;
+
+template <int ST>
+struct TnTmaCfg {
+  static constexpr int NB = ST / 16, MT = ST / 8;
+  static constexpr int S = (ST >= 48) ? 2 : 4;
+  static constexpr size_t box = (size_t)TT_RB * 16 * 8;  // 8 KB
+  static constexpr size_t stage = (NB + 1) * box;
+  static constexpr size_t bar_off = S * stage;
+  static constexpr size_t bytes = bar_off + 2 * S * 8 + 1024;
+  static constexpr unsigned tx = (unsigned)stage;
+};
+
+template <int ST>
+__global__ void __launch_bounds__(288, 2) gemm_tn_tma_kernel(
+    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
+    int64_t q, int s, int w, double* __restrict__ C, int64_t ldc, double* __restrict__ part) {
+  using CF = TnTmaCfg<ST>;
+  constexpr int S = CF::S, MT = CF::MT, NT = 2, WP = 16;
+  extern __shared__ unsigned char smraw[];
+  unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(sm + CF::bar_off);
+  uint64_t* empty = full + S;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int s0 = blockIdx.x * ST;
+  const int split = blockIdx.y, nsplit = gridDim.y;
+  const int64_t chunks = (q + TT_RB - 1) / TT_RB;
+  const int64_t c_beg = chunks * split / nsplit, c_end = chunks * (split + 1) / nsplit;
+  const int nsteps = (int)(c_end - c_beg);
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 8) {
+    if (lane == 0) {
+      for (int j = 0; j < nsteps; ++j) {
+        const int st = j % S;
+        const unsigned u = (unsigned)(j / S);
+        if (j >= S) mbar_wait(&empty[st], (u - 1) & 1);
+        const int r0 = (int)((c_beg + j) * TT_RB);
+        unsigned char* base = sm + (size_t)st * CF::stage;
+        mbar_expect_tx(&full[st], CF::tx);
+#pragma unroll
+        for (int b = 0; b < CF::NB; ++b)
+          tma_load_2d(base + b * CF::box, &xmap, s0 + b * 16, r0, &full[st]);
+        tma_load_2d(base + CF::NB * CF::box, &ymap, 0, r0, &full[st]);
+      }
+    }
+    return;
+  }
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < NT; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+  for (int j = 0; j < nsteps; ++j) {
+    const int st = j % S;
+    mbar_wait(&full[st], (unsigned)(j / S) & 1);
+    const unsigned char* base = sm + (size_t)st * CF::stage;
+    const double* ys = (const double*)(base + CF::NB * CF::box);
+#pragma unroll 1
+    for (int h = 0; h < 2; ++h) {
+      const int kr = warp * 8 + 2 * tig + h, sw = kr & 7;
+      double a[MT], b[NT];
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi) {
+        const double* xb = (const double*)(base + (mi >> 1) * CF::box);
+        const int c = (mi & 1) * 8 + gid;
+        a[mi] = xb[kr * 16 + (((c >> 1) ^ sw) << 1) + (c & 1)];
+      }
+#pragma unroll
+      for (int ni = 0; ni < NT; ++ni) {
+        const int c = ni * 8 + gid;
+        b[ni] = ys[kr * 16 + (((c >> 1) ^ sw) << 1) + (c & 1)];
+      }
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni) dmma884(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+  // fixed-order cross-warp reduction into stage memory (idle once every
+  // consumer is past its last step; all loads were consumed)
+  bar_consumers();
+  double* Cs = (double*)sm;
+  for (int wv = 0; wv < 8; ++wv) {
+    if (warp == wv) {
+#pragma unroll
+      for (int mi = 0; mi < MT; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int i = mi * 8 + gid, jj = ni * 8 + 2 * tig + e;
+            if (wv == 0)
+              Cs[i * WP + jj] = acc[mi][ni][e];
+            else
+              Cs[i * WP + jj] += acc[mi][ni][e];
+          }
+    }
+    bar_consumers();
+  }
+  const int scols = min(ST, s - s0);
+  for (int idx = tid; idx < ST * WP; idx += 256) {
+    const int i = idx / WP, jj = idx % WP;
+    if (i < scols && jj < w) {
+      if (nsplit == 1)
+        C[(int64_t)(s0 + i) * ldc + jj] = Cs[idx];
+      else
+        part[((int64_t)split * s + s0 + i) * w + jj] = Cs[idx];
+    }
+  }
+}
+
 // Fixed-order split-K reduction: lanes own 32 consecutive outputs, warp k of
 // the CTA sums partials k, k+8, k+16, ... (two interleaved accumulators), the
 // 8 warp sums are added in warp order.  Deterministic for a given nparts.
@@ -260,6 +454,40 @@ static void tn_launch(dim3 grid, const double* X, int64_t ldx, const double* Y, 
   TSVD_CHECK_LAUNCH();
 }
 
+bool g_tn_tma = getenv("TSVD_TN_TMA") ? atoi(getenv("TSVD_TN_TMA")) != 0 : true;
+
+template <int ST>
+static void tn_tma_go(const CUtensorMap& xm, const CUtensorMap& ym, int64_t q, int s, int w,
+                      double* C, int64_t ldc, double* part, cudaStream_t st) {
+  using CF = TnTmaCfg<ST>;
+  const int s_tiles = (s + ST - 1) / ST;
+  const int64_t chunks = (q + TT_RB - 1) / TT_RB;
+  int64_t splits = (int64_t)(2 * 148) / s_tiles;
+  if (splits > chunks / 4) splits = chunks / 4;
+  if (splits < 1) splits = 1;
+  static bool attr = false;
+  if (!attr) {
+    TSVD_CUDA(cudaFuncSetAttribute(gemm_tn_tma_kernel<ST>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
+    attr = true;
+  }
+  gemm_tn_tma_kernel<ST><<<dim3(s_tiles, (unsigned)splits), 288, CF::bytes, st>>>(
+      xm, ym, q, s, w, C, ldc, part);
+  TSVD_CHECK_LAUNCH();
+  if (splits > 1) reduce_launch(part, (int)splits, (int64_t)s * w, C, w, ldc == w ? 0 : ldc, st);
+}
+
+static bool tn_tma_launch(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t q,
+                          int s, int w, double* C, int64_t ldc, double* part, cudaStream_t st) {
+  CUtensorMap xm, ym;
+  if (!make_map(&xm, X, q, s, ldx, TT_RB) || !make_map(&ym, Y, q, w, ldy, TT_RB)) return false;
+  if (s <= 16) tn_tma_go<16>(xm, ym, q, s, w, C, ldc, part, st);
+  else if (s <= 32) tn_tma_go<32>(xm, ym, q, s, w, C, ldc, part, st);
+  else if (s <= 48) tn_tma_go<48>(xm, ym, q, s, w, C, ldc, part, st);
+  else tn_tma_go<64>(xm, ym, q, s, w, C, ldc, part, st);
+  return true;
+}
+
 void gemm_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t q, int s,
              int w, double* C, int64_t ldc, double* part, cudaStream_t st) {
   if (s <= 0 || w <= 0) return;
@@ -273,9 +501,12 @@ void gemm_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t
       TSVD_CUDA(cudaMemsetAsync(C + (int64_t)i * ldc, 0, w * sizeof(double), st));
     return;
   }
+  const bool v2 = aligned16(X, ldx) && aligned16(Y, ldy);
+  if (w > 8 && w <= 16 && v2 && g_tn_tma && q < ((int64_t)1 << 31) &&
+      tn_tma_launch(X, ldx, Y, ldy, q, s, w, C, ldc, part, st))
+    return;
   const TnGeom g = tn_geom(q, s, w);
   dim3 grid(g.s_tiles, g.splits);
-  const bool v2 = aligned16(X, ldx) && aligned16(Y, ldy);
 #define TN_CASE(WPV)                                                              \
   if (v2)                                                                         \
     tn_launch<WPV, 2>(grid, X, ldx, Y, ldy, q, s, w, C, ldc, part, st);          \
@@ -679,37 +910,6 @@ struct NnTmaCfg {
   static constexpr unsigned tx = (unsigned)stage;
 };
 
-__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-  unsigned done = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(smem_u32(b)), "r"(parity)
-        : "memory");
-  } while (!done);
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1,
-                                            uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void bar_consumers() { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }
 
 template <int KC, int S>
 __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
@@ -883,40 +1083,6 @@ __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
       if (i < w && jc < w) gram[(int64_t)blockIdx.x * w * w + i * w + jc] = sum;
     }
   }
-}
-
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult qr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr) ==
-            cudaSuccess &&
-        qr == cudaDriverEntryPointSuccess)
-      fn = (EncodeTiledFn)p;
-  }
-  return fn;
-}
-
-// row-major rows x cols (ld) f64 matrix, box = 16 columns x box_rows, 128B swizzle
-static bool make_map(CUtensorMap* m, const double* base, int64_t rows, int64_t cols, int64_t ld,
-                     int box_rows) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) return false;
-  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)ld * 8};
-  const cuuint32_t box[2] = {16, (cuuint32_t)box_rows};
-  const cuuint32_t es[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 constexpr int NNT_KC = 32, NNT_S = 2;
