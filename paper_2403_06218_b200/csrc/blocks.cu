@@ -134,9 +134,14 @@ static int breakdown(Ctx& c) { return c.deferred ? 0 : read_flags(c); }
 // Row-sharded reductions: every X^T Y or Gram computed on this
 // rank's rows is a partial sum over the row partition; it is all-reduced
 // before use so all ranks continue with identical small matrices.
-static void reduce_gram(Ctx& c, const double* gram, int np, int w, double* Wred) {
-  reduce_partials(gram, np, (int64_t)w * w, Wred, c.st);
+// Single GPU: the finaliser sums the partials itself.  Row partition: sum
+// here (same order), all-reduce, finalise the reduced W (np = 1).
+static const double* reduce_gram(Ctx& c, const double* gram, int& np, int w, double* Wred) {
+  if (!c.comm) return gram;
+  gram_reduce(gram, np, w, Wred, c.st);
   allreduce_sum(c, Wred, (size_t)w * w);
+  np = 1;
+  return Wred;
 }
 
 // TRSM Q = Y L^{-T} (Alg. 4 S3/S6, Alg. 5 S5/S10) is applied as the product
@@ -158,8 +163,9 @@ int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
   }
   {
     Prof p(c, P_SMALL, 0, 0);
-    reduce_gram(c, gram, np, w, Wred);
-    chol_from_w(Wred, w, L1, T1, ortho_flags(c) + 0, c.st);                      // S2
+    int k = np;
+    const double* W = reduce_gram(c, gram, k, w, Wred);
+    chol_finalize(W, k, w, L1, T1, ortho_flags(c) + 0, c.st);                    // S2
   }
   {  // S3 + S4: S = Y L^{-T}, Wbar = S^T S
     Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 3.0 * q * w * w);
@@ -167,8 +173,9 @@ int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
   }
   {
     Prof p(c, P_SMALL, 0, 0);
-    reduce_gram(c, gram, np, w, Wred);
-    chol2_from_w(Wred, w, L1, L2, T2, R, nullptr, nullptr, 0, ortho_flags(c) + 1, c.st);  // S5, S7
+    int k = np;
+    const double* W = reduce_gram(c, gram, k, w, Wred);
+    chol2_finalize(W, k, w, L1, L2, T2, R, nullptr, nullptr, 0, ortho_flags(c) + 1, c.st);  // S5, S7
   }
   if (breakdown(c)) {
     Prof p(c, P_OTHER, 0, 0);
@@ -210,8 +217,9 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
   }
   {
     Prof p(c, P_SMALL, 0, 0);
-    reduce_gram(c, gram, np, w, Wred);
-    chol_from_w(Wred, w, L1, T1, ortho_flags(c) + 0, c.st);                           // S4
+    int k = np;
+    const double* W = reduce_gram(c, gram, k, w, Wred);
+    chol_finalize(W, k, w, L1, T1, ortho_flags(c) + 0, c.st);                         // S4
   }
   {
     Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 1.0 * q * w * w);
@@ -228,8 +236,9 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
   }
   {
     Prof p(c, P_SMALL, 0, 0);
-    reduce_gram(c, gram, np, w, Wred);
-    chol2_from_w(Wred, w, L1, L2, T2, R, H, Hbar, s, ortho_flags(c) + 1, c.st);      // S9,S11,S12
+    int k = np;
+    const double* W = reduce_gram(c, gram, k, w, Wred);
+    chol2_finalize(W, k, w, L1, L2, T2, R, H, Hbar, s, ortho_flags(c) + 1, c.st);    // S9,S11,S12
   }
   if (breakdown(c)) {
     Prof p(c, P_OTHER, 0, 0);

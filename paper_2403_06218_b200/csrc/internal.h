@@ -109,18 +109,16 @@ void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const d
              double alpha, double beta, double* gram, cudaStream_t st);
 
 // small (single-CTA) finalisers (small.cu)
-// W = sum of nparts partial (w x w) Grams; L = chol(W), T = L^{-T}; flag |= breakdown.
-// Wred: w*w workspace for the reduced Gram.
-void chol_finalize(const double* gram, int nparts, int w, double* Wred, double* L, double* T,
-                   int* flag, cudaStream_t st);
+// W = sum of np partial (w x w) Grams; L = chol(W), T = L^{-T}; flag |= breakdown.
+void chol_finalize(const double* gram, int np, int w, double* L, double* T, int* flag,
+                   cudaStream_t st);
 // Lbar = chol(Wbar), Tbar = Lbar^{-T}; R = Lbar^T Lprev^T; H (s x w) += Hbar Lprev^T.
-void chol2_finalize(const double* gram, int nparts, int w, double* Wred, const double* Lprev,
-                    double* L2, double* T2, double* R, double* H, const double* Hbar, int s,
-                    int* flag, cudaStream_t st);
-// the Cholesky finalisers on an already reduced (and all-reduced) Gram W
-void chol_from_w(const double* W, int w, double* L, double* T, int* flag, cudaStream_t st);
-void chol2_from_w(const double* W, int w, const double* Lprev, double* L2, double* T2,
-                  double* R, double* H, const double* Hbar, int s, int* flag, cudaStream_t st);
+void chol2_finalize(const double* gram, int np, int w, const double* Lprev, double* L2,
+                    double* T2, double* R, double* H, const double* Hbar, int s, int* flag,
+                    cudaStream_t st);
+// W = the same fixed-order sum of np Gram partials the finalisers form (for
+// the all-reduce of the multi-GPU path; then finalise with np = 1)
+void gram_reduce(const double* gram, int np, int w, double* Wred, cudaStream_t st);
 // out[i] = sum_p part[p*count + i], fixed order
 void reduce_partials(const double* part, int nparts, int64_t count, double* out,
                      cudaStream_t st);

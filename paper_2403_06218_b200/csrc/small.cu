@@ -56,102 +56,191 @@ __device__ void warp_tri_inverse_t(const double* Lo, double* Xs, double* Tout, i
     for (int i = 0; i < w; ++i) Tout[j * w + i] = Xs[i * 33 + j];  // T[j][i] = Linv[i][j]
 }
 
-__global__ void chol_finalize_kernel(const double* __restrict__ gram, int nparts, int w,
-                                     double* __restrict__ L, double* __restrict__ T,
-                                     int* __restrict__ flag) {
-  __shared__ double Ws[32 * 33];
-  __shared__ double Lo[32 * 32];
-  __shared__ int bad;
-  const int tid = threadIdx.x;
-  if (tid == 0) bad = 0;
-  for (int i = tid; i < w * w; i += blockDim.x) {
-    double s = 0.0;
-    for (int p = 0; p < nparts; ++p) s += gram[(int64_t)p * w * w + i];
-    Ws[i] = s;
-  }
-  for (int i = tid; i < 32 * 32; i += blockDim.x) Lo[i] = 0.0;
-  __syncthreads();
-  if (tid < 32) warp_cholesky(Ws, Lo, w, &bad);
-  __syncthreads();
-  for (int i = tid; i < w * w; i += blockDim.x) L[i] = Lo[(i / w) * 32 + (i % w)];
-  if (tid < 32) warp_tri_inverse_t(Lo, Ws, T, w);
-  if (tid == 0 && bad) *flag = 1;
-}
+// Fused Gram finaliser, one CTA of FIN_T threads:
+//   1. W = sum of the np per-CTA Gram partials in a fixed order (thread t sums
+//      partials g, g+G, g+2G, ... of entry e = t mod w^2, g = t div w^2,
+//      G = FIN_T div w^2; the G group sums are added in g order).  np = 1
+//      passes an already reduced W through bit for bit.
+//   2. mode >= 1: L = chol(W) with the breakdown test of P:275 and
+//      T = L^{-T}; w <= 16 in registers (row i of W in lane i, right-looking
+//      updates by shuffles; the column scaling multiplies by 1/l_jj =
+//      rsqrt(pivot) as LAPACK's potf2 scales by a reciprocal, and the same
+//      reciprocals serve the triangular inverse - no f64 divisions, which are
+//      long dependent sequences on the GPU), else the shared-memory routines.
+//   3. mode 2: R = Lbar^T Lprev^T (R4), H += Hbar Lprev^T (R5); Hbar is
+//      staged into shared memory by all threads while step 2 runs.
+// mode 0 only writes W (the multi-GPU path all-reduces it, then calls mode
+// 1/2 with np = 1), so one and several ranks see identical arithmetic.
+constexpr int FIN_T = 512;
+constexpr int FIN_HB = 8192;  // doubles of Hbar staged per chunk (64 KB dynamic smem)
 
-void chol_from_w(const double* W, int w, double* L, double* T, int* flag, cudaStream_t st) {
-  chol_finalize_kernel<<<1, 256, 0, st>>>(W, 1, w, L, T, flag);
-  TSVD_CHECK_LAUNCH();
-}
-
-void chol_finalize(const double* gram, int nparts, int w, double* Wred, double* L, double* T,
-                   int* flag, cudaStream_t st) {
-  reduce_partials(gram, nparts, (int64_t)w * w, Wred, st);
-  chol_finalize_kernel<<<1, 256, 0, st>>>(Wred, 1, w, L, T, flag);
-  TSVD_CHECK_LAUNCH();
-}
-
-// Second pass: Lbar = chol(Wbar), Tbar = Lbar^{-T}; R = Lbar^T Lprev^T (Alg. 4 S7 /
-// Alg. 5 S11, reading R4); H (s x w) += Hbar Lprev^T (Alg. 5 S12, reading R5).
-__global__ void chol2_finalize_kernel(const double* __restrict__ gram, int nparts, int w,
-                                      const double* __restrict__ Lprev, double* __restrict__ L2,
-                                      double* __restrict__ T2, double* __restrict__ R,
-                                      double* __restrict__ H, const double* __restrict__ Hbar,
-                                      int s, int* __restrict__ flag) {
+template <int WT>  // WT > 0: w == WT (all loops unrolled, no divergence); 0: any w <= 32
+__global__ void __launch_bounds__(FIN_T) finalize_kernel(
+    const double* __restrict__ gram, int np, int w_, int mode, double* __restrict__ Wout,
+    const double* __restrict__ Lprev, double* __restrict__ L, double* __restrict__ T,
+    double* __restrict__ R, double* __restrict__ H, const double* __restrict__ Hbar, int s,
+    int* __restrict__ flag) {
+  __shared__ double red[FIN_T];
   __shared__ double Ws[32 * 33];
   __shared__ double Lo[32 * 32];
   __shared__ double Lp[32 * 32];
+  __shared__ double Xs[32 * 33];
+  __shared__ double rsd[32];
   __shared__ int bad;
-  const int tid = threadIdx.x;
+  extern __shared__ double hbs[];
+  const int w = WT > 0 ? WT : w_;
+  const int tid = threadIdx.x, C = w * w, G = FIN_T / C;
+  const int64_t nh = (mode == 2 && H) ? (int64_t)s * w : 0;
   if (tid == 0) bad = 0;
-  for (int i = tid; i < w * w; i += blockDim.x) {
-    double sum = 0.0;
-    for (int p = 0; p < nparts; ++p) sum += gram[(int64_t)p * w * w + i];
-    Ws[i] = sum;
-    Lp[i] = Lprev[i];
+  if (tid < G * C) {
+    const int e = tid % C, g = tid / C;
+    double a = 0.0;
+#pragma unroll 16
+    for (int p = g; p < np; p += G) a += gram[(int64_t)p * C + e];
+    red[tid] = a;
   }
-  for (int i = tid; i < 32 * 32; i += blockDim.x) Lo[i] = 0.0;
-  __syncthreads();
-  if (tid < 32) warp_cholesky(Ws, Lo, w, &bad);
-  __syncthreads();
-  if (tid < 32) warp_tri_inverse_t(Lo, Ws, T2, w);
-  for (int i = tid; i < w * w; i += blockDim.x) {
-    const int r = i / w, c = i % w;
-    L2[i] = Lo[r * 32 + c];
-    // R[r][c] = sum_k Lbar[k][r] * Lprev[c][k]
-    double sum = 0.0;
-    for (int k = 0; k < w; ++k) sum = fma(Lo[k * 32 + r], Lp[c * w + k], sum);
-    R[i] = sum;
+  if (mode == 2)
+    for (int i = tid; i < C; i += FIN_T) Lp[i] = Lprev[i];
+  for (int i = tid; i < 32 * 32; i += FIN_T) Lo[i] = 0.0;
+  // first Hbar chunk in flight during the Cholesky
+  {
+    const int n0 = (int)(nh < FIN_HB ? nh : FIN_HB);
+    for (int i = tid; i < n0; i += FIN_T) hbs[i] = Hbar[i];
   }
-  if (H) {
-    // one H row per thread: its w Hbar entries are loaded together
-    for (int r = tid; r < s; r += blockDim.x) {
-      double hb[32];
+  __syncthreads();
+  if (tid < C) {
+    double a = red[tid];
+    for (int g = 1; g < G; ++g) a += red[g * C + tid];
+    Ws[tid] = a;
+    if (mode == 0) Wout[tid] = a;
+  }
+  __syncthreads();
+  if (mode == 0) return;
+  if constexpr (WT > 0) {
+    if (tid < 32) {
+      const int lane = tid;
+      double a[WT];
 #pragma unroll
-      for (int k = 0; k < 32; ++k) hb[k] = k < w ? Hbar[(int64_t)r * w + k] : 0.0;
-      for (int c = 0; c < w; ++c) {
-        double sum = 0.0;
+      for (int k = 0; k < WT; ++k) a[k] = (lane < WT && k <= lane) ? Ws[lane * WT + k] : 0.0;
+      int bd = 0;
 #pragma unroll
-        for (int k = 0; k < 32; ++k)
-          if (k < w) sum = fma(hb[k], Lp[c * w + k], sum);
-        H[(int64_t)r * w + c] += sum;
+      for (int j = 0; j < WT; ++j) {
+        double piv = __shfl_sync(~0u, a[j], j);
+        if (!(piv > 0.0) || !isfinite(piv)) {
+          bd = 1;
+          piv = 1.0;
+        }
+        const double rj = rsqrt(piv);
+        if (lane == 0) rsd[j] = rj;
+        const double lij = lane > j ? a[j] * rj : (lane == j ? piv * rj : 0.0);
+        a[j] = lij;
+#pragma unroll
+        for (int k = j + 1; k < WT; ++k) {
+          const double lkj = __shfl_sync(~0u, lij, k);
+          a[k] = (lane >= k) ? fma(-lij, lkj, a[k]) : a[k];
+        }
       }
+      if (lane == 0 && bd) bad = 1;
+      if (lane < WT)
+#pragma unroll
+        for (int k = 0; k < WT; ++k) Lo[lane * 32 + k] = a[k];
+      __syncwarp();
+      // column `lane` of L^{-1} by forward substitution (x[m] kept in Xs);
+      // 1/l_ii = rsd[i] from the factorisation
+#pragma unroll
+      for (int i = 0; i < WT; ++i) {
+        double v = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+        for (int m = 0; m < i; ++m) v = fma(-__shfl_sync(~0u, a[m], i), Xs[m * 33 + lane], v);
+        Xs[i * 33 + lane] = (i >= lane) ? v * rsd[i] : 0.0;
+      }
+    }
+  } else if (tid < 32) {
+    warp_cholesky(Ws, Lo, w, &bad);
+    warp_tri_inverse_t(Lo, Ws, T, w);  // Ws is free now; writes T
+  }
+  __syncthreads();
+  for (int i = tid; i < C; i += FIN_T) {
+    const int r = i / w, c = i % w;
+    L[i] = Lo[r * 32 + c];
+    if constexpr (WT > 0) T[i] = Xs[c * 33 + r];  // T[r][c] = Linv[c][r]
+    if (mode == 2) {
+      double sum = 0.0;  // R[r][c] = sum_k Lbar[k][r] Lprev[c][k]
+      if constexpr (WT > 0) {
+#pragma unroll
+        for (int k = 0; k < WT; ++k) sum = fma(Lo[k * 32 + r], Lp[c * WT + k], sum);
+      } else {
+        for (int k = 0; k < w; ++k) sum = fma(Lo[k * 32 + r], Lp[c * w + k], sum);
+      }
+      R[i] = sum;
+    }
+  }
+  // H[r][c] += sum_k Hbar[r][k] Lprev[c][k], Hbar staged in chunks of whole rows
+  const int rows_per = FIN_HB / w;
+  for (int r0 = 0; (int64_t)r0 * w < nh; r0 += rows_per) {
+    const int cnt = (rows_per < s - r0 ? rows_per : s - r0) * w;
+    if (r0 > 0) {
+      __syncthreads();
+      for (int i = tid; i < cnt; i += FIN_T) hbs[i] = Hbar[(int64_t)r0 * w + i];
+      __syncthreads();
+    }
+    for (int i = tid; i < cnt; i += FIN_T) {
+      const int r = i / w, c = i % w;
+      const double* hb = hbs + r * w;
+      double sum = 0.0;
+      if constexpr (WT > 0) {
+#pragma unroll
+        for (int k = 0; k < WT; ++k) sum = fma(hb[k], Lp[c * WT + k], sum);
+      } else {
+        for (int k = 0; k < w; ++k) sum = fma(hb[k], Lp[c * w + k], sum);
+      }
+      H[(int64_t)r0 * w + i] += sum;
     }
   }
   if (tid == 0 && bad) *flag = 1;
 }
 
-void chol2_from_w(const double* W, int w, const double* Lprev, double* L2, double* T2,
-                  double* R, double* H, const double* Hbar, int s, int* flag, cudaStream_t st) {
-  chol2_finalize_kernel<<<1, 256, 0, st>>>(W, 1, w, Lprev, L2, T2, R, H, Hbar, s, flag);
+static void fin_launch(const double* gram, int np, int w, int mode, double* Wout,
+                       const double* Lprev, double* L, double* T, double* R, double* H,
+                       const double* Hbar, int s, int* flag, cudaStream_t st) {
+  static bool attr = false;
+  const int dyn = FIN_HB * 8;
+  if (!attr) {
+    TSVD_CUDA(cudaFuncSetAttribute(finalize_kernel<0>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    TSVD_CUDA(cudaFuncSetAttribute(finalize_kernel<4>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    TSVD_CUDA(cudaFuncSetAttribute(finalize_kernel<8>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    TSVD_CUDA(cudaFuncSetAttribute(finalize_kernel<16>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    attr = true;
+  }
+#define FIN_GO(WTV)                                                                           \
+  finalize_kernel<WTV><<<1, FIN_T, dyn, st>>>(gram, np, w, mode, Wout, Lprev, L, T, R, H, Hbar, \
+                                              s, flag)
+  if (w == 16) FIN_GO(16);
+  else if (w == 8) FIN_GO(8);
+  else if (w == 4) FIN_GO(4);
+  else FIN_GO(0);
+#undef FIN_GO
   TSVD_CHECK_LAUNCH();
 }
 
-void chol2_finalize(const double* gram, int nparts, int w, double* Wred, const double* Lprev,
-                    double* L2, double* T2, double* R, double* H, const double* Hbar, int s,
-                    int* flag, cudaStream_t st) {
-  reduce_partials(gram, nparts, (int64_t)w * w, Wred, st);
-  chol2_finalize_kernel<<<1, 256, 0, st>>>(Wred, 1, w, Lprev, L2, T2, R, H, Hbar, s, flag);
-  TSVD_CHECK_LAUNCH();
+void gram_reduce(const double* gram, int np, int w, double* Wred, cudaStream_t st) {
+  fin_launch(gram, np, w, 0, Wred, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0,
+             nullptr, st);
+}
+
+void chol_finalize(const double* gram, int np, int w, double* L, double* T, int* flag,
+                   cudaStream_t st) {
+  fin_launch(gram, np, w, 1, nullptr, nullptr, L, T, nullptr, nullptr, nullptr, 0, flag, st);
+}
+
+void chol2_finalize(const double* gram, int np, int w, const double* Lprev, double* L2,
+                    double* T2, double* R, double* H, const double* Hbar, int s, int* flag,
+                    cudaStream_t st) {
+  fin_launch(gram, np, w, 2, nullptr, Lprev, L2, T2, R, H, Hbar, s, flag, st);
 }
 
 // --------------------------------------------------------------- helpers ---
