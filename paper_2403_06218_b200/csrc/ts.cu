@@ -1085,6 +1085,132 @@ __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
   }
 }
 
+// Output products Z = X H with w up to 64 (Alg. 2 S8/S9: V = P Vbar_r,
+// U = Pbar Ubar_r; Alg. 1 S6/S7), beta = 0 and no Gram: the same TMA ring
+// as gemm_nn_tma_kernel with 4 H boxes (64 columns) per stage, one
+// accumulator set of 2 x 8 DMMA tiles per warp, and Z stored straight from
+// the accumulator fragments (no shared out tile).  These products are
+// DMMA-bound (2 s w flops per 8 s bytes).
+template <int KC, int S>
+struct NnOutCfg {
+  static constexpr int NB = KC / 16;
+  static constexpr size_t xbox = (size_t)NT_R * 16 * 8;
+  static constexpr size_t hbox = (size_t)KC * 16 * 8;
+  static constexpr size_t stage = NB * xbox + 4 * hbox;
+  static constexpr size_t bar_off = S * stage;
+  static constexpr size_t bytes = bar_off + 2 * S * 8 + 1024;
+  static constexpr unsigned tx = (unsigned)stage;
+};
+
+template <int KC, int S, int NT>  // NT = 8-column tiles computed (w <= 8 NT <= 64)
+__global__ void __launch_bounds__(288, 1) gemm_nn_out_tma_kernel(
+    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap, double* Z,
+    int64_t ldz, int64_t q, int s, int w, double alpha) {
+  using CF = NnOutCfg<KC, S>;
+  extern __shared__ unsigned char smraw[];
+  unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = (uint64_t*)(sm + CF::bar_off);
+  uint64_t* empty = full + S;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int prow = ((gid & 1) << 2) | (gid >> 1);
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t ntiles = (q + NT_R - 1) / NT_R;
+  const int64_t my_tiles =
+      (ntiles > (int64_t)blockIdx.x) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int nk = (s + KC - 1) / KC;
+  const int64_t nsteps = my_tiles * nk;
+  if (warp == 8) {
+    if (lane == 0) {
+      for (int64_t j = 0; j < nsteps; ++j) {
+        const int st = (int)(j % S);
+        const unsigned u = (unsigned)(j / S);
+        if (j >= S) mbar_wait(&empty[st], (u - 1) & 1);
+        const int64_t lt = j / nk;
+        const int kc = (int)(j % nk);
+        const int r0 = (int)((blockIdx.x + lt * gridDim.x) * NT_R);
+        unsigned char* base = sm + (size_t)st * CF::stage;
+        mbar_expect_tx(&full[st], CF::tx);
+#pragma unroll
+        for (int b = 0; b < CF::NB; ++b)
+          tma_load_2d(base + b * CF::xbox, &xmap, kc * KC + b * 16, r0, &full[st]);
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+          tma_load_2d(base + CF::NB * CF::xbox + b * CF::hbox, &hmap, b * 16, kc * KC, &full[st]);
+      }
+    }
+    return;
+  }
+  const bool vec = ((ldz & 1) == 0) && ((((uintptr_t)Z) & 15) == 0);
+  double acc[2][NT][2];
+  for (int64_t j = 0; j < nsteps; ++j) {
+    const int st = (int)(j % S);
+    const int kc = (int)(j % nk);
+    const int64_t r0 = (blockIdx.x + (j / nk) * gridDim.x) * NT_R;
+    if (kc == 0) {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+    }
+    mbar_wait(&full[st], (unsigned)(j / S) & 1);
+    {
+      const unsigned char* base = sm + (size_t)st * CF::stage;
+      const unsigned char* hb0 = base + CF::NB * CF::xbox;
+#pragma unroll
+      for (int kk2 = 0; kk2 < KC / 8; ++kk2) {
+        const double* xb = (const double*)(base + (kk2 >> 1) * CF::xbox);
+        const int chunk = (((kk2 & 1) << 2) | tig) ^ prow;
+        const double2 a0 =
+            *reinterpret_cast<const double2*>(xb + (warp * 16 + prow) * 16 + chunk * 2);
+        const double2 a1 =
+            *reinterpret_cast<const double2*>(xb + (warp * 16 + 8 + prow) * 16 + chunk * 2);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int hr = kk2 * 8 + 2 * tig + h;
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) {
+            const double* hs = (const double*)(hb0 + (ni >> 1) * CF::hbox);
+            const int c = (ni & 1) * 8 + gid;
+            const double b = hs[hr * 16 + (((c >> 1) ^ (hr & 7)) << 1) + (c & 1)];
+            dmma884(acc[0][ni][0], acc[0][ni][1], h ? a0.y : a0.x, b);
+            dmma884(acc[1][ni][0], acc[1][ni][1], h ? a1.y : a1.x, b);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (kc == nk - 1) {
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        const int64_t row = r0 + warp * 16 + mi * 8 + prow;
+        if (row < q) {
+          double* zr = Z + row * ldz;
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) {
+            const int c = ni * 8 + 2 * tig;
+            const double z0 = alpha * acc[mi][ni][0], z1 = alpha * acc[mi][ni][1];
+            if (vec && c + 1 < w) {
+              *reinterpret_cast<double2*>(zr + c) = make_double2(z0, z1);
+            } else {
+              if (c < w) zr[c] = z0;
+              if (c + 1 < w) zr[c + 1] = z1;
+            }
+          }
+        }
+      }
+    }
+  }
+}
+
 constexpr int NNT_KC = 32, NNT_S = 2;
 
 static bool nn_tma_launch(const double* X, int64_t ldx, const double* H, int64_t ldh,
@@ -1103,6 +1229,39 @@ static bool nn_tma_launch(const double* X, int64_t ldx, const double* H, int64_t
   }
   gemm_nn_tma_kernel<NNT_KC, NNT_S><<<nn_ctas(q, 16), 288, CF::bytes, st>>>(
       xm, hm, Y, ldy, T, Z, ldz, q, s, w, alpha, beta, gram);
+  TSVD_CHECK_LAUNCH();
+  return true;
+}
+
+static bool nn_out_tma_launch(const double* X, int64_t ldx, const double* H, int64_t ldh,
+                              double* Z, int64_t ldz, int64_t q, int s, int w, double alpha,
+                              cudaStream_t st) {
+  if (q >= (int64_t)1 << 31 || s >= (1 << 30)) return false;
+  CUtensorMap xm, hm;
+  if (!make_map(&xm, X, q, s, ldx, NT_R) || !make_map(&hm, H, s, w, ldh, NNT_KC)) return false;
+  constexpr int OS = 4;  // one CTA per SM (register-heavy), deeper ring
+  using CF = NnOutCfg<NNT_KC, OS>;
+  static bool attr = false;
+  if (!attr) {
+    TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_out_tma_kernel<NNT_KC, OS, 5>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
+    TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_out_tma_kernel<NNT_KC, OS, 6>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
+    TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_out_tma_kernel<NNT_KC, OS, 7>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
+    TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_out_tma_kernel<NNT_KC, OS, 8>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
+    attr = true;
+  }
+  const int nt = (w + 7) / 8;
+#define OUT_GO(NTV)                                                                       \
+  gemm_nn_out_tma_kernel<NNT_KC, OS, NTV><<<nn_ctas(q, 32), 288, CF::bytes, st>>>(xm, hm, Z, \
+                                                                                ldz, q, s, w, alpha)
+  if (nt <= 5) OUT_GO(5);
+  else if (nt == 6) OUT_GO(6);
+  else if (nt == 7) OUT_GO(7);
+  else OUT_GO(8);
+#undef OUT_GO
   TSVD_CHECK_LAUNCH();
   return true;
 }
@@ -1130,6 +1289,13 @@ void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const d
   if (w <= 0 || q <= 0) return;
   if (w > 32) {
     if (T || gram) throw Error{TSVD_EINVAL, "gemm_nn: T/gram need w <= 32"};
+    if (beta == 0.0 && s > 0 && g_nn_tma && aligned16(X, ldx) && aligned16(H, ldh)) {
+      bool done = true;
+      for (int c0 = 0; c0 < w && done; c0 += 64)
+        done = nn_out_tma_launch(X, ldx, H + c0, ldh, Z + c0, ldz, q, s, std::min(64, w - c0),
+                                 alpha, st);
+      if (done) return;
+    }
     const int cw = (beta == 0.0) ? 64 : 32;  // wide products (outputs) in one pass per 64 cols
     if (w > cw) {
       for (int c0 = 0; c0 < w; c0 += cw)

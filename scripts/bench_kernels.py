@@ -94,6 +94,20 @@ def sweep_bench():
               f"nn {ms_nn:.3f} ms {gnn:5.0f} GB/s ({gnn / HBM:.2f})", flush=True)
 
 
+def out_bench():
+    """output products Z = X H (beta = 0), w = r = 50 and 64 (U = Pbar Ubar_r)"""
+    q, s = 1_000_000, 384
+    X = torch.randn((q, s + 16), dtype=torch.float64, device="cuda")
+    H = torch.randn((s, s), dtype=torch.float64, device="cuda")
+    for w in (50, 64, 16):
+        Z = torch.empty((q, w), dtype=torch.float64, device="cuda")
+        ms = timeit(lambda: T.lib().tsvd_dbg_gemm_nn(X.data_ptr(), X.stride(0), H.data_ptr(), s,
+                                                     Z.data_ptr(), w, q, s, w, 1.0, 0.0, None))
+        tf = 2.0 * q * s * w / (ms * 1e-3) / 1e12
+        gb = 8.0 * q * (s + w) / (ms * 1e-3) / 1e9
+        print(f"gemm_nn(out) q={q} s={s} w={w}: {ms:.3f} ms  {tf:.1f} TF/s  {gb:.0f} GB/s", flush=True)
+
+
 def nn0_bench():
     """single s=0 and s=384 gemm_nn launches (for ncu)"""
     q, w = 1_000_000, 16
