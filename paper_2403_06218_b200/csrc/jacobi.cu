@@ -24,6 +24,9 @@
 //   [g_p g_q] <- [g_p g_q] [[cs, sn], [-sn, cs]].
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace tsvd {
@@ -42,9 +45,19 @@ static int jac_nb(int d) {
   return nb;
 }
 
+static size_t jac_layout(size_t d, size_t dp) { return d * dp + dp * dp + dp; }
+
 size_t small_svd_work(int d) {
-  const size_t nb = (size_t)jac_nb(d), dp = nb * JC;
-  return (size_t)d * dp + dp * dp + dp + 64;
+  const size_t dp8 = (size_t)jac_nb(d) * JC;
+  size_t n = jac_layout(d, dp8);
+  const size_t dp4 = (size_t)(((d + 3) / 4 + 1) & ~1) * 4 + 8;
+  n = std::max(n, jac_layout(d, dp4));
+  const size_t dp2 = (size_t)(((d + 1) / 2 + 1) & ~1) * 2 + 8;
+  n = std::max(n, jac_layout(d, dp2));
+  return n + 64;  // control words live in the last 64 doubles
+}
+static unsigned* jac_ctl(double* work, int d) {
+  return (unsigned*)(work + small_svd_work(d) - 64);
 }
 
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
@@ -268,8 +281,6 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(double* __restrict__ 
 // threads accumulate them into the 2JC x 2JC orthogonal J (shared memory).
 // After the inner sweep the V rows are streamed through registers and
 // multiplied by J.
-constexpr int JR_T = 256;
-
 __host__ __device__ constexpr int cpair_lo(int t, int r, int jw) {
   const int p = (t == 0) ? 0 : ((t - 1 + r) % (jw - 1)) + 1;
   const int q = ((jw - 2 - t + r) % (jw - 1)) + 1;
@@ -281,7 +292,142 @@ __host__ __device__ constexpr int cpair_hi(int t, int r, int jw) {
   return p < q ? q : p;
 }
 
-template <int RG, int JC>
+// one recursive-halving level: M live values -> M/2 (lanes with bit o set
+// keep the upper half)
+template <int NVP, int M, int O>
+__device__ __forceinline__ void rs_level(double (&v)[NVP], int lane) {
+  if constexpr (O >= 1) {
+    const bool up = (lane & O) != 0;
+#pragma unroll
+    for (int i = 0; i < M / 2; ++i) {
+      const double send = up ? v[i] : v[i + M / 2], keep = up ? v[i + M / 2] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, O);
+    }
+    rs_level<NVP, M / 2, O / 2>(v, lane);
+  }
+}
+
+// warp reduce-scatter; afterwards NVP >= 32: v[j] = warp sum of value
+// lane * (NVP/32) + j; NVP == 16: v[0] = warp sum of value lane % 16
+template <int NVP>
+__device__ __forceinline__ void warp_reduce_scatter(double (&v)[NVP], int lane) {
+  if constexpr (NVP == 16) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], 16);
+    rs_level<16, 16, 8>(v, lane);
+  } else {
+    rs_level<NVP, NVP, 16>(v, lane);
+  }
+}
+
+// pair t of inner round ir: MODE 0 = circle over all 2 JB columns (2 JB - 1
+// inner rounds), 1 = inside each of the two blocks (JB - 1), 2 = the JB x JB
+// cross pairs (JB inner rounds)
+template <int JB, int MODE>
+__device__ __forceinline__ void jac_pair(int t, int ir, int& p, int& q) {
+  if constexpr (MODE == 0) {
+    p = cpair_lo(t, ir, 2 * JB);
+    q = cpair_hi(t, ir, 2 * JB);
+  } else if constexpr (MODE == 1) {
+    const int h = JB / 2;
+    const int off = t < h ? 0 : JB, tt = t < h ? t : t - h;
+    p = off + cpair_lo(tt, ir, JB);
+    q = off + cpair_hi(tt, ir, JB);
+  } else {
+    p = t;
+    q = JB + (t + ir) % JB;
+  }
+}
+
+
+// One inner round on the 2 JB columns held in registers (RG rows per
+// thread, NTHR threads): dot products -> warp reduce-scatter -> fixed-order
+// sum over warps -> JB rotations (Rutishauser) -> apply to the columns and to J.
+template <int RG, int JB, int MODE, int NTHR>
+__device__ __forceinline__ void jac_inner(int ir, double (&x)[RG][2 * JB],
+                                          double (*red)[3 * JB + 1], double* rot_cs,
+                                          double* rot_sn, double (*Js)[2 * JB + 1], int* any_rot,
+                                          double tol) {
+  constexpr int JW = 2 * JB, NV = 3 * JB;
+  constexpr int NVP = NV <= 16 ? 16 : (NV <= 32 ? 32 : 64);
+  constexpr int NW = NTHR / 32;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double v[NVP];
+#pragma unroll
+  for (int i = NV; i < NVP; ++i) v[i] = 0.0;
+#pragma unroll
+  for (int t = 0; t < JB; ++t) {
+    int p, q;
+    jac_pair<JB, MODE>(t, ir, p, q);
+    double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+    for (int k = 0; k < RG; ++k) {
+      a = fma(x[k][p], x[k][p], a);
+      b = fma(x[k][q], x[k][q], b);
+      c = fma(x[k][p], x[k][q], c);
+    }
+    v[3 * t] = a;
+    v[3 * t + 1] = b;
+    v[3 * t + 2] = c;
+  }
+  warp_reduce_scatter<NVP>(v, lane);
+  if constexpr (NVP >= 32) {
+#pragma unroll
+    for (int j = 0; j < NVP / 32; ++j) {
+      const int idx = lane * (NVP / 32) + j;
+      if (idx < NV) red[warp][idx] = v[j];
+    }
+  } else {
+    if (lane < NV) red[warp][lane] = v[0];
+  }
+  __syncthreads();
+  if (tid < JB) {
+    double a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+    for (int w2 = 0; w2 < NW; ++w2) {
+      a += red[w2][3 * tid];
+      b += red[w2][3 * tid + 1];
+      c += red[w2][3 * tid + 2];
+    }
+    double cs = 1.0, sn = 0.0;
+    if (a > 0.0 && b > 0.0 && fabs(c) > tol * sqrt(a * b)) {
+      const double h = 0.5 * (b - a);
+      const double t = (h >= 0.0 ? c : -c) / (fabs(h) + sqrt(fma(h, h, c * c)));
+      cs = rsqrt(fma(t, t, 1.0));
+      sn = cs * t;
+      *any_rot = 1;
+    }
+    rot_cs[tid] = cs;
+    rot_sn[tid] = sn;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int t = 0; t < JB; ++t) {
+    int p, q;
+    jac_pair<JB, MODE>(t, ir, p, q);
+    const double cs = rot_cs[t], sn = rot_sn[t];
+#pragma unroll
+    for (int k = 0; k < RG; ++k) {
+      const double xp = x[k][p], xq = x[k][q];
+      x[k][p] = cs * xp - sn * xq;
+      x[k][q] = sn * xp + cs * xq;
+    }
+  }
+  static_assert(JB * 2 * JB <= NTHR, "J update: one thread per entry");
+  if (tid < JB * JW) {
+    const int t = tid / JW, i = tid % JW;
+    int p, q;
+    jac_pair<JB, MODE>(t, ir, p, q);
+    const double cs = rot_cs[t], sn = rot_sn[t];
+    const double jp = Js[i][p], jq = Js[i][q];
+    Js[i][p] = cs * jp - sn * jq;
+    Js[i][q] = sn * jp + cs * jq;
+  }
+}
+
+constexpr int JR_T = 256;
+
+template <int RG, int JC, bool CYC>
 __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict__ G,
                                                             double* __restrict__ V, int d, int nb,
                                                             double* __restrict__ nrm,
@@ -292,7 +438,6 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
   constexpr int JW = 2 * JC;   // columns of a block pair (shadows the file-scope JW)
   constexpr int NW = JR_T / 32;
   constexpr int NV = 3 * JC;  // partial sums per inner round
-  constexpr int NVP = NV > 16 ? 32 : 16;
   __shared__ double red[NW][NV + 1];
   __shared__ double rot_cs[JC], rot_sn[JC];
   __shared__ double Js[JW][JW + 1];
@@ -305,10 +450,19 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
   const double tol = (double)d * 0x1.0p-53;
   double x[RG][JW];
   int sweep = 0;
+  // CYC: cyclic-by-blocks sweep (round 0 inside the home blocks 2k, 2k+1,
+  // then nb-1 rounds of cross pairs: every pair once, ~d inner rounds);
+  // else each round sweeps all pairs of the 2 JC columns (~2d inner rounds)
+  const int nrounds = CYC ? nb : nb - 1;
   for (; sweep < kMaxSweeps; ++sweep) {
-    for (int round = 0; round < nb - 1; ++round) {
+    for (int round = 0; round < nrounds; ++round) {
       int bi, bj;
-      circle_pair(blockIdx.x, round, nb, bi, bj);
+      if (CYC && round == 0) {
+        bi = 2 * blockIdx.x;
+        bj = 2 * blockIdx.x + 1;
+      } else {
+        circle_pair(blockIdx.x, CYC ? round - 1 : round, nb, bi, bj);
+      }
 #pragma unroll
       for (int k = 0; k < RG; ++k) {
         const int row = tid + JR_T * k;
@@ -318,91 +472,32 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
           x[k][c] = row < d ? G[(size_t)col * d + row] : 0.0;
         }
       }
+      // this round's V rows: in flight during the inner rounds (the pair's V
+      // columns belong to this CTA until the grid barrier)
+      double vv[RG][JW];
+#pragma unroll
+      for (int k = 0; k < RG; ++k) {
+        const int row = tid + JR_T * k;
+#pragma unroll
+        for (int c = 0; c < JW; ++c) {
+          const int col = c < JC ? bi * JC + c : bj * JC + (c - JC);
+          vv[k][c] = row < dp ? V[(size_t)col * dp + row] : 0.0;
+        }
+      }
       if (tid < JW * JW) Js[tid / JW][tid % JW] = (tid / JW == tid % JW) ? 1.0 : 0.0;
       if (tid == 0) any_rot = 0;
+      if (!CYC) {
 #pragma unroll
-      for (int ir = 0; ir < JW - 1; ++ir) {
-        double v[NVP];
+        for (int ir = 0; ir < JW - 1; ++ir)
+          jac_inner<RG, JC, 0, JR_T>(ir, x, red, rot_cs, rot_sn, Js, &any_rot, tol);
+      } else if (round == 0) {
 #pragma unroll
-        for (int i = NV; i < NVP; ++i) v[i] = 0.0;
+        for (int ir = 0; ir < JC - 1; ++ir)
+          jac_inner<RG, JC, 1, JR_T>(ir, x, red, rot_cs, rot_sn, Js, &any_rot, tol);
+      } else {
 #pragma unroll
-        for (int t = 0; t < JC; ++t) {
-          const int p = cpair_lo(t, ir, JW), q = cpair_hi(t, ir, JW);
-          double a = 0.0, b = 0.0, c = 0.0;
-#pragma unroll
-          for (int k = 0; k < RG; ++k) {
-            a = fma(x[k][p], x[k][p], a);
-            b = fma(x[k][q], x[k][q], b);
-            c = fma(x[k][p], x[k][q], c);
-          }
-          v[3 * t] = a;
-          v[3 * t + 1] = b;
-          v[3 * t + 2] = c;
-        }
-        // recursive-halving butterfly over 32 lanes on NV (zero-padded to NVP)
-        // values: afterwards lane l holds the warp sum of value l % NVP
-        if constexpr (NVP == 32) {
-          const bool up = (lane & 16) != 0;
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const double lo = v[i], hi = v[i + 16];
-            const double send = up ? lo : hi, keep = up ? hi : lo;
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < NVP; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], 16);
-        }
-#pragma unroll
-        for (int o = 8; o >= 1; o >>= 1) {
-          const bool up = (lane & o) != 0;
-#pragma unroll
-          for (int i = 0; i < o; ++i) {
-            const double send = up ? v[i] : v[i + o], keep = up ? v[i + o] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-          }
-        }
-        if (lane < NV) red[warp][lane] = v[0];
-        __syncthreads();
-        if (tid < JC) {
-          double a = 0.0, b = 0.0, c = 0.0;
-#pragma unroll
-          for (int w2 = 0; w2 < NW; ++w2) {
-            a += red[w2][3 * tid];
-            b += red[w2][3 * tid + 1];
-            c += red[w2][3 * tid + 2];
-          }
-          double cs = 1.0, sn = 0.0;
-          if (a > 0.0 && b > 0.0 && fabs(c) > tol * sqrt(a * b)) {
-            const double h = 0.5 * (b - a);
-            const double t = (h >= 0.0 ? c : -c) / (fabs(h) + sqrt(fma(h, h, c * c)));
-            cs = rsqrt(fma(t, t, 1.0));
-            sn = cs * t;
-            any_rot = 1;
-          }
-          rot_cs[tid] = cs;
-          rot_sn[tid] = sn;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int t = 0; t < JC; ++t) {
-          const int p = cpair_lo(t, ir, JW), q = cpair_hi(t, ir, JW);
-          const double cs = rot_cs[t], sn = rot_sn[t];
-#pragma unroll
-          for (int k = 0; k < RG; ++k) {
-            const double xp = x[k][p], xq = x[k][q];
-            x[k][p] = cs * xp - sn * xq;
-            x[k][q] = sn * xp + cs * xq;
-          }
-        }
-        if (tid < JC * JW) {
-          const int t = tid / JW, i = tid % JW;
-          const int p = cpair_lo(t, ir, JW), q = cpair_hi(t, ir, JW);
-          const double cs = rot_cs[t], sn = rot_sn[t];
-          const double jp = Js[i][p], jq = Js[i][q];
-          Js[i][p] = cs * jp - sn * jq;
-          Js[i][q] = sn * jp + cs * jq;
-        }
+        for (int ir = 0; ir < JC; ++ir)
+          jac_inner<RG, JC, 2, JR_T>(ir, x, red, rot_cs, rot_sn, Js, &any_rot, tol);
       }
       __syncthreads();
       if (any_rot) {
@@ -417,23 +512,19 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
             }
           }
         }
-        // V pair <- V pair J, rows streamed through registers
-#pragma unroll 1
-        for (int row = tid; row < dp; row += JR_T) {
-          double acc[JW];
+        // V pair <- V pair J (rows loaded at the start of the round)
 #pragma unroll
-          for (int c = 0; c < JW; ++c) acc[c] = 0.0;
-#pragma unroll 4
-          for (int l = 0; l < JW; ++l) {
-            const int coll = l < JC ? bi * JC + l : bj * JC + (l - JC);
-            const double yl = V[(size_t)coll * dp + row];
+        for (int k = 0; k < RG; ++k) {
+          const int row = tid + JR_T * k;
+          if (row < dp) {
 #pragma unroll
-            for (int c = 0; c < JW; ++c) acc[c] = fma(yl, Js[l][c], acc[c]);
-          }
+            for (int c = 0; c < JW; ++c) {
+              double acc = 0.0;
 #pragma unroll
-          for (int c = 0; c < JW; ++c) {
-            const int col = c < JC ? bi * JC + c : bj * JC + (c - JC);
-            V[(size_t)col * dp + row] = acc[c];
+              for (int l = 0; l < JW; ++l) acc = fma(vv[k][l], Js[l][c], acc);
+              const int col = c < JC ? bi * JC + c : bj * JC + (c - JC);
+              V[(size_t)col * dp + row] = acc;
+            }
           }
         }
         if (tid == 0) atomicOr(rot + (sweep & 1), 1u);
@@ -475,9 +566,42 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
   }
 }
 
+bool g_jacobi_cyc = getenv("TSVD_JACOBI_CYC") ? atoi(getenv("TSVD_JACOBI_CYC")) != 0 : true;
+
+int g_jacobi_jc = getenv("TSVD_JACOBI_JC") ? atoi(getenv("TSVD_JACOBI_JC")) : 4;
+
+template <int JCV>
+static bool reg_launch(const double* B, int d, double* Ub, double* S, double* Vb, double* work,
+                       unsigned* ctl, cudaStream_t st) {
+  int nbr = (d + JCV - 1) / JCV;
+  if (nbr < 2) nbr = 2;
+  if (nbr & 1) ++nbr;
+  const int dpr = nbr * JCV;
+  if (nbr / 2 > 148 || jac_layout(d, dpr) + 64 > small_svd_work(d)) return false;
+  const int RG = (d + JR_T - 1) / JR_T;
+  void* fn = nullptr;
+#define REG_FN(R)                                                                      \
+  fn = g_jacobi_cyc ? (void*)jacobi_reg_kernel<R, JCV, true> : (void*)jacobi_reg_kernel<R, JCV, false>
+  if (RG <= 1) REG_FN(1);
+  else if (RG == 2) REG_FN(2);
+  else if (RG == 3) REG_FN(3);
+  else if (RG == 4) REG_FN(4);
+  else return false;
+#undef REG_FN
+  double* G = work;
+  double* V = G + (size_t)d * dpr;
+  double* nrm = V + (size_t)dpr * dpr;
+  jacobi_init_kernel<<<148 * 4, 256, 0, st>>>(B, d, dpr, G, V, ctl);
+  TSVD_CHECK_LAUNCH();
+  int nblocks = nbr / 2, nbv = nbr;
+  void* args[] = {&G, &V, &d, &nbv, &nrm, &Ub, &S, &Vb, &ctl};
+  TSVD_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(JR_T), args, 0, st));
+  TSVD_CHECK_LAUNCH();
+  return true;
+}
+
 int small_svd_sweeps(const double* work, int d) {
-  const int nb = jac_nb(d), dp = nb * JC;
-  const unsigned* ctl = (const unsigned*)(work + (size_t)d * dp + (size_t)dp * dp + dp);
+  const unsigned* ctl = jac_ctl(const_cast<double*>(work), d);
   unsigned h = 0;
   TSVD_CUDA(cudaMemcpy(&h, ctl + 4, sizeof(unsigned), cudaMemcpyDeviceToHost));
   return (int)h;
@@ -490,35 +614,15 @@ void small_svd(const double* B, int d, double* Ub, double* S, double* Vb, double
   double* G = work;
   double* V = G + (size_t)d * dp;
   double* nrm = V + (size_t)dp * dp;
-  unsigned* ctl = (unsigned*)(nrm + dp);
+  unsigned* ctl = jac_ctl(work, d);
   {
-    // register path: blocks of kRegJC columns (pairs of 2 kRegJC); the
-    // sequential chain is ~2d inner rounds per sweep whatever the block size,
-    // and narrower pairs make each inner round cheaper
-    constexpr int kRegJC = 4;
-    int nb4 = (d + kRegJC - 1) / kRegJC;
-    if (nb4 < 2) nb4 = 2;
-    if (nb4 & 1) ++nb4;
-    const int dp4 = nb4 * kRegJC;
-    const int RG = (d + JR_T - 1) / JR_T;
-    void* fn = nullptr;
-    if (RG <= 1) fn = (void*)jacobi_reg_kernel<1, kRegJC>;
-    else if (RG == 2) fn = (void*)jacobi_reg_kernel<2, kRegJC>;
-    else if (RG == 3) fn = (void*)jacobi_reg_kernel<3, kRegJC>;
-    else if (RG == 4) fn = (void*)jacobi_reg_kernel<4, kRegJC>;
-    if (fn && nb4 / 2 <= 148) {
-      double* G4 = work;
-      double* V4 = G4 + (size_t)d * dp4;
-      double* nrm4 = V4 + (size_t)dp4 * dp4;
-      unsigned* ctl4 = (unsigned*)(nrm + dp);  // same control words as the JC path
-      jacobi_init_kernel<<<148 * 4, 256, 0, st>>>(B, d, dp4, G4, V4, ctl4);
-      TSVD_CHECK_LAUNCH();
-      int nblocks = nb4 / 2, nbv = nb4;
-      void* args[] = {&G4, &V4, &d, &nbv, &nrm4, &Ub, &S, &Vb, &ctl4};
-      TSVD_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(JR_T), args, 0, st));
-      TSVD_CHECK_LAUNCH();
-      return;
-    }
+    // register path: blocks of JC columns, one CTA per block pair; the
+    // cyclic-by-blocks sweep has ~d inner rounds whatever JC, so JC trades
+    // per-round overheads (grid barrier, G / V traffic) against CTA count
+    const int jc = g_jacobi_jc;
+    if (jc == 2 && reg_launch<2>(B, d, Ub, S, Vb, work, ctl, st)) return;
+    if (jc == 4 && reg_launch<4>(B, d, Ub, S, Vb, work, ctl, st)) return;
+    if (jc == 8 && reg_launch<8>(B, d, Ub, S, Vb, work, ctl, st)) return;
   }
   jacobi_init_kernel<<<148 * 4, 256, 0, st>>>(B, d, dp, G, V, ctl);
   TSVD_CHECK_LAUNCH();

@@ -30,9 +30,11 @@ def timeit(fn, reps=5, warm=2):
 
 
 def svd_bench():
-    for d in (28, 128, 384, 704):
+    for d in [int(x) for x in os.environ.get("SVD_D", "28,128,200,384,450,704").split(",")]:
         rng = np.random.default_rng(d)
         B = torch.from_numpy(np.tril(rng.standard_normal((d, d))) * (0.97 ** np.arange(d))).cuda()
+        if d == 384 and os.path.exists(os.path.join(os.path.dirname(__file__), "B384_lanczos.npy")):
+            B = torch.from_numpy(np.load(os.path.join(os.path.dirname(__file__), "B384_lanczos.npy"))).cuda()
         Ub = torch.empty((d, d), dtype=torch.float64, device="cuda")
         Vb = torch.empty_like(Ub)
         S = torch.empty(d, dtype=torch.float64, device="cuda")

@@ -242,7 +242,7 @@ def test_cgs_qr_parity(q, l, bq):
     assert np.abs(Q - Qo).max() <= 1e-9
 
 
-@pytest.mark.parametrize("d", [1, 5, 28, 64, 97])
+@pytest.mark.parametrize("d", [1, 5, 28, 64, 97, 200, 384, 513])
 def test_small_svd_parity(d):
     rng = np.random.default_rng(d)
     B = np.tril(rng.standard_normal((d, d))) - np.tril(rng.standard_normal((d, d)), -5)
