@@ -902,41 +902,46 @@ struct NnTmaCfg {
   static constexpr size_t xbox = (size_t)NT_R * 16 * 8;    // 16 KB
   static constexpr size_t hbox = (size_t)KC * 16 * 8;
   static constexpr size_t stage = NB * xbox + hbox;        // multiple of 1024
-  static constexpr int OP = 16 + 4;
-  static constexpr size_t os_off = S * stage;
+  static constexpr size_t y_off = S * stage;               // Y tile (one box, own barriers)
+  static constexpr int OP = 16 + 4, TP = 16 + 4;
+  static constexpr size_t os_off = y_off + xbox;
   static constexpr size_t ts_off = os_off + (size_t)NT_R * OP * 8;
-  static constexpr size_t bar_off = ts_off + 16 * 16 * 8;
-  static constexpr size_t bytes = bar_off + 2 * S * 8 + 1024;  // + alignment slack
+  static constexpr size_t bar_off = ts_off + 16 * TP * 8;
+  static constexpr size_t bytes = bar_off + (2 * S + 2) * 8 + 1024;  // + alignment slack
   static constexpr unsigned tx = (unsigned)stage;
 };
-
 
 template <int KC, int S>
 __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
-    const double* Y, int64_t ldy, const double* __restrict__ T, double* Z, int64_t ldz, int64_t q,
-    int s, int w, double alpha, double beta, double* __restrict__ gram) {
+    const __grid_constant__ CUtensorMap ymap, int use_y, const double* __restrict__ T, double* Z,
+    int64_t ldz, int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram) {
   using CF = NnTmaCfg<KC, S>;
-  constexpr int WP = 16, NT = 2, OP = CF::OP, KY = WP / 4, NPAIR = NT * NT;
+  constexpr int WP = 16, NT = 2, OP = CF::OP, TP = CF::TP, NPAIR = NT * NT;
   constexpr int KSPLIT = 8 / NPAIR, KSTEPS = NT_R / 4 / KSPLIT;
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  const double* Ys = (const double*)(sm + CF::y_off);
   double* Os = (double*)(sm + CF::os_off);
   double* Ts = (double*)(sm + CF::ts_off);
   uint64_t* full = (uint64_t*)(sm + CF::bar_off);
   uint64_t* empty = full + S;
+  uint64_t* yfull = empty + S;
+  uint64_t* yempty = yfull + 1;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int prow = ((gid & 1) << 2) | (gid >> 1);
   for (int i = tid; i < WP * WP; i += 288) {
     const int r = i / WP, c = i % WP;
-    Ts[i] = (r < w && c < w) ? (T ? T[r * w + c] : (r == c ? 1.0 : 0.0)) : 0.0;
+    Ts[r * TP + c] = (r < w && c < w) ? (T ? T[r * w + c] : (r == c ? 1.0 : 0.0)) : 0.0;
   }
   if (tid == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 8);
     }
+    mbar_init(yfull, 1);
+    mbar_init(yempty, 8);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -945,7 +950,7 @@ __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
       (ntiles > (int64_t)blockIdx.x) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   const int nk = (s + KC - 1) / KC;
   const int64_t nsteps = my_tiles * nk;
-  if (warp == 8) {  // producer
+  if (warp == 8) {  // producer: X/H chunks into the ring, the tile's Y rows into Ys
     if (lane == 0) {
       for (int64_t j = 0; j < nsteps; ++j) {
         const int st = (int)(j % S);
@@ -960,6 +965,11 @@ __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
         for (int b = 0; b < CF::NB; ++b)
           tma_load_2d(base + b * CF::xbox, &xmap, kc * KC + b * 16, r0, &full[st]);
         tma_load_2d(base + CF::NB * CF::xbox, &hmap, 0, kc * KC, &full[st]);
+        if (use_y && kc == nk - 1) {  // with the tile's last chunk: never stalls the X ring
+          if (lt > 0) mbar_wait(yempty, (unsigned)(lt - 1) & 1);
+          mbar_expect_tx(yfull, (unsigned)CF::xbox);
+          tma_load_2d(sm + CF::y_off, &ymap, 0, r0, yfull);
+        }
       }
     }
     return;
@@ -967,18 +977,6 @@ __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
   double g[2][2];
   g[0][0] = g[0][1] = g[1][0] = g[1][1] = 0.0;
   double acc[2][2][NT][2];
-  double ya[2][KY];
-  auto load_ya = [&](double (&dst)[2][KY], int64_t rbase) {
-#pragma unroll
-    for (int mi = 0; mi < 2; ++mi) {
-      const int64_t row = rbase + warp * 16 + mi * 8 + prow;
-#pragma unroll
-      for (int kk = 0; kk < KY; ++kk) {
-        const int col = kk * 4 + tig;
-        dst[mi][kk] = (beta != 0.0 && Y && row < q && col < w) ? Y[row * ldy + col] : 0.0;
-      }
-    }
-  };
   for (int64_t j = 0; j < nsteps; ++j) {
     const int st = (int)(j % S);
     const unsigned u = (unsigned)(j / S);
@@ -993,7 +991,6 @@ __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
 #pragma unroll
           for (int ni = 0; ni < NT; ++ni) acc[h][mi][ni][0] = acc[h][mi][ni][1] = 0.0;
     }
-    if (kc == nk - 1) load_ya(ya, r0);  // latency overlaps the chunk's DMMAs
     mbar_wait(&full[st], u & 1);
     {
       const unsigned char* base = sm + (size_t)st * CF::stage;
@@ -1022,20 +1019,37 @@ __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
     if (kc == nk - 1) {
+      // epilogue: Z = alpha acc + beta (Y T); Y rows from the TMA-loaded tile
+      // as paired-k A-fragments (same swizzle / row permutation as X)
       double yt[2][NT][2];
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
         for (int ni = 0; ni < NT; ++ni) yt[mi][ni][0] = yt[mi][ni][1] = 0.0;
-      if (beta != 0.0) {
+      if (use_y) {
+        mbar_wait(yfull, (unsigned)lt & 1);
+        double2 ya[2][2];
 #pragma unroll
-        for (int kk = 0; kk < KY; ++kk)
+        for (int kk2 = 0; kk2 < 2; ++kk2) {
+          const int chunk = (((kk2 & 1) << 2) | tig) ^ prow;
+          ya[0][kk2] = *reinterpret_cast<const double2*>(Ys + (warp * 16 + prow) * 16 + chunk * 2);
+          ya[1][kk2] =
+              *reinterpret_cast<const double2*>(Ys + (warp * 16 + 8 + prow) * 16 + chunk * 2);
+        }
 #pragma unroll
-          for (int ni = 0; ni < NT; ++ni) {
-            const double b = Ts[(kk * 4 + tig) * WP + ni * 8 + gid];
-            dmma884(yt[0][ni][0], yt[0][ni][1], ya[0][kk], b);
-            dmma884(yt[1][ni][0], yt[1][ni][1], ya[1][kk], b);
-          }
+        for (int kk2 = 0; kk2 < 2; ++kk2)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int ni = 0; ni < NT; ++ni) {
+              const double b = Ts[(kk2 * 8 + 2 * tig + h) * TP + ni * 8 + gid];
+              dmma884(yt[0][ni][0], yt[0][ni][1], h ? ya[0][kk2].y : ya[0][kk2].x, b);
+              dmma884(yt[1][ni][0], yt[1][ni][1], h ? ya[1][kk2].y : ya[1][kk2].x, b);
+            }
+        // release Ys only after the DMMAs consumed the loaded fragments (an
+        // arrive right after the LDS could overtake them)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(yempty);
       }
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi)
@@ -1218,8 +1232,12 @@ static bool nn_tma_launch(const double* X, int64_t ldx, const double* H, int64_t
                           int64_t q, int s, int w, double alpha, double beta, double* gram,
                           cudaStream_t st) {
   if (q >= (int64_t)1 << 31 || s >= (1 << 30)) return false;
-  CUtensorMap xm, hm;
+  const int use_y = (beta != 0.0 && Y) ? 1 : 0;
+  if (use_y && !aligned16(Y, ldy)) return false;
+  CUtensorMap xm, hm, ym;
   if (!make_map(&xm, X, q, s, ldx, NT_R) || !make_map(&hm, H, s, w, ldh, NNT_KC)) return false;
+  if (use_y ? !make_map(&ym, Y, q, w, ldy, NT_R) : !make_map(&ym, X, q, s, ldx, NT_R))
+    return false;
   using CF = NnTmaCfg<NNT_KC, NNT_S>;
   static bool attr = false;
   if (!attr) {
@@ -1228,7 +1246,7 @@ static bool nn_tma_launch(const double* X, int64_t ldx, const double* H, int64_t
     attr = true;
   }
   gemm_nn_tma_kernel<NNT_KC, NNT_S><<<nn_ctas(q, 16), 288, CF::bytes, st>>>(
-      xm, hm, Y, ldy, T, Z, ldz, q, s, w, alpha, beta, gram);
+      xm, hm, ym, use_y, T, Z, ldz, q, s, w, alpha, beta, gram);
   TSVD_CHECK_LAUNCH();
   return true;
 }
