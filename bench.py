@@ -45,6 +45,15 @@ CONFIG_TEXT = {
 }
 
 
+def workload_text(cfg_name: str, algo: str) -> str:
+    from tsvd_inputs import CONFIGS
+    t = CONFIG_TEXT.get(cfg_name, "")
+    if algo == "rsvd":
+        c = CONFIGS[cfg_name]
+        t = t.split(", block Lanczos")[0] + f", rSVD p={c['rsvd_p']} q={c['rsvd_q']}"
+    return f"{cfg_name}: {t}"
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -205,6 +214,64 @@ def oracle_sample(cfg_name: str, budget_s: float, cycles: int, seed: int):
                 measured_s=sum(times) + t_svd + t_start)
 
 
+def oracle_sample_rsvd(cfg_name: str, budget_s: float, seed: int):
+    """Time the oracle's RandSVD (Alg. 1, calling only oracle/) on the host:
+    power iterations S1-S4 are run until ~budget_s has passed (at least one),
+    their mean time is extrapolated to the q+1 iterations of the config, plus
+    the small SVD of R_p and the output products S6-S7 (run once)."""
+    import numpy as np
+    from threadpoolctl import threadpool_info
+    import oracle
+    from oracle.core import DrawCtx, cgs_qr, small_svd
+    from oracle.philox import gaussian_block
+    cfg, _, work = make_workload(cfg_name, 0)
+    op = oracle.Operator(dense=work["A"]) if "A" in work else oracle.Operator(csr=work["csr"], shape=work["shape"])
+    n, r, p, q = cfg["n"], cfg["r"], cfg["rsvd_p"], cfg["rsvd_q"]
+    l, bq = r + p, 16
+    ctx = DrawCtx(seed)
+    Q = gaussian_block(n, l, seed, draw=0)
+    its = []
+    t_begin = time.perf_counter()
+    while True:
+        ts = time.perf_counter()
+        Qb, _ = cgs_qr(op.matmul(Q), bq, ctx)
+        Q, R = cgs_qr(op.rmatmul(Qb), bq, ctx)
+        its.append(time.perf_counter() - ts)
+        if time.perf_counter() - t_begin > budget_s or len(its) >= q + 1:
+            break
+    ts = time.perf_counter()
+    Ub, S, Vb = small_svd(R)
+    _ = Qb @ Vb[:, :r], Q @ Ub[:, :r]
+    t_tail = time.perf_counter() - ts
+    est = (q + 1) * float(np.mean(its)) + t_tail
+    threads = max((x.get("num_threads", 1) for x in threadpool_info()), default=1)
+    sample = (f"{cfg_name} RandSVD l={l}, b_qr={bq}: {len(its)} of {q + 1} power iterations "
+              f"measured ({sum(its):.1f} s) + SVD(R_p) and outputs ({t_tail:.2f} s); mean "
+              f"iteration time extrapolated to q+1 = {q + 1}")
+    return dict(value=est, unit="s", cores=int(threads), kind="oracle", sample=sample,
+                measured_s=sum(its) + t_tail)
+
+
+def residual_check(dwork, U, S, V):
+    """Acceptance numbers of the returned triplets (not timed): e_i =
+    ||A v_i - sigma_i u_i|| / sigma_1 (Eq. 14 as corrected, reading R13) and
+    the orthogonality of U, V.  Uses torch's CUDA sparse/dense matmul as an
+    independent checker of the library's output."""
+    import torch
+    if "csr" in dwork:
+        rp, ci, va = dwork["csr"]
+        m, n = dwork["shape"]
+        A = torch.sparse_csr_tensor(rp, ci.to(torch.int64), va, size=(m, n))
+        AV = A @ V
+    else:
+        AV = dwork["A"] @ V
+    e = torch.linalg.vector_norm(AV - U * S, dim=0) / S[0]
+    I = torch.eye(U.shape[1], dtype=U.dtype, device=U.device)
+    return {"e_max": float(e.max()), "e_median": float(e.median()),
+            "UtU_minus_I_max": float((U.T @ U - I).abs().max()),
+            "VtV_minus_I_max": float((V.T @ V - I).abs().max())}
+
+
 # ------------------------------------------------------------------- main --
 def main():
     ap = argparse.ArgumentParser()
@@ -212,6 +279,9 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2")
+    ap.add_argument("--algo", default="lanczos", choices=["lanczos", "rsvd"],
+                    help="lanczos = tsvd_block_lanczos (default); rsvd = tsvd_rsvd(r, p, q) "
+                         "with the config's oversampling p and power iterations q")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -231,7 +301,10 @@ def main():
         budget = max(5.0, 150.0 / max(1, args.steps + args.warmup))
         vals, last = [], None
         for it in range(args.warmup + args.steps):
-            last = oracle_sample(cfg_name, budget, cycles=1, seed=SEEDS[cfg_name])
+            if args.algo == "rsvd":
+                last = oracle_sample_rsvd(cfg_name, budget, seed=SEEDS[cfg_name])
+            else:
+                last = oracle_sample(cfg_name, budget, cycles=1, seed=SEEDS[cfg_name])
             if it >= args.warmup:
                 vals.append(last["value"])
         v = statistics.median(vals)
@@ -239,7 +312,7 @@ def main():
                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
                "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "weak",
                "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-               "config": {"workload": f"{cfg_name}: {CONFIG_TEXT.get(cfg_name, '')}",
+               "config": {"workload": workload_text(cfg_name, args.algo), "algo": args.algo,
                           "m": cfg["m"], "n": cfg["n"], "r": cfg["r"], "b": cfg["b"],
                           "d": cfg["d"], "tol": cfg["tol"]},
                "cpu_baseline": {"value": v, "unit": "s", "cores": last["cores"],
@@ -286,8 +359,17 @@ def main():
     h = T.TruncatedSVD(**dwork, dist=dist_kw) if dist_kw else T.TruncatedSVD(**dwork)
     h.set_seed(seed)
     h.set_krylov_dim(d)
+    rsvd = args.algo == "rsvd"
+    if rsvd and "rsvd_p" not in cfg:
+        raise SystemExit(f"config {cfg_name} has no rSVD settings")
+
+    def solve(hh):
+        if rsvd:
+            return hh.rsvd(r, cfg["rsvd_p"], cfg["rsvd_q"])
+        return hh.block_lanczos(r, b, tol, maxit)
+
     for _ in range(args.warmup):
-        h.block_lanczos(r, b, tol, maxit)
+        solve(h)
     h.set_profiling(True)
     h.reset_profile()
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
@@ -302,7 +384,7 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):
-        h.block_lanczos(r, b, tol, maxit)
+        solve(h)
         inf = h.info()
         infos.append(inf)
         launches += int(inf["launches"])
@@ -318,8 +400,12 @@ def main():
         ms = float(t.item())
     prof = h.profile()
     h.set_profiling(False)
-    U, S, V = h.get()
+    U, S, V = h.get(device=True)
     h.close()
+    accuracy = None
+    if not use_dist:
+        accuracy = residual_check(dwork, U, S, V)
+    del U, S, V
 
     # roofline of the dominant phase
     peak, peak_kind = _peaks()
@@ -332,7 +418,8 @@ def main():
         tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tfile):
             try:
-                tr = json.load(open(tfile)).get(dom[0])
+                tj = json.load(open(tfile))
+                tr = tj.get(f"{dom[0]}:{'csr' if 'csr' in work else 'dense'}") or tj.get(dom[0])
                 if tr:
                     traffic = tr["dram_over_alg"] * dom[1]["bytes"] / max(1, dom[1]["calls"])
             except Exception:
@@ -371,7 +458,7 @@ def main():
                 h2d = hwork["A"].nbytes
             h2.set_seed(seed)
             h2.set_krylov_dim(d)
-            h2.block_lanczos(r, b, tol, maxit)
+            solve(h2)
             U2, S2, V2 = h2.get()
             h2.close()
             torch.cuda.synchronize()
@@ -388,7 +475,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = oracle_sample(cfg_name, args.cpu_budget, cycles=infos[-1]["cycles"], seed=seed)
+            cpu = (oracle_sample_rsvd(cfg_name, args.cpu_budget, seed=seed) if rsvd else
+                   oracle_sample(cfg_name, args.cpu_budget, cycles=infos[-1]["cycles"], seed=seed))
             cpu.pop("measured_s", None)
         except Exception as ex:  # report, never fake
             cpu = {"value": None, "error": repr(ex)}
@@ -399,13 +487,14 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
         "higher_is_better": False, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg_name}: {CONFIG_TEXT.get(cfg_name, '')}",
+        "config": {"workload": workload_text(cfg_name, args.algo), "algo": args.algo,
                    "m": cfg["m"], "n": cfg["n"], "nnz": int(len(work["csr"][1])) if "csr" in work else None,
                    "r": r, "b": b, "d": d, "tol": tol, "maxit": maxit,
                    "l2": "no flush: working set (A, A^T, bases) >> 126 MB L2",
                    "parallelism": f"row-partitioned x{world} (NCCL)" if world > 1 else "single"},
         "solver": {"cycles": last["cycles"], "nconv": last["nconv"], "rho_max": last["rho_max"],
                    "breakdowns": last["breakdowns"], "sigma1": last["sigma1"]},
+        "accuracy": accuracy,
         "roofline": roof,
         "phases": phases,
         "cpu_baseline": cpu,

@@ -70,30 +70,70 @@ def to_bytes(s):
     return float(val.replace(",", "")) * mult
 
 
+PROBE_PHASE = {"nn": "ortho_nn", "tn": "ortho_tn", "spmm": "apply_A:csr",
+               "dense_nn": "apply_A:dense", "dense_tn": "apply_AT:dense"}
+
+
+def write_launch_summary(lpath, out_md, tag, what):
+    agg = launch_summary(lpath)
+    tot = sum(v[1] for v in agg.values())
+    with open(out_md, "w") as f:
+        f.write(f"# ncu launch list summary ({tag})\n\n")
+        f.write("`ncu --metrics gpu__time_duration.sum --clock-control none` over "
+                f"`{what}` (handle creation + one solve + the untimed residual check). "
+                "Per-launch times are cold-cache and serialised: compare shares.\n\n")
+        f.write("| kernel | launches | total us | share |\n|---|---|---|---|\n")
+        for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+            f.write(f"| `{k}` | {v[0]} | {v[1]:.1f} | {100 * v[1] / tot:.1f}% |\n")
+
+
 def main():
     tag = sys.argv[1]
     src = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out")
     prof = os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
-    lpath = os.path.join(src, "launches.csv")
-    if os.path.exists(lpath):
-        shutil.copy(lpath, os.path.join(prof, f"{tag}_launches.csv"))
-        agg = launch_summary(lpath)
-        tot = sum(v[1] for v in agg.values())
-        with open(os.path.join(prof, f"{tag}_launch_summary.md"), "w") as f:
-            f.write(f"# ncu launch list summary ({tag})\n\n")
-            f.write("`ncu --metrics gpu__time_duration.sum --clock-control none` over "
-                    "`bench.py --steps 1 --warmup 0` (handle creation + one C2 solve). "
-                    "Per-launch times are cold-cache and serialised: compare shares.\n\n")
-            f.write("| kernel | launches | total us | share |\n|---|---|---|---|\n")
-            for k, v in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-                f.write(f"| `{k}` | {v[0]} | {v[1]:.1f} | {100 * v[1] / tot:.1f}% |\n")
+    for fn in sorted(os.listdir(src)):
+        m = re.fullmatch(r"launches(_(\w+?)_(lanczos|rsvd))?\.csv", fn)
+        if not m:
+            continue
+        suffix = f"_{m.group(2)}_{m.group(3)}" if m.group(1) else ""
+        shutil.copy(os.path.join(src, fn), os.path.join(prof, f"{tag}{suffix}_launches.csv"))
+        what = (f"bench.py --config {m.group(2)} --algo {m.group(3)} --steps 1 --warmup 0"
+                if m.group(1) else "bench.py --steps 1 --warmup 0")
+        write_launch_summary(os.path.join(src, fn),
+                             os.path.join(prof, f"{tag}{suffix}_launch_summary.md"), tag, what)
     full = {}
     for fn in sorted(os.listdir(src)):
         if fn.startswith("full_") and fn.endswith(".ncu-rep"):
             m = full_metrics(os.path.join(src, fn))
             if m:
                 full[fn[5:-8]] = m
+    # traffic probes: one launch at a known shape (scripts/traffic_probe.py)
+    tfile = os.path.join(prof, "ncu_traffic.json")
+    traffic = json.load(open(tfile)) if os.path.exists(tfile) else {}
+    for fn in sorted(os.listdir(src)):
+        m = re.fullmatch(r"traffic_(\w+)\.ncu-rep", fn)
+        if not m or not os.path.exists(os.path.join(src, f"traffic_{m.group(1)}.json")):
+            continue
+        mode = m.group(1)
+        met = full_metrics(os.path.join(src, fn))
+        probe = json.loads(open(os.path.join(src, f"traffic_{mode}.json")).read().strip()
+                           .splitlines()[-1])
+        if not met or "dram__bytes_read.sum" not in met:
+            continue
+        dram = to_bytes(met["dram__bytes_read.sum"]) + to_bytes(met["dram__bytes_write.sum"])
+        full[f"traffic_{mode}"] = met
+        traffic[PROBE_PHASE[mode]] = {
+            "kernel": met["kernel"][:80], "probe": probe, "dram_bytes": dram,
+            "alg_bytes": probe["alg_bytes"], "dram_over_alg": round(dram / probe["alg_bytes"], 4),
+            "source": f"profiles/{tag}_ncu_full.json (traffic_{mode})"}
+    traffic["_doc"] = ("dram__bytes_read.sum + dram__bytes_write.sum of one `ncu --set full` "
+                       "launch at a known shape (scripts/traffic_probe.py) divided by that "
+                       "launch's ALGORITHMIC bytes (DESIGN.md section 6); bench.py multiplies the "
+                       "ratio by the phase's average algorithmic bytes per launch to report "
+                       "roofline.traffic.")
+    with open(tfile, "w") as f:
+        json.dump(traffic, f, indent=1)
     with open(os.path.join(prof, f"{tag}_ncu_full.json"), "w") as f:
         json.dump(full, f, indent=1)
     print(json.dumps(full, indent=1))
