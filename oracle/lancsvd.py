@@ -13,6 +13,24 @@ R17, R1); Qbar_{k+1} is kept to supply Rbar_k (R18); the restart block is the
 first b left Ritz vectors (R19) re-orthonormalised with CholQR2 (R11);
 V_r = P_k Vbar (Eq. 12, R2); convergence rho_i = ||Rbar_k Vbar[last b, i]||
 <= tol * sigma_1 (from Eq. 10, R12).
+
+keep = l > 0 selects the THICK restart (the paper's own
+future work, after Baglama-Reichel, ref. [2] P:509) instead
+of Alg. 2 S7.  It is not in the paper's listing, so it is written from the
+Lanczos relations of Eq. 7 (reading R1) that the listing maintains:
+  A P_k = Pbar_k B_k + Qbar_{k+1} Rbar_k E_k^T,   A^T Pbar_k = P_k B_k^T.
+With B_k = Ubar Sigma Vbar^T, the l largest Ritz vectors Pbar' = Pbar_k
+Ubar[:, :l], P' = P_k Vbar[:, :l] satisfy
+  A P' = Pbar' Sigma_l + Qbar_{k+1} S,  S = Rbar_k Vbar[last b rows, :l],
+  A^T Pbar' = P' Sigma_l,
+so the next cycle starts from Pbar = [Pbar' | Qbar_{k+1}], P = [P'], and
+continues the block recurrence (S2-S5, full reorthogonalisation) for
+(d - l)/b block steps.  Its projected matrix B' = Pbar^T A P is
+  [ Sigma_l   0    0  ... ]
+  [ S         L_1  0  ... ]      (lower "arrow" + block bidiagonal)
+  [ 0         Rb_1 L_2 ...]
+and rho_i, the outputs and the convergence test are unchanged.  l must be a
+multiple of b (d - l too); l >= r is required.
 """
 from __future__ import annotations
 
@@ -37,23 +55,35 @@ class LancResult:
 
 
 def lancsvd(op, r: int, b: int, d: int, tol: float, maxit: int, seed: int,
-            start=None, debug: bool = False) -> LancResult:
+            start=None, debug: bool = False, keep: int = 0) -> LancResult:
     m, n = op.m, op.n
     assert m >= n and 1 <= r <= d <= n and d % b == 0 and maxit >= 1
-    k = d // b
+    assert keep == 0 or (keep % b == 0 and r <= keep < d)
     ctx = DrawCtx(seed)
     G = gaussian_block(m, b, seed, draw=0) if start is None else np.array(start, dtype=np.float64)
     Qbar, _ = cholqr2(G, ctx)                                   # S1
+    thick = None
     for cycle in range(1, maxit + 1):                            # j = 1..p
         Pbar = np.zeros((m, d + b))
         P = np.zeros((n, d))
         B = np.zeros((d, d))
-        Pbar[:, 0:b] = Qbar
+        s0 = 0
+        if thick is None:
+            Pbar[:, 0:b] = Qbar
+        else:                                                    # N1: thick restart
+            s0 = keep
+            Pbar_o, P_o, Ub_o, S_o, Vb_o, Rb_o = thick
+            Pbar[:, :s0] = Pbar_o[:, :d] @ Ub_o[:, :s0]
+            P[:, :s0] = P_o @ Vb_o[:, :s0]
+            Pbar[:, s0:s0 + b] = Pbar_o[:, d:d + b]              # Qbar_{k+1}
+            B[:s0, :s0] = np.diag(S_o[:s0])
+            B[s0:s0 + b, :s0] = Rb_o @ Vb_o[d - b:d, :s0]        # S
+        k = (d - s0) // b
         Rb = None
         for i in range(k):                                       # i = 1..k
-            lo, hi = i * b, (i + 1) * b
+            lo, hi = s0 + i * b, s0 + (i + 1) * b
             Y = op.rmatmul(Pbar[:, lo:hi])                       # S2
-            if i == 0:
+            if lo == 0:
                 Q, R = cholqr2(Y, ctx)                           # S3a
             else:
                 Q, _, R = cgs_cqr2(Y, P[:, :lo], ctx)            # S3b
@@ -65,12 +95,15 @@ def lancsvd(op, r: int, b: int, d: int, tol: float, maxit: int, seed: int,
             if i < k - 1:
                 B[hi:hi + b, lo:hi] = Rb                         # Rbar_i
         Ub, S, Vb = small_svd(B)                                 # SVD(B_k)
-        rho = np.linalg.norm(Rb @ Vb[(k - 1) * b:k * b, :], axis=0)
+        rho = np.linalg.norm(Rb @ Vb[d - b:d, :], axis=0)
         ok = rho[:r] <= tol * S[0]
         converged = bool(np.all(ok))
         if converged or cycle == maxit:
             break
-        Qbar, _ = cholqr2(Pbar[:, :d] @ Ub[:, :b], ctx)          # S7 (+R11)
+        if keep:
+            thick = (Pbar, P, Ub, S, Vb, Rb)
+        else:
+            Qbar, _ = cholqr2(Pbar[:, :d] @ Ub[:, :b], ctx)      # S7 (+R11)
     U = Pbar[:, :d] @ Ub[:, :r]                                  # S9
     V = P @ Vb[:, :r]                                            # S8 (Eq. 12)
     U, V = sign_normalize(U, V)

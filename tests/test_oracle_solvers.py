@@ -222,3 +222,60 @@ def test_spmm_oracle_matches_dense_and_diagonal():
     opd = oracle.Operator(csr=(np.arange(51), np.arange(50), dv), shape=(50, 50))
     Xd = np.random.default_rng(5).standard_normal((50, 3))
     assert np.array_equal(opd.matmul(Xd), dv[:, None] * Xd)
+
+
+# ---- N1 thick restart (oracle/lancsvd.py header) -------------
+def _slow_decay(n=120, m=240, seed=8):
+    s = 10.0 * 0.93 ** np.arange(n)
+    return oracle.Operator(dense=dense_prescribed(m, n, s, seed=seed)), s
+
+
+@pytest.mark.parametrize("b,d,keep", [(4, 20, 8), (2, 16, 6), (3, 24, 12)])
+def test_thick_restart_relations(b, d, keep):
+    """After >= 1 thick restart the Lanczos relation A P = Pbar B + Qbar R E^T
+    and Pbar^T A P = B (arrow + block bidiagonal) still hold, the bases stay
+    orthonormal, and rho equals the explicit residual."""
+    op, s = _slow_decay()
+    res = oracle.lancsvd(op, r=4, b=b, d=d, tol=1e-30, maxit=3, seed=11, debug=True, keep=keep)
+    assert res.cycles == 3
+    r1, r2, o1, o2 = _lanczos_relations(op, res, b)
+    assert r1 <= 1e-13 and r2 <= 1e-12 and o1 <= 1e-13 and o2 <= 1e-13
+    B = res.debug["B"]
+    # structure: diagonal Sigma_l block, S row block below it, zeros elsewhere
+    assert np.all(B[:keep, :keep] == np.diag(np.diag(B[:keep, :keep])))
+    assert np.all(B[:keep, keep:] == 0.0)
+    assert np.all(B[keep + b:, :keep] == 0.0)
+    assert np.all(np.diff(np.diag(B[:keep, :keep])) <= 0)   # the kept Ritz values, sorted
+    e, _ = oracle.residuals(op, res.U, res.S, res.V)
+    assert np.abs(res.rho - e * res.S[0]).max() <= 1e-13 * s[0]
+
+
+def test_thick_restart_first_cycle_equals_paper_restart():
+    op, _ = _slow_decay()
+    a = oracle.lancsvd(op, r=4, b=4, d=20, tol=1e-30, maxit=1, seed=3, keep=8)
+    b_ = oracle.lancsvd(op, r=4, b=4, d=20, tol=1e-30, maxit=1, seed=3)
+    assert np.array_equal(a.S, b_.S) and np.array_equal(a.U, b_.U)
+
+
+def test_thick_restart_converges_where_paper_restart_stalls():
+    """C1 with d = 20 < 28: the paper's restart keeps only b = 4 Ritz vectors
+    and stalls (SURVEY 7.3 [calib]); keeping l = 12 >= r converges to the
+    prescribed Eq. 16 spectrum (closed form) in a few cycles."""
+    op, s = _c1()
+    res = oracle.lancsvd(op, r=10, b=4, d=20, tol=1e-12, maxit=10, seed=SEEDS["C1"], keep=12)
+    assert res.converged and res.cycles <= 4
+    assert np.abs(res.S - s[:10]).max() / s[0] <= 1e-10
+    e, _ = oracle.residuals(op, res.U, res.S, res.V)
+    assert e.max() <= 1e-8
+    assert np.abs(res.U.T @ res.U - np.eye(10)).max() <= 1e-12
+    assert np.abs(res.V.T @ res.V - np.eye(10)).max() <= 1e-12
+    ey = oracle.eckart_young_2norm(op, res.U, res.S, res.V)
+    assert ey == pytest.approx(s[10], rel=1e-6)
+
+
+def test_thick_restart_slow_decay_closed_form():
+    op, s = _slow_decay()
+    res = oracle.lancsvd(op, r=4, b=4, d=16, tol=1e-10, maxit=60, seed=5, keep=8)
+    paper = oracle.lancsvd(op, r=4, b=4, d=16, tol=1e-10, maxit=60, seed=5)
+    assert res.converged and res.cycles < paper.cycles
+    assert np.abs(res.S - s[:4]).max() <= 1e-10 * s[0]
