@@ -167,7 +167,8 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------- cpu baseline --
-def oracle_sample(cfg_name: str, budget_s: float, cycles: int, seed: int):
+def oracle_sample(cfg_name: str, budget_s: float, cycles: int, seed: int, keep: int = 0,
+                  d: int | None = None):
     """Time the oracle's LancSVD block steps (Alg. 2 S2-S5, calling only
     oracle/) for ~budget_s on the host, fit t_i = a + c*i and extrapolate to
     `cycles` full cycles of k = d/b steps plus the small SVD."""
@@ -177,7 +178,8 @@ def oracle_sample(cfg_name: str, budget_s: float, cycles: int, seed: int):
     from oracle.core import DrawCtx, cholqr2, cgs_cqr2, small_svd
     cfg, seed_, work = make_workload(cfg_name, 0)
     op = oracle.Operator(dense=work["A"]) if "A" in work else oracle.Operator(csr=work["csr"], shape=work["shape"])
-    m, n, b, d = cfg["m"], cfg["n"], cfg["b"], cfg["d"]
+    m, n, b = cfg["m"], cfg["n"], cfg["b"]
+    d = d or cfg["d"]
     k = d // b
     ctx = DrawCtx(seed)
     t0 = time.perf_counter()
@@ -204,12 +206,19 @@ def oracle_sample(cfg_name: str, budget_s: float, cycles: int, seed: int):
     t_svd = time.perf_counter() - ts
     idx = np.arange(len(times))
     c, a = np.polyfit(idx, np.array(times), 1) if len(times) > 1 else (0.0, times[0])
-    per_cycle = float(sum(max(a + c * i, times[0] * 0.5) for i in range(k))) + t_svd
-    est = t_start + cycles * per_cycle
+    def t_of(i):
+        return max(a + c * i, times[0] * 0.5)
+    per_cycle = float(sum(t_of(i) for i in range(k))) + t_svd
+    if keep:  # thick restart: later cycles run steps keep/b .. k-1 (+ restart products)
+        later = float(sum(t_of(i) for i in range(keep // b, k))) + t_svd + t_of(k - 1)
+        est = t_start + per_cycle + (cycles - 1) * later
+    else:
+        est = t_start + cycles * per_cycle
     threads = max((x.get("num_threads", 1) for x in threadpool_info()), default=1)
     sample = (f"{cfg_name} LancSVD block steps i=0..{len(times)-1} of k={k} of cycle 1 "
               f"({sum(times):.1f} s measured) + SVD({d}) ({t_svd:.2f} s); t_i fitted "
-              f"linearly in i and extrapolated to {cycles} cycle(s) x {k} steps")
+              f"linearly in i and extrapolated to {cycles} cycle(s) x {k} steps"
+              + (f" (thick restart: cycles > 1 run steps {keep // b}..{k - 1})" if keep else ""))
     return dict(value=est, unit="s", cores=int(threads), kind="oracle", sample=sample,
                 measured_s=sum(times) + t_svd + t_start)
 
@@ -283,6 +292,10 @@ def main():
                     help="lanczos = tsvd_block_lanczos (default); rsvd = tsvd_rsvd(r, p, q) "
                          "with the config's oversampling p and power iterations q")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--keep", type=int, default=None,
+                    help="thick restart keeping L Ritz pairs (SURVEY 8(f) N1); 0 = the paper's "
+                         "restart (Alg. 2 S7); default: the config's setting")
+    ap.add_argument("--d", type=int, default=None, help="override the config's Krylov dimension")
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -354,11 +367,17 @@ def main():
     else:
         hwork = dict(work)
     dwork = _to_device(hwork)
+    if args.d is not None:
+        cfg["d"] = args.d
+    if args.keep is not None:
+        cfg["keep"] = args.keep
+    keep = cfg.get("keep", 0)
     r, b, d, tol, maxit = cfg["r"], cfg["b"], cfg["d"], cfg["tol"], cfg["maxit"]
     stream = torch.cuda.current_stream()
     h = T.TruncatedSVD(**dwork, dist=dist_kw) if dist_kw else T.TruncatedSVD(**dwork)
     h.set_seed(seed)
     h.set_krylov_dim(d)
+    h.set_thick_restart(keep)
     rsvd = args.algo == "rsvd"
     if rsvd and "rsvd_p" not in cfg:
         raise SystemExit(f"config {cfg_name} has no rSVD settings")
@@ -458,6 +477,7 @@ def main():
                 h2d = hwork["A"].nbytes
             h2.set_seed(seed)
             h2.set_krylov_dim(d)
+            h2.set_thick_restart(keep)
             solve(h2)
             U2, S2, V2 = h2.get()
             h2.close()
@@ -476,7 +496,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             cpu = (oracle_sample_rsvd(cfg_name, args.cpu_budget, seed=seed) if rsvd else
-                   oracle_sample(cfg_name, args.cpu_budget, cycles=infos[-1]["cycles"], seed=seed))
+                   oracle_sample(cfg_name, args.cpu_budget, cycles=infos[-1]["cycles"], seed=seed,
+                                 keep=keep, d=d))
             cpu.pop("measured_s", None)
         except Exception as ex:  # report, never fake
             cpu = {"value": None, "error": repr(ex)}
@@ -490,10 +511,13 @@ def main():
         "config": {"workload": workload_text(cfg_name, args.algo), "algo": args.algo,
                    "m": cfg["m"], "n": cfg["n"], "nnz": int(len(work["csr"][1])) if "csr" in work else None,
                    "r": r, "b": b, "d": d, "tol": tol, "maxit": maxit,
+                   "restart": (f"thick, keep {keep} (SURVEY 8(f) N1)" if keep else
+                               "paper (Alg. 2 S7)"),
                    "l2": "no flush: working set (A, A^T, bases) >> 126 MB L2",
                    "parallelism": f"row-partitioned x{world} (NCCL)" if world > 1 else "single"},
         "solver": {"cycles": last["cycles"], "nconv": last["nconv"], "rho_max": last["rho_max"],
-                   "breakdowns": last["breakdowns"], "sigma1": last["sigma1"]},
+                   "breakdowns": last["breakdowns"], "replaced": last["replaced"],
+                   "sigma1": last["sigma1"]},
         "accuracy": accuracy,
         "roofline": roof,
         "phases": phases,

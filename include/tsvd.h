@@ -47,6 +47,8 @@ typedef int tsvd_status;
 enum {
   TSVD_OK = 0,
   TSVD_WARN_NOTCONV = 1, /* maxit reached before max_{i<=r} rho_i <= tol*sigma_1 */
+  TSVD_WARN_FALLBACK = 2, /* tsvd_dbg_cholqr2 / _cgs_cqr2 only: the Cholesky breakdown
+                             test fired and the CGS2 fallback gave the result */
   TSVD_EINVAL = -1,      /* bad argument (NULL, non-canonical CSR, tol <= 0 ...) */
   TSVD_ESHAPE = -2,      /* m < n, r > n, d % b != 0, r > d, r + p > n ...     */
   TSVD_ENOMEM = -3,      /* device allocation failed                            */
@@ -119,6 +121,17 @@ tsvd_status tsvd_set_seed(tsvd_t h, uint64_t seed);
  * multiple of b with r <= d <= n.  0 => default min(n, max(4r, 2b)) rounded
  * down to a multiple of b. */
 tsvd_status tsvd_set_krylov_dim(tsvd_t h, int d);
+/* Restart of LancSVD.  keep = 0 (default): the paper's restart, Alg. 2 S7
+ * (P:200-203): the next cycle starts from the first b left Ritz vectors.
+ * keep = l > 0: THICK restart (SURVEY 8(f) N1 -- the paper's future work,
+ * P:212/P:500, after Baglama-Reichel, ref. [2] P:509): the l largest Ritz
+ * pairs are kept as the first l columns of the next cycle's bases, Qbar_{k+1}
+ * follows them, and the block recurrence continues for (d - l)/b steps; the
+ * projected matrix becomes [Sigma_l 0; S L_1 ...] with S = Rbar_k Vbar[last
+ * b rows, :l] (derivation: oracle/lancsvd.py header).  Requirements checked
+ * at solve time: l % b == 0 and r <= l < d, else TSVD_ESHAPE.  keep < 0 =>
+ * TSVD_EINVAL. */
+tsvd_status tsvd_set_thick_restart(tsvd_t h, int keep);
 /* Panel width of CGS-QR (Alg. 3) inside RandSVD; default 16. */
 tsvd_status tsvd_set_qr_block(tsvd_t h, int b_qr);
 /* Optional exact start block instead of the Philox one: for LancSVD the
@@ -152,11 +165,14 @@ typedef struct {
   int cycles;       /* LancSVD restart cycles run (RandSVD: q + 1)        */
   int nconv;        /* i < r with rho_i <= tol*sigma_1 (LancSVD)          */
   int r, d, b;      /* parameters of the last solve (RandSVD: d = l)      */
-  int breakdowns;   /* Cholesky breakdowns handled by the CGS2 fallback   */
+  int breakdowns;   /* orthogonalisations whose Cholesky breakdown test
+                       fired and that the CGS2 fallback redid     */
   double rho_max;   /* max_{i<r} rho_i / sigma_1 (LancSVD)                */
   double sigma1;
   double ms_total;  /* device time of the last solve (CUDA events)        */
   int64_t launches; /* kernels launched by the last solve                 */
+  int replaced;     /* dependent columns the fallback replaced by Philox
+                       draws (reading R16)                                */
 } tsvd_info;
 tsvd_status tsvd_get_info(tsvd_t h, tsvd_info* out);
 /* rho_i / sigma_1 for i < r of the last LancSVD cycle (host buffer). */
@@ -206,12 +222,14 @@ tsvd_status tsvd_dbg_philox_words(const uint32_t* ctr, const uint32_t* key,
  * with the handle's CSR or dense A.  w >= 1 (any width). */
 tsvd_status tsvd_dbg_apply(tsvd_t h, int trans, const double* X, int64_t ldx,
                            double* Y, int64_t ldy, int w);
-/* CholeskyQR2 in place (Alg. 4): Y (q x w, ld) -> Q, R (w x w row-major). */
+/* CholeskyQR2 in place (Alg. 4): Y (q x w, ld) -> Q, R (w x w row-major).
+ * Returns TSVD_WARN_FALLBACK if the CGS2 fallback produced the result. */
 tsvd_status tsvd_dbg_cholqr2(double* Y, int64_t q, int w, int64_t ld,
                              double* R, uint64_t seed, void* stream);
 /* CGS-CQR2 (Alg. 5): Y (q x w) against P (q x s); both inside ONE row-major
  * buffer `basis` with leading dimension ld: P = columns [0, s), Y = columns
- * [s, s+w).  Outputs H (s x w), R (w x w) row-major. */
+ * [s, s+w).  Outputs H (s x w), R (w x w) row-major.  TSVD_WARN_FALLBACK as
+ * for tsvd_dbg_cholqr2. */
 tsvd_status tsvd_dbg_cgs_cqr2(double* basis, int64_t q, int s, int w,
                               int64_t ld, double* H, double* R, uint64_t seed,
                               void* stream);

@@ -20,7 +20,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtsvd.so")
 
-TSVD_OK, TSVD_WARN_NOTCONV = 0, 1
+TSVD_OK, TSVD_WARN_NOTCONV, TSVD_WARN_FALLBACK = 0, 1, 2
 TSVD_EINVAL, TSVD_ESHAPE, TSVD_ENOMEM, TSVD_ECUDA, TSVD_ENCCL, TSVD_ESTATE = -1, -2, -3, -4, -5, -6
 TSVD_HOST, TSVD_DEVICE = 0, 1
 TSVD_ROW_MAJOR, TSVD_COL_MAJOR = 0, 1
@@ -28,7 +28,7 @@ TSVD_ROW_MAJOR, TSVD_COL_MAJOR = 0, 1
 # every symbol include/tsvd.h declares (tests check the .so exports them)
 EXPORTS = [
     "tsvd_create_csr", "tsvd_create_dense", "tsvd_set_stream", "tsvd_set_seed",
-    "tsvd_set_krylov_dim", "tsvd_set_qr_block", "tsvd_set_start", "tsvd_block_lanczos",
+    "tsvd_set_krylov_dim", "tsvd_set_thick_restart", "tsvd_set_qr_block", "tsvd_set_start", "tsvd_block_lanczos",
     "tsvd_rsvd", "tsvd_get", "tsvd_get_info", "tsvd_get_rho", "tsvd_destroy",
     "tsvd_strerror", "tsvd_last_error", "tsvd_dbg_philox", "tsvd_dbg_philox_words",
     "tsvd_dbg_apply", "tsvd_dbg_cholqr2", "tsvd_dbg_cgs_cqr2", "tsvd_dbg_cgs_qr",
@@ -42,7 +42,8 @@ EXPORTS = [
 class TsvdInfo(C.Structure):
     _fields_ = [("cycles", C.c_int), ("nconv", C.c_int), ("r", C.c_int), ("d", C.c_int),
                 ("b", C.c_int), ("breakdowns", C.c_int), ("rho_max", C.c_double),
-                ("sigma1", C.c_double), ("ms_total", C.c_double), ("launches", C.c_int64)]
+                ("sigma1", C.c_double), ("ms_total", C.c_double), ("launches", C.c_int64),
+                ("replaced", C.c_int)]
 
 
 class TsvdDist(C.Structure):
@@ -76,6 +77,7 @@ _SIGS = {
     "tsvd_set_stream": [vp, vp],
     "tsvd_set_seed": [vp, u64],
     "tsvd_set_krylov_dim": [vp, i32],
+    "tsvd_set_thick_restart": [vp, i32],
     "tsvd_set_qr_block": [vp, i32],
     "tsvd_set_start": [vp, vp, i64, i64, i64, i32],
     "tsvd_block_lanczos": [vp, i32, i32, dbl, i32],
@@ -259,6 +261,10 @@ class TruncatedSVD:
     def set_krylov_dim(self, d: int):
         _check(lib().tsvd_set_krylov_dim(self._h, int(d)), "tsvd_set_krylov_dim")
 
+    def set_thick_restart(self, keep: int):
+        """keep = 0: Alg. 2 S7 restart; keep = l > 0: thick restart (N1)."""
+        _check(lib().tsvd_set_thick_restart(self._h, int(keep)), "tsvd_set_thick_restart")
+
     def set_qr_block(self, b_qr: int):
         _check(lib().tsvd_set_qr_block(self._h, int(b_qr)), "tsvd_set_qr_block")
 
@@ -396,17 +402,21 @@ def dbg_apply(h: TruncatedSVD, trans: bool, X, Y):
                                 X.shape[1]), "tsvd_dbg_apply")
 
 
-def dbg_cholqr2(Y, R, seed: int = 0, stream=None):
+def dbg_cholqr2(Y, R, seed: int = 0, stream=None) -> bool:
+    """Returns True if the CGS2 fallback produced the result."""
     q, w = Y.shape
-    _check(lib().tsvd_dbg_cholqr2(_dp(Y), q, w, Y.stride(0), _dp(R), int(seed),
-                                  _stream_ptr(stream)), "tsvd_dbg_cholqr2")
+    return _check(lib().tsvd_dbg_cholqr2(_dp(Y), q, w, Y.stride(0), _dp(R), int(seed),
+                                         _stream_ptr(stream)), "tsvd_dbg_cholqr2",
+                  allow_warn=True) == TSVD_WARN_FALLBACK
 
 
-def dbg_cgs_cqr2(basis, s: int, w: int, H, R, seed: int = 0, stream=None):
+def dbg_cgs_cqr2(basis, s: int, w: int, H, R, seed: int = 0, stream=None) -> bool:
+    """Returns True if the CGS2 fallback produced the result."""
     q = basis.shape[0]
-    _check(lib().tsvd_dbg_cgs_cqr2(_dp(basis), q, s, w, basis.stride(0),
-                                   _dp(H) if s > 0 else None, _dp(R), int(seed),
-                                   _stream_ptr(stream)), "tsvd_dbg_cgs_cqr2")
+    return _check(lib().tsvd_dbg_cgs_cqr2(_dp(basis), q, s, w, basis.stride(0),
+                                          _dp(H) if s > 0 else None, _dp(R), int(seed),
+                                          _stream_ptr(stream)), "tsvd_dbg_cgs_cqr2",
+                  allow_warn=True) == TSVD_WARN_FALLBACK
 
 
 def dbg_cgs_qr(Y, bq: int, R, seed: int = 0, stream=None):

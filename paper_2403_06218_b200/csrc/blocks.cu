@@ -277,6 +277,7 @@ void cgs2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H,
     gemm_tn(basis, ld, x, ldx2, q, nb, 1, cc, 1, part, c.st);
     allreduce_sum(c, cc, (size_t)nb);
   };
+  ++c.breakdowns;
   fill_zero(R, (int64_t)w * w, c.st);
   for (int j = 0; j < w; ++j) {
     const int nb = s + j;
@@ -307,7 +308,7 @@ void cgs2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H,
       gemm_nn(nullptr, 0, nullptr, 0, S, 1, nullptr, nullptr, 0, q, 0, 1, 0.0, 1.0, gram, c.st);
       gram1(sc + 1);
       cgs2_col_finalize(c1, c1, 0, sc + 1, sc + 1, 0.0, coef + nb, sc + 2, dep, c.st);
-      ++c.breakdowns;
+      ++c.replaced;
     } else {
       TSVD_CUDA(cudaMemcpyAsync(R + (int64_t)j * w + j, sc + 2, sizeof(double),
                                 cudaMemcpyDeviceToDevice, c.st));

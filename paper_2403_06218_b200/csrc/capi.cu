@@ -60,6 +60,7 @@ const char* tsvd_strerror(tsvd_status s) {
   switch (s) {
     case TSVD_OK: return "ok";
     case TSVD_WARN_NOTCONV: return "not converged within maxit (results retrievable)";
+    case TSVD_WARN_FALLBACK: return "Cholesky breakdown: CGS2 fallback used (P:275)";
     case TSVD_EINVAL: return "invalid argument";
     case TSVD_ESHAPE: return "invalid shape";
     case TSVD_ENOMEM: return "device out of memory";
@@ -320,6 +321,12 @@ tsvd_status tsvd_set_krylov_dim(tsvd_t h, int d) {
   return TSVD_OK;
 }
 
+tsvd_status tsvd_set_thick_restart(tsvd_t h, int keep) {
+  if (!h || keep < 0) return TSVD_EINVAL;
+  h->thick_keep = keep;
+  return TSVD_OK;
+}
+
 tsvd_status tsvd_set_qr_block(tsvd_t h, int b_qr) {
   if (!h || b_qr < 1 || b_qr > 32) return TSVD_EINVAL;
   h->b_qr = b_qr;
@@ -481,9 +488,9 @@ tsvd_status tsvd_dbg_cholqr2(double* Y, int64_t q, int w, int64_t ld, double* R,
   tsvd_ctx* c = dbg_ctx(stream);
   c->seed = seed;
   c->draw_next = 1;
-  cholqr2(*c, Y, q, w, ld, R);
+  const int fb = cholqr2(*c, Y, q, w, ld, R);
   TSVD_CUDA(cudaStreamSynchronize(c->st));
-  return TSVD_OK;
+  return fb ? TSVD_WARN_FALLBACK : TSVD_OK;
   TSVD_API_END
 }
 
@@ -495,9 +502,9 @@ tsvd_status tsvd_dbg_cgs_cqr2(double* basis, int64_t q, int s, int w, int64_t ld
   tsvd_ctx* c = dbg_ctx(stream);
   c->seed = seed;
   c->draw_next = 1;
-  cgs_cqr2(*c, basis, q, s, w, ld, H, R);
+  const int fb = cgs_cqr2(*c, basis, q, s, w, ld, H, R);
   TSVD_CUDA(cudaStreamSynchronize(c->st));
-  return TSVD_OK;
+  return fb ? TSVD_WARN_FALLBACK : TSVD_OK;
   TSVD_API_END
 }
 

@@ -37,6 +37,7 @@ struct tsvd_ctx {
   uint64_t seed = 0x2403062180ULL;
   uint64_t draw_next = 1;    // Philox draw id of the next breakdown replacement
   int krylov_d = 0;
+  int thick_keep = 0;         // N1 thick restart: Ritz vectors kept (0 = Alg. 2 S7)
   int b_qr = 16;
   std::vector<double> start;  // optional exact start block (row-major, dense)
   int64_t start_rows = 0, start_cols = 0;
@@ -57,7 +58,8 @@ struct tsvd_ctx {
   bool have = false;
   std::vector<double> rho;    // rho_i / sigma_1, i < r (LancSVD)
   tsvd_info info{};
-  int breakdowns = 0;
+  int breakdowns = 0;         // orthogonalisations that fell back to CGS2
+  int replaced = 0;           // dependent columns replaced by Philox draws
   // instrumentation (tsvd_set_profiling)
   bool prof_on = false;
   std::vector<tsvd::ProfRec> prof_open;   // recorded, not yet harvested

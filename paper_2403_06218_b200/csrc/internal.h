@@ -143,6 +143,9 @@ int small_svd_sweeps(const double* work, int d);  // sweeps of the last small_sv
 // rho_i = || Rbar * Vb[(k-1)b:kb, i] || / S[0] for i < cnt
 void lanczos_rho(const double* Rbar, int b, const double* Vb, int d, const double* S, int cnt,
                  double* rho, cudaStream_t st);
+// thick restart (N1): B'[:l,:l] = diag(S), B'[l:l+b, :l] = Rbar Vbar[d-b:d, :l]
+void thick_arrow(const double* Rbar, int b, const double* Vb, int d, const double* S, int l,
+                 double* B, cudaStream_t st);
 
 // sign normalisation (reading R28): sgn[i] = sign of the largest-|.| entry of
 // V[:, i] (lowest index on ties); flip_columns multiplies columns by sgn.

@@ -108,11 +108,21 @@ __global__ void __launch_bounds__(FIN_T) finalize_kernel(
     for (int i = tid; i < n0; i += FIN_T) hbs[i] = Hbar[i];
   }
   __syncthreads();
-  if (tid < C) {
-    double a = red[tid];
-    for (int g = 1; g < G; ++g) a += red[g * C + tid];
-    Ws[tid] = a;
-    if (mode == 0) Wout[tid] = a;
+  if (G >= 1) {
+    if (tid < C) {
+      double a = red[tid];
+      for (int g = 1; g < G; ++g) a += red[g * C + tid];
+      Ws[tid] = a;
+      if (mode == 0) Wout[tid] = a;
+    }
+  } else {
+    // w^2 > FIN_T (w >= 23): each thread sums whole entries, partials in order
+    for (int e = tid; e < C; e += FIN_T) {
+      double a = 0.0;
+      for (int p = 0; p < np; ++p) a += gram[(int64_t)p * C + e];
+      Ws[e] = a;
+      if (mode == 0) Wout[e] = a;
+    }
   }
   __syncthreads();
   if (mode == 0) return;
@@ -324,6 +334,31 @@ __global__ void lanczos_rho_kernel(const double* __restrict__ Rbar, int b,
 void lanczos_rho(const double* Rbar, int b, const double* Vb, int d, const double* S, int cnt,
                  double* rho, cudaStream_t st) {
   lanczos_rho_kernel<<<(cnt + 127) / 128, 128, 0, st>>>(Rbar, b, Vb, d, S, cnt, rho);
+  TSVD_CHECK_LAUNCH();
+}
+
+// Thick restart (oracle/lancsvd.py header): the first l
+// columns/rows of the next cycle's projected matrix B' (d x d, row-major,
+// zero elsewhere on entry):  B'[:l, :l] = diag(Sigma_l) and the "arrow" row
+// block  B'[l:l+b, :l] = S = Rbar_k Vbar[d-b:d, :l]  (A P' = Pbar' Sigma_l +
+// Qbar_{k+1} S).  One thread per column j < l.
+__global__ void thick_arrow_kernel(const double* __restrict__ Rbar, int b,
+                                   const double* __restrict__ Vb, int d,
+                                   const double* __restrict__ S, int l,
+                                   double* __restrict__ B) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= l) return;
+  B[(int64_t)j * d + j] = S[j];
+  for (int i = 0; i < b; ++i) {
+    double t = 0.0;
+    for (int c = 0; c < b; ++c) t = fma(Rbar[i * b + c], Vb[(int64_t)(d - b + c) * d + j], t);
+    B[(int64_t)(l + i) * d + j] = t;
+  }
+}
+
+void thick_arrow(const double* Rbar, int b, const double* Vb, int d, const double* S, int l,
+                 double* B, cudaStream_t st) {
+  thick_arrow_kernel<<<(l + 127) / 128, 128, 0, st>>>(Rbar, b, Vb, d, S, l, B);
   TSVD_CHECK_LAUNCH();
 }
 

@@ -77,10 +77,13 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   }
   if (d % b != 0 || d < r || d > c.ng || d < b) return TSVD_ESHAPE;
   if (!c.start.empty() && (c.start_rows != m || c.start_cols != b)) return TSVD_ESHAPE;
+  const int keep = c.thick_keep;  // N1 thick restart (0: Alg. 2 S7)
+  if (keep && (keep % b != 0 || keep < r || keep >= d)) return TSVD_ESHAPE;
   const int k = d / b;
   const int64_t ldb = d + b, ldp = d;
   c.have = false;
   c.breakdowns = 0;
+  c.replaced = 0;
   c.draw_next = 1;
   const int64_t launches0 = g_launches.load();
   EventTimer timer(c.st);
@@ -118,8 +121,10 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   double rho_max = 0.0;
   int* flog = (int*)buf(c, "flag_log", sizeof(int) * 4 * (size_t)k);
   std::vector<int> hlog(4 * (size_t)k);
+  fill_zero(B, (int64_t)d * d, c.st);
+  int s0 = 0;  // columns carried over by a thick restart (block steps start there)
   for (cycle = 1; cycle <= maxit; ++cycle) {
-    fill_zero(B, (int64_t)d * d, c.st);
+    const int kc = (d - s0) / b;  // block steps of this cycle
     // Block steps, first with deferred breakdown checks (no host sync per
     // orthogonalisation); if the log shows a breakdown in call `slot`
     // (2i: n side of step i, 2i+1: m side) the steps are replayed from there
@@ -129,13 +134,13 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
     c.deferred = true;
     int from_slot = 0;
     for (int pass = 0; pass < 2; ++pass) {
-      for (int i = from_slot / 2; i < k; ++i) {
-        const int lo = i * b;
+      for (int i = from_slot / 2; i < kc; ++i) {
+        const int lo = s0 + i * b;
         if (!(i == from_slot / 2 && (from_slot & 1))) {
           apply(c, true, Pb + lo, ldb, P + lo, ldp, b);                  // S2: A^T Qbar_i
           n_side();
           c.flag_slot = 2 * i;
-          if (i == 0)
+          if (lo == 0)
             cholqr2(c, P, n, b, ldp, R);                                 // S3a
           else
             cgs_cqr2(c, P, n, lo, b, ldp, H, R);                         // S3b
@@ -145,7 +150,7 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
         m_side();
         c.flag_slot = 2 * i + 1;
         cgs_cqr2(c, Pb, m, lo + b, b, ldb, H, Rb);                       // S5
-        if (i < k - 1)
+        if (i < kc - 1)
           copy_block(Rb, b, B + (int64_t)(lo + b) * d + lo, d, b, b, false, c.st);  // Rbar_i
       }
       if (!c.deferred) break;
@@ -154,7 +159,7 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
       TSVD_CUDA(cudaStreamSynchronize(c.st));
       c.deferred = false;
       int bad = -1;
-      for (int sl = 0; sl < 2 * k && bad < 0; ++sl)
+      for (int sl = 0; sl < 2 * kc && bad < 0; ++sl)
         if (hlog[2 * sl] || hlog[2 * sl + 1]) bad = sl;
       if (bad < 0) break;
       from_slot = bad;
@@ -179,6 +184,30 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
     }
     conv = (nconv == r);
     if (conv || cycle == maxit) break;
+    if (keep) {
+      // N1 thick restart (oracle/lancsvd.py header): Pbar' = Pbar_k Ubar[:, :l],
+      // P' = P_k Vbar[:, :l] (computed into scratch panels, then copied over
+      // the bases' first l columns), Qbar_{k+1} moved behind them, and the
+      // next B' starts as [Sigma_l; S] with S = Rbar_k Vbar[d-b:d, :l].
+      double* tPb = dbuf(c, "thick_Pb", (size_t)m * keep);
+      double* tP = dbuf(c, "thick_P", (size_t)n * keep);
+      {
+        Prof p(c, P_RESTART, 8.0 * (m + n) * (d + 3.0 * keep) + 16.0 * m * b,
+               2.0 * (m + n) * d * keep);
+        gemm_nn(Pb, ldb, Ub, d, nullptr, 0, nullptr, tPb, keep, m, d, keep, 1.0, 0.0, nullptr,
+                c.st);
+        gemm_nn(P, ldp, Vb, d, nullptr, 0, nullptr, tP, keep, n, d, keep, 1.0, 0.0, nullptr,
+                c.st);
+        copy_block(tPb, keep, Pb, ldb, m, keep, false, c.st);
+        copy_block(tP, keep, P, ldp, n, keep, false, c.st);
+        copy_block(Pb + d, ldb, Pb + keep, ldb, m, b, false, c.st);
+      }
+      fill_zero(B, (int64_t)d * d, c.st);
+      thick_arrow(Rb, b, Vb, d, Sg, keep, B, c.st);
+      s0 = keep;
+      continue;
+    }
+    fill_zero(B, (int64_t)d * d, c.st);
     // S7: Qbar_1 = Pbar_k Ubar_1 (first b left Ritz vectors, reading R19),
     // re-orthonormalised (reading R11); computed into the spare slot.
     {
@@ -215,6 +244,7 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   c.info.d = d;
   c.info.b = b;
   c.info.breakdowns = c.breakdowns;
+  c.info.replaced = c.replaced;
   c.info.rho_max = rho_max;
   c.info.sigma1 = hs[0];
   c.info.ms_total = ms;
@@ -231,6 +261,7 @@ tsvd_status rsvd_solve(Ctx& c, int r, int p, int q) {
   const int bq = std::min(std::max(1, c.b_qr), 32);
   c.have = false;
   c.breakdowns = 0;
+  c.replaced = 0;
   c.draw_next = 1;
   const int64_t launches0 = g_launches.load();
   EventTimer timer(c.st);
@@ -286,6 +317,7 @@ tsvd_status rsvd_solve(Ctx& c, int r, int p, int q) {
   c.info.d = l;
   c.info.b = bq;
   c.info.breakdowns = c.breakdowns;
+  c.info.replaced = c.replaced;
   c.info.sigma1 = s1;
   c.info.ms_total = ms;
   c.info.launches = g_launches.load() - launches0;

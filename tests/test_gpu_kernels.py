@@ -167,14 +167,16 @@ def _cond_matrix(q, w, kappa, rng):
 
 
 @pytest.mark.parametrize("q,w,kappa", [(100, 4, 10.0), (5000, 16, 1e6), (70001, 32, 1e3),
-                                       (333, 7, 1e7)])
+                                       (333, 7, 1e7), (9000, 23, 1e5), (12345, 31, 1e6),
+                                       (3000, 32, 1e7)])
 def test_cholqr2_parity(q, w, kappa):
     rng = np.random.default_rng(q + w)
     Y = _cond_matrix(q, w, kappa, rng) * 3.0
     Qo, Ro = oracle.cholqr2(Y, DrawCtx(1))
     Yg = cu(Y)
     Rg = torch.zeros((w, w), dtype=torch.float64, device="cuda")
-    T.dbg_cholqr2(Yg, Rg, seed=1)
+    fb = T.dbg_cholqr2(Yg, Rg, seed=1)
+    assert not fb  # kappa <= 1e7: no Cholesky breakdown (u kappa^2 < 1)
     Q, R = Yg.cpu().numpy(), Rg.cpu().numpy()
     assert np.abs(Q.T @ Q - np.eye(w)).max() <= 10 * w * U
     assert np.linalg.norm(Y - Q @ R) / np.linalg.norm(Y) <= 100 * U
@@ -183,7 +185,8 @@ def test_cholqr2_parity(q, w, kappa):
 
 
 @pytest.mark.parametrize("q,s,w,kappa", [(1000, 8, 4, 1.0), (20000, 100, 16, 1e4),
-                                         (4099, 37, 32, 1e7), (50000, 384, 16, 1e2)])
+                                         (4099, 37, 32, 1e7), (50000, 384, 16, 1e2),
+                                         (30000, 320, 32, 1e3), (7000, 50, 27, 1e4)])
 def test_cgs_cqr2_parity(q, s, w, kappa):
     rng = np.random.default_rng(q + s)
     P, _ = np.linalg.qr(rng.standard_normal((q, s)))
@@ -192,7 +195,8 @@ def test_cgs_cqr2_parity(q, s, w, kappa):
     basis = cu(np.hstack([P, Y]))
     Hg = torch.zeros((s, w), dtype=torch.float64, device="cuda")
     Rg = torch.zeros((w, w), dtype=torch.float64, device="cuda")
-    T.dbg_cgs_cqr2(basis, s, w, Hg, Rg, seed=2)
+    fb = T.dbg_cgs_cqr2(basis, s, w, Hg, Rg, seed=2)
+    assert not fb
     B = basis.cpu().numpy()
     Q, H, R = B[:, s:], Hg.cpu().numpy(), Rg.cpu().numpy()
     assert np.array_equal(B[:, :s], P)          # P untouched
@@ -216,7 +220,7 @@ def test_breakdown_fallback_parity():
     basis = cu(np.hstack([P, Y]))
     Hg = torch.zeros((5, 4), dtype=torch.float64, device="cuda")
     Rg = torch.zeros((4, 4), dtype=torch.float64, device="cuda")
-    T.dbg_cgs_cqr2(basis, 5, 4, Hg, Rg, seed=7)
+    assert T.dbg_cgs_cqr2(basis, 5, 4, Hg, Rg, seed=7)   # fallback taken
     Q, H, R = basis.cpu().numpy()[:, 5:], Hg.cpu().numpy(), Rg.cpu().numpy()
     assert np.abs(Q.T @ Q - np.eye(4)).max() < 1e-14
     assert np.abs(P.T @ Q).max() < 1e-14

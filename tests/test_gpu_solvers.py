@@ -196,3 +196,78 @@ def test_errors():
     with pytest.raises(T.TsvdError):   # unsorted columns
         T.TruncatedSVD(csr=(np.array([0, 2, 2], np.int64), np.array([1, 0], np.int32),
                             np.ones(2)), shape=(2, 2))
+
+
+# ---- N1 thick restart (tsvd_set_thick_restart; oracle/lancsvd.py keep=l) ---
+@pytest.mark.parametrize("inject", [True, False])
+def test_c1_thick_restart(inject):
+    """C1 at d = 20 < 28: the paper's restart stalls, keeping l = 12 Ritz
+    pairs converges; same cycle count and triplets as the oracle."""
+    A, s = _c1()
+    op = oracle.Operator(dense=A)
+    seed = SEEDS["C1"]
+    G = oracle.gaussian_block(200, 4, seed, draw=0)
+    ro = oracle.lancsvd(op, r=10, b=4, d=20, tol=1e-12, maxit=10, seed=seed, keep=12,
+                        start=G if inject else None)
+    with T.TruncatedSVD(A) as h:
+        h.set_seed(seed)
+        if inject:
+            h.set_start(G)
+        h.set_thick_restart(12)
+        st = h.block_lanczos(r=10, b=4, tol=1e-12, maxit=10, d=20)
+        Ug, Sg, Vg = h.get()
+        info = h.info()
+    assert ro.converged and st == T.TSVD_OK
+    assert info["cycles"] == ro.cycles and info["cycles"] > 1
+    _accept(op, Ug, Sg, Vg, ro.S)
+    assert np.abs(Sg - s[:10]).max() / s[0] <= 1e-10
+    _vec_parity(Ug, Vg, ro.U, ro.V, ro.S)
+
+
+def test_thick_restart_slow_decay_parity():
+    n = 120
+    s = 10.0 * 0.93 ** np.arange(n)
+    A = dense_prescribed(240, n, s, seed=8)
+    op = oracle.Operator(dense=A)
+    ro = oracle.lancsvd(op, r=4, b=4, d=16, tol=1e-10, maxit=60, seed=5, keep=8)
+    with T.TruncatedSVD(A) as h:
+        h.set_seed(5)
+        h.set_thick_restart(8)
+        st = h.block_lanczos(r=4, b=4, tol=1e-10, maxit=60, d=16)
+        Ug, Sg, Vg = h.get()
+        info = h.info()
+    assert st == T.TSVD_OK and ro.converged
+    assert abs(info["cycles"] - ro.cycles) <= 1
+    _accept(op, Ug, Sg, Vg, ro.S)
+    assert np.abs(Sg - s[:4]).max() <= 1e-10 * s[0]
+
+
+@pytest.mark.parametrize("b,d,keep", [(16, 96, 32), (8, 64, 24)])
+def test_sparse_powerlaw_thick_parity(b, d, keep):
+    m = n = 20000
+    csr = powerlaw_csr(m, n, 200000, 2.5, seed=21)
+    op = oracle.Operator(csr=csr, shape=(m, n))
+    seed = 0x1234
+    ro = oracle.lancsvd(op, r=10, b=b, d=d, tol=1e-8, maxit=6, seed=seed, keep=keep)
+    with T.TruncatedSVD(csr=csr, shape=(m, n)) as h:
+        h.set_seed(seed)
+        h.set_thick_restart(keep)
+        h.block_lanczos(r=10, b=b, tol=1e-8, maxit=6, d=d)
+        Ug, Sg, Vg = h.get()
+        rho = h.rho()
+        info = h.info()
+    conv = (rho <= 1e-8) & (ro.rho <= 1e-8 * ro.S[0])
+    assert conv.sum() >= 8
+    _accept(op, Ug, Sg, Vg, ro.S, conv_mask=conv)
+    assert info["cycles"] == ro.cycles
+
+
+def test_thick_restart_shape_errors():
+    A, _ = _c1()
+    with T.TruncatedSVD(A) as h:
+        for keep in (6, 8, 28):   # not a multiple of b=4 / < r=10 / >= d
+            h.set_thick_restart(keep)
+            with pytest.raises(T.TsvdError):
+                h.block_lanczos(r=10, b=4, tol=1e-12, maxit=2, d=28)
+        with pytest.raises(T.TsvdError):
+            h.set_thick_restart(-1)
