@@ -74,13 +74,17 @@ __device__ void warp_tri_inverse_t(const double* Lo, double* Xs, double* Tout, i
 constexpr int FIN_T = 512;
 constexpr int FIN_HB = 8192;  // doubles of Hbar staged per chunk (64 KB dynamic smem)
 
+// 32 x 32 register Cholesky needs > 128 registers/thread: 256 threads then
+constexpr int fin_threads(int wt) { return wt == 32 ? 256 : FIN_T; }
+
 template <int WT>  // WT > 0: w == WT (all loops unrolled, no divergence); 0: any w <= 32
-__global__ void __launch_bounds__(FIN_T) finalize_kernel(
+__global__ void __launch_bounds__(fin_threads(WT)) finalize_kernel(
     const double* __restrict__ gram, int np, int w_, int mode, double* __restrict__ Wout,
     const double* __restrict__ Lprev, double* __restrict__ L, double* __restrict__ T,
     double* __restrict__ R, double* __restrict__ H, const double* __restrict__ Hbar, int s,
     int* __restrict__ flag) {
-  __shared__ double red[FIN_T];
+  constexpr int NTH = fin_threads(WT);
+  __shared__ double red[NTH];
   __shared__ double Ws[32 * 33];
   __shared__ double Lo[32 * 32];
   __shared__ double Lp[32 * 32];
@@ -89,7 +93,7 @@ __global__ void __launch_bounds__(FIN_T) finalize_kernel(
   __shared__ int bad;
   extern __shared__ double hbs[];
   const int w = WT > 0 ? WT : w_;
-  const int tid = threadIdx.x, C = w * w, G = FIN_T / C;
+  const int tid = threadIdx.x, C = w * w, G = NTH / C;
   const int64_t nh = (mode == 2 && H) ? (int64_t)s * w : 0;
   if (tid == 0) bad = 0;
   if (tid < G * C) {
@@ -100,12 +104,12 @@ __global__ void __launch_bounds__(FIN_T) finalize_kernel(
     red[tid] = a;
   }
   if (mode == 2)
-    for (int i = tid; i < C; i += FIN_T) Lp[i] = Lprev[i];
-  for (int i = tid; i < 32 * 32; i += FIN_T) Lo[i] = 0.0;
+    for (int i = tid; i < C; i += NTH) Lp[i] = Lprev[i];
+  for (int i = tid; i < 32 * 32; i += NTH) Lo[i] = 0.0;
   // first Hbar chunk in flight during the Cholesky
   {
     const int n0 = (int)(nh < FIN_HB ? nh : FIN_HB);
-    for (int i = tid; i < n0; i += FIN_T) hbs[i] = Hbar[i];
+    for (int i = tid; i < n0; i += NTH) hbs[i] = Hbar[i];
   }
   __syncthreads();
   if (G >= 1) {
@@ -116,9 +120,10 @@ __global__ void __launch_bounds__(FIN_T) finalize_kernel(
       if (mode == 0) Wout[tid] = a;
     }
   } else {
-    // w^2 > FIN_T (w >= 23): each thread sums whole entries, partials in order
-    for (int e = tid; e < C; e += FIN_T) {
+    // w^2 > NTH (w >= 23): each thread sums whole entries, partials in order
+    for (int e = tid; e < C; e += NTH) {
       double a = 0.0;
+#pragma unroll 16
       for (int p = 0; p < np; ++p) a += gram[(int64_t)p * C + e];
       Ws[e] = a;
       if (mode == 0) Wout[e] = a;
@@ -170,7 +175,7 @@ __global__ void __launch_bounds__(FIN_T) finalize_kernel(
     warp_tri_inverse_t(Lo, Ws, T, w);  // Ws is free now; writes T
   }
   __syncthreads();
-  for (int i = tid; i < C; i += FIN_T) {
+  for (int i = tid; i < C; i += NTH) {
     const int r = i / w, c = i % w;
     L[i] = Lo[r * 32 + c];
     if constexpr (WT > 0) T[i] = Xs[c * 33 + r];  // T[r][c] = Linv[c][r]
@@ -191,10 +196,10 @@ __global__ void __launch_bounds__(FIN_T) finalize_kernel(
     const int cnt = (rows_per < s - r0 ? rows_per : s - r0) * w;
     if (r0 > 0) {
       __syncthreads();
-      for (int i = tid; i < cnt; i += FIN_T) hbs[i] = Hbar[(int64_t)r0 * w + i];
+      for (int i = tid; i < cnt; i += NTH) hbs[i] = Hbar[(int64_t)r0 * w + i];
       __syncthreads();
     }
-    for (int i = tid; i < cnt; i += FIN_T) {
+    for (int i = tid; i < cnt; i += NTH) {
       const int r = i / w, c = i % w;
       const double* hb = hbs + r * w;
       double sum = 0.0;
@@ -224,12 +229,15 @@ static void fin_launch(const double* gram, int np, int w, int mode, double* Wout
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
     TSVD_CUDA(cudaFuncSetAttribute(finalize_kernel<16>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    TSVD_CUDA(cudaFuncSetAttribute(finalize_kernel<32>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
     attr = true;
   }
 #define FIN_GO(WTV)                                                                           \
-  finalize_kernel<WTV><<<1, FIN_T, dyn, st>>>(gram, np, w, mode, Wout, Lprev, L, T, R, H, Hbar, \
+  finalize_kernel<WTV><<<1, fin_threads(WTV), dyn, st>>>(gram, np, w, mode, Wout, Lprev, L, T, R, H, Hbar, \
                                               s, flag)
-  if (w == 16) FIN_GO(16);
+  if (w == 32) FIN_GO(32);
+  else if (w == 16) FIN_GO(16);
   else if (w == 8) FIN_GO(8);
   else if (w == 4) FIN_GO(4);
   else FIN_GO(0);

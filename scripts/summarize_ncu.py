@@ -113,12 +113,19 @@ def main():
     traffic = json.load(open(tfile)) if os.path.exists(tfile) else {}
     for fn in sorted(os.listdir(src)):
         m = re.fullmatch(r"traffic_(\w+)\.ncu-rep", fn)
-        if not m or not os.path.exists(os.path.join(src, f"traffic_{m.group(1)}.json")):
+        if not m:
             continue
         mode = m.group(1)
+        probe = None
+        for ext in ("json", "err"):  # ncu may route the probe's stdout to either
+            fp = os.path.join(src, f"traffic_{mode}.{ext}")
+            if os.path.exists(fp):
+                for ln in open(fp):
+                    if ln.startswith('{"mode"'):
+                        probe = json.loads(ln)
+        if probe is None:
+            continue
         met = full_metrics(os.path.join(src, fn))
-        probe = json.loads(open(os.path.join(src, f"traffic_{mode}.json")).read().strip()
-                           .splitlines()[-1])
         if not met or "dram__bytes_read.sum" not in met:
             continue
         dram = to_bytes(met["dram__bytes_read.sum"]) + to_bytes(met["dram__bytes_write.sum"])
