@@ -268,23 +268,24 @@ __global__ void __launch_bounds__(256, (WP == 32) ? 1 : 2) gemm_tn_kernel(const 
 // the swizzle.  ST adapts to s (16..64) so small-s passes do no zero work.
 constexpr int TT_RB = 64;
 
-template <int ST>
+template <int ST, int NYB = 1>  // NYB = 16-column boxes of Y (w <= 16 NYB)
 struct TnTmaCfg {
   static constexpr int NB = ST / 16, MT = ST / 8;
-  static constexpr int S = (ST >= 48) ? 2 : 4;
+  static constexpr int S = NYB == 2 ? (ST >= 32 ? 3 : 4) : (ST >= 48 ? 2 : 4);
   static constexpr size_t box = (size_t)TT_RB * 16 * 8;  // 8 KB
-  static constexpr size_t stage = (NB + 1) * box;
+  static constexpr size_t stage = (NB + NYB) * box;
   static constexpr size_t bar_off = S * stage;
   static constexpr size_t bytes = bar_off + 2 * S * 8 + 1024;
   static constexpr unsigned tx = (unsigned)stage;
 };
 
-template <int ST>
+template <int ST, int NYB>
 __global__ void __launch_bounds__(288, 2) gemm_tn_tma_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
     int64_t q, int s, int w, double* __restrict__ C, int64_t ldc, double* __restrict__ part) {
-  using CF = TnTmaCfg<ST>;
-  constexpr int S = CF::S, MT = CF::MT, NT = 2, WP = 16;
+  using CF = TnTmaCfg<ST, NYB>;
+  constexpr int S = CF::S, MT = CF::MT, NT = 2 * NYB, WP = 16 * NYB;
+  static_assert((size_t)ST * WP * 8 <= CF::stage * CF::S, "reduction tile must fit the ring");
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(sm + CF::bar_off);
@@ -316,7 +317,9 @@ __global__ void __launch_bounds__(288, 2) gemm_tn_tma_kernel(
 #pragma unroll
         for (int b = 0; b < CF::NB; ++b)
           tma_load_2d(base + b * CF::box, &xmap, s0 + b * 16, r0, &full[st]);
-        tma_load_2d(base + CF::NB * CF::box, &ymap, 0, r0, &full[st]);
+#pragma unroll
+        for (int b = 0; b < NYB; ++b)
+          tma_load_2d(base + (CF::NB + b) * CF::box, &ymap, b * 16, r0, &full[st]);
       }
     }
     return;
@@ -330,7 +333,6 @@ __global__ void __launch_bounds__(288, 2) gemm_tn_tma_kernel(
     const int st = j % S;
     mbar_wait(&full[st], (unsigned)(j / S) & 1);
     const unsigned char* base = sm + (size_t)st * CF::stage;
-    const double* ys = (const double*)(base + CF::NB * CF::box);
 #pragma unroll 1
     for (int h = 0; h < 2; ++h) {
       const int kr = warp * 8 + 2 * tig + h, sw = kr & 7;
@@ -343,7 +345,8 @@ __global__ void __launch_bounds__(288, 2) gemm_tn_tma_kernel(
       }
 #pragma unroll
       for (int ni = 0; ni < NT; ++ni) {
-        const int c = ni * 8 + gid;
+        const double* ys = (const double*)(base + (CF::NB + (ni >> 1)) * CF::box);
+        const int c = (ni & 1) * 8 + gid;
         b[ni] = ys[kr * 16 + (((c >> 1) ^ sw) << 1) + (c & 1)];
       }
 #pragma unroll
@@ -456,10 +459,10 @@ static void tn_launch(dim3 grid, const double* X, int64_t ldx, const double* Y, 
 
 bool g_tn_tma = getenv("TSVD_TN_TMA") ? atoi(getenv("TSVD_TN_TMA")) != 0 : true;
 
-template <int ST>
+template <int ST, int NYB>
 static void tn_tma_go(const CUtensorMap& xm, const CUtensorMap& ym, int64_t q, int s, int w,
                       double* C, int64_t ldc, double* part, cudaStream_t st) {
-  using CF = TnTmaCfg<ST>;
+  using CF = TnTmaCfg<ST, NYB>;
   const int s_tiles = (s + ST - 1) / ST;
   const int64_t chunks = (q + TT_RB - 1) / TT_RB;
   int64_t splits = (int64_t)(2 * 148) / s_tiles;
@@ -467,11 +470,11 @@ static void tn_tma_go(const CUtensorMap& xm, const CUtensorMap& ym, int64_t q, i
   if (splits < 1) splits = 1;
   static bool attr = false;
   if (!attr) {
-    TSVD_CUDA(cudaFuncSetAttribute(gemm_tn_tma_kernel<ST>,
+    TSVD_CUDA(cudaFuncSetAttribute(gemm_tn_tma_kernel<ST, NYB>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
     attr = true;
   }
-  gemm_tn_tma_kernel<ST><<<dim3(s_tiles, (unsigned)splits), 288, CF::bytes, st>>>(
+  gemm_tn_tma_kernel<ST, NYB><<<dim3(s_tiles, (unsigned)splits), 288, CF::bytes, st>>>(
       xm, ym, q, s, w, C, ldc, part);
   TSVD_CHECK_LAUNCH();
   if (splits > 1) reduce_launch(part, (int)splits, (int64_t)s * w, C, w, ldc == w ? 0 : ldc, st);
@@ -481,10 +484,15 @@ static bool tn_tma_launch(const double* X, int64_t ldx, const double* Y, int64_t
                           int s, int w, double* C, int64_t ldc, double* part, cudaStream_t st) {
   CUtensorMap xm, ym;
   if (!make_map(&xm, X, q, s, ldx, TT_RB) || !make_map(&ym, Y, q, w, ldy, TT_RB)) return false;
-  if (s <= 16) tn_tma_go<16>(xm, ym, q, s, w, C, ldc, part, st);
-  else if (s <= 32) tn_tma_go<32>(xm, ym, q, s, w, C, ldc, part, st);
-  else if (s <= 48) tn_tma_go<48>(xm, ym, q, s, w, C, ldc, part, st);
-  else tn_tma_go<64>(xm, ym, q, s, w, C, ldc, part, st);
+  if (w > 16) {  // 16 < w <= 32: two Y boxes, s-tiles of at most 32 (registers)
+    if (s <= 16) tn_tma_go<16, 2>(xm, ym, q, s, w, C, ldc, part, st);
+    else tn_tma_go<32, 2>(xm, ym, q, s, w, C, ldc, part, st);
+    return true;
+  }
+  if (s <= 16) tn_tma_go<16, 1>(xm, ym, q, s, w, C, ldc, part, st);
+  else if (s <= 32) tn_tma_go<32, 1>(xm, ym, q, s, w, C, ldc, part, st);
+  else if (s <= 48) tn_tma_go<48, 1>(xm, ym, q, s, w, C, ldc, part, st);
+  else tn_tma_go<64, 1>(xm, ym, q, s, w, C, ldc, part, st);
   return true;
 }
 
@@ -502,7 +510,7 @@ void gemm_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t
     return;
   }
   const bool v2 = aligned16(X, ldx) && aligned16(Y, ldy);
-  if (w > 8 && w <= 16 && v2 && g_tn_tma && q < ((int64_t)1 << 31) &&
+  if (w > 8 && w <= 32 && v2 && g_tn_tma && q < ((int64_t)1 << 31) &&
       tn_tma_launch(X, ldx, Y, ldy, q, s, w, C, ldc, part, st))
     return;
   const TnGeom g = tn_geom(q, s, w);
@@ -896,29 +904,33 @@ __global__ void __launch_bounds__(256) rowT_kernel(const double* Y, int64_t ldy,
 constexpr int NT_R = 128;
 bool g_nn_tma = getenv("TSVD_NN_TMA") ? atoi(getenv("TSVD_NN_TMA")) != 0 : true;
 
-template <int KC, int S>
+template <int KC, int S, int NYB = 1>  // NYB = 16-column boxes of H / Y (w <= 16 NYB)
 struct NnTmaCfg {
   static constexpr int NB = KC / 16;                       // 16-column boxes per stage
+  static constexpr int WP = 16 * NYB;
   static constexpr size_t xbox = (size_t)NT_R * 16 * 8;    // 16 KB
   static constexpr size_t hbox = (size_t)KC * 16 * 8;
-  static constexpr size_t stage = NB * xbox + hbox;        // multiple of 1024
-  static constexpr size_t y_off = S * stage;               // Y tile (one box, own barriers)
-  static constexpr int OP = 16 + 4, TP = 16 + 4;
-  static constexpr size_t os_off = y_off + xbox;
+  static constexpr size_t stage = NB * xbox + NYB * hbox;  // multiple of 1024
+  static constexpr size_t y_off = S * stage;               // Y tile (NYB boxes, own barriers)
+  static constexpr int OP = WP + 4, TP = WP + 4;
+  static constexpr size_t os_off = y_off + NYB * xbox;
   static constexpr size_t ts_off = os_off + (size_t)NT_R * OP * 8;
-  static constexpr size_t bar_off = ts_off + 16 * TP * 8;
+  static constexpr size_t bar_off = ts_off + WP * TP * 8;
   static constexpr size_t bytes = bar_off + (2 * S + 2) * 8 + 1024;  // + alignment slack
   static constexpr unsigned tx = (unsigned)stage;
 };
 
-template <int KC, int S>
-__global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
+template <int KC, int S, int NYB>
+__global__ void __launch_bounds__(288, NYB == 1 ? 2 : 1) gemm_nn_tma_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
     const __grid_constant__ CUtensorMap ymap, int use_y, const double* __restrict__ T, double* Z,
     int64_t ldz, int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram) {
-  using CF = NnTmaCfg<KC, S>;
-  constexpr int WP = 16, NT = 2, OP = CF::OP, TP = CF::TP, NPAIR = NT * NT;
-  constexpr int KSPLIT = 8 / NPAIR, KSTEPS = NT_R / 4 / KSPLIT;
+  using CF = NnTmaCfg<KC, S, NYB>;
+  constexpr int WP = CF::WP, NT = 2 * NYB, OP = CF::OP, TP = CF::TP, NPAIR = NT * NT;
+  // Gram: NPAIR 8x8 output tiles over 8 warps (KSPLIT warps share a tile and
+  // split its rows when NPAIR < 8; PPW tiles per warp when NPAIR > 8)
+  constexpr int KSPLIT = NPAIR >= 8 ? 1 : 8 / NPAIR, PPW = NPAIR >= 8 ? NPAIR / 8 : 1;
+  constexpr int KSTEPS = NT_R / 4 / KSPLIT;
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
   const double* Ys = (const double*)(sm + CF::y_off);
@@ -964,18 +976,23 @@ __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
 #pragma unroll
         for (int b = 0; b < CF::NB; ++b)
           tma_load_2d(base + b * CF::xbox, &xmap, kc * KC + b * 16, r0, &full[st]);
-        tma_load_2d(base + CF::NB * CF::xbox, &hmap, 0, kc * KC, &full[st]);
+#pragma unroll
+        for (int b = 0; b < NYB; ++b)
+          tma_load_2d(base + CF::NB * CF::xbox + b * CF::hbox, &hmap, b * 16, kc * KC, &full[st]);
         if (use_y && kc == nk - 1) {  // with the tile's last chunk: never stalls the X ring
           if (lt > 0) mbar_wait(yempty, (unsigned)(lt - 1) & 1);
-          mbar_expect_tx(yfull, (unsigned)CF::xbox);
-          tma_load_2d(sm + CF::y_off, &ymap, 0, r0, yfull);
+          mbar_expect_tx(yfull, (unsigned)(NYB * CF::xbox));
+#pragma unroll
+          for (int b = 0; b < NYB; ++b)
+            tma_load_2d(sm + CF::y_off + b * CF::xbox, &ymap, b * 16, r0, yfull);
         }
       }
     }
     return;
   }
-  double g[2][2];
-  g[0][0] = g[0][1] = g[1][0] = g[1][1] = 0.0;
+  double g[PPW][2][2];
+#pragma unroll
+  for (int p = 0; p < PPW; ++p) g[p][0][0] = g[p][0][1] = g[p][1][0] = g[p][1][1] = 0.0;
   double acc[2][2][NT][2];
   for (int64_t j = 0; j < nsteps; ++j) {
     const int st = (int)(j % S);
@@ -994,7 +1011,6 @@ __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
     mbar_wait(&full[st], u & 1);
     {
       const unsigned char* base = sm + (size_t)st * CF::stage;
-      const double* hs = (const double*)(base + CF::NB * CF::xbox);
 #pragma unroll
       for (int kk2 = 0; kk2 < KC / 8; ++kk2) {
         const double* xb = (const double*)(base + (kk2 >> 1) * CF::xbox);
@@ -1008,7 +1024,8 @@ __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
           const int hr = kk2 * 8 + 2 * tig + h;
 #pragma unroll
           for (int ni = 0; ni < NT; ++ni) {
-            const int c = ni * 8 + gid;
+            const double* hs = (const double*)(base + CF::NB * CF::xbox + (ni >> 1) * CF::hbox);
+            const int c = (ni & 1) * 8 + gid;
             const double b = hs[hr * 16 + (((c >> 1) ^ (hr & 7)) << 1) + (c & 1)];
             dmma884(acc[h][0][ni][0], acc[h][0][ni][1], h ? a0.y : a0.x, b);
             dmma884(acc[h][1][ni][0], acc[h][1][ni][1], h ? a1.y : a1.x, b);
@@ -1028,16 +1045,17 @@ __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
         for (int ni = 0; ni < NT; ++ni) yt[mi][ni][0] = yt[mi][ni][1] = 0.0;
       if (use_y) {
         mbar_wait(yfull, (unsigned)lt & 1);
-        double2 ya[2][2];
+        double2 ya[2][2 * NYB];
 #pragma unroll
-        for (int kk2 = 0; kk2 < 2; ++kk2) {
+        for (int kk2 = 0; kk2 < 2 * NYB; ++kk2) {
+          const double* yb = Ys + (kk2 >> 1) * (CF::xbox / 8);
           const int chunk = (((kk2 & 1) << 2) | tig) ^ prow;
-          ya[0][kk2] = *reinterpret_cast<const double2*>(Ys + (warp * 16 + prow) * 16 + chunk * 2);
+          ya[0][kk2] = *reinterpret_cast<const double2*>(yb + (warp * 16 + prow) * 16 + chunk * 2);
           ya[1][kk2] =
-              *reinterpret_cast<const double2*>(Ys + (warp * 16 + 8 + prow) * 16 + chunk * 2);
+              *reinterpret_cast<const double2*>(yb + (warp * 16 + 8 + prow) * 16 + chunk * 2);
         }
 #pragma unroll
-        for (int kk2 = 0; kk2 < 2; ++kk2)
+        for (int kk2 = 0; kk2 < 2 * NYB; ++kk2)
 #pragma unroll
           for (int h = 0; h < 2; ++h)
 #pragma unroll
@@ -1070,15 +1088,18 @@ __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
         }
       }
       if (gram) {
-        const int pair = warp % NPAIR;
-        const int k0 = (warp / NPAIR) * KSTEPS;
-        const int mi = pair / NT, ni = pair % NT;
+#pragma unroll
+        for (int p = 0; p < PPW; ++p) {
+          const int pair = (KSPLIT > 1) ? (warp % NPAIR) : (warp + 8 * p);
+          const int k0 = (KSPLIT > 1) ? (warp / NPAIR) * KSTEPS : 0;
+          const int mi = pair / NT, ni = pair % NT;
 #pragma unroll 8
-        for (int kk = 0; kk < KSTEPS; ++kk) {
-          const int kr = (k0 + kk) * 4 + tig;
-          const double a = Os[kr * OP + mi * 8 + gid];
-          const double b = Os[kr * OP + ni * 8 + gid];
-          dmma884(g[kk & 1][0], g[kk & 1][1], a, b);
+          for (int kk = 0; kk < KSTEPS; ++kk) {
+            const int kr = (k0 + kk) * 4 + tig;
+            const double a = Os[kr * OP + mi * 8 + gid];
+            const double b = Os[kr * OP + ni * 8 + gid];
+            dmma884(g[p][kk & 1][0], g[p][kk & 1][1], a, b);
+          }
         }
       }
       bar_consumers();
@@ -1086,8 +1107,12 @@ __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
   }
   if (gram) {
     double* red = Os;  // free now: every consumer passed the last barrier
+    // 8 warps x PPW tiles x 64 values; tile (pair) of KSPLIT group k at slot k*NPAIR+pair
 #pragma unroll
-    for (int e = 0; e < 2; ++e) red[warp * 64 + gid * 8 + 2 * tig + e] = g[0][e] + g[1][e];
+    for (int p = 0; p < PPW; ++p)
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        red[(warp + 8 * p) * 64 + gid * 8 + 2 * tig + e] = g[p][0][e] + g[p][1][e];
     bar_consumers();
     for (int idx = tid; idx < NPAIR * 64; idx += 256) {
       const int pair = idx / 64, ii = (idx % 64) / 8, jj = idx % 8;
@@ -1238,14 +1263,27 @@ static bool nn_tma_launch(const double* X, int64_t ldx, const double* H, int64_t
   if (!make_map(&xm, X, q, s, ldx, NT_R) || !make_map(&hm, H, s, w, ldh, NNT_KC)) return false;
   if (use_y ? !make_map(&ym, Y, q, w, ldy, NT_R) : !make_map(&ym, X, q, s, ldx, NT_R))
     return false;
-  using CF = NnTmaCfg<NNT_KC, NNT_S>;
+  if (w > 16) {  // 16 < w <= 32: two H / Y boxes, one CTA per SM, 3-stage ring
+    using CF2 = NnTmaCfg<NNT_KC, 3, 2>;
+    static bool attr2 = false;
+    if (!attr2) {
+      TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_tma_kernel<NNT_KC, 3, 2>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF2::bytes));
+      attr2 = true;
+    }
+    gemm_nn_tma_kernel<NNT_KC, 3, 2><<<nn_ctas(q, 32), 288, CF2::bytes, st>>>(
+        xm, hm, ym, use_y, T, Z, ldz, q, s, w, alpha, beta, gram);
+    TSVD_CHECK_LAUNCH();
+    return true;
+  }
+  using CF = NnTmaCfg<NNT_KC, NNT_S, 1>;
   static bool attr = false;
   if (!attr) {
-    TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_tma_kernel<NNT_KC, NNT_S>,
+    TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_tma_kernel<NNT_KC, NNT_S, 1>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
     attr = true;
   }
-  gemm_nn_tma_kernel<NNT_KC, NNT_S><<<nn_ctas(q, 16), 288, CF::bytes, st>>>(
+  gemm_nn_tma_kernel<NNT_KC, NNT_S, 1><<<nn_ctas(q, 16), 288, CF::bytes, st>>>(
       xm, hm, ym, use_y, T, Z, ldz, q, s, w, alpha, beta, gram);
   TSVD_CHECK_LAUNCH();
   return true;
@@ -1338,7 +1376,7 @@ void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const d
     return;
   }
   const bool v2 = s == 0 || (aligned16(X, ldx) && aligned16(H, ldh));
-  if (w > 8 && w <= 16 && s > 0 && v2 && g_nn_tma &&
+  if (w > 8 && w <= 32 && s > 0 && v2 && g_nn_tma &&
       nn_tma_launch(X, ldx, H, ldh, Y, ldy, T, Z, ldz, q, s, w, alpha, beta, gram, st))
     return;
 #define NN_CASE(WPV)                                                                      \

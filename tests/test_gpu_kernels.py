@@ -63,7 +63,9 @@ def test_philox_normal_ulp(q, w, row0, qt, draw):
 
 
 @pytest.mark.parametrize("q,s,w", [(1, 1, 1), (100, 7, 3), (1000, 33, 16), (4097, 130, 32),
-                                   (200000, 64, 16), (3000, 10, 40), (129, 300, 8)])
+                                   (200000, 64, 16), (3000, 10, 40), (129, 300, 8),
+                                   (100000, 300, 32), (5000, 20, 28), (64001, 16, 32),
+                                   (30000, 640, 24)])
 def test_gemm_tn(q, s, w):
     rng = np.random.default_rng(q + s + w)
     X = rng.standard_normal((q, s))
@@ -77,7 +79,9 @@ def test_gemm_tn(q, s, w):
 
 @pytest.mark.parametrize("q,s,w,alpha,beta", [(1, 1, 1, 1.0, 0.0), (100, 7, 3, -1.0, 1.0),
                                               (4097, 130, 32, -1.0, 1.0), (1000, 0, 16, 0.0, 1.0),
-                                              (3000, 50, 40, 1.0, 0.0), (65, 700, 8, 2.0, 0.5)])
+                                              (3000, 50, 40, 1.0, 0.0), (65, 700, 8, 2.0, 0.5),
+                                              (50000, 320, 32, -1.0, 1.0), (20001, 96, 24, 1.0, 0.0),
+                                              (777, 40, 18, 0.5, -2.0), (9000, 2000, 32, 1.0, 0.0)])
 def test_gemm_nn(q, s, w, alpha, beta):
     rng = np.random.default_rng(q * 7 + s + w)
     X = rng.standard_normal((q, max(s, 1)))[:, :s]
