@@ -45,6 +45,18 @@ CONFIG_TEXT = {
 }
 
 
+def _fp64_peak():
+    """FP64 DMMA (mma.sync m8n8k4 f64) peak measured on this pool's B200 by
+    scripts/peaks.cu (profiles/box_facts_r01.json); MEASURED_PEAKS.json has no
+    FP64 entry and tcgen05 has no f64 kind."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "box_facts_r01.json")) as f:
+            return float(json.load(f)["dmma_m8n8k4_f64_tflops"]), \
+                "profiles/box_facts_r01.json dmma_m8n8k4_f64_tflops (measured, scripts/peaks.cu)"
+    except Exception:
+        return 37.0, "fallback 37 TF/s (FP64 DMMA)"
+
+
 def workload_text(cfg_name: str, algo: str) -> str:
     from tsvd_inputs import CONFIGS
     t = CONFIG_TEXT.get(cfg_name, "")
@@ -426,35 +438,50 @@ def main():
         accuracy = residual_check(dwork, U, S, V)
     del U, S, V
 
-    # roofline of the dominant phase
+    # roofline of the dominant phase: the binding roof of its algorithmic work
+    # -- HBM bytes vs the measured copy bandwidth, or FP64
+    # flops vs the measured DMMA peak, whichever needs more time at peak
     peak, peak_kind = _peaks()
-    hbm_phases = {k: v for k, v in prof.items() if v["calls"] > 0 and v["bytes"] > 0}
+    fpeak, fpeak_src = _fp64_peak()
     dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
-    roof = None
-    if dom[1]["bytes"] > 0:
-        ach = dom[1]["bytes"] / (dom[1]["ms"] * 1e-3) / 1e9
-        traffic = None
-        tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tfile):
-            try:
-                tj = json.load(open(tfile))
-                tr = tj.get(f"{dom[0]}:{'csr' if 'csr' in work else 'dense'}") or tj.get(dom[0])
-                if tr:
-                    traffic = tr["dram_over_alg"] * dom[1]["bytes"] / max(1, dom[1]["calls"])
-            except Exception:
-                traffic = None
-        roof = {"bound": "hbm", "kernel": dom[0], "achieved": round(ach, 1), "peak": peak,
-                "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": traffic,
-                "alg_bytes_per_launch": dom[1]["bytes"] / max(1, dom[1]["calls"]),
-                "avg_launch_ms": dom[1]["ms"] / max(1, dom[1]["calls"]),
-                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
-    else:
-        roof = {"bound": "alu", "kernel": dom[0], "achieved": None, "peak": None,
+    dn, dv = dom
+    calls = max(1, dv["calls"])
+    t_hbm = dv["bytes"] / (peak * 1e9) if dv["bytes"] > 0 else 0.0
+    t_fp = dv["flops"] / (fpeak * 1e12) if dv["flops"] > 0 else 0.0
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile) and dv["bytes"] > 0:
+        try:
+            tj = json.load(open(tfile))
+            tr = tj.get(f"{dn}:{'csr' if 'csr' in work else 'dense'}") or tj.get(dn)
+            if tr:
+                traffic = tr["dram_over_alg"] * dv["bytes"] / calls
+        except Exception:
+            traffic = None
+    sec = dv["ms"] * 1e-3
+    if t_hbm == 0.0 and t_fp == 0.0:
+        roof = {"bound": "alu", "kernel": dn, "achieved": None, "peak": None,
                 "unit": "GFLOP/s", "frac": None, "traffic": None}
+    elif t_fp > t_hbm:
+        ach = dv["flops"] / sec / 1e12
+        roof = {"bound": "tensor", "kernel": dn, "achieved": round(ach, 2), "peak": fpeak,
+                "unit": "TFLOP/s", "frac": round(ach / fpeak, 4), "traffic": traffic,
+                "alg_flops_per_launch": dv["flops"] / calls,
+                "hbm_GBps": round(dv["bytes"] / sec / 1e9, 1),
+                "peak_source": fpeak_src}
+    else:
+        ach = dv["bytes"] / sec / 1e9
+        roof = {"bound": "hbm", "kernel": dn, "achieved": round(ach, 1), "peak": peak,
+                "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": traffic,
+                "fp64_TFps": round(dv["flops"] / sec / 1e12, 2),
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
+    roof["alg_bytes_per_launch"] = dv["bytes"] / calls
+    roof["avg_launch_ms"] = dv["ms"] / calls
     total_ms = sum(v["ms"] for v in prof.values()) or 1.0
     phases = {k: {"ms_per_step": round(v["ms"] / args.steps, 3),
                   "share": round(v["ms"] / total_ms, 4),
                   "GBps": round(v["bytes"] / (v["ms"] * 1e-3) / 1e9, 1) if v["ms"] > 0 and v["bytes"] > 0 else None,
+                  "TFps": round(v["flops"] / (v["ms"] * 1e-3) / 1e12, 2) if v["ms"] > 0 and v["flops"] > 0 else None,
                   "calls_per_step": v["calls"] / args.steps}
               for k, v in prof.items() if v["calls"] > 0}
 

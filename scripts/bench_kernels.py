@@ -13,7 +13,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2403_06218_b200 as T  # noqa: E402
 
-HBM = 6540.8
+HBM = 6548.5
 
 
 def timeit(fn, reps=5, warm=2):
@@ -59,8 +59,9 @@ def tn_bench():
         ms = timeit(lambda: T.lib().tsvd_dbg_gemm_tn(Xv.data_ptr(), X.stride(0), Yv.data_ptr(),
                                                      X.stride(0), q, s, w, C.data_ptr(), None))
         gb = 8.0 * q * (s + w) / (ms * 1e-3) / 1e9
-        print(f"gemm_tn q={q} s={s} w={w}: {ms:.3f} ms  {gb:.0f} GB/s ({gb / HBM:.2f} of HBM)",
-              flush=True)
+        tf = 2.0 * q * s * w / (ms * 1e-3) / 1e12
+        print(f"gemm_tn q={q} s={s} w={w}: {ms:.3f} ms  {gb:.0f} GB/s ({gb / HBM:.2f} of HBM) "
+              f"{tf:.1f} TF/s ({tf / 37.1:.2f} of DMMA)", flush=True)
 
 
 def nn_bench():
@@ -73,8 +74,9 @@ def nn_bench():
         ms = timeit(lambda: T.lib().tsvd_dbg_gemm_nn(X.data_ptr(), X.stride(0), H.data_ptr(), w,
                                                      Z.data_ptr(), w, q, s, w, -1.0, 1.0, None))
         gb = 8.0 * q * (s + 2 * w) / (ms * 1e-3) / 1e9
-        print(f"gemm_nn q={q} s={s} w={w}: {ms:.3f} ms  {gb:.0f} GB/s ({gb / HBM:.2f} of HBM)",
-              flush=True)
+        tf = 2.0 * q * (s + w) * w / (ms * 1e-3) / 1e12
+        print(f"gemm_nn q={q} s={s} w={w}: {ms:.3f} ms  {gb:.0f} GB/s ({gb / HBM:.2f} of HBM) "
+              f"{tf:.1f} TF/s ({tf / 37.1:.2f} of DMMA)", flush=True)
 
 
 def sweep_bench():
@@ -138,6 +140,25 @@ def spmm_bench():
             gb = (12.0 * nnz + 8 * (m + 1) + 8.0 * w * (m + n)) / (ms * 1e-3) / 1e9
             print(f"spmm w={w} trans={tr}: {ms:.3f} ms  {gb:.0f} GB/s compulsory "
                   f"({gb / HBM:.2f} of HBM)", flush=True)
+
+
+def dense_bench():
+    """C4's dense products A.X / A^T.X (FP64 DMMA-bound for w >= 32)"""
+    m, n = 40_000, 20_000
+    A = torch.randn((m, n), dtype=torch.float64, device="cuda")
+    h = T.TruncatedSVD(A)
+    for w in (16, 32, 210):
+        X = torch.randn((n, w), dtype=torch.float64, device="cuda")
+        Xt = torch.randn((m, w), dtype=torch.float64, device="cuda")
+        Y = torch.empty((m, w), dtype=torch.float64, device="cuda")
+        Z = torch.empty((n, w), dtype=torch.float64, device="cuda")
+        for tr, xin, yout in ((False, X, Y), (True, Xt, Z)):
+            ms = timeit(lambda: T.dbg_apply(h, tr, xin, yout))
+            tf = 2.0 * m * n * w / (ms * 1e-3) / 1e12
+            gb = 8.0 * (m * n + w * (m + n)) / (ms * 1e-3) / 1e9
+            print(f"dense w={w} trans={tr}: {ms:.3f} ms  {tf:.1f} TF/s ({tf / 37.1:.2f} of DMMA)  "
+                  f"{gb:.0f} GB/s ({gb / HBM:.2f} of HBM)", flush=True)
+    h.close()
 
 
 def cqr_bench():
