@@ -352,9 +352,14 @@ static void apply_local(Ctx& c, bool trans, const double* X, int64_t ldx, double
   const double flops = c.dense ? 2.0 * c.m * c.ng * w : 2.0 * c.A.nnz * w;
   Prof p(c, trans ? P_APPLY_AT : P_APPLY_A, bytes, flops);
   if (c.dense) {
-    if (!trans)
+    if (!trans) {
+      // split-K scratch for the few-row-tile dense product (ts.cu pick_split)
+      const bool few_tiles = c.m < (int64_t)128 * 8 * 148;
+      const size_t cap = few_tiles ? (size_t)8 * c.m * std::min(w, 64) : 0;
+      double* part = few_tiles ? dbuf(c, "nn_split", cap) : nullptr;
       gemm_nn(c.Ad, c.lda, X, ldx, nullptr, 0, nullptr, Y, ldy, c.m, (int)c.ng, w, 1.0, 0.0,
-              nullptr, c.st);
+              nullptr, c.st, part, cap);
+    }
     else
       gemm_tn(c.Ad, c.lda, X, ldx, c.m, (int)c.ng, w, Y, ldy, part_tn(c, c.m, (int)c.ng), c.st);
   } else {

@@ -104,9 +104,12 @@ void gemm_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t
 // gram != null: per-CTA partial Gram Z^T Z (w x w) at gram[cta*w*w] for
 // nn_ctas(q, w) CTAs.
 int nn_ctas(int64_t q, int w);
+// part/part_cap (doubles): optional scratch for split-K partials of plain
+// products (beta = 0, no T/gram) with few row tiles; nullptr disables the split.
 void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const double* Y,
              int64_t ldy, const double* T, double* Z, int64_t ldz, int64_t q, int s, int w,
-             double alpha, double beta, double* gram, cudaStream_t st);
+             double alpha, double beta, double* gram, cudaStream_t st, double* part = nullptr,
+             size_t part_cap = 0);
 
 // small (single-CTA) finalisers (small.cu)
 // W = sum of np partial (w x w) Grams; L = chol(W), T = L^{-T}; flag |= breakdown.

@@ -924,7 +924,11 @@ template <int KC, int S, int NYB>
 __global__ void __launch_bounds__(288, NYB == 1 ? 2 : 1) gemm_nn_tma_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
     const __grid_constant__ CUtensorMap ymap, int use_y, const double* __restrict__ T, double* Z,
-    int64_t ldz, int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram) {
+    int64_t ldz, int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram,
+    int64_t zsplit) {
+  // split-K (gridDim.y > 1, plain products only: no Y / T / Gram): CTA row y
+  // takes K chunks [nk_all y / Y, nk_all (y+1) / Y) and writes its partial
+  // product to Z + y zsplit; the caller sums the partials in a fixed order.
   using CF = NnTmaCfg<KC, S, NYB>;
   constexpr int WP = CF::WP, NT = 2 * NYB, OP = CF::OP, TP = CF::TP, NPAIR = NT * NT;
   // Gram: NPAIR 8x8 output tiles over 8 warps (KSPLIT warps share a tile and
@@ -960,8 +964,11 @@ __global__ void __launch_bounds__(288, NYB == 1 ? 2 : 1) gemm_nn_tma_kernel(
   const int64_t ntiles = (q + NT_R - 1) / NT_R;
   const int64_t my_tiles =
       (ntiles > (int64_t)blockIdx.x) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int nk = (s + KC - 1) / KC;
+  const int nk_all = (s + KC - 1) / KC;
+  const int kb = (int)((int64_t)nk_all * blockIdx.y / gridDim.y);
+  const int nk = (int)((int64_t)nk_all * (blockIdx.y + 1) / gridDim.y) - kb;
   const int64_t nsteps = my_tiles * nk;
+  Z += (int64_t)blockIdx.y * zsplit;
   if (warp == 8) {  // producer: X/H chunks into the ring, the tile's Y rows into Ys
     if (lane == 0) {
       for (int64_t j = 0; j < nsteps; ++j) {
@@ -975,10 +982,11 @@ __global__ void __launch_bounds__(288, NYB == 1 ? 2 : 1) gemm_nn_tma_kernel(
         mbar_expect_tx(&full[st], CF::tx);
 #pragma unroll
         for (int b = 0; b < CF::NB; ++b)
-          tma_load_2d(base + b * CF::xbox, &xmap, kc * KC + b * 16, r0, &full[st]);
+          tma_load_2d(base + b * CF::xbox, &xmap, (kb + kc) * KC + b * 16, r0, &full[st]);
 #pragma unroll
         for (int b = 0; b < NYB; ++b)
-          tma_load_2d(base + CF::NB * CF::xbox + b * CF::hbox, &hmap, b * 16, kc * KC, &full[st]);
+          tma_load_2d(base + CF::NB * CF::xbox + b * CF::hbox, &hmap, b * 16, (kb + kc) * KC,
+                      &full[st]);
         if (use_y && kc == nk - 1) {  // with the tile's last chunk: never stalls the X ring
           if (lt > 0) mbar_wait(yempty, (unsigned)(lt - 1) & 1);
           mbar_expect_tx(yfull, (unsigned)(NYB * CF::xbox));
@@ -1144,8 +1152,8 @@ struct NnOutCfg {
 template <int KC, int S, int NT>  // NT = 8-column tiles computed (w <= 8 NT <= 64)
 __global__ void __launch_bounds__(288, 1) gemm_nn_out_tma_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap, double* Z,
-    int64_t ldz, int64_t q, int s, int w, double alpha) {
-  using CF = NnOutCfg<KC, S>;
+    int64_t ldz, int64_t q, int s, int w, double alpha, int64_t zsplit) {
+  using CF = NnOutCfg<KC, S>;  // split-K over blockIdx.y as in gemm_nn_tma_kernel
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(sm + CF::bar_off);
@@ -1164,8 +1172,11 @@ __global__ void __launch_bounds__(288, 1) gemm_nn_out_tma_kernel(
   const int64_t ntiles = (q + NT_R - 1) / NT_R;
   const int64_t my_tiles =
       (ntiles > (int64_t)blockIdx.x) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const int nk = (s + KC - 1) / KC;
+  const int nk_all = (s + KC - 1) / KC;
+  const int kb = (int)((int64_t)nk_all * blockIdx.y / gridDim.y);
+  const int nk = (int)((int64_t)nk_all * (blockIdx.y + 1) / gridDim.y) - kb;
   const int64_t nsteps = my_tiles * nk;
+  Z += (int64_t)blockIdx.y * zsplit;
   if (warp == 8) {
     if (lane == 0) {
       for (int64_t j = 0; j < nsteps; ++j) {
@@ -1179,10 +1190,11 @@ __global__ void __launch_bounds__(288, 1) gemm_nn_out_tma_kernel(
         mbar_expect_tx(&full[st], CF::tx);
 #pragma unroll
         for (int b = 0; b < CF::NB; ++b)
-          tma_load_2d(base + b * CF::xbox, &xmap, kc * KC + b * 16, r0, &full[st]);
+          tma_load_2d(base + b * CF::xbox, &xmap, (kb + kc) * KC + b * 16, r0, &full[st]);
 #pragma unroll
         for (int b = 0; b < 4; ++b)
-          tma_load_2d(base + CF::NB * CF::xbox + b * CF::hbox, &hmap, b * 16, kc * KC, &full[st]);
+          tma_load_2d(base + CF::NB * CF::xbox + b * CF::hbox, &hmap, b * 16, (kb + kc) * KC,
+                      &full[st]);
       }
     }
     return;
@@ -1252,10 +1264,33 @@ __global__ void __launch_bounds__(288, 1) gemm_nn_out_tma_kernel(
 
 constexpr int NNT_KC = 32, NNT_S = 2;
 
+// Split-K factor for a plain product with few row tiles (dense A.X: 313
+// tiles of 128 rows on 148 SMs would leave a 2.1-wave tail): the grid is
+// (ctas / ks) x ks, each CTA takes ceil(tiles / (ctas / ks)) tiles for 1/ks
+// of K; ks maximises that balance (>= 4 K chunks per unit, partials fit).
+static int pick_split(int64_t q, int s, int w, int ctas, size_t part_cap) {
+  const int64_t tiles = (q + NT_R - 1) / NT_R;
+  const int nk_all = (s + NNT_KC - 1) / NNT_KC;
+  if (part_cap == 0 || tiles >= 8 * (int64_t)ctas) return 1;
+  const double ideal = (double)tiles / ctas;
+  double best_eff = ideal / (double)((tiles + ctas - 1) / ctas);
+  int best = 1;
+  for (int ks = 2; ks <= 8; ++ks) {
+    if (nk_all / ks < 4 || (size_t)ks * q * w > part_cap) break;
+    const int gx = ctas / ks;
+    const double eff = ideal / ((double)((tiles + gx - 1) / gx) / ks);
+    if (eff > best_eff * 1.03) {
+      best_eff = eff;
+      best = ks;
+    }
+  }
+  return best;
+}
+
 static bool nn_tma_launch(const double* X, int64_t ldx, const double* H, int64_t ldh,
                           const double* Y, int64_t ldy, const double* T, double* Z, int64_t ldz,
                           int64_t q, int s, int w, double alpha, double beta, double* gram,
-                          cudaStream_t st) {
+                          cudaStream_t st, double* part, size_t part_cap) {
   if (q >= (int64_t)1 << 31 || s >= (1 << 30)) return false;
   const int use_y = (beta != 0.0 && Y) ? 1 : 0;
   if (use_y && !aligned16(Y, ldy)) return false;
@@ -1271,8 +1306,17 @@ static bool nn_tma_launch(const double* X, int64_t ldx, const double* H, int64_t
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF2::bytes));
       attr2 = true;
     }
-    gemm_nn_tma_kernel<NNT_KC, 3, 2><<<nn_ctas(q, 32), 288, CF2::bytes, st>>>(
-        xm, hm, ym, use_y, T, Z, ldz, q, s, w, alpha, beta, gram);
+    const int ctas = nn_ctas(q, 32);
+    const int ks = (use_y || T || gram) ? 1 : pick_split(q, s, w, ctas, part_cap);
+    if (ks > 1) {
+      gemm_nn_tma_kernel<NNT_KC, 3, 2><<<dim3(ctas / ks, ks), 288, CF2::bytes, st>>>(
+          xm, hm, ym, 0, nullptr, part, w, q, s, w, alpha, 0.0, nullptr, q * w);
+      TSVD_CHECK_LAUNCH();
+      reduce_launch(part, ks, q * w, Z, w, ldz == w ? 0 : ldz, st);
+      return true;
+    }
+    gemm_nn_tma_kernel<NNT_KC, 3, 2><<<ctas, 288, CF2::bytes, st>>>(
+        xm, hm, ym, use_y, T, Z, ldz, q, s, w, alpha, beta, gram, 0);
     TSVD_CHECK_LAUNCH();
     return true;
   }
@@ -1283,15 +1327,24 @@ static bool nn_tma_launch(const double* X, int64_t ldx, const double* H, int64_t
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
     attr = true;
   }
-  gemm_nn_tma_kernel<NNT_KC, NNT_S, 1><<<nn_ctas(q, 16), 288, CF::bytes, st>>>(
-      xm, hm, ym, use_y, T, Z, ldz, q, s, w, alpha, beta, gram);
+  const int ctas = nn_ctas(q, 16);
+  const int ks = (use_y || T || gram) ? 1 : pick_split(q, s, w, ctas, part_cap);
+  if (ks > 1) {
+    gemm_nn_tma_kernel<NNT_KC, NNT_S, 1><<<dim3(ctas / ks, ks), 288, CF::bytes, st>>>(
+        xm, hm, ym, 0, nullptr, part, w, q, s, w, alpha, 0.0, nullptr, q * w);
+    TSVD_CHECK_LAUNCH();
+    reduce_launch(part, ks, q * w, Z, w, ldz == w ? 0 : ldz, st);
+    return true;
+  }
+  gemm_nn_tma_kernel<NNT_KC, NNT_S, 1><<<ctas, 288, CF::bytes, st>>>(
+      xm, hm, ym, use_y, T, Z, ldz, q, s, w, alpha, beta, gram, 0);
   TSVD_CHECK_LAUNCH();
   return true;
 }
 
 static bool nn_out_tma_launch(const double* X, int64_t ldx, const double* H, int64_t ldh,
                               double* Z, int64_t ldz, int64_t q, int s, int w, double alpha,
-                              cudaStream_t st) {
+                              cudaStream_t st, double* part, size_t part_cap) {
   if (q >= (int64_t)1 << 31 || s >= (1 << 30)) return false;
   CUtensorMap xm, hm;
   if (!make_map(&xm, X, q, s, ldx, NT_R) || !make_map(&hm, H, s, w, ldh, NNT_KC)) return false;
@@ -1310,15 +1363,20 @@ static bool nn_out_tma_launch(const double* X, int64_t ldx, const double* H, int
     attr = true;
   }
   const int nt = (w + 7) / 8;
+  const int ctas = nn_ctas(q, 32);
+  const int ks = pick_split(q, s, w, ctas, part_cap);
+  double* zo = ks > 1 ? part : Z;
+  const int64_t ldo = ks > 1 ? w : ldz;
 #define OUT_GO(NTV)                                                                       \
-  gemm_nn_out_tma_kernel<NNT_KC, OS, NTV><<<nn_ctas(q, 32), 288, CF::bytes, st>>>(xm, hm, Z, \
-                                                                                ldz, q, s, w, alpha)
+  gemm_nn_out_tma_kernel<NNT_KC, OS, NTV><<<dim3(ctas / ks, ks), 288, CF::bytes, st>>>(    \
+      xm, hm, zo, ldo, q, s, w, alpha, ks > 1 ? q * w : 0)
   if (nt <= 5) OUT_GO(5);
   else if (nt == 6) OUT_GO(6);
   else if (nt == 7) OUT_GO(7);
   else OUT_GO(8);
 #undef OUT_GO
   TSVD_CHECK_LAUNCH();
+  if (ks > 1) reduce_launch(part, ks, q * w, Z, w, ldz == w ? 0 : ldz, st);
   return true;
 }
 
@@ -1341,7 +1399,8 @@ static void nn_launch(const double* X, int64_t ldx, const double* H, int64_t ldh
 
 void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const double* Y,
              int64_t ldy, const double* T, double* Z, int64_t ldz, int64_t q, int s, int w,
-             double alpha, double beta, double* gram, cudaStream_t st) {
+             double alpha, double beta, double* gram, cudaStream_t st, double* part,
+             size_t part_cap) {
   if (w <= 0 || q <= 0) return;
   if (w > 32) {
     if (T || gram) throw Error{TSVD_EINVAL, "gemm_nn: T/gram need w <= 32"};
@@ -1349,7 +1408,7 @@ void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const d
       bool done = true;
       for (int c0 = 0; c0 < w && done; c0 += 64)
         done = nn_out_tma_launch(X, ldx, H + c0, ldh, Z + c0, ldz, q, s, std::min(64, w - c0),
-                                 alpha, st);
+                                 alpha, st, part, part_cap);
       if (done) return;
     }
     const int cw = (beta == 0.0) ? 64 : 32;  // wide products (outputs) in one pass per 64 cols
@@ -1377,7 +1436,8 @@ void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const d
   }
   const bool v2 = s == 0 || (aligned16(X, ldx) && aligned16(H, ldh));
   if (w > 8 && w <= 32 && s > 0 && v2 && g_nn_tma &&
-      nn_tma_launch(X, ldx, H, ldh, Y, ldy, T, Z, ldz, q, s, w, alpha, beta, gram, st))
+      nn_tma_launch(X, ldx, H, ldh, Y, ldy, T, Z, ldz, q, s, w, alpha, beta, gram, st, part,
+                    part_cap))
     return;
 #define NN_CASE(WPV)                                                                      \
   if (v2)                                                                                 \

@@ -148,19 +148,22 @@ def test_spmm_parity(kind, w):
     h.close()
 
 
-def test_dense_apply_parity():
-    rng = np.random.default_rng(3)
-    A = rng.standard_normal((3000, 1100))
+@pytest.mark.parametrize("m,n,ws", [(3000, 1100, (4, 12, 32, 37)), (20000, 2500, (16, 29, 69)),
+                                    (41000, 700, (32, 64))])
+def test_dense_apply_parity(m, n, ws):
+    """Dense A.X / A^T.X; few row tiles -> split-K partials summed in order."""
+    rng = np.random.default_rng(m + n)
+    A = rng.standard_normal((m, n))
     h = T.TruncatedSVD(A)
-    for w in (4, 32, 37):
-        X = rng.standard_normal((1100, w))
-        Xt = rng.standard_normal((3000, w))
-        Yg = torch.zeros((3000, w), dtype=torch.float64, device="cuda")
-        Zg = torch.zeros((1100, w), dtype=torch.float64, device="cuda")
+    for w in ws:
+        X = rng.standard_normal((n, w))
+        Xt = rng.standard_normal((m, w))
+        Yg = torch.zeros((m, w), dtype=torch.float64, device="cuda")
+        Zg = torch.zeros((n, w), dtype=torch.float64, device="cuda")
         T.dbg_apply(h, False, cu(X), Yg)
         T.dbg_apply(h, True, cu(Xt), Zg)
-        assert np.all(np.abs(Yg.cpu().numpy() - A @ X) <= 4 * 1100 * U * np.abs(A) @ np.abs(X))
-        assert np.all(np.abs(Zg.cpu().numpy() - A.T @ Xt) <= 4 * 3000 * U * np.abs(A.T) @ np.abs(Xt))
+        assert np.all(np.abs(Yg.cpu().numpy() - A @ X) <= 4 * n * U * np.abs(A) @ np.abs(X))
+        assert np.all(np.abs(Zg.cpu().numpy() - A.T @ Xt) <= 4 * m * U * np.abs(A.T) @ np.abs(Xt))
     h.close()
 
 
