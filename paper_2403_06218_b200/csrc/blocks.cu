@@ -190,7 +190,7 @@ int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
 }
 
 int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H,
-             double* R) {
+             double* R, bool need_h) {
   if (s == 0) return cholqr2(c, basis, q, w, ld, R);
   if (w > 32) throw Error{TSVD_EINVAL, "cgs_cqr2: block wider than 32"};
   double* Y = basis + s;
@@ -238,7 +238,8 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
     Prof p(c, P_SMALL, 0, 0);
     int k = np;
     const double* W = reduce_gram(c, gram, k, w, Wred);
-    chol2_finalize(W, k, w, L1, L2, T2, R, H, Hbar, s, ortho_flags(c) + 1, c.st);    // S9,S11,S12
+    chol2_finalize(W, k, w, L1, L2, T2, R, need_h ? H : nullptr, Hbar, s, ortho_flags(c) + 1,
+                   c.st);                                                             // S9,S11,S12
   }
   if (breakdown(c)) {
     Prof p(c, P_OTHER, 0, 0);

@@ -93,8 +93,10 @@ void prof_release(Ctx& c);
 // dimension ld; "basis" holds P in columns [0, s) and the block Y being
 // orthogonalised in columns [s, s+w).
 int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R);
+// need_h = false: the caller discards H (LancSVD, reading R17), so S12's
+// H += Hbar L^T is skipped (H still holds the first projection P^T Y).
 int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H,
-             double* R);
+             double* R, bool need_h = true);
 void cgs2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H, double* R);
 int cgs_qr(Ctx& c, double* Y, int64_t q, int l, int64_t ld, int bq, double* R);
 void apply(Ctx& c, bool trans, const double* X, int64_t ldx, double* Y, int64_t ldy, int w);

@@ -54,11 +54,17 @@ size_t small_svd_work(int d) {
   n = std::max(n, jac_layout(d, dp4));
   const size_t dp2 = (size_t)(((d + 1) / 2 + 1) & ~1) * 2 + 8;
   n = std::max(n, jac_layout(d, dp2));
-  return n + 64;  // control words live in the last 64 doubles
+  return n + 64 + 1024;  // flags (1024 doubles), then control words (last 64 doubles)
 }
 static unsigned* jac_ctl(double* work, int d) {
   return (unsigned*)(work + small_svd_work(d) - 64);
 }
+// register path: per-sweep "rotated" words [0, kMaxSweeps) and per-block
+// version counters [32, 32 + nb) (dataflow hand-off between CTAs)
+static unsigned* jac_flags(double* work, int d) {
+  return (unsigned*)(work + small_svd_work(d) - 64 - 1024);
+}
+constexpr int kJacFlagVer = 32;
 
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblocks) {
   __syncthreads();
@@ -90,7 +96,10 @@ __device__ __forceinline__ void circle_pair(int t, int round, int ne, int& p, in
 
 __global__ void jacobi_init_kernel(const double* __restrict__ B, int d, int dp,
                                    double* __restrict__ G, double* __restrict__ V,
-                                   unsigned* __restrict__ ctl) {
+                                   unsigned* __restrict__ ctl, unsigned* __restrict__ flags) {
+  if (flags)
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < 2048; i += gridDim.x * blockDim.x)
+      flags[i] = 0u;
   const int64_t total = (int64_t)d * dp + (int64_t)dp * dp;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -266,8 +275,8 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(double* __restrict__ 
     const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
     if (lane == 0) S[cnt] = sj;
     for (int i = lane; i < d; i += 32) {
-      Ub[(size_t)i * d + cnt] = G[(size_t)j * d + i] * inv;
-      Vb[(size_t)i * d + cnt] = V[(size_t)j * dp + i];
+      Ub[(size_t)i * d + cnt] = __ldcg(G + (size_t)j * d + i) * inv;
+      Vb[(size_t)i * d + cnt] = __ldcg(V + (size_t)j * dp + i);
     }
   }
 }
@@ -341,17 +350,22 @@ __device__ __forceinline__ void jac_pair(int t, int ir, int& p, int& q) {
 
 
 // One inner round on the 2 JB columns held in registers (RG rows per
-// thread, NTHR threads): dot products -> warp reduce-scatter -> fixed-order
-// sum over warps -> JB rotations (Rutishauser) -> apply to the columns and to J.
+// thread, NTHR threads): dot products -> warp reduce-scatter -> one CTA
+// barrier -> every warp sums the per-warp partials in warp order and computes
+// the JB rotations (Rutishauser) redundantly (lane t: rotation t, broadcast by
+// shuffles) -> apply to the columns; warp 0 also applies them to J.  red is
+// double-buffered by inner-round parity, so one barrier per inner round
+// suffices (a warp reads red[ir & 1] before it can reach barrier ir + 1).
 template <int RG, int JB, int MODE, int NTHR>
 __device__ __forceinline__ void jac_inner(int ir, double (&x)[RG][2 * JB],
-                                          double (*red)[3 * JB + 1], double* rot_cs,
-                                          double* rot_sn, double (*Js)[2 * JB + 1], int* any_rot,
-                                          double tol) {
+                                          double (*red)[3 * JB + 1],
+                                          double (*Js)[2 * JB + 1], int* any_rot, double tol) {
   constexpr int JW = 2 * JB, NV = 3 * JB;
   constexpr int NVP = NV <= 16 ? 16 : (NV <= 32 ? 32 : 64);
   constexpr int NW = NTHR / 32;
+  static_assert(JB <= 32, "one lane per rotation");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double (*rb)[NV + 1] = red + (ir & 1) * NW;
   double v[NVP];
 #pragma unroll
   for (int i = NV; i < NVP; ++i) v[i] = 0.0;
@@ -375,57 +389,72 @@ __device__ __forceinline__ void jac_inner(int ir, double (&x)[RG][2 * JB],
 #pragma unroll
     for (int j = 0; j < NVP / 32; ++j) {
       const int idx = lane * (NVP / 32) + j;
-      if (idx < NV) red[warp][idx] = v[j];
+      if (idx < NV) rb[warp][idx] = v[j];
     }
   } else {
-    if (lane < NV) red[warp][lane] = v[0];
+    if (lane < NV) rb[warp][lane] = v[0];
   }
   __syncthreads();
-  if (tid < JB) {
+  double cs = 1.0, sn = 0.0;
+  if (lane < JB) {
     double a = 0.0, b = 0.0, c = 0.0;
 #pragma unroll
     for (int w2 = 0; w2 < NW; ++w2) {
-      a += red[w2][3 * tid];
-      b += red[w2][3 * tid + 1];
-      c += red[w2][3 * tid + 2];
+      a += rb[w2][3 * lane];
+      b += rb[w2][3 * lane + 1];
+      c += rb[w2][3 * lane + 2];
     }
-    double cs = 1.0, sn = 0.0;
     if (a > 0.0 && b > 0.0 && fabs(c) > tol * sqrt(a * b)) {
       const double h = 0.5 * (b - a);
       const double t = (h >= 0.0 ? c : -c) / (fabs(h) + sqrt(fma(h, h, c * c)));
       cs = rsqrt(fma(t, t, 1.0));
       sn = cs * t;
-      *any_rot = 1;
+      if (warp == 0) *any_rot = 1;
     }
-    rot_cs[tid] = cs;
-    rot_sn[tid] = sn;
   }
-  __syncthreads();
 #pragma unroll
   for (int t = 0; t < JB; ++t) {
     int p, q;
     jac_pair<JB, MODE>(t, ir, p, q);
-    const double cs = rot_cs[t], sn = rot_sn[t];
+    const double ct = __shfl_sync(0xffffffffu, cs, t), st = __shfl_sync(0xffffffffu, sn, t);
 #pragma unroll
     for (int k = 0; k < RG; ++k) {
       const double xp = x[k][p], xq = x[k][q];
-      x[k][p] = cs * xp - sn * xq;
-      x[k][q] = sn * xp + cs * xq;
+      x[k][p] = ct * xp - st * xq;
+      x[k][q] = st * xp + ct * xq;
     }
   }
-  static_assert(JB * 2 * JB <= NTHR, "J update: one thread per entry");
-  if (tid < JB * JW) {
-    const int t = tid / JW, i = tid % JW;
-    int p, q;
-    jac_pair<JB, MODE>(t, ir, p, q);
-    const double cs = rot_cs[t], sn = rot_sn[t];
-    const double jp = Js[i][p], jq = Js[i][q];
-    Js[i][p] = cs * jp - sn * jq;
-    Js[i][q] = sn * jp + cs * jq;
+  if (warp == 0) {
+    // J <- J G_t for every rotation t: lane i owns row i of J (JW <= 32)
+    static_assert(2 * JB <= 32, "J rows: one lane each");
+#pragma unroll
+    for (int t = 0; t < JB; ++t) {
+      int p, q;
+      jac_pair<JB, MODE>(t, ir, p, q);
+      const double ct = __shfl_sync(0xffffffffu, cs, t), st = __shfl_sync(0xffffffffu, sn, t);
+      if (lane < JW) {
+        const double jp = Js[lane][p], jq = Js[lane][q];
+        Js[lane][p] = ct * jp - st * jq;
+        Js[lane][q] = st * jp + ct * jq;
+      }
+    }
   }
 }
 
 constexpr int JR_T = 256;
+
+// Rounds hand blocks from CTA to CTA by dataflow instead of a grid barrier:
+// every block b carries a version counter (the number of rounds it has been
+// through); a CTA starts global round g on its pair (bi, bj) once both
+// versions reach g, and publishes g + 1 after writing the blocks back
+// (release / acquire through __threadfence + atomics; block data is read
+// with L1-bypassing loads).  Each round visits every block exactly once, so
+// a block's owner in round g is unique.  One grid barrier per sweep decides
+// convergence from the per-sweep "rotated" word.
+__device__ __forceinline__ void jac_wait_ver(unsigned* ver, int b, unsigned g) {
+  volatile unsigned* v = ver + b;
+  while (*v < g) __nanosleep(32);
+}
 
 template <int RG, int JC, bool CYC>
 __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict__ G,
@@ -434,17 +463,18 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
                                                             double* __restrict__ Ub,
                                                             double* __restrict__ S,
                                                             double* __restrict__ Vb,
-                                                            unsigned* __restrict__ ctl) {
+                                                            unsigned* __restrict__ ctl,
+                                                            unsigned* __restrict__ flags) {
   constexpr int JW = 2 * JC;   // columns of a block pair (shadows the file-scope JW)
   constexpr int NW = JR_T / 32;
   constexpr int NV = 3 * JC;  // partial sums per inner round
-  __shared__ double red[NW][NV + 1];
-  __shared__ double rot_cs[JC], rot_sn[JC];
+  __shared__ double red[2 * NW][NV + 1];
   __shared__ double Js[JW][JW + 1];
   __shared__ int any_rot;
   unsigned* bar = ctl;
-  unsigned* rot = ctl + 2;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  unsigned* rot = flags;                 // [sweep]
+  unsigned* ver = flags + kJacFlagVer;   // [block]
+  const int tid = threadIdx.x;
   const int dp = nb * JC;
   const unsigned nblk = gridDim.x;
   const double tol = (double)d * 0x1.0p-53;
@@ -454,8 +484,9 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
   // then nb-1 rounds of cross pairs: every pair once, ~d inner rounds);
   // else each round sweeps all pairs of the 2 JC columns (~2d inner rounds)
   const int nrounds = CYC ? nb : nb - 1;
+  unsigned g = 0;  // global round counter
   for (; sweep < kMaxSweeps; ++sweep) {
-    for (int round = 0; round < nrounds; ++round) {
+    for (int round = 0; round < nrounds; ++round, ++g) {
       int bi, bj;
       if (CYC && round == 0) {
         bi = 2 * blockIdx.x;
@@ -463,17 +494,23 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
       } else {
         circle_pair(blockIdx.x, CYC ? round - 1 : round, nb, bi, bj);
       }
+      if (tid == 0) {
+        jac_wait_ver(ver, bi, g);
+        jac_wait_ver(ver, bj, g);
+        __threadfence();
+      }
+      __syncthreads();
 #pragma unroll
       for (int k = 0; k < RG; ++k) {
         const int row = tid + JR_T * k;
 #pragma unroll
         for (int c = 0; c < JW; ++c) {
           const int col = c < JC ? bi * JC + c : bj * JC + (c - JC);
-          x[k][c] = row < d ? G[(size_t)col * d + row] : 0.0;
+          x[k][c] = row < d ? __ldcg(G + (size_t)col * d + row) : 0.0;
         }
       }
       // this round's V rows: in flight during the inner rounds (the pair's V
-      // columns belong to this CTA until the grid barrier)
+      // columns belong to this CTA until it publishes the new versions)
       double vv[RG][JW];
 #pragma unroll
       for (int k = 0; k < RG; ++k) {
@@ -481,23 +518,24 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
 #pragma unroll
         for (int c = 0; c < JW; ++c) {
           const int col = c < JC ? bi * JC + c : bj * JC + (c - JC);
-          vv[k][c] = row < dp ? V[(size_t)col * dp + row] : 0.0;
+          vv[k][c] = row < dp ? __ldcg(V + (size_t)col * dp + row) : 0.0;
         }
       }
       if (tid < JW * JW) Js[tid / JW][tid % JW] = (tid / JW == tid % JW) ? 1.0 : 0.0;
       if (tid == 0) any_rot = 0;
+      // Js / any_rot initialised before warp 0 updates them (first inner barrier)
       if (!CYC) {
 #pragma unroll
         for (int ir = 0; ir < JW - 1; ++ir)
-          jac_inner<RG, JC, 0, JR_T>(ir, x, red, rot_cs, rot_sn, Js, &any_rot, tol);
+          jac_inner<RG, JC, 0, JR_T>(ir, x, red, Js, &any_rot, tol);
       } else if (round == 0) {
 #pragma unroll
         for (int ir = 0; ir < JC - 1; ++ir)
-          jac_inner<RG, JC, 1, JR_T>(ir, x, red, rot_cs, rot_sn, Js, &any_rot, tol);
+          jac_inner<RG, JC, 1, JR_T>(ir, x, red, Js, &any_rot, tol);
       } else {
 #pragma unroll
         for (int ir = 0; ir < JC; ++ir)
-          jac_inner<RG, JC, 2, JR_T>(ir, x, red, rot_cs, rot_sn, Js, &any_rot, tol);
+          jac_inner<RG, JC, 2, JR_T>(ir, x, red, Js, &any_rot, tol);
       }
       __syncthreads();
       if (any_rot) {
@@ -508,7 +546,7 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
 #pragma unroll
             for (int c = 0; c < JW; ++c) {
               const int col = c < JC ? bi * JC + c : bj * JC + (c - JC);
-              G[(size_t)col * d + row] = x[k][c];
+              __stcg(G + (size_t)col * d + row, x[k][c]);
             }
           }
         }
@@ -523,23 +561,29 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
 #pragma unroll
               for (int l = 0; l < JW; ++l) acc = fma(vv[k][l], Js[l][c], acc);
               const int col = c < JC ? bi * JC + c : bj * JC + (c - JC);
-              V[(size_t)col * dp + row] = acc;
+              __stcg(V + (size_t)col * dp + row, acc);
             }
           }
         }
-        if (tid == 0) atomicOr(rot + (sweep & 1), 1u);
       }
-      grid_barrier(bar, nblk);
-      if (round == 0 && blockIdx.x == 0 && tid == 0) atomicExch(rot + ((sweep + 1) & 1), 0u);
+      __syncthreads();
+      if (tid == 0) {
+        if (any_rot) atomicOr(rot + sweep, 1u);
+        __threadfence();
+        atomicExch(ver + bi, g + 1);
+        atomicExch(ver + bj, g + 1);
+      }
     }
-    const unsigned any = *((volatile unsigned*)(rot + (sweep & 1)));
+    grid_barrier(bar, nblk);
+    const unsigned any = *((volatile unsigned*)(rot + sweep));
     if (!any) break;
   }
+  const int warp = tid >> 5, lane = tid & 31;
   if (blockIdx.x == 0 && tid == 0) ctl[4] = (unsigned)sweep;
   for (int j = blockIdx.x * NW + warp; j < dp; j += nblk * NW) {
     double a = 0.0;
     for (int i = lane; i < d; i += 32) {
-      const double g = G[(size_t)j * d + i];
+      const double g = __ldcg(G + (size_t)j * d + i);
       a = fma(g, g, a);
     }
 #pragma unroll
@@ -560,8 +604,8 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
     const double inv = sj > 0.0 ? 1.0 / sj : 0.0;
     if (lane == 0) S[cnt] = sj;
     for (int i = lane; i < d; i += 32) {
-      Ub[(size_t)i * d + cnt] = G[(size_t)j * d + i] * inv;
-      Vb[(size_t)i * d + cnt] = V[(size_t)j * dp + i];
+      Ub[(size_t)i * d + cnt] = __ldcg(G + (size_t)j * d + i) * inv;
+      Vb[(size_t)i * d + cnt] = __ldcg(V + (size_t)j * dp + i);
     }
   }
 }
@@ -591,10 +635,12 @@ static bool reg_launch(const double* B, int d, double* Ub, double* S, double* Vb
   double* G = work;
   double* V = G + (size_t)d * dpr;
   double* nrm = V + (size_t)dpr * dpr;
-  jacobi_init_kernel<<<148 * 4, 256, 0, st>>>(B, d, dpr, G, V, ctl);
+  unsigned* flags = jac_flags(work, d);
+  if (nbr + kJacFlagVer > 2048) return false;
+  jacobi_init_kernel<<<148 * 4, 256, 0, st>>>(B, d, dpr, G, V, ctl, flags);
   TSVD_CHECK_LAUNCH();
   int nblocks = nbr / 2, nbv = nbr;
-  void* args[] = {&G, &V, &d, &nbv, &nrm, &Ub, &S, &Vb, &ctl};
+  void* args[] = {&G, &V, &d, &nbv, &nrm, &Ub, &S, &Vb, &ctl, &flags};
   TSVD_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(JR_T), args, 0, st));
   TSVD_CHECK_LAUNCH();
   return true;
@@ -624,7 +670,7 @@ void small_svd(const double* B, int d, double* Ub, double* S, double* Vb, double
     if (jc == 4 && reg_launch<4>(B, d, Ub, S, Vb, work, ctl, st)) return;
     if (jc == 8 && reg_launch<8>(B, d, Ub, S, Vb, work, ctl, st)) return;
   }
-  jacobi_init_kernel<<<148 * 4, 256, 0, st>>>(B, d, dp, G, V, ctl);
+  jacobi_init_kernel<<<148 * 4, 256, 0, st>>>(B, d, dp, G, V, ctl, nullptr);
   TSVD_CHECK_LAUNCH();
   const size_t smem = sizeof(double) * ((size_t)d * JP + 2 * JW * JP);
   static int attr_for = -1;

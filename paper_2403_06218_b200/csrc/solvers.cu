@@ -143,13 +143,13 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
           if (lo == 0)
             cholqr2(c, P, n, b, ldp, R);                                 // S3a
           else
-            cgs_cqr2(c, P, n, lo, b, ldp, H, R);                         // S3b
+            cgs_cqr2(c, P, n, lo, b, ldp, H, R, false);                  // S3b (H unused, R17)
           copy_block(R, b, B + (int64_t)lo * d + lo, d, b, b, true, c.st);  // L_i = R^T
         }
         apply(c, false, P + lo, ldp, Pb + lo + b, ldb, b);               // S4: A Q_i
         m_side();
         c.flag_slot = 2 * i + 1;
-        cgs_cqr2(c, Pb, m, lo + b, b, ldb, H, Rb);                       // S5
+        cgs_cqr2(c, Pb, m, lo + b, b, ldb, H, Rb, false);                // S5 (H unused, R17)
         if (i < kc - 1)
           copy_block(Rb, b, B + (int64_t)(lo + b) * d + lo, d, b, b, false, c.st);  // Rbar_i
       }
