@@ -24,37 +24,14 @@ constexpr int kLongRow = 64;   // rows up to this length: sub-warp groups (sorte
 constexpr int kMedRow = 512;   // rows up to this length: one warp each (sorted)
 constexpr int kSeg = 2048;     // longer rows: CTA segments of this many nonzeros
 
-// L2 residency: the gathered dense operand X (n x w, ~L2-sized for C2) is
-// loaded with an evict_last policy, the streamed CSR arrays with evict-first
-// (.cs) loads and Y with streaming stores, so the single pass over A and Y
-// does not push reused X rows out of the 126 MB L2.
-__device__ __forceinline__ uint64_t l2_evict_last_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-
 template <int VEC>
-__device__ __forceinline__ void ldx_vec(const double* p, double (&x)[VEC], uint64_t pol) {
+__device__ __forceinline__ void ldx_vec(const double* p, double (&x)[VEC]) {
   if constexpr (VEC == 2) {
-    double a, b;
-    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
-                 : "=d"(a), "=d"(b) : "l"(p), "l"(pol));
-    x[0] = a;
-    x[1] = b;
+    const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    x[0] = t.x;
+    x[1] = t.y;
   } else {
-    double a;
-    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(a) : "l"(p), "l"(pol));
-    x[0] = a;
-  }
-}
-
-template <int VEC>
-__device__ __forceinline__ void sty_vec(double* p, const double (&y)[VEC]) {
-  if constexpr (VEC == 2) {
-    __stcs(reinterpret_cast<double2*>(p), make_double2(y[0], y[1]));
-  } else {
-    __stcs(p, y[0]);
+    x[0] = __ldg(p);
   }
 }
 
@@ -80,7 +57,6 @@ __device__ __forceinline__ void spmm_short_dev(
   const int64_t beg = __ldg(rowptr + row), end = __ldg(rowptr + row + 1);
   const bool active = c < w;
   const double* Xc = X + c;
-  const uint64_t pol = l2_evict_last_policy();
   double acc0[VEC], acc1[VEC];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) acc0[e] = acc1[e] = 0.0;
@@ -90,14 +66,14 @@ __device__ __forceinline__ void spmm_short_dev(
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const bool ok = k + u < end;
-      col[u] = ok ? __ldcs(colidx + k + u) : 0;
-      v[u] = ok ? __ldcs(vals + k + u) : 0.0;
+      col[u] = ok ? __ldg(colidx + k + u) : 0;
+      v[u] = ok ? __ldg(vals + k + u) : 0.0;
     }
     double x[8][VEC];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       if (active && k + u < end)
-        ldx_vec<VEC>(Xc + (int64_t)col[u] * ldx, x[u], pol);
+        ldx_vec<VEC>(Xc + (int64_t)col[u] * ldx, x[u]);
       else
 #pragma unroll
         for (int e = 0; e < VEC; ++e) x[u][e] = 0.0;
@@ -111,10 +87,11 @@ __device__ __forceinline__ void spmm_short_dev(
       }
   }
   if (active) {
-    double y[VEC];
-#pragma unroll
-    for (int e = 0; e < VEC; ++e) y[e] = acc0[e] + acc1[e];
-    sty_vec<VEC>(Y + row * ldy + c, y);
+    if constexpr (VEC == 2) {
+      *reinterpret_cast<double2*>(Y + row * ldy + c) = make_double2(acc0[0] + acc1[0], acc0[1] + acc1[1]);
+    } else {
+      Y[row * ldy + c] = acc0[0] + acc1[0];
+    }
   }
 }
 
@@ -134,7 +111,6 @@ __device__ __forceinline__ void spmm_medium_dev(
   const int g = lane / L, c = (lane % L) * VEC;
   const bool active = c < w;
   const double* Xc = X + c;
-  const uint64_t pol = l2_evict_last_policy();
   const int64_t row = __ldg(order + widx);
   const int64_t beg = __ldg(rowptr + row), end = __ldg(rowptr + row + 1);
   double acc0[VEC], acc1[VEC];
@@ -146,14 +122,14 @@ __device__ __forceinline__ void spmm_medium_dev(
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const bool ok = k + u * G < end;
-      col[u] = ok ? __ldcs(colidx + k + u * G) : 0;
-      v[u] = ok ? __ldcs(vals + k + u * G) : 0.0;
+      col[u] = ok ? __ldg(colidx + k + u * G) : 0;
+      v[u] = ok ? __ldg(vals + k + u * G) : 0.0;
     }
     double x[8][VEC];
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       if (active && k + u * G < end)
-        ldx_vec<VEC>(Xc + (int64_t)col[u] * ldx, x[u], pol);
+        ldx_vec<VEC>(Xc + (int64_t)col[u] * ldx, x[u]);
       else
 #pragma unroll
         for (int e = 0; e < VEC; ++e) x[u][e] = 0.0;
@@ -173,7 +149,13 @@ __device__ __forceinline__ void spmm_medium_dev(
 #pragma unroll
     for (int o = L; o < 32; o <<= 1) r[e] += __shfl_xor_sync(0xffffffffu, r[e], o);
   }
-  if (g == 0 && active) sty_vec<VEC>(Y + row * ldy + c, r);
+  if (g == 0 && active) {
+    if constexpr (VEC == 2) {
+      *reinterpret_cast<double2*>(Y + row * ldy + c) = make_double2(r[0], r[1]);
+    } else {
+      Y[row * ldy + c] = r[0];
+    }
+  }
 }
 
 // Long rows: one CTA per segment of <= kSeg nonzeros; 256/L groups strided
@@ -194,7 +176,6 @@ __device__ __forceinline__ void spmm_long_dev(
   const int64_t beg = seg_beg[s], end = seg_end[s];
   const bool active = c < w;
   const double* Xc = X + c;
-  const uint64_t pol = l2_evict_last_policy();
   double acc0[VEC], acc1[VEC];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) acc0[e] = acc1[e] = 0.0;
@@ -204,14 +185,14 @@ __device__ __forceinline__ void spmm_long_dev(
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const bool ok = k + u * G < end;
-      col[u] = ok ? __ldcs(colidx + k + u * G) : 0;
-      v[u] = ok ? __ldcs(vals + k + u * G) : 0.0;
+      col[u] = ok ? __ldg(colidx + k + u * G) : 0;
+      v[u] = ok ? __ldg(vals + k + u * G) : 0.0;
     }
     double x[4][VEC];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       if (active && k + u * G < end)
-        ldx_vec<VEC>(Xc + (int64_t)col[u] * ldx, x[u], pol);
+        ldx_vec<VEC>(Xc + (int64_t)col[u] * ldx, x[u]);
       else
 #pragma unroll
         for (int e = 0; e < VEC; ++e) x[u][e] = 0.0;
