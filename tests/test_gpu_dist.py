@@ -30,12 +30,15 @@ def _solve(h, algo):
     h.set_seed(5)
     if algo == "lanczos":
         st = h.block_lanczos(r=10, b=4, tol=1e-10, maxit=6, d=40)
+    elif algo == "thick":
+        h.set_thick_restart(16)
+        st = h.block_lanczos(r=10, b=4, tol=1e-10, maxit=6, d=28)
     else:
         st = h.rsvd(r=10, p=6, q=2)
     return st, h.get()
 
 
-@pytest.mark.parametrize("algo", ["lanczos", "rsvd"])
+@pytest.mark.parametrize("algo", ["lanczos", "rsvd", "thick"])
 @pytest.mark.parametrize("kind", ["dense", "csr"])
 def test_dist_world1_equals_single(kind, algo):
     if kind == "dense":
