@@ -132,6 +132,14 @@ tsvd_status tsvd_set_krylov_dim(tsvd_t h, int d);
  * at solve time: l % b == 0 and r <= l < d, else TSVD_ESHAPE.  keep < 0 =>
  * TSVD_EINVAL. */
 tsvd_status tsvd_set_thick_restart(tsvd_t h, int keep);
+/* Device memory: every library allocation (A, CSR(A^T), bases, workspaces)
+ * is stream-ordered (cudaMallocAsync on the handle's stream) from the current
+ * device's default memory pool; at first use the pool's release threshold is
+ * raised so blocks freed by tsvd_destroy stay reserved for the next handle
+ * (no cudaMalloc per solve).  tsvd_trim_memory synchronises the device and
+ * returns reserved-but-unused pool memory above keep_bytes to the system.
+ * Returns TSVD_ECUDA without a usable device. */
+tsvd_status tsvd_trim_memory(size_t keep_bytes);
 /* Panel width of CGS-QR (Alg. 3) inside RandSVD; default 16. */
 tsvd_status tsvd_set_qr_block(tsvd_t h, int b_qr);
 /* Optional exact start block instead of the Philox one: for LancSVD the

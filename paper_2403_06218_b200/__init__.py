@@ -18,7 +18,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtsvd.so")
+# TSVD_LIB: an alternative build of the same library (development A/B runs)
+LIB_PATH = os.environ.get("TSVD_LIB") or os.path.join(_HERE, "libtsvd.so")
 
 TSVD_OK, TSVD_WARN_NOTCONV, TSVD_WARN_FALLBACK = 0, 1, 2
 TSVD_EINVAL, TSVD_ESHAPE, TSVD_ENOMEM, TSVD_ECUDA, TSVD_ENCCL, TSVD_ESTATE = -1, -2, -3, -4, -5, -6
@@ -28,7 +29,7 @@ TSVD_ROW_MAJOR, TSVD_COL_MAJOR = 0, 1
 # every symbol include/tsvd.h declares (tests check the .so exports them)
 EXPORTS = [
     "tsvd_create_csr", "tsvd_create_dense", "tsvd_set_stream", "tsvd_set_seed",
-    "tsvd_set_krylov_dim", "tsvd_set_thick_restart", "tsvd_set_qr_block", "tsvd_set_start", "tsvd_block_lanczos",
+    "tsvd_set_krylov_dim", "tsvd_set_thick_restart", "tsvd_trim_memory", "tsvd_set_qr_block", "tsvd_set_start", "tsvd_block_lanczos",
     "tsvd_rsvd", "tsvd_get", "tsvd_get_info", "tsvd_get_rho", "tsvd_destroy",
     "tsvd_strerror", "tsvd_last_error", "tsvd_dbg_philox", "tsvd_dbg_philox_words",
     "tsvd_dbg_apply", "tsvd_dbg_cholqr2", "tsvd_dbg_cgs_cqr2", "tsvd_dbg_cgs_qr",
@@ -78,6 +79,7 @@ _SIGS = {
     "tsvd_set_seed": [vp, u64],
     "tsvd_set_krylov_dim": [vp, i32],
     "tsvd_set_thick_restart": [vp, i32],
+    "tsvd_trim_memory": [C.c_size_t],
     "tsvd_set_qr_block": [vp, i32],
     "tsvd_set_start": [vp, vp, i64, i64, i64, i32],
     "tsvd_block_lanczos": [vp, i32, i32, dbl, i32],
@@ -360,6 +362,11 @@ class TruncatedSVD:
 
     def __exit__(self, *a):
         self.close()
+
+
+def trim_memory(keep_bytes: int = 0):
+    """Return the library's reserved-but-unused device pool memory (tsvd_trim_memory)."""
+    _check(lib().tsvd_trim_memory(int(keep_bytes)), "tsvd_trim_memory")
 
 
 def nccl_unique_id() -> bytes:

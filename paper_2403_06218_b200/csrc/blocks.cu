@@ -19,23 +19,45 @@
 
 namespace tsvd {
 
+static void pool_init() {
+  static bool done = false;
+  if (done) return;
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done = true;
+}
+
+void* dmalloc(size_t bytes, cudaStream_t st) {
+  pool_init();
+  void* p = nullptr;
+  TSVD_CUDA(cudaMallocAsync(&p, bytes ? bytes : 8, st));
+  return p;
+}
+
+void dfree(void* p, cudaStream_t st) {
+  if (p) cudaFreeAsync(p, st);
+}
+
 void* buf(Ctx& c, const std::string& name, size_t bytes) {
   if (bytes == 0) bytes = 8;
   auto it = c.bufs.find(name);
   if (it != c.bufs.end() && it->second.second >= bytes) return it->second.first;
   if (it != c.bufs.end()) {
-    TSVD_CUDA(cudaStreamSynchronize(c.st));
-    cudaFree(it->second.first);
+    dfree(it->second.first, c.st);  // stream-ordered: pending work on c.st finishes first
     c.bufs.erase(it);
   }
-  void* p = nullptr;
-  TSVD_CUDA(cudaMalloc(&p, bytes));
+  void* p = dmalloc(bytes, c.st);
   c.bufs[name] = {p, bytes};
   return p;
 }
 
 void free_bufs(Ctx& c) {
-  for (auto& kv : c.bufs) cudaFree(kv.second.first);
+  for (auto& kv : c.bufs) dfree(kv.second.first, c.st);
   c.bufs.clear();
 }
 

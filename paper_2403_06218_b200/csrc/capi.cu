@@ -42,9 +42,9 @@ static tsvd_status init_ctx(tsvd_ctx* c) {
 static void destroy_ctx(tsvd_ctx* c) {
   if (!c) return;
   if (c->st) cudaStreamSynchronize(c->st);
-  csr_free(c->A);
-  csr_free(c->AT);
-  cudaFree(c->Ad);
+  csr_free(c->A, c->st);
+  csr_free(c->AT, c->st);
+  dfree(c->Ad, c->st);
   free_bufs(*c);
   prof_release(*c);
   comm_destroy(*c);
@@ -89,28 +89,21 @@ static tsvd_status setup_csr(tsvd_ctx* c, int64_t nnz, const int64_t* rowptr,
     TSVD_CUDA(cudaMemcpy(hrp.data(), rowptr, (m + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
   } else {
     std::memcpy(hrp.data(), rowptr, (m + 1) * sizeof(int64_t));
-    // host-side validation (cheap, exact)
+    // row pointer checked here (O(m)); the column indices on the device below
     if (hrp[0] != 0 || hrp[m] != nnz) return TSVD_EINVAL;
-    for (int64_t i = 0; i < m; ++i) {
+    for (int64_t i = 0; i < m; ++i)
       if (hrp[i + 1] < hrp[i]) return TSVD_EINVAL;
-      int64_t prev = -1;
-      for (int64_t k = hrp[i]; k < hrp[i + 1]; ++k) {
-        const int64_t cj = colidx[k];
-        if (cj <= prev || cj >= n) return TSVD_EINVAL;
-        prev = cj;
-      }
-    }
   }
-  TSVD_CUDA(cudaMalloc(&A.rowptr, (m + 1) * sizeof(int64_t)));
-  TSVD_CUDA(cudaMalloc(&A.colidx, std::max<int64_t>(1, nnz) * sizeof(int32_t)));
-  TSVD_CUDA(cudaMalloc(&A.vals, std::max<int64_t>(1, nnz) * sizeof(double)));
+  dmalloc_t(&A.rowptr, m + 1, c->st);
+  dmalloc_t(&A.colidx, std::max<int64_t>(1, nnz), c->st);
+  dmalloc_t(&A.vals, std::max<int64_t>(1, nnz), c->st);
   TSVD_CUDA(cudaMemcpyAsync(A.rowptr, rowptr, (m + 1) * sizeof(int64_t), kind, c->st));
   if (nnz > 0) {
     TSVD_CUDA(cudaMemcpyAsync(A.colidx, colidx, nnz * sizeof(int32_t), kind, c->st));
     TSVD_CUDA(cudaMemcpyAsync(A.vals, vals, nnz * sizeof(double), kind, c->st));
   }
   TSVD_CUDA(cudaStreamSynchronize(c->st));
-  if (mem_kind == TSVD_DEVICE && csr_validate_device(A, c->st) != 0) return TSVD_EINVAL;
+  if (csr_validate_device(A, c->st) != 0) return TSVD_EINVAL;  // warp per row, exact
   csr_transpose(A, c->AT, c->st);
   csr_build_plan(A, hrp.data(), c->st);
   std::vector<int64_t> hrpt(n + 1);
@@ -125,7 +118,7 @@ static tsvd_status setup_dense(tsvd_ctx* c, const double* Ain, int64_t lda, int 
   const int64_t m = c->m, n = c->ng;
   c->dense = true;
   c->lda = n;
-  TSVD_CUDA(cudaMalloc(&c->Ad, (size_t)std::max<int64_t>(1, m) * n * sizeof(double)));
+  dmalloc_t(&c->Ad, (size_t)std::max<int64_t>(1, m) * n, c->st);
   const cudaMemcpyKind kind = mem_kind == TSVD_DEVICE ? cudaMemcpyDeviceToDevice
                                                       : cudaMemcpyHostToDevice;
   if (layout == TSVD_ROW_MAJOR) {
@@ -135,12 +128,12 @@ static tsvd_status setup_dense(tsvd_ctx* c, const double* Ain, int64_t lda, int 
   } else {
     // column-major input: upload as an n x m row-major block, transpose on device
     double* tmp;
-    TSVD_CUDA(cudaMalloc(&tmp, (size_t)m * n * sizeof(double)));
+    dmalloc_t(&tmp, (size_t)m * n, c->st);
     TSVD_CUDA(cudaMemcpy2DAsync(tmp, m * sizeof(double), Ain, lda * sizeof(double),
                                 m * sizeof(double), n, kind, c->st));
     copy_block(tmp, m, c->Ad, n, m, (int)n, true, c->st);
     TSVD_CUDA(cudaStreamSynchronize(c->st));
-    cudaFree(tmp);
+    dfree(tmp, c->st);
   }
   TSVD_CUDA(cudaStreamSynchronize(c->st));
   return TSVD_OK;
@@ -318,6 +311,20 @@ tsvd_status tsvd_set_seed(tsvd_t h, uint64_t seed) {
 tsvd_status tsvd_set_krylov_dim(tsvd_t h, int d) {
   if (!h || d < 0) return TSVD_EINVAL;
   h->krylov_d = d;
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_trim_memory(size_t keep_bytes) {
+  int dev = 0;
+  cudaMemPool_t pool;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return TSVD_ECUDA;
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess || cudaMemPoolTrimTo(pool, keep_bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return TSVD_ECUDA;
+  }
   return TSVD_OK;
 }
 

@@ -86,9 +86,18 @@ void launch_spmm_wide(const Csr& A, const double* X, int64_t ldx, double* Y, int
 
 // CSR transpose on the device (stable: rows of A^T list original rows in
 // increasing order).  Allocates T's arrays.
+// Device memory of the library: stream-ordered allocations from the
+// device's default memory pool, whose release threshold is raised at first
+// use so blocks freed by one handle are reused by the next (no cudaMalloc /
+// OS round trip per handle); tsvd_trim_memory() returns them.
+void* dmalloc(size_t bytes, cudaStream_t st);
+void dfree(void* p, cudaStream_t st);
+template <class T> inline void dmalloc_t(T** p, size_t count, cudaStream_t st) {
+  *p = (T*)dmalloc(count * sizeof(T), st);
+}
 void csr_transpose(const Csr& A, Csr& T, cudaStream_t st);
 void csr_build_plan(Csr& A, const int64_t* host_rowptr, cudaStream_t st);
-void csr_free(Csr& A);
+void csr_free(Csr& A, cudaStream_t st);
 // device validation of a CSR: returns 0 if canonical
 int csr_validate_device(const Csr& A, cudaStream_t st);
 

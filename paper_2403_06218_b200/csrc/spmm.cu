@@ -363,12 +363,12 @@ void csr_build_plan(Csr& A, const int64_t* hrp, cudaStream_t st) {
   A.nmed = (int64_t)morder.size();
   auto up64 = [&](std::vector<int64_t>& v, int64_t** d) {
     if (v.empty()) return;
-    TSVD_CUDA(cudaMalloc(d, v.size() * sizeof(int64_t)));
+    dmalloc_t(d, v.size(), st);
     TSVD_CUDA(cudaMemcpyAsync(*d, v.data(), v.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   };
   auto up32 = [&](std::vector<int32_t>& v, int32_t** d) {
     if (v.empty()) return;
-    TSVD_CUDA(cudaMalloc(d, v.size() * sizeof(int32_t)));
+    dmalloc_t(d, v.size(), st);
     TSVD_CUDA(cudaMemcpyAsync(*d, v.data(), v.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   };
   up64(srow, &A.seg_row);
@@ -383,19 +383,19 @@ void csr_build_plan(Csr& A, const int64_t* hrp, cudaStream_t st) {
   TSVD_CUDA(cudaStreamSynchronize(st));
 }
 
-void csr_free(Csr& A) {
-  cudaFree(A.rowptr);
-  cudaFree(A.colidx);
-  cudaFree(A.vals);
-  cudaFree(A.seg_row);
-  cudaFree(A.seg_beg);
-  cudaFree(A.seg_end);
-  cudaFree(A.seg_slot);
-  cudaFree(A.split_row);
-  cudaFree(A.split_first);
-  cudaFree(A.split_count);
-  cudaFree(A.short_rows);
-  cudaFree(A.med_rows);
+void csr_free(Csr& A, cudaStream_t st) {
+  dfree(A.rowptr, st);
+  dfree(A.colidx, st);
+  dfree(A.vals, st);
+  dfree(A.seg_row, st);
+  dfree(A.seg_beg, st);
+  dfree(A.seg_end, st);
+  dfree(A.seg_slot, st);
+  dfree(A.split_row, st);
+  dfree(A.split_first, st);
+  dfree(A.split_count, st);
+  dfree(A.short_rows, st);
+  dfree(A.med_rows, st);
   A = Csr{};
 }
 
@@ -449,19 +449,19 @@ void csr_transpose(const Csr& A, Csr& T, cudaStream_t st) {
   T.nnz = A.nnz;
   if (A.nnz >= (int64_t)INT32_MAX) throw Error{TSVD_EINVAL, "nnz >= 2^31 per shard"};
   const int nnz = (int)A.nnz;
-  TSVD_CUDA(cudaMalloc(&T.rowptr, (T.rows + 1) * sizeof(int64_t)));
-  TSVD_CUDA(cudaMalloc(&T.colidx, std::max<int64_t>(1, T.nnz) * sizeof(int32_t)));
-  TSVD_CUDA(cudaMalloc(&T.vals, std::max<int64_t>(1, T.nnz) * sizeof(double)));
+  dmalloc_t(&T.rowptr, T.rows + 1, st);
+  dmalloc_t(&T.colidx, std::max<int64_t>(1, T.nnz), st);
+  dmalloc_t(&T.vals, std::max<int64_t>(1, T.nnz), st);
   if (nnz == 0) {
     TSVD_CUDA(cudaMemsetAsync(T.rowptr, 0, (T.rows + 1) * sizeof(int64_t), st));
     TSVD_CUDA(cudaStreamSynchronize(st));
     return;
   }
   int32_t *row_of, *perm_in, *perm_out, *keys_out;
-  TSVD_CUDA(cudaMalloc(&row_of, nnz * sizeof(int32_t)));
-  TSVD_CUDA(cudaMalloc(&perm_in, nnz * sizeof(int32_t)));
-  TSVD_CUDA(cudaMalloc(&perm_out, nnz * sizeof(int32_t)));
-  TSVD_CUDA(cudaMalloc(&keys_out, nnz * sizeof(int32_t)));
+  dmalloc_t(&row_of, nnz, st);
+  dmalloc_t(&perm_in, nnz, st);
+  dmalloc_t(&perm_out, nnz, st);
+  dmalloc_t(&keys_out, nnz, st);
   const unsigned grid = 148 * 8;
   row_of_nz_kernel<<<grid, 256, 0, st>>>(A.rowptr, A.rows, A.nnz, row_of);
   iota_kernel<<<grid, 256, 0, st>>>(perm_in, A.nnz);
@@ -472,18 +472,18 @@ void csr_transpose(const Csr& A, Csr& T, cudaStream_t st) {
   TSVD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, A.colidx, keys_out, perm_in,
                                             perm_out, nnz, 0, end_bit, st));
   void* tmp;
-  TSVD_CUDA(cudaMalloc(&tmp, tmp_bytes));
+  tmp = dmalloc(tmp_bytes, st);
   TSVD_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, A.colidx, keys_out, perm_in,
                                             perm_out, nnz, 0, end_bit, st));
   gather_t_kernel<<<grid, 256, 0, st>>>(perm_out, row_of, A.vals, T.colidx, T.vals, A.nnz);
   t_rowptr_kernel<<<grid, 256, 0, st>>>(keys_out, A.nnz, T.rows, T.rowptr);
   TSVD_CHECK_LAUNCH();
   TSVD_CUDA(cudaStreamSynchronize(st));
-  cudaFree(tmp);
-  cudaFree(row_of);
-  cudaFree(perm_in);
-  cudaFree(perm_out);
-  cudaFree(keys_out);
+  dfree(tmp, st);
+  dfree(row_of, st);
+  dfree(perm_in, st);
+  dfree(perm_out, st);
+  dfree(keys_out, st);
 }
 
 // one warp per row: bounds, monotone row pointer, strictly increasing
@@ -513,14 +513,14 @@ __global__ void csr_validate_kernel(const int64_t* __restrict__ rowptr,
 
 int csr_validate_device(const Csr& A, cudaStream_t st) {
   int* d;
-  TSVD_CUDA(cudaMalloc(&d, sizeof(int)));
+  dmalloc_t(&d, 1, st);
   TSVD_CUDA(cudaMemsetAsync(d, 0, sizeof(int), st));
   csr_validate_kernel<<<148 * 4, 256, 0, st>>>(A.rowptr, A.colidx, A.rows, A.cols, A.nnz, d);
   TSVD_CHECK_LAUNCH();
   int h = 0;
   TSVD_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st));
   TSVD_CUDA(cudaStreamSynchronize(st));
-  cudaFree(d);
+  dfree(d, st);
   return h;
 }
 

@@ -782,6 +782,9 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
 // by T held in B-fragment registers, stores Z from the accumulator fragments
 // and accumulates the tile's Gram by DMMA through an 8-row warp-private
 // shared tile.  Per-CTA Gram partials are summed over warps in warp order.
+#ifndef ROWT_PF
+#define ROWT_PF 4
+#endif
 template <int WP>
 __global__ void __launch_bounds__(256) rowT_kernel(const double* Y, int64_t ldy,
                                                    const double* __restrict__ T, double* Z,
@@ -806,7 +809,7 @@ __global__ void __launch_bounds__(256) rowT_kernel(const double* Y, int64_t ldy,
   const int64_t ntiles = (q + 7) / 8;
   const int64_t gw = (int64_t)blockIdx.x * 8 + warp, nw = (int64_t)gridDim.x * 8;
   // PF tiles of Y in flight per warp (register ring)
-  constexpr int PF = 4;
+  constexpr int PF = ROWT_PF;
   double yr[PF][KY];
   auto load = [&](double (&dst)[KY], int64_t t) {
     const int64_t row = t * 8 + gid;
