@@ -785,14 +785,16 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
 #ifndef ROWT_PF
 #define ROWT_PF 4
 #endif
+bool g_rowt32 = getenv("TSVD_ROWT32") ? atoi(getenv("TSVD_ROWT32")) != 0 : true;
 template <int WP>
 __global__ void __launch_bounds__(256) rowT_kernel(const double* Y, int64_t ldy,
                                                    const double* __restrict__ T, double* Z,
                                                    int64_t ldz, int64_t q, int w, double beta,
                                                    double* __restrict__ gram) {
   constexpr int NT = WP / 8, KY = WP / 4, NPAIR = NT * NT, ZP = WP + 4;
+  constexpr int GCH = NPAIR < 4 ? NPAIR : 4;  // Gram tiles reduced per chunk (static smem)
   __shared__ double zs[8][8 * ZP];
-  __shared__ double gred[8][NPAIR * 64];
+  __shared__ double gred[8][GCH * 64];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   double tb[KY][NT];
@@ -876,17 +878,21 @@ __global__ void __launch_bounds__(256) rowT_kernel(const double* Y, int64_t ldy,
   (void)it;
   if (gram) {
 #pragma unroll
-    for (int p = 0; p < NPAIR; ++p)
+    for (int p0 = 0; p0 < NPAIR; p0 += GCH) {
+      if (p0 > 0) __syncthreads();
 #pragma unroll
-      for (int e = 0; e < 2; ++e) gred[warp][p * 64 + gid * 8 + 2 * tig + e] = g[p][e];
-    __syncthreads();
-    for (int idx = tid; idx < NPAIR * 64; idx += 256) {
-      double sum = 0.0;
+      for (int p = 0; p < GCH; ++p)
 #pragma unroll
-      for (int k = 0; k < 8; ++k) sum += gred[k][idx];
-      const int p = idx / 64, ii = (idx % 64) / 8, jj = idx % 8;
-      const int i = (p / NT) * 8 + ii, j = (p % NT) * 8 + jj;
-      if (i < w && j < w) gram[(int64_t)blockIdx.x * w * w + i * w + j] = sum;
+        for (int e = 0; e < 2; ++e) gred[warp][p * 64 + gid * 8 + 2 * tig + e] = g[p0 + p][e];
+      __syncthreads();
+      for (int idx = tid; idx < GCH * 64; idx += 256) {
+        double sum = 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) sum += gred[k][idx];
+        const int p = p0 + idx / 64, ii = (idx % 64) / 8, jj = idx % 8;
+        const int i = (p / NT) * 8 + ii, j = (p % NT) * 8 + jj;
+        if (i < w && j < w) gram[(int64_t)blockIdx.x * w * w + i * w + j] = sum;
+      }
     }
   }
 }
@@ -1428,12 +1434,13 @@ void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const d
       return;
     }
   }
-  if (s == 0 && w <= 16) {  // streaming row pass (WP = 32 keeps the tiled path: smem)
-    const int ctas = nn_ctas(q, w);
+  if (s == 0 && w <= 32 && g_rowt32 | (w <= 16)) {  // streaming row pass
     if (w <= 8)
-      rowT_kernel<8><<<ctas, 256, 0, st>>>(Y, ldy, T, Z, ldz, q, w, beta, gram);
-    else
-      rowT_kernel<16><<<ctas, 256, 0, st>>>(Y, ldy, T, Z, ldz, q, w, beta, gram);
+      rowT_kernel<8><<<nn_ctas(q, w), 256, 0, st>>>(Y, ldy, T, Z, ldz, q, w, beta, gram);
+    else if (w <= 16)
+      rowT_kernel<16><<<nn_ctas(q, w), 256, 0, st>>>(Y, ldy, T, Z, ldz, q, w, beta, gram);
+    else  // nn_ctas(q, w) CTAs: the callers finalise that many Gram partials
+      rowT_kernel<32><<<nn_ctas(q, w), 256, 0, st>>>(Y, ldy, T, Z, ldz, q, w, beta, gram);
     TSVD_CHECK_LAUNCH();
     return;
   }

@@ -81,7 +81,8 @@ def test_gemm_tn(q, s, w):
                                               (4097, 130, 32, -1.0, 1.0), (1000, 0, 16, 0.0, 1.0),
                                               (3000, 50, 40, 1.0, 0.0), (65, 700, 8, 2.0, 0.5),
                                               (50000, 320, 32, -1.0, 1.0), (20001, 96, 24, 1.0, 0.0),
-                                              (777, 40, 18, 0.5, -2.0), (9000, 2000, 32, 1.0, 0.0)])
+                                              (777, 40, 18, 0.5, -2.0), (9000, 2000, 32, 1.0, 0.0),
+                                              (5000, 0, 32, 0.0, 1.0), (3001, 0, 24, 0.0, -0.5)])
 def test_gemm_nn(q, s, w, alpha, beta):
     rng = np.random.default_rng(q * 7 + s + w)
     X = rng.standard_normal((q, max(s, 1)))[:, :s]
