@@ -189,9 +189,10 @@ tsvd_status tsvd_get_rho(tsvd_t h, double* rho);
 /* Per-phase device-time instrumentation (CUDA events on the handle's stream
  * around each phase call).  Phases (index: name): 0 apply_A (A.X, Alg. 2
  * S4 / Alg. 1 S1), 1 apply_AT (A^T.X, S2 / S3), 2 ortho_tn (gemm_tn passes
- * of Alg. 4/5), 3 ortho_nn (gemm_nn passes of Alg. 4/5, incl. TRSM-only
- * passes), 4 ortho_small (b x b Cholesky / reductions), 5 small_svd,
- * 6 restart_out (restart product, outputs, sign), 7 other.  bytes/flops are
+ * of Alg. 4/5), 3 ortho_nn (gemm_nn passes of Alg. 4/5 against the basis),
+ * 4 ortho_small (b x b Cholesky / reductions), 5 small_svd, 6 restart_out
+ * (restart product, outputs, sign), 7 other, 8 ortho_rowT (the basis-free
+ * passes: Gram of Y and the TRSM-as-multiply S L^{-T}).  bytes/flops are
  * ALGORITHMIC (compulsory) counts per DESIGN.md "Roofline", not measured
  * traffic.  Aggregates accumulate over solves until reset. */
 typedef struct {
@@ -202,7 +203,7 @@ typedef struct {
   double bytes;       /* summed algorithmic bytes */
   double flops;       /* summed algorithmic flops */
 } tsvd_prof_entry;
-enum { TSVD_NPROF = 8 };
+enum { TSVD_NPROF = 9 };
 tsvd_status tsvd_set_profiling(tsvd_t h, int on);
 tsvd_status tsvd_get_profile(tsvd_t h, tsvd_prof_entry* out /* TSVD_NPROF */);
 tsvd_status tsvd_reset_profile(tsvd_t h);

@@ -58,7 +58,7 @@ class TsvdProfEntry(C.Structure):
                 ("ms", C.c_double), ("bytes", C.c_double), ("flops", C.c_double)]
 
 
-NPROF = 8
+NPROF = 9
 
 
 class TsvdError(RuntimeError):

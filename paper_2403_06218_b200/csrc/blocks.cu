@@ -61,8 +61,9 @@ void free_bufs(Ctx& c) {
   c.bufs.clear();
 }
 
-static const char* kProfNames[TSVD_NPROF] = {"apply_A", "apply_AT", "ortho_tn", "ortho_nn",
-                                             "ortho_small", "small_svd", "restart_out", "other"};
+static const char* kProfNames[TSVD_NPROF] = {"apply_A",     "apply_AT",  "ortho_tn",
+                                             "ortho_nn",    "ortho_small", "small_svd",
+                                             "restart_out", "other",     "ortho_rowT"};
 
 static cudaEvent_t pool_get(Ctx& c) {
   if (!c.ev_pool.empty()) {
@@ -180,7 +181,7 @@ int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
   const int np = nn_ctas(q, w);
   clear_flags(c);
   {  // S1: W = Y^T Y
-    Prof p(c, P_NN, nn_bytes(q, 0, w, true, false), 2.0 * q * w * w);
+    Prof p(c, P_ROWT, nn_bytes(q, 0, w, true, false), 2.0 * q * w * w);
     gemm_nn(nullptr, 0, nullptr, 0, Y, ld, nullptr, nullptr, 0, q, 0, w, 0.0, 1.0, gram, c.st);
   }
   {
@@ -190,7 +191,7 @@ int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
     chol_finalize(W, k, w, L1, T1, ortho_flags(c) + 0, c.st);                    // S2
   }
   {  // S3 + S4: S = Y L^{-T}, Wbar = S^T S
-    Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 3.0 * q * w * w);
+    Prof p(c, P_ROWT, nn_bytes(q, 0, w, true, true), 3.0 * q * w * w);
     gemm_nn(nullptr, 0, nullptr, 0, Y, ld, T1, S, w, q, 0, w, 0.0, 1.0, gram, c.st);
   }
   {
@@ -205,7 +206,7 @@ int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
     return 1;
   }
   {  // S6: Q = S Lbar^{-T}
-    Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 1.0 * q * w * w);
+    Prof p(c, P_ROWT, nn_bytes(q, 0, w, true, true), 1.0 * q * w * w);
     gemm_nn(nullptr, 0, nullptr, 0, S, w, T2, Y, ld, q, 0, w, 0.0, 1.0, nullptr, c.st);
   }
   return 0;
@@ -244,7 +245,7 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
     chol_finalize(W, k, w, L1, T1, ortho_flags(c) + 0, c.st);                         // S4
   }
   {
-    Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 1.0 * q * w * w);
+    Prof p(c, P_ROWT, nn_bytes(q, 0, w, true, true), 1.0 * q * w * w);
     gemm_nn(nullptr, 0, nullptr, 0, S, w, T1, S, w, q, 0, w, 0.0, 1.0, nullptr, c.st);  // S5
   }
   {
@@ -269,7 +270,7 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
     return 1;
   }
   {
-    Prof p(c, P_NN, nn_bytes(q, 0, w, true, true), 1.0 * q * w * w);
+    Prof p(c, P_ROWT, nn_bytes(q, 0, w, true, true), 1.0 * q * w * w);
     gemm_nn(nullptr, 0, nullptr, 0, S, w, T2, Y, ld, q, 0, w, 0.0, 1.0, nullptr, c.st);  // S10
   }
   return 0;

@@ -8,7 +8,8 @@
 #include "internal.h"
 
 namespace tsvd {
-enum ProfCat { P_APPLY_A = 0, P_APPLY_AT, P_TN, P_NN, P_SMALL, P_SVD, P_RESTART, P_OTHER };
+// P_ROWT: the s = 0 passes (Gram of Y, TRSM-as-multiply S T) - rowT_kernel
+enum ProfCat { P_APPLY_A = 0, P_APPLY_AT, P_TN, P_NN, P_SMALL, P_SVD, P_RESTART, P_OTHER, P_ROWT };
 struct ProfRec {
   int cat;
   cudaEvent_t a, b;

@@ -66,7 +66,7 @@ def tn_bench():
 
 def nn_bench():
     for q, s, w in ((1_000_000, 384, 16), (1_000_000, 128, 16), (1_000_000, 0, 16),
-                    (1_000_000, 704, 32), (1_000_000, 384, 32)):
+                    (1_000_000, 704, 32), (1_000_000, 384, 32), (4_000_000, 0, 32)):
         X = torch.randn((q, max(s, 1) + w), dtype=torch.float64, device="cuda")
         H = torch.randn((max(s, 1), w), dtype=torch.float64, device="cuda")
         Z = torch.empty((q, w), dtype=torch.float64, device="cuda")
