@@ -451,6 +451,16 @@ constexpr int JR_T = 256;
 // with L1-bypassing loads).  Each round visits every block exactly once, so
 // a block's owner in round g is unique.  One grid barrier per sweep decides
 // convergence from the per-sweep "rotated" word.
+#ifdef JAC_TIMING
+// development instrumentation (A/B build only): CTA 0 accumulates clock64
+// cycles per round phase: [0] wait, [1] loads, [2] inner steps, [3] stores +
+// fence + publish, [4] rounds
+__device__ unsigned long long g_jac_t[8];
+#define JT(k) do { if (blockIdx.x == 0 && threadIdx.x == 0) { const long long t_ = clock64(); g_jac_t[k] += t_ - jt0; jt0 = t_; } } while (0)
+#else
+#define JT(k) do { } while (0)
+#endif
+
 __device__ __forceinline__ void jac_wait_ver(unsigned* ver, int b, unsigned g) {
   volatile unsigned* v = ver + b;
   while (*v < g) __nanosleep(32);
@@ -485,8 +495,12 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
   // else each round sweeps all pairs of the 2 JC columns (~2d inner rounds)
   const int nrounds = CYC ? nb : nb - 1;
   unsigned g = 0;  // global round counter
+#ifdef JAC_TIMING
+  long long jt0 = clock64();
+#endif
   for (; sweep < kMaxSweeps; ++sweep) {
     for (int round = 0; round < nrounds; ++round, ++g) {
+      JT(5);
       int bi, bj;
       if (CYC && round == 0) {
         bi = 2 * blockIdx.x;
@@ -500,6 +514,7 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
         __threadfence();
       }
       __syncthreads();
+      JT(0);
 #pragma unroll
       for (int k = 0; k < RG; ++k) {
         const int row = tid + JR_T * k;
@@ -523,6 +538,14 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
       }
       if (tid < JW * JW) Js[tid / JW][tid % JW] = (tid / JW == tid % JW) ? 1.0 : 0.0;
       if (tid == 0) any_rot = 0;
+#ifdef JAC_TIMING
+      { double sink = 0.0;
+#pragma unroll
+        for (int k = 0; k < RG; ++k) sink += x[k][0];
+        if (sink == 1.2345e300) any_rot = 2; }
+      __syncthreads();
+#endif
+      JT(1);
       // Js / any_rot initialised before warp 0 updates them (first inner barrier)
       if (!CYC) {
 #pragma unroll
@@ -538,6 +561,7 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
           jac_inner<RG, JC, 2, JR_T>(ir, x, red, Js, &any_rot, tol);
       }
       __syncthreads();
+      JT(2);
       if (any_rot) {
 #pragma unroll
         for (int k = 0; k < RG; ++k) {
@@ -573,6 +597,10 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
         atomicExch(ver + bi, g + 1);
         atomicExch(ver + bj, g + 1);
       }
+      JT(3);
+#ifdef JAC_TIMING
+      if (blockIdx.x == 0 && tid == 0) g_jac_t[4] += 1;
+#endif
     }
     grid_barrier(bar, nblk);
     const unsigned any = *((volatile unsigned*)(rot + sweep));
@@ -645,6 +673,16 @@ static bool reg_launch(const double* B, int d, double* Ub, double* S, double* Vb
   TSVD_CHECK_LAUNCH();
   return true;
 }
+
+#ifdef JAC_TIMING
+extern "C" int tsvd_dev_jacobi_timing(unsigned long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, g_jac_t, sizeof(unsigned long long) * 8);
+}
+extern "C" int tsvd_dev_jacobi_timing_reset() {
+  unsigned long long z[8] = {0};
+  return (int)cudaMemcpyToSymbol(g_jac_t, z, sizeof(z));
+}
+#endif
 
 int small_svd_sweeps(const double* work, int d) {
   const unsigned* ctl = jac_ctl(const_cast<double*>(work), d);
