@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(double* __restrict__ 
             b += __shfl_xor_sync(0xffffffffu, b, o);
             c += __shfl_xor_sync(0xffffffffu, c, o);
           }
-          if (a > 0.0 && b > 0.0 && fabs(c) > tol * sqrt(a * b)) {
+          if (a > 0.0 && b > 0.0 && c * c > (tol * tol) * (a * b)) {  // |c| > tol sqrt(ab)
             // t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = h / c, h = (b - a)/2,
             // rewritten as sign(h) c / (|h| + sqrt(h^2 + c^2)) (one division)
             const double h = 0.5 * (b - a);
@@ -358,8 +358,8 @@ __device__ __forceinline__ void jac_pair(int t, int ir, int& p, int& q) {
 // suffices (a warp reads red[ir & 1] before it can reach barrier ir + 1).
 template <int RG, int JB, int MODE, int NTHR>
 __device__ __forceinline__ void jac_inner(int ir, double (&x)[RG][2 * JB],
-                                          double (*red)[3 * JB + 1],
-                                          double (*Js)[2 * JB + 1], int* any_rot, double tol) {
+                                          double (&vv)[RG][2 * JB],
+                                          double (*red)[3 * JB + 1], int* any_rot, double tol) {
   constexpr int JW = 2 * JB, NV = 3 * JB;
   constexpr int NVP = NV <= 16 ? 16 : (NV <= 32 ? 32 : 64);
   constexpr int NW = NTHR / 32;
@@ -404,7 +404,7 @@ __device__ __forceinline__ void jac_inner(int ir, double (&x)[RG][2 * JB],
       b += rb[w2][3 * lane + 1];
       c += rb[w2][3 * lane + 2];
     }
-    if (a > 0.0 && b > 0.0 && fabs(c) > tol * sqrt(a * b)) {
+    if (a > 0.0 && b > 0.0 && c * c > (tol * tol) * (a * b)) {  // |c| > tol sqrt(ab)
       const double h = 0.5 * (b - a);
       const double t = (h >= 0.0 ? c : -c) / (fabs(h) + sqrt(fma(h, h, c * c)));
       cs = rsqrt(fma(t, t, 1.0));
@@ -422,21 +422,11 @@ __device__ __forceinline__ void jac_inner(int ir, double (&x)[RG][2 * JB],
       const double xp = x[k][p], xq = x[k][q];
       x[k][p] = ct * xp - st * xq;
       x[k][q] = st * xp + ct * xq;
-    }
-  }
-  if (warp == 0) {
-    // J <- J G_t for every rotation t: lane i owns row i of J (JW <= 32)
-    static_assert(2 * JB <= 32, "J rows: one lane each");
-#pragma unroll
-    for (int t = 0; t < JB; ++t) {
-      int p, q;
-      jac_pair<JB, MODE>(t, ir, p, q);
-      const double ct = __shfl_sync(0xffffffffu, cs, t), st = __shfl_sync(0xffffffffu, sn, t);
-      if (lane < JW) {
-        const double jp = Js[lane][p], jq = Js[lane][q];
-        Js[lane][p] = ct * jp - st * jq;
-        Js[lane][q] = st * jp + ct * jq;
-      }
+      // the same rotation on this thread's rows of V (held in registers for
+      // the round): no accumulated J, no serial J update on the step's path
+      const double vp = vv[k][p], vq = vv[k][q];
+      vv[k][p] = ct * vp - st * vq;
+      vv[k][q] = st * vp + ct * vq;
     }
   }
 }
@@ -479,7 +469,6 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
   constexpr int NW = JR_T / 32;
   constexpr int NV = 3 * JC;  // partial sums per inner round
   __shared__ double red[2 * NW][NV + 1];
-  __shared__ double Js[JW][JW + 1];
   __shared__ int any_rot;
   unsigned* bar = ctl;
   unsigned* rot = flags;                 // [sweep]
@@ -536,7 +525,6 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
           vv[k][c] = row < dp ? __ldcg(V + (size_t)col * dp + row) : 0.0;
         }
       }
-      if (tid < JW * JW) Js[tid / JW][tid % JW] = (tid / JW == tid % JW) ? 1.0 : 0.0;
       if (tid == 0) any_rot = 0;
 #ifdef JAC_TIMING
       { double sink = 0.0;
@@ -546,19 +534,19 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
       __syncthreads();
 #endif
       JT(1);
-      // Js / any_rot initialised before warp 0 updates them (first inner barrier)
+      // any_rot initialised before warp 0 may set it (first inner barrier)
       if (!CYC) {
 #pragma unroll
         for (int ir = 0; ir < JW - 1; ++ir)
-          jac_inner<RG, JC, 0, JR_T>(ir, x, red, Js, &any_rot, tol);
+          jac_inner<RG, JC, 0, JR_T>(ir, x, vv, red, &any_rot, tol);
       } else if (round == 0) {
 #pragma unroll
         for (int ir = 0; ir < JC - 1; ++ir)
-          jac_inner<RG, JC, 1, JR_T>(ir, x, red, Js, &any_rot, tol);
+          jac_inner<RG, JC, 1, JR_T>(ir, x, vv, red, &any_rot, tol);
       } else {
 #pragma unroll
         for (int ir = 0; ir < JC; ++ir)
-          jac_inner<RG, JC, 2, JR_T>(ir, x, red, Js, &any_rot, tol);
+          jac_inner<RG, JC, 2, JR_T>(ir, x, vv, red, &any_rot, tol);
       }
       __syncthreads();
       JT(2);
@@ -574,18 +562,15 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
             }
           }
         }
-        // V pair <- V pair J (rows loaded at the start of the round)
+        // V pair rows, rotated in registers alongside G
 #pragma unroll
         for (int k = 0; k < RG; ++k) {
           const int row = tid + JR_T * k;
           if (row < dp) {
 #pragma unroll
             for (int c = 0; c < JW; ++c) {
-              double acc = 0.0;
-#pragma unroll
-              for (int l = 0; l < JW; ++l) acc = fma(vv[k][l], Js[l][c], acc);
               const int col = c < JC ? bi * JC + c : bj * JC + (c - JC);
-              __stcg(V + (size_t)col * dp + row, acc);
+              __stcg(V + (size_t)col * dp + row, vv[k][c]);
             }
           }
         }
