@@ -431,7 +431,6 @@ __device__ __forceinline__ void jac_inner(int ir, double (&x)[RG][2 * JB],
   }
 }
 
-constexpr int JR_T = 256;
 
 // Rounds hand blocks from CTA to CTA by dataflow instead of a grid barrier:
 // every block b carries a version counter (the number of rounds it has been
@@ -456,7 +455,7 @@ __device__ __forceinline__ void jac_wait_ver(unsigned* ver, int b, unsigned g) {
   while (*v < g) __nanosleep(32);
 }
 
-template <int RG, int JC, bool CYC>
+template <int RG, int JC, bool CYC, int JR_T>
 __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict__ G,
                                                             double* __restrict__ V, int d, int nb,
                                                             double* __restrict__ nrm,
@@ -626,6 +625,8 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
 bool g_jacobi_cyc = getenv("TSVD_JACOBI_CYC") ? atoi(getenv("TSVD_JACOBI_CYC")) != 0 : true;
 
 int g_jacobi_jc = getenv("TSVD_JACOBI_JC") ? atoi(getenv("TSVD_JACOBI_JC")) : 4;
+// TSVD_JACOBI_NT = 64 | 128 | 256 forces the CTA size (0, default: by d)
+int g_jacobi_nt = getenv("TSVD_JACOBI_NT") ? atoi(getenv("TSVD_JACOBI_NT")) : 0;
 
 template <int JCV>
 static bool reg_launch(const double* B, int d, double* Ub, double* S, double* Vb, double* work,
@@ -635,15 +636,38 @@ static bool reg_launch(const double* B, int d, double* Ub, double* S, double* Vb
   if (nbr & 1) ++nbr;
   const int dpr = nbr * JCV;
   if (nbr / 2 > 148 || jac_layout(d, dpr) + 64 > small_svd_work(d)) return false;
-  const int RG = (d + JR_T - 1) / JR_T;
+  // threads per CTA: fewer warps make the per-step cross-warp reduction and
+  // barrier cheaper (the step is latency-bound): 64 up to d = 384, 128 up to
+  // d = 768 (RG <= 6 rows per thread), else 256 (RG <= 4)
+  const int nth = g_jacobi_nt ? g_jacobi_nt : (d <= 384 ? 64 : (d <= 768 ? 128 : 256));
+  const int RG = (d + nth - 1) / nth;
   void* fn = nullptr;
-#define REG_FN(R)                                                                      \
-  fn = g_jacobi_cyc ? (void*)jacobi_reg_kernel<R, JCV, true> : (void*)jacobi_reg_kernel<R, JCV, false>
-  if (RG <= 1) REG_FN(1);
-  else if (RG == 2) REG_FN(2);
-  else if (RG == 3) REG_FN(3);
-  else if (RG == 4) REG_FN(4);
-  else return false;
+#define REG_FN(R, NT)                                                                  \
+  fn = g_jacobi_cyc ? (void*)jacobi_reg_kernel<R, JCV, true, NT>                        \
+                    : (void*)jacobi_reg_kernel<R, JCV, false, NT>
+  if (nth == 64) {
+    if (RG <= 1) REG_FN(1, 64);
+    else if (RG == 2) REG_FN(2, 64);
+    else if (RG == 3) REG_FN(3, 64);
+    else if (RG == 4) REG_FN(4, 64);
+    else if (RG == 5) REG_FN(5, 64);
+    else if (RG == 6) REG_FN(6, 64);
+    else return false;
+  } else if (nth == 128) {
+    if (RG <= 1) REG_FN(1, 128);
+    else if (RG == 2) REG_FN(2, 128);
+    else if (RG == 3) REG_FN(3, 128);
+    else if (RG == 4) REG_FN(4, 128);
+    else if (RG == 5) REG_FN(5, 128);
+    else if (RG == 6) REG_FN(6, 128);
+    else return false;
+  } else {
+    if (RG <= 1) REG_FN(1, 256);
+    else if (RG == 2) REG_FN(2, 256);
+    else if (RG == 3) REG_FN(3, 256);
+    else if (RG == 4) REG_FN(4, 256);
+    else return false;
+  }
 #undef REG_FN
   double* G = work;
   double* V = G + (size_t)d * dpr;
@@ -654,7 +678,7 @@ static bool reg_launch(const double* B, int d, double* Ub, double* S, double* Vb
   TSVD_CHECK_LAUNCH();
   int nblocks = nbr / 2, nbv = nbr;
   void* args[] = {&G, &V, &d, &nbv, &nrm, &Ub, &S, &Vb, &ctl, &flags};
-  TSVD_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(JR_T), args, 0, st));
+  TSVD_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(nth), args, 0, st));
   TSVD_CHECK_LAUNCH();
   return true;
 }
