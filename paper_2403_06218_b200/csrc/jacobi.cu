@@ -637,9 +637,10 @@ static bool reg_launch(const double* B, int d, double* Ub, double* S, double* Vb
   const int dpr = nbr * JCV;
   if (nbr / 2 > 148 || jac_layout(d, dpr) + 64 > small_svd_work(d)) return false;
   // threads per CTA: fewer warps make the per-step cross-warp reduction and
-  // barrier cheaper (the step is latency-bound): 64 up to d = 384, 128 up to
-  // d = 768 (RG <= 6 rows per thread), else 256 (RG <= 4)
-  const int nth = g_jacobi_nt ? g_jacobi_nt : (d <= 384 ? 64 : (d <= 768 ? 128 : 256));
+  // barrier cheaper (the step is latency-bound), too few leave the rows'
+  // FMA chains exposed: 128 up to d = 768 (RG <= 6 rows per thread), else 256
+  // (measured at d = 384: 64 threads 8.4 ms, 128 6.8 ms, 256 8.1 ms)
+  const int nth = g_jacobi_nt ? g_jacobi_nt : (d <= 768 ? 128 : 256);
   const int RG = (d + nth - 1) / nth;
   void* fn = nullptr;
 #define REG_FN(R, NT)                                                                  \
