@@ -42,6 +42,8 @@ CONFIG_TEXT = {
     "C3": "synthetic sparse rectangular CSR, m=4e6, n=5e5, nnz~5e7, r=100, block Lanczos b=32",
     "C4": "synthetic dense 40000x20000 FP64 with slowly decaying spectrum, r=200, "
           "block Lanczos b=32",
+    "C5": "large synthetic sparse CSR, m=n=5e7, nnz~1e9, r=100, b=32; fixed work: one "
+          "restart cycle at d=160 (SURVEY 8(d) C5 (i))",
 }
 
 
@@ -80,6 +82,13 @@ def make_workload(cfg_name: str, rank: int = 0):
     from tsvd_inputs import CONFIGS, SEEDS, dense_prescribed, powerlaw_csr, spectrum_eq16
     cfg = dict(CONFIGS[cfg_name])
     seed = SEEDS[cfg_name] + 1000 * rank
+    if cfg.get("device_gen"):  # C5: 1e9 nonzeros, generated in HBM (tsvd_inputs)
+        from tsvd_inputs import powerlaw_csr_device
+        t0 = time.time()
+        csr = powerlaw_csr_device(cfg["m"], cfg["n"], cfg["nnz"], cfg["alpha"], seed)
+        print(f"{cfg_name}: generated {csr[1].numel()} nonzeros in HBM in {time.time() - t0:.1f} s",
+              file=sys.stderr, flush=True)
+        return cfg, seed, dict(csr=csr, shape=(cfg["m"], cfg["n"]))
     if cfg["kind"] == "csr":
         csr = powerlaw_csr(cfg["m"], cfg["n"], cfg["nnz"], cfg["alpha"], seed)
         return cfg, seed, dict(csr=csr, shape=(cfg["m"], cfg["n"]))
@@ -113,7 +122,8 @@ def _to_device(work):
     import torch
     out = dict(work)
     if "csr" in work:
-        out["csr"] = tuple(torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in work["csr"])
+        out["csr"] = tuple(x if torch.is_tensor(x) else torch.from_numpy(np.ascontiguousarray(x)).cuda()
+                           for x in work["csr"])
     else:
         out["A"] = torch.from_numpy(work["A"]).cuda()
     return out
@@ -188,6 +198,9 @@ def oracle_sample(cfg_name: str, budget_s: float, cycles: int, seed: int, keep: 
     from threadpoolctl import threadpool_info
     import oracle
     from oracle.core import DrawCtx, cholqr2, cgs_cqr2, small_svd
+    scale = 1.0
+    if cfg_name == "C5":  # host-sized sample: C5 scaled down 10x (same alpha, mean row)
+        cfg_name, scale = "C5s", 10.0
     cfg, seed_, work = make_workload(cfg_name, 0)
     op = oracle.Operator(dense=work["A"]) if "A" in work else oracle.Operator(csr=work["csr"], shape=work["shape"])
     m, n, b = cfg["m"], cfg["n"], cfg["b"]
@@ -226,11 +239,13 @@ def oracle_sample(cfg_name: str, budget_s: float, cycles: int, seed: int, keep: 
         est = t_start + per_cycle + (cycles - 1) * later
     else:
         est = t_start + cycles * per_cycle
+    est *= scale  # every step is linear in m, n and nnz at fixed d, b
     threads = max((x.get("num_threads", 1) for x in threadpool_info()), default=1)
     sample = (f"{cfg_name} LancSVD block steps i=0..{len(times)-1} of k={k} of cycle 1 "
               f"({sum(times):.1f} s measured) + SVD({d}) ({t_svd:.2f} s); t_i fitted "
               f"linearly in i and extrapolated to {cycles} cycle(s) x {k} steps"
-              + (f" (thick restart: cycles > 1 run steps {keep // b}..{k - 1})" if keep else ""))
+              + (f" (thick restart: cycles > 1 run steps {keep // b}..{k - 1})" if keep else "")
+              + (f"; x{scale:g} for C5 (linear in m, n, nnz at fixed d, b)" if scale != 1.0 else ""))
     return dict(value=est, unit="s", cores=int(threads), kind="oracle", sample=sample,
                 measured_s=sum(times) + t_svd + t_start)
 
@@ -308,6 +323,7 @@ def main():
                     help="thick restart keeping L Ritz pairs (SURVEY 8(f) N1); 0 = the paper's "
                          "restart (Alg. 2 S7); default: the config's setting")
     ap.add_argument("--d", type=int, default=None, help="override the config's Krylov dimension")
+    ap.add_argument("--maxit", type=int, default=None, help="override the config's maxit")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -383,10 +399,28 @@ def main():
         cfg["d"] = args.d
     if args.keep is not None:
         cfg["keep"] = args.keep
+    if args.maxit is not None:
+        cfg["maxit"] = args.maxit
     keep = cfg.get("keep", 0)
     r, b, d, tol, maxit = cfg["r"], cfg["b"], cfg["d"], cfg["tol"], cfg["maxit"]
     stream = torch.cuda.current_stream()
+    t0 = time.time()
     h = T.TruncatedSVD(**dwork, dist=dist_kw) if dist_kw else T.TruncatedSVD(**dwork)
+    big = bool(cfg.get("device_gen"))
+    if big:
+        print(f"{cfg_name}: tsvd_create_csr {time.time() - t0:.1f} s", file=sys.stderr, flush=True)
+    nnz_total = int(work["csr"][1].numel() if big else len(work["csr"][1])) if "csr" in work else None
+    if big:
+        # C5: the library holds its own copies of A and CSR(A^T); free the
+        # generator's so the d = 160 bases (141 GB) fit, and let the outputs be
+        # formed in place (tsvd_set_output_mode AUTO)
+        del dwork, work, hwork
+        dwork = work = hwork = None
+        torch.cuda.empty_cache()
+        T.trim_memory(0)
+        free, total = torch.cuda.mem_get_info()
+        print(f"C5: A resident in the library, {free / 1e9:.1f} of {total / 1e9:.1f} GB free",
+              file=sys.stderr, flush=True)
     h.set_seed(seed)
     h.set_krylov_dim(d)
     h.set_thick_restart(keep)
@@ -399,8 +433,13 @@ def main():
             return hh.rsvd(r, cfg["rsvd_p"], cfg["rsvd_q"])
         return hh.block_lanczos(r, b, tol, maxit)
 
-    for _ in range(args.warmup):
+    for it in range(args.warmup):
+        t0 = time.time()
         solve(h)
+        if big:
+            torch.cuda.synchronize()
+            print(f"{cfg_name}: warm-up solve {it}: {time.time() - t0:.1f} s {h.info()}",
+                  file=sys.stderr, flush=True)
     h.set_profiling(True)
     h.reset_profile()
     vis = os.environ.get("CUDA_VISIBLE_DEVICES")
@@ -431,12 +470,16 @@ def main():
         ms = float(t.item())
     prof = h.profile()
     h.set_profiling(False)
-    U, S, V = h.get(device=True)
-    h.close()
     accuracy = None
-    if not use_dist:
-        accuracy = residual_check(dwork, U, S, V)
-    del U, S, V
+    if big:  # no room for A's user copy next to U, V (80 GB); rho is the residual (R12)
+        accuracy = {"skipped": "C5: A's user copy freed to fit the bases; see solver.rho_max "
+                               "(= explicit residual, pinned by tests/test_oracle_solvers.py::test_lancsvd_relations)"}
+    else:
+        U, S, V = h.get(device=True)
+        if not use_dist:
+            accuracy = residual_check(dwork, U, S, V)
+        del U, S, V
+    h.close()
 
     # roofline of the dominant phase: the binding roof of its algorithmic work
     # -- HBM bytes vs the measured copy bandwidth, or FP64
@@ -487,7 +530,9 @@ def main():
 
     # end-to-end through the public API with host buffers
     e2e = None
-    if args.e2e_steps > 0:
+    if big:
+        e2e = {"value": None, "unit": "s", "skipped": "C5: U, V alone are 80 GB of host copies"}
+    elif args.e2e_steps > 0:
         torch.cuda.synchronize()
         times = []
         h2d = d2h = 0
@@ -550,7 +595,7 @@ def main():
         "higher_is_better": False, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_text(cfg_name, args.algo), "algo": args.algo,
-                   "m": cfg["m"], "n": cfg["n"], "nnz": int(len(work["csr"][1])) if "csr" in work else None,
+                   "m": cfg["m"], "n": cfg["n"], "nnz": nnz_total,
                    "r": r, "b": b, "d": d, "tol": tol, "maxit": maxit,
                    "restart": (f"thick, keep {keep} (SURVEY 8(f) N1)" if keep else
                                "paper (Alg. 2 S7)"),

@@ -140,6 +140,17 @@ tsvd_status tsvd_set_thick_restart(tsvd_t h, int keep);
  * returns reserved-but-unused pool memory above keep_bytes to the system.
  * Returns TSVD_ECUDA without a usable device. */
 tsvd_status tsvd_trim_memory(size_t keep_bytes);
+/* Where the outputs U_r = Pbar_k Ubar[:, :r], V_r = P_k Vbar[:, :r] (Eq. 12;
+ * RandSVD Alg. 1 S6/S7) are formed.  TSVD_OUT_AUTO (default): in separate
+ * result buffers when (m + n) r doubles fit in the free device memory, else
+ * in place.  TSVD_OUT_SEPARATE: always separate buffers.  TSVD_OUT_INPLACE:
+ * over the first r columns of the bases themselves (row-local products,
+ * computed in row chunks through the pass scratch buffer, so no m x r buffer
+ * is allocated: what lets C5 -- m = n = 5e7, d = 160, 141 GB of bases -- run
+ * on one 180 GB GPU).  The bases are then overwritten; results are read by
+ * tsvd_get as usual.  Other values => TSVD_EINVAL. */
+enum { TSVD_OUT_AUTO = 0, TSVD_OUT_SEPARATE = 1, TSVD_OUT_INPLACE = 2 };
+tsvd_status tsvd_set_output_mode(tsvd_t h, int mode);
 /* Panel width of CGS-QR (Alg. 3) inside RandSVD; default 16. */
 tsvd_status tsvd_set_qr_block(tsvd_t h, int b_qr);
 /* Optional exact start block instead of the Philox one: for LancSVD the

@@ -25,11 +25,12 @@ TSVD_OK, TSVD_WARN_NOTCONV, TSVD_WARN_FALLBACK = 0, 1, 2
 TSVD_EINVAL, TSVD_ESHAPE, TSVD_ENOMEM, TSVD_ECUDA, TSVD_ENCCL, TSVD_ESTATE = -1, -2, -3, -4, -5, -6
 TSVD_HOST, TSVD_DEVICE = 0, 1
 TSVD_ROW_MAJOR, TSVD_COL_MAJOR = 0, 1
+TSVD_OUT_AUTO, TSVD_OUT_SEPARATE, TSVD_OUT_INPLACE = 0, 1, 2
 
 # every symbol include/tsvd.h declares (tests check the .so exports them)
 EXPORTS = [
     "tsvd_create_csr", "tsvd_create_dense", "tsvd_set_stream", "tsvd_set_seed",
-    "tsvd_set_krylov_dim", "tsvd_set_thick_restart", "tsvd_trim_memory", "tsvd_set_qr_block", "tsvd_set_start", "tsvd_block_lanczos",
+    "tsvd_set_krylov_dim", "tsvd_set_thick_restart", "tsvd_set_output_mode", "tsvd_trim_memory", "tsvd_set_qr_block", "tsvd_set_start", "tsvd_block_lanczos",
     "tsvd_rsvd", "tsvd_get", "tsvd_get_info", "tsvd_get_rho", "tsvd_destroy",
     "tsvd_strerror", "tsvd_last_error", "tsvd_dbg_philox", "tsvd_dbg_philox_words",
     "tsvd_dbg_apply", "tsvd_dbg_cholqr2", "tsvd_dbg_cgs_cqr2", "tsvd_dbg_cgs_qr",
@@ -79,6 +80,7 @@ _SIGS = {
     "tsvd_set_seed": [vp, u64],
     "tsvd_set_krylov_dim": [vp, i32],
     "tsvd_set_thick_restart": [vp, i32],
+    "tsvd_set_output_mode": [vp, i32],
     "tsvd_trim_memory": [C.c_size_t],
     "tsvd_set_qr_block": [vp, i32],
     "tsvd_set_start": [vp, vp, i64, i64, i64, i32],
@@ -266,6 +268,10 @@ class TruncatedSVD:
     def set_thick_restart(self, keep: int):
         """keep = 0: Alg. 2 S7 restart; keep = l > 0: thick restart (N1)."""
         _check(lib().tsvd_set_thick_restart(self._h, int(keep)), "tsvd_set_thick_restart")
+
+    def set_output_mode(self, mode: int):
+        """TSVD_OUT_AUTO / TSVD_OUT_SEPARATE / TSVD_OUT_INPLACE (include/tsvd.h)."""
+        _check(lib().tsvd_set_output_mode(self._h, int(mode)), "tsvd_set_output_mode")
 
     def set_qr_block(self, b_qr: int):
         _check(lib().tsvd_set_qr_block(self._h, int(b_qr)), "tsvd_set_qr_block")

@@ -35,7 +35,21 @@ static void pool_init() {
 void* dmalloc(size_t bytes, cudaStream_t st) {
   pool_init();
   void* p = nullptr;
-  TSVD_CUDA(cudaMallocAsync(&p, bytes ? bytes : 8, st));
+  cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 8, st);
+  if (e == cudaErrorMemoryAllocation) {
+    // the pool retains freed blocks (release threshold raised in pool_init);
+    // blocks of other sizes (e.g. create-time transposition temporaries) can
+    // not serve a large request, so hand them back to the system and retry
+    cudaGetLastError();
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaStreamSynchronize(st) == cudaSuccess && cudaGetDevice(&dev) == cudaSuccess &&
+        cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+      cudaMemPoolTrimTo(pool, 0);
+    cudaGetLastError();
+    e = cudaMallocAsync(&p, bytes ? bytes : 8, st);
+  }
+  TSVD_CUDA(e);
   return p;
 }
 

@@ -334,6 +334,12 @@ tsvd_status tsvd_set_thick_restart(tsvd_t h, int keep) {
   return TSVD_OK;
 }
 
+tsvd_status tsvd_set_output_mode(tsvd_t h, int mode) {
+  if (!h || mode < TSVD_OUT_AUTO || mode > TSVD_OUT_INPLACE) return TSVD_EINVAL;
+  h->out_mode = mode;
+  return TSVD_OK;
+}
+
 tsvd_status tsvd_set_qr_block(tsvd_t h, int b_qr) {
   if (!h || b_qr < 1 || b_qr > 32) return TSVD_EINVAL;
   h->b_qr = b_qr;
@@ -385,10 +391,10 @@ tsvd_status tsvd_get(tsvd_t h, double* U, int64_t ldu, double* S, double* V, int
   const cudaMemcpyKind k = mem_kind == TSVD_DEVICE ? cudaMemcpyDeviceToDevice
                                                    : cudaMemcpyDeviceToHost;
   if (U)
-    TSVD_CUDA(cudaMemcpy2DAsync(U, ldu * sizeof(double), h->U, r * sizeof(double),
+    TSVD_CUDA(cudaMemcpy2DAsync(U, ldu * sizeof(double), h->U, h->ldU * sizeof(double),
                                 r * sizeof(double), h->m, k, h->st));
   if (V)
-    TSVD_CUDA(cudaMemcpy2DAsync(V, ldv * sizeof(double), h->V, r * sizeof(double),
+    TSVD_CUDA(cudaMemcpy2DAsync(V, ldv * sizeof(double), h->V, h->ldV * sizeof(double),
                                 r * sizeof(double), h->n, k, h->st));
   if (S) TSVD_CUDA(cudaMemcpyAsync(S, h->S, r * sizeof(double), k, h->st));
   TSVD_CUDA(cudaStreamSynchronize(h->st));

@@ -55,6 +55,8 @@ struct tsvd_ctx {
   int* hflags = nullptr;      // pinned host mirror
   // results of the last solve
   double *U = nullptr, *S = nullptr, *V = nullptr;
+  int64_t ldU = 0, ldV = 0;   // row pitch of U / V (r, or the basis ld in place)
+  int out_mode = 0;           // TSVD_OUT_* (tsvd_set_output_mode)
   int r = 0;
   bool have = false;
   std::vector<double> rho;    // rho_i / sigma_1, i < r (LancSVD)

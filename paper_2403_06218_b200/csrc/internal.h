@@ -63,10 +63,12 @@ struct Csr {  // device CSR (canonical)
   int32_t* split_first = nullptr;// first partial slot of that row
   int32_t* split_count = nullptr;// number of slots
   int64_t nslots = 0;            // partial slots
-  int64_t nshort = 0;            // rows with <= kLongRow nonzeros ...
-  int32_t* short_rows = nullptr; // ... ordered by decreasing length (stable)
-  int64_t nmed = 0;              // rows with kLongRow < len <= kMedRow ...
-  int32_t* med_rows = nullptr;   // ... ordered by decreasing length (stable)
+  // row-sorted layout (csr_build_plan): after the plan, rowptr/colidx/vals
+  // hold the rows in the order [short | medium | long], position p being
+  // output row perm[p]; short and medium rows by decreasing length (stable)
+  int64_t nshort = 0;            // rows with <= kLongRow nonzeros
+  int64_t nmed = 0;              // rows with kLongRow < len <= kMedRow
+  int32_t* perm = nullptr;       // output row of each position
 };
 
 

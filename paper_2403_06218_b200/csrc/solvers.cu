@@ -22,10 +22,10 @@ static void upload_start(Ctx& c, double* dst, int64_t rows, int cols, int64_t ld
 }
 
 // sign of the largest-|.| entry of each column of the (row-sharded) V (R28)
-static double* signs_of(Ctx& c, const double* V, int64_t n, int r) {
+static double* signs_of(Ctx& c, const double* V, int64_t n, int64_t ldv, int r) {
   double* work = dbuf(c, "sign_work", col_signs_work(r, c.world));
   double* sgn = dbuf(c, "sign", (size_t)r);
-  double* loc = col_signs_local(V, n, r, r, c.n0, work, c.st);
+  double* loc = col_signs_local(V, n, ldv, r, c.n0, work, c.st);
   if (c.comm) {
     double* all = dbuf(c, "sign_all", (size_t)3 * r * c.world);
     all_gather(c, loc, all, (size_t)3 * r);
@@ -36,11 +36,59 @@ static double* signs_of(Ctx& c, const double* V, int64_t n, int r) {
   return sgn;
 }
 
-static void alloc_results(Ctx& c, int r) {
-  c.U = dbuf(c, "res_U", (size_t)c.m * r);
-  c.V = dbuf(c, "res_V", (size_t)c.n * r);
-  c.S = dbuf(c, "res_S", (size_t)r);
-  c.r = r;
+// tsvd_set_output_mode: form U_r, V_r in place over the bases when separate
+// m x r and n x r buffers do not fit in the free device memory (C5 on one GPU).
+static bool outputs_in_place(Ctx& c, int r) {
+  if (c.out_mode == TSVD_OUT_INPLACE) return true;
+  if (c.out_mode == TSVD_OUT_SEPARATE) return false;
+  size_t have = 0;
+  for (const char* nm : {"res_U", "res_V"}) {
+    auto it = c.bufs.find(nm);
+    if (it != c.bufs.end()) have += it->second.second;
+  }
+  const size_t need = (size_t)(c.m + c.n) * r * sizeof(double);
+  if (need <= have) return false;
+  size_t fr = 0, tot = 0;
+  TSVD_CUDA(cudaMemGetInfo(&fr, &tot));
+  int dev = 0;
+  cudaMemPool_t pool;
+  size_t pool_free = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t res = 0, used = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res) == cudaSuccess &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess &&
+        res > used)
+      pool_free = (size_t)(res - used);
+  }
+  cudaGetLastError();
+  const size_t margin = (size_t)2 << 30;
+  return need - have + margin > fr + pool_free;
+}
+
+// Output product Z = X[:, :s] H[:, :r] (Eq. 12; Alg. 1 S6/S7), row-local.
+// Separate: into the named result buffer.  In place: over X's first r
+// columns, in row chunks staged through the pass scratch buffer (a chunk's
+// rows are read completely by the product before the copy overwrites them).
+static double* out_product(Ctx& c, const char* name, double* X, int64_t ldx, int64_t rows,
+                           int s, const double* H, int64_t ldh, int r, bool inplace,
+                           int64_t* ld) {
+  if (!inplace) {
+    double* Z = dbuf(c, name, (size_t)rows * r);
+    gemm_nn(X, ldx, H, ldh, nullptr, 0, nullptr, Z, r, rows, s, r, 1.0, 0.0, nullptr, c.st);
+    *ld = r;
+    return Z;
+  }
+  const size_t cap = (size_t)std::max(c.m, c.n) * 32;  // pre-sized by the solvers
+  double* stage = dbuf(c, "scratch", cap);
+  const int64_t chunk = std::max<int64_t>(1, (int64_t)(cap / r));
+  for (int64_t r0 = 0; r0 < rows; r0 += chunk) {
+    const int64_t rc = std::min(chunk, rows - r0);
+    gemm_nn(X + r0 * ldx, ldx, H, ldh, nullptr, 0, nullptr, stage, r, rc, s, r, 1.0, 0.0,
+            nullptr, c.st);
+    copy_block(stage, r, X + r0 * ldx, ldx, rc, r, false, c.st);
+  }
+  *ld = ldx;
+  return X;
 }
 
 struct EventTimer {
@@ -221,16 +269,18 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
     }
   }
   if (cycle > maxit) cycle = maxit;
-  alloc_results(c, r);
+  const bool inplace = outputs_in_place(c, r);
+  c.S = dbuf(c, "res_S", (size_t)r);
+  c.r = r;
   {
     Prof p(c, P_RESTART, 8.0 * (m + n) * (d + r), 2.0 * (m + n) * d * r);
     // S8 (Eq. 12): V = P_k Vbar[:, :r]; signs (R28) from V, folded into
     // Ubar's columns before S9: U = Pbar_k Ubar[:, :r]
-    gemm_nn(P, ldp, Vb, d, nullptr, 0, nullptr, c.V, r, n, d, r, 1.0, 0.0, nullptr, c.st);
-    double* sgn = signs_of(c, c.V, n, r);
-    flip_columns(c.V, n, r, r, sgn, c.st);
+    c.V = out_product(c, "res_V", P, ldp, n, d, Vb, d, r, inplace, &c.ldV);
+    double* sgn = signs_of(c, c.V, n, c.ldV, r);
+    flip_columns(c.V, n, c.ldV, r, sgn, c.st);
     flip_columns(Ub, d, d, r, sgn, c.st);
-    gemm_nn(Pb, ldb, Ub, d, nullptr, 0, nullptr, c.U, r, m, d, r, 1.0, 0.0, nullptr, c.st);
+    c.U = out_product(c, "res_U", Pb, ldb, m, d, Ub, d, r, inplace, &c.ldU);
     TSVD_CUDA(cudaMemcpyAsync(c.S, Sg, r * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
   }
   const double ms = timer.stop();
@@ -295,14 +345,16 @@ tsvd_status rsvd_solve(Ctx& c, int r, int p, int q) {
     Prof p(c, P_SVD, 16.0 * l * l, 0);
     small_svd(R, l, Ub, Sg, Vb, jw, c.st);                             // S5
   }
-  alloc_results(c, r);
+  const bool inplace = outputs_in_place(c, r);
+  c.S = dbuf(c, "res_S", (size_t)r);
+  c.r = r;
   {
     Prof p(c, P_RESTART, 8.0 * (m + n) * (l + r), 2.0 * (m + n) * l * r);
-    gemm_nn(Q, l, Ub, l, nullptr, 0, nullptr, c.V, r, n, l, r, 1.0, 0.0, nullptr, c.st);   // S7
-    double* sgn = signs_of(c, c.V, n, r);
-    flip_columns(c.V, n, r, r, sgn, c.st);
+    c.V = out_product(c, "res_V", Q, l, n, l, Ub, l, r, inplace, &c.ldV);    // S7
+    double* sgn = signs_of(c, c.V, n, c.ldV, r);
+    flip_columns(c.V, n, c.ldV, r, sgn, c.st);
     flip_columns(Vb, l, l, r, sgn, c.st);
-    gemm_nn(Qb, l, Vb, l, nullptr, 0, nullptr, c.U, r, m, l, r, 1.0, 0.0, nullptr, c.st);  // S6
+    c.U = out_product(c, "res_U", Qb, l, m, l, Vb, l, r, inplace, &c.ldU);   // S6
     TSVD_CUDA(cudaMemcpyAsync(c.S, Sg, r * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
   }
   double s1 = 0.0;

@@ -44,17 +44,18 @@ template <int L, int VEC>
 __device__ __forceinline__ void spmm_short_dev(
     const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
     const double* __restrict__ vals, const double* __restrict__ X, int64_t ldx,
-    double* __restrict__ Y, int64_t ldy, const int32_t* __restrict__ order, int64_t nrows,
+    double* __restrict__ Y, int64_t ldy, const int32_t* __restrict__ perm, int64_t nrows,
     int w, int64_t bidx) {
   constexpr int RPW = 32 / L;  // rows per warp
   const int lane = threadIdx.x & 31;
   const int64_t warp = (bidx * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t idx = warp * RPW + lane / L;
+  const int64_t pos = warp * RPW + lane / L;
   const int c = (lane % L) * VEC;
-  if (idx >= nrows) return;
-  // rows of similar length share a warp (order = short rows by decreasing length)
-  const int64_t row = __ldg(order + idx);
-  const int64_t beg = __ldg(rowptr + row), end = __ldg(rowptr + row + 1);
+  if (pos >= nrows) return;
+  // row-sorted layout: position pos holds output row perm[pos]; rows of
+  // similar length share a warp and their nonzeros are adjacent in memory
+  const int64_t row = __ldg(perm + pos);
+  const int64_t beg = __ldg(rowptr + pos), end = __ldg(rowptr + pos + 1);
   const bool active = c < w;
   const double* Xc = X + c;
   double acc0[VEC], acc1[VEC];
@@ -102,7 +103,7 @@ template <int L, int VEC>
 __device__ __forceinline__ void spmm_medium_dev(
     const int64_t* __restrict__ rowptr, const int32_t* __restrict__ colidx,
     const double* __restrict__ vals, const double* __restrict__ X, int64_t ldx,
-    double* __restrict__ Y, int64_t ldy, const int32_t* __restrict__ order, int64_t nrows,
+    double* __restrict__ Y, int64_t ldy, const int32_t* __restrict__ perm, int64_t nrows,
     int w, int64_t bidx) {
   constexpr int G = 32 / L;
   const int lane = threadIdx.x & 31;
@@ -111,8 +112,8 @@ __device__ __forceinline__ void spmm_medium_dev(
   const int g = lane / L, c = (lane % L) * VEC;
   const bool active = c < w;
   const double* Xc = X + c;
-  const int64_t row = __ldg(order + widx);
-  const int64_t beg = __ldg(rowptr + row), end = __ldg(rowptr + row + 1);
+  const int64_t row = __ldg(perm + widx);
+  const int64_t beg = __ldg(rowptr + widx), end = __ldg(rowptr + widx + 1);
   double acc0[VEC], acc1[VEC];
 #pragma unroll
   for (int e = 0; e < VEC; ++e) acc0[e] = acc1[e] = 0.0;
@@ -233,11 +234,11 @@ __global__ void __launch_bounds__(256) spmm_kernel(Csr A, const double* __restri
     spmm_long_dev<L, VEC>(A.seg_row, A.seg_beg, A.seg_end, A.seg_slot, A.colidx, A.vals, X, ldx,
                           Y, ldy, w, part, b);
   } else if (b < nb_long + nb_med) {
-    spmm_medium_dev<L, VEC>(A.rowptr, A.colidx, A.vals, X, ldx, Y, ldy, A.med_rows, A.nmed, w,
-                            b - nb_long);
+    spmm_medium_dev<L, VEC>(A.rowptr + A.nshort, A.colidx, A.vals, X, ldx, Y, ldy,
+                            A.perm + A.nshort, A.nmed, w, b - nb_long);
   } else {
-    spmm_short_dev<L, VEC>(A.rowptr, A.colidx, A.vals, X, ldx, Y, ldy, A.short_rows, A.nshort,
-                           w, b - nb_long - nb_med);
+    spmm_short_dev<L, VEC>(A.rowptr, A.colidx, A.vals, X, ldx, Y, ldy, A.perm, A.nshort, w,
+                           b - nb_long - nb_med);
   }
 }
 
@@ -314,13 +315,63 @@ void launch_spmm_wide(const Csr& A, const double* X, int64_t ldx, double* Y, int
 }
 
 // ------------------------------------------------------- plan / transpose --
+// Copies the nonzeros of the rows in permuted order: position p of the new
+// layout holds row perm[p] (one warp per row, lane-strided).
+__global__ void csr_permute_kernel(const int64_t* __restrict__ old_rp,
+                                   const int32_t* __restrict__ old_ci,
+                                   const double* __restrict__ old_va,
+                                   const int32_t* __restrict__ perm,
+                                   const int64_t* __restrict__ new_rp, int64_t rows,
+                                   int32_t* __restrict__ new_ci, double* __restrict__ new_va) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < rows;
+       p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t ob = old_rp[perm[p]], nb = new_rp[p], len = new_rp[p + 1] - nb;
+    for (int64_t k = lane; k < len; k += 32) {
+      new_ci[nb + k] = old_ci[ob + k];
+      new_va[nb + k] = old_va[ob + k];
+    }
+  }
+}
+
+// Row-sorted layout + load-balancing plan (called once per CSR, after the
+// transposition).  Rows are permuted to [short rows by decreasing length |
+// medium rows by decreasing length | long rows] (stable), the nonzeros are
+// moved to that order (A.rowptr becomes the permuted row pointer, A.perm the
+// output row of each position), and long rows are cut into segments.  A warp
+// of short rows then reads adjacent rows' nonzeros (one chain fewer than an
+// order[] -> rowptr[row] indirection) and writes Y[perm[p]].
 void csr_build_plan(Csr& A, const int64_t* hrp, cudaStream_t st) {
+  auto len_of = [&](int64_t i) { return hrp[i + 1] - hrp[i]; };
+  // short rows, counting-sorted by decreasing length (stable in the row index)
+  std::vector<int64_t> cnt(kLongRow + 2, 0);
+  for (int64_t i = 0; i < A.rows; ++i)
+    if (len_of(i) <= kLongRow) ++cnt[kLongRow - len_of(i) + 1];
+  for (int k = 1; k <= kLongRow + 1; ++k) cnt[k] += cnt[k - 1];
+  const int64_t nshort = cnt[kLongRow + 1];
+  std::vector<int32_t> perm(A.rows);
+  for (int64_t i = 0; i < A.rows; ++i)
+    if (len_of(i) <= kLongRow) perm[cnt[kLongRow - len_of(i)]++] = (int32_t)i;
+  // medium rows by decreasing length, then long rows in row order
+  std::vector<std::pair<int64_t, int32_t>> med;
+  for (int64_t i = 0; i < A.rows; ++i)
+    if (len_of(i) > kLongRow && len_of(i) <= kMedRow) med.push_back({-len_of(i), (int32_t)i});
+  std::stable_sort(med.begin(), med.end(),
+                   [](const auto& a, const auto& b) { return a.first < b.first; });
+  int64_t p = nshort;
+  for (auto& e : med) perm[p++] = e.second;
+  const int64_t nmed = (int64_t)med.size();
+  for (int64_t i = 0; i < A.rows; ++i)
+    if (len_of(i) > kMedRow) perm[p++] = (int32_t)i;
+  std::vector<int64_t> nrp(A.rows + 1);
+  nrp[0] = 0;
+  for (int64_t q = 0; q < A.rows; ++q) nrp[q + 1] = nrp[q] + len_of(perm[q]);
+  // long rows: segments of <= kSeg nonzeros in the new layout
   std::vector<int64_t> srow, sbeg, send, sprow;
   std::vector<int32_t> sslot, spfirst, spcnt;
   int32_t slots = 0;
-  for (int64_t i = 0; i < A.rows; ++i) {
-    const int64_t len = hrp[i + 1] - hrp[i];
-    if (len <= kMedRow) continue;
+  for (int64_t q = nshort + nmed; q < A.rows; ++q) {
+    const int64_t i = perm[q], len = len_of(i);
     const int64_t nseg = (len + kSeg - 1) / kSeg;
     if (nseg > 1) {
       sprow.push_back(i);
@@ -329,38 +380,16 @@ void csr_build_plan(Csr& A, const int64_t* hrp, cudaStream_t st) {
     }
     for (int64_t s = 0; s < nseg; ++s) {
       srow.push_back(i);
-      sbeg.push_back(hrp[i] + s * kSeg);
-      send.push_back(std::min(hrp[i + 1], hrp[i] + (s + 1) * kSeg));
+      sbeg.push_back(nrp[q] + s * kSeg);
+      send.push_back(std::min(nrp[q + 1], nrp[q] + (s + 1) * kSeg));
       sslot.push_back(nseg > 1 ? slots++ : -1);
     }
   }
   A.nseg = (int64_t)srow.size();
   A.nsplit = (int64_t)sprow.size();
   A.nslots = slots;
-  // short rows, counting-sorted by decreasing length (stable in the row index)
-  std::vector<int64_t> cnt(kLongRow + 2, 0);
-  for (int64_t i = 0; i < A.rows; ++i) {
-    const int64_t len = hrp[i + 1] - hrp[i];
-    if (len <= kLongRow) ++cnt[kLongRow - len + 1];
-  }
-  for (int k = 1; k <= kLongRow + 1; ++k) cnt[k] += cnt[k - 1];
-  std::vector<int32_t> order(cnt[kLongRow + 1]);
-  for (int64_t i = 0; i < A.rows; ++i) {
-    const int64_t len = hrp[i + 1] - hrp[i];
-    if (len <= kLongRow) order[cnt[kLongRow - len]++] = (int32_t)i;
-  }
-  A.nshort = (int64_t)order.size();
-  // medium rows by decreasing length
-  std::vector<std::pair<int64_t, int32_t>> med;
-  for (int64_t i = 0; i < A.rows; ++i) {
-    const int64_t len = hrp[i + 1] - hrp[i];
-    if (len > kLongRow && len <= kMedRow) med.push_back({-len, (int32_t)i});
-  }
-  std::stable_sort(med.begin(), med.end(),
-                   [](const auto& a, const auto& b) { return a.first < b.first; });
-  std::vector<int32_t> morder(med.size());
-  for (size_t k = 0; k < med.size(); ++k) morder[k] = med[k].second;
-  A.nmed = (int64_t)morder.size();
+  A.nshort = nshort;
+  A.nmed = nmed;
   auto up64 = [&](std::vector<int64_t>& v, int64_t** d) {
     if (v.empty()) return;
     dmalloc_t(d, v.size(), st);
@@ -378,8 +407,25 @@ void csr_build_plan(Csr& A, const int64_t* hrp, cudaStream_t st) {
   up64(sprow, &A.split_row);
   up32(spfirst, &A.split_first);
   up32(spcnt, &A.split_count);
-  up32(order, &A.short_rows);
-  up32(morder, &A.med_rows);
+  up32(perm, &A.perm);
+  // move the nonzeros into the permuted layout
+  int64_t* new_rp = nullptr;
+  up64(nrp, &new_rp);
+  if (A.rows > 0 && A.nnz > 0) {
+    int32_t* nci;
+    double* nva;
+    dmalloc_t(&nci, A.nnz, st);
+    dmalloc_t(&nva, A.nnz, st);
+    csr_permute_kernel<<<148 * 8, 256, 0, st>>>(A.rowptr, A.colidx, A.vals, A.perm, new_rp,
+                                                A.rows, nci, nva);
+    TSVD_CHECK_LAUNCH();
+    dfree(A.colidx, st);
+    dfree(A.vals, st);
+    A.colidx = nci;
+    A.vals = nva;
+  }
+  dfree(A.rowptr, st);
+  A.rowptr = new_rp ? new_rp : A.rowptr;
   TSVD_CUDA(cudaStreamSynchronize(st));
 }
 
@@ -394,8 +440,7 @@ void csr_free(Csr& A, cudaStream_t st) {
   dfree(A.split_row, st);
   dfree(A.split_first, st);
   dfree(A.split_count, st);
-  dfree(A.short_rows, st);
-  dfree(A.med_rows, st);
+  dfree(A.perm, st);
   A = Csr{};
 }
 

@@ -127,19 +127,32 @@ def nn0_bench():
 
 
 def spmm_bench():
+    """SpMM on the solver's operand layout: X and Y are column slices of the
+    row-major bases (ld = d + b on the m side, d on the n side)."""
     from tsvd_inputs import powerlaw_csr
-    m = n = 1_000_000
-    csr = powerlaw_csr(m, n, 10_000_000, 2.5, seed=0x2403062182)
-    h = T.TruncatedSVD(csr=csr, shape=(m, n))
-    nnz = len(csr[1])
-    for w in (16, 32):
-        X = torch.randn((n, w), dtype=torch.float64, device="cuda")
-        Y = torch.empty((m, w), dtype=torch.float64, device="cuda")
+    shapes = os.environ.get("SPMM_CFG", "C2,C3").split(",")
+    for cfgn in shapes:
+        if cfgn == "C2":
+            m, n, nnz, w, d = 1_000_000, 1_000_000, 10_000_000, 16, 384
+            seed = 0x2403062182
+        else:
+            m, n, nnz, w, d = 4_000_000, 500_000, 50_000_000, 32, 640
+            seed = 0x2403062183
+        csr = powerlaw_csr(m, n, nnz, 2.5, seed=seed)
+        h = T.TruncatedSVD(csr=csr, shape=(m, n))
+        nnz = len(csr[1])
+        Pb = torch.randn((m, d + w), dtype=torch.float64, device="cuda")
+        P = torch.randn((n, d), dtype=torch.float64, device="cuda")
         for tr in (False, True):
+            # A.Q: X = n-side slice of P, Y = m-side slice of Pbar; A^T.Qbar the reverse
+            X, Y = (Pb[:, 64:64 + w], P[:, 64:64 + w]) if tr else (P[:, 64:64 + w], Pb[:, 64:64 + w])
             ms = timeit(lambda: T.dbg_apply(h, tr, X, Y))
-            gb = (12.0 * nnz + 8 * (m + 1) + 8.0 * w * (m + n)) / (ms * 1e-3) / 1e9
-            print(f"spmm w={w} trans={tr}: {ms:.3f} ms  {gb:.0f} GB/s compulsory "
-                  f"({gb / HBM:.2f} of HBM)", flush=True)
+            rows, cols = (n, m) if tr else (m, n)
+            gb = (12.0 * nnz + 8 * (rows + 1) + 8.0 * w * (rows + cols)) / (ms * 1e-3) / 1e9
+            print(f"spmm {cfgn} w={w} trans={tr} slice={os.environ.get('TSVD_SPMM_SLICE', '0')}: "
+                  f"{ms:.3f} ms  {gb:.0f} GB/s compulsory ({gb / HBM:.2f} of HBM)", flush=True)
+        h.close()
+        del Pb, P
 
 
 def dense_bench():

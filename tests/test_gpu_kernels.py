@@ -133,8 +133,9 @@ def test_spmm_parity(kind, w):
     rng = np.random.default_rng(w)
     X = rng.standard_normal((n, w))
     Xt = rng.standard_normal((m, w))
-    Yg = torch.zeros((m, w), dtype=torch.float64, device="cuda")
-    Zg = torch.zeros((n, w), dtype=torch.float64, device="cuda")
+    # NaN-filled outputs: every row (empty rows included) must be written
+    Yg = torch.full((m, w), float("nan"), dtype=torch.float64, device="cuda")
+    Zg = torch.full((n, w), float("nan"), dtype=torch.float64, device="cuda")
     T.dbg_apply(h, False, cu(X), Yg)
     T.dbg_apply(h, True, cu(Xt), Zg)
     Aabs = oracle.Operator(csr=(csr[0], csr[1], np.abs(csr[2])), shape=shape)

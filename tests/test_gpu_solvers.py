@@ -271,3 +271,36 @@ def test_thick_restart_shape_errors():
                 h.block_lanczos(r=10, b=4, tol=1e-12, maxit=2, d=28)
         with pytest.raises(T.TsvdError):
             h.set_thick_restart(-1)
+
+
+# ---- tsvd_set_output_mode: outputs formed in place over the bases ----------
+@pytest.mark.parametrize("algo", ["lanczos", "rsvd"])
+def test_inplace_outputs_match_separate(algo):
+    """Eq. 12 / Alg. 1 S6-S7 formed over the bases' first r columns in row
+    chunks (the C5 memory plan) give the same triplets as separate buffers;
+    r = 100 at m = 200 makes the chunked path take several chunks."""
+    A, s = _c1()
+    res = {}
+    for mode in (T.TSVD_OUT_SEPARATE, T.TSVD_OUT_INPLACE):
+        with T.TruncatedSVD(A) as h:
+            h.set_seed(11)
+            h.set_output_mode(mode)
+            if algo == "lanczos":
+                h.block_lanczos(r=100, b=4, tol=1e-30, maxit=1, d=100)
+            else:
+                h.rsvd(r=60, p=40, q=1)
+            res[mode] = h.get()
+    for a, b in zip(res[T.TSVD_OUT_SEPARATE], res[T.TSVD_OUT_INPLACE]):
+        assert np.abs(a - b).max() <= 1e-14 * max(1.0, np.abs(a).max())
+    Ug, Sg, Vg = res[T.TSVD_OUT_INPLACE]
+    r = len(Sg)
+    assert np.abs(Ug.T @ Ug - np.eye(r))[:40, :40].max() <= 1e-12
+    assert np.abs(Sg[:10] - s[:10]).max() / s[0] <= 1e-10
+
+
+def test_output_mode_errors():
+    A, _ = _c1()
+    with T.TruncatedSVD(A) as h:
+        for bad in (-1, 3):
+            with pytest.raises(T.TsvdError):
+                h.set_output_mode(bad)

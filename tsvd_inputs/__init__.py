@@ -25,12 +25,15 @@ Recipes (DESIGN.md "Input recipe"):
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 __all__ = [
     "spectrum_eq16",
     "dense_prescribed",
     "powerlaw_csr",
+    "powerlaw_csr_device",
     "blockdiag_csr",
     "gaussian_block",
     "CONFIGS",
@@ -43,6 +46,7 @@ SEEDS = {
     "C3": 0x2403062183,
     "C4": 0x2403062184,
     "C5": 0x2403062185,
+    "C5s": 0x2403062185,
 }
 
 # BASELINE.json configs with the solver settings of SURVEY.md 8(a)/8(d).
@@ -180,6 +184,86 @@ def _powerlaw_csr(m, n, nnz, alpha, seed, oversample):
     rowptr = np.zeros(m + 1, dtype=np.int64)
     rowptr[1:] = np.cumsum(np.bincount(r, minlength=m))
     return rowptr, c, np.ascontiguousarray(vsum, dtype=np.float64)
+
+
+def powerlaw_csr_device(m: int, n: int, nnz: int, alpha: float, seed: int, device="cuda",
+                        exact_after_dedup: bool = True):
+    """G1 Chung-Lu CSR generated with torch on `device` -- the same recipe
+    and distributions as powerlaw_csr, for C5 (m = n = 5e7, nnz = 1e9), where
+    the host generator would need many minutes and > 60 GB of host memory.
+    The random stream is torch's (Philox on CUDA), so the bytes differ from
+    powerlaw_csr at the same seed; they are deterministic for a given seed and
+    device type.  Returns (rowptr int64[m+1], colidx int32, vals f64) tensors
+    on `device`, canonical (sorted, duplicates summed in sorted order)."""
+    out = _powerlaw_csr_device(m, n, nnz, alpha, seed, 1.0, device)
+    if exact_after_dedup and out[1].numel() < 0.99 * nnz:
+        got = out[1].numel()
+        del out
+        out = _powerlaw_csr_device(m, n, nnz, alpha, seed, nnz / max(1, got), device)
+    return out
+
+
+def _powerlaw_csr_device(m, n, nnz, alpha, seed, oversample, device):
+    import sys
+    import time
+    import torch
+    t0 = time.time()
+
+    def log(what):
+        if os.environ.get("TSVD_GEN_VERBOSE"):
+            print(f"[gen] {what}: {time.time() - t0:.1f} s", file=sys.stderr, flush=True)
+    f64 = torch.float64
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    want = int(nnz * oversample)
+    # row lengths (_row_lengths): Pareto weights scaled to the mean, capped at n
+    u = torch.rand(m, generator=g, dtype=f64, device=device)
+    target = (1.0 - u) ** (-1.0 / (alpha - 1.0))
+    target = torch.clamp(target * (want / float(target.sum())), max=float(n))
+    L = torch.floor(target).to(torch.int64)
+    rem = want - int(L.sum())
+    if rem > 0:
+        frac = target - L
+        frac[L >= n] = -1.0
+        idx = torch.argsort(frac, descending=True)[:min(rem, m)]
+        L[idx] += 1
+        del frac, idx
+    L.clamp_(max=n)
+    del u, target
+    log("row lengths")
+    # column weights under a random permutation, inverse-CDF draws
+    u = torch.rand(n, generator=g, dtype=f64, device=device)
+    cw = ((1.0 - u) ** (-1.0 / (alpha - 1.0)))[torch.randperm(n, generator=g, device=device)]
+    cdf = torch.cumsum(cw, 0)
+    cdf /= cdf[-1].clone()
+    del u, cw
+    total = int(L.sum())
+    key = torch.repeat_interleave(torch.arange(m, device=device, dtype=torch.int64), L)
+    key *= n
+    cols = torch.searchsorted(cdf, torch.rand(total, generator=g, dtype=f64, device=device),
+                              right=True)
+    cols.clamp_(max=n - 1)
+    key += cols
+    del cols, cdf, L
+    log("keys")
+    vals = torch.randn(total, generator=g, dtype=f64, device=device)
+    key, order = torch.sort(key, stable=True)
+    vals = vals[order]
+    del order
+    log("sort")
+    uniq, counts = torch.unique_consecutive(key, return_counts=True)
+    del key
+    if uniq.numel() < total:
+        vals = torch.segment_reduce(vals, "sum", lengths=counts)
+    del counts
+    r = uniq // n
+    colidx = (uniq - r * n).to(torch.int32)
+    del uniq
+    rowptr = torch.zeros(m + 1, dtype=torch.int64, device=device)
+    rowptr[1:] = torch.cumsum(torch.bincount(r, minlength=m), 0)
+    del r
+    log("dedup + rowptr")
+    return rowptr, colidx, vals.contiguous()
 
 
 def blockdiag_csr(m: int, n: int, mean_row: float, alpha: float, seed: int,
