@@ -59,8 +59,13 @@ CONFIGS = {
                r=100, b=32, d=640, tol=1e-8, maxit=6, rsvd_p=10, rsvd_q=2),
     "C4": dict(kind="dense", m=40_000, n=20_000, r=200, b=32, d=704, tol=1e-6,
                maxit=6, rsvd_p=10, rsvd_q=8),
+    # C5 (i): fixed-work runs, one restart cycle at d = 160; the
+    # matrix is generated on the device (powerlaw_csr_device)
     "C5": dict(kind="csr", m=50_000_000, n=50_000_000, nnz=1_000_000_000,
-               alpha=2.5, r=100, b=32, d=160, tol=1e-8, maxit=6),
+               alpha=2.5, r=100, b=32, d=160, tol=1e-8, maxit=1, device_gen=True),
+    # C5 scaled down by 10 (SURVEY 8(d) "Oracle timing"): the host oracle's sample
+    "C5s": dict(kind="csr", m=5_000_000, n=5_000_000, nnz=100_000_000,
+                alpha=2.5, r=100, b=32, d=160, tol=1e-8, maxit=1),
 }
 
 
