@@ -1060,7 +1060,23 @@ __global__ void __launch_bounds__(288, NYB == 1 ? 2 : 1) gemm_nn_tma_kernel(
       for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
         for (int ni = 0; ni < NT; ++ni) yt[mi][ni][0] = yt[mi][ni][1] = 0.0;
-      if (use_y) {
+      if (use_y && !T) {
+        // no T (Alg. 5 S2 / S7: Y - P H): the Y values in accumulator layout,
+        // straight from the swizzled tile (row r = warp*16 + mi*8 + prow,
+        // columns ni*8 + 2 tig + {0,1} = one 16-byte chunk) -- no identity DMMAs
+        mbar_wait(yfull, (unsigned)lt & 1);
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) {
+            const double2 yv = *reinterpret_cast<const double2*>(
+                Ys + (ni >> 1) * (CF::xbox / 8) + (warp * 16 + mi * 8 + prow) * 16 +
+                ((((ni & 1) << 2) | tig) ^ prow) * 2);
+            yt[mi][ni][0] = yv.x;
+            yt[mi][ni][1] = yv.y;
+          }
+        // Ys is released below, once the values were consumed into Os
+      } else if (use_y) {
         mbar_wait(yfull, (unsigned)lt & 1);
         double2 ya[2][2 * NYB];
 #pragma unroll
@@ -1096,6 +1112,10 @@ __global__ void __launch_bounds__(288, NYB == 1 ? 2 : 1) gemm_nn_tma_kernel(
             const double z = alpha * (acc[0][mi][ni][e] + acc[1][mi][ni][e]) + beta * yt[mi][ni][e];
             Os[r * OP + c] = (c < w && r0 + r < q) ? z : 0.0;
           }
+      if (use_y && !T) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(yempty);
+      }
       bar_consumers();
       if (Z) {
         for (int idx = tid; idx < NT_R * WP; idx += 256) {
