@@ -120,13 +120,27 @@ __global__ void __launch_bounds__(fin_threads(WT)) finalize_kernel(
       if (mode == 0) Wout[tid] = a;
     }
   } else {
-    // w^2 > NTH (w >= 23): each thread sums whole entries, partials in order
-    for (int e = tid; e < C; e += NTH) {
-      double a = 0.0;
-#pragma unroll 16
-      for (int p = 0; p < np; ++p) a += gram[(int64_t)p * C + e];
-      Ws[e] = a;
-      if (mode == 0) Wout[e] = a;
+    // w^2 > NTH (w >= 23): each thread sums whole entries, partials in order;
+    // its EPT entries advance side by side so their loads overlap (the order
+    // of the additions of each entry is unchanged: p = 0, 1, ..., np - 1)
+    constexpr int EPT = (32 * 32 + NTH - 1) / NTH;
+    double a[EPT];
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) a[j] = 0.0;
+#pragma unroll 8
+    for (int p = 0; p < np; ++p)
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        const int e = tid + j * NTH;
+        if (e < C) a[j] += gram[(int64_t)p * C + e];
+      }
+#pragma unroll
+    for (int j = 0; j < EPT; ++j) {
+      const int e = tid + j * NTH;
+      if (e < C) {
+        Ws[e] = a[j];
+        if (mode == 0) Wout[e] = a[j];
+      }
     }
   }
   __syncthreads();
