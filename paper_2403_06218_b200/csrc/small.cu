@@ -60,7 +60,9 @@ __device__ void warp_tri_inverse_t(const double* Lo, double* Xs, double* Tout, i
 //   1. W = sum of the np per-CTA Gram partials in a fixed order (thread t sums
 //      partials g, g+G, g+2G, ... of entry e = t mod w^2, g = t div w^2,
 //      G = FIN_T div w^2; the G group sums are added in g order).  np = 1
-//      passes an already reduced W through bit for bit.
+//      passes an already reduced W through bit for bit; for w >= 23 the
+//      launcher first reduces the partials with gram_prereduce_kernel (one
+//      CTA per 32 entries) and calls this kernel with np = 1.
 //   2. mode >= 1: L = chol(W) with the breakdown test of P:275 and
 //      T = L^{-T}; w <= 16 in registers (row i of W in lane i, right-looking
 //      updates by shuffles; the column scaling multiplies by 1/l_jj =
@@ -229,9 +231,41 @@ __global__ void __launch_bounds__(fin_threads(WT)) finalize_kernel(
   if (tid == 0 && bad) *flag = 1;
 }
 
+// Gram partial reduction for w >= 23 (w^2 entries > the finaliser's threads):
+// CTA b sums entries [32 b, 32 b + 32) over the np partials -- 8 groups of 32
+// threads take partials g, g + 8, g + 16, ... (all their loads in flight), the
+// group sums are added in g order (fixed order, deterministic) -- and writes
+// the total over partial slot 0 (only this CTA reads or writes those
+// entries).  The single-CTA finaliser then runs with np = 1.
+__global__ void __launch_bounds__(256) gram_prereduce_kernel(double* __restrict__ gram, int np,
+                                                             int C) {
+  __shared__ double red[8][33];
+  const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
+  double a = 0.0;
+  if (e < C) {
+#pragma unroll 4
+    for (int p = g; p < np; p += 8) a += gram[(int64_t)p * C + e];
+  }
+  red[g][lane] = a;
+  __syncthreads();
+  if (g == 0 && e < C) {
+    double t = red[0][lane];
+#pragma unroll
+    for (int k = 1; k < 8; ++k) t += red[k][lane];
+    gram[e] = t;
+  }
+}
+
 static void fin_launch(const double* gram, int np, int w, int mode, double* Wout,
                        const double* Lprev, double* L, double* T, double* R, double* H,
                        const double* Hbar, int s, int* flag, cudaStream_t st) {
+  if (np > 1 && w * w > fin_threads(w == 32 ? 32 : 0)) {
+    gram_prereduce_kernel<<<(w * w + 31) / 32, 256, 0, st>>>(const_cast<double*>(gram), np,
+                                                             w * w);
+    TSVD_CHECK_LAUNCH();
+    np = 1;
+  }
   static bool attr = false;
   const int dyn = FIN_HB * 8;
   if (!attr) {

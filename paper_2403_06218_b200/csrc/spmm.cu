@@ -416,7 +416,9 @@ void csr_build_plan(Csr& A, const int64_t* hrp, cudaStream_t st) {
     double* nva;
     dmalloc_t(&nci, A.nnz, st);
     dmalloc_t(&nva, A.nnz, st);
-    csr_permute_kernel<<<148 * 8, 256, 0, st>>>(A.rowptr, A.colidx, A.vals, A.perm, new_rp,
+    // one warp per row, up to 64 CTAs per SM in flight (latency-bound)
+    const unsigned pg = (unsigned)std::min<int64_t>((A.rows + 7) / 8, 148 * 64);
+    csr_permute_kernel<<<pg, 256, 0, st>>>(A.rowptr, A.colidx, A.vals, A.perm, new_rp,
                                                 A.rows, nci, nva);
     TSVD_CHECK_LAUNCH();
     dfree(A.colidx, st);
@@ -560,7 +562,8 @@ int csr_validate_device(const Csr& A, cudaStream_t st) {
   int* d;
   dmalloc_t(&d, 1, st);
   TSVD_CUDA(cudaMemsetAsync(d, 0, sizeof(int), st));
-  csr_validate_kernel<<<148 * 4, 256, 0, st>>>(A.rowptr, A.colidx, A.rows, A.cols, A.nnz, d);
+  const unsigned vg = (unsigned)std::max<int64_t>(1, std::min<int64_t>((A.rows + 7) / 8, 148 * 64));
+  csr_validate_kernel<<<vg, 256, 0, st>>>(A.rowptr, A.colidx, A.rows, A.cols, A.nnz, d);
   TSVD_CHECK_LAUNCH();
   int h = 0;
   TSVD_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st));

@@ -117,12 +117,14 @@ def dense_prescribed(m: int, n: int, sigma: np.ndarray, seed: int,
         import torch
         A = torch.zeros((m, n), dtype=torch.float64, device=device)
         A.diagonal().copy_(torch.from_numpy(sigma))
+        # rank-1 updates in place (addr_): no m x n temporaries, so m = 1e6,
+        # n = 1e4 (80 GB) builds within the device memory
         for y in ys:  # A <- A (I - 2 y y^T)   (Y^T from the right)
             yt = torch.from_numpy(y).to(device)
-            A.sub_(2.0 * torch.outer(A @ yt, yt))
+            A.addr_(A @ yt, yt, alpha=-2.0)
         for x in xs:  # A <- (I - 2 x x^T) A
             xt = torch.from_numpy(x).to(device)
-            A.sub_(2.0 * torch.outer(xt, xt @ A))
+            A.addr_(xt, xt @ A, alpha=-2.0)
         return A
     A = np.zeros((m, n))
     A[np.arange(n), np.arange(n)] = sigma
