@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(fin_threads(WT)) finalize_kernel(
   }
   __syncthreads();
   if (mode == 0) return;
-  if constexpr (WT > 0) {
+  if constexpr (WT > 0 && WT <= 16) {
     if (tid < 32) {
       const int lane = tid;
       double a[WT];
@@ -183,6 +183,52 @@ __global__ void __launch_bounds__(fin_threads(WT)) finalize_kernel(
         double v = (i == lane) ? 1.0 : 0.0;
 #pragma unroll
         for (int m = 0; m < i; ++m) v = fma(-__shfl_sync(~0u, a[m], i), Xs[m * 33 + lane], v);
+        Xs[i * 33 + lane] = (i >= lane) ? v * rsd[i] : 0.0;
+      }
+    }
+  } else if constexpr (WT == 32) {
+    // Right-looking Cholesky + forward-substitution inverse in ROLLED loops
+    // over shared memory (lane i owns row i; Lo = W's lower triangle, updated
+    // in place).  The arithmetic and its order are those of the register
+    // version above, but that version's ~19 000 straight-line instructions
+    // for w = 32 ran from a cold instruction cache after every big pass
+    // (58 us per call in ncu, 39 us rolled); for w <= 16 (5 900
+    // instructions) the register version stays faster.
+    if (tid < 32) {
+      const int lane = tid;
+      for (int k = 0; k < WT; ++k)
+        Lo[lane * 32 + k] = (lane < WT && k <= lane) ? Ws[lane * WT + k] : 0.0;
+      __syncwarp();
+      int bd = 0;
+#pragma unroll 1
+      for (int j = 0; j < WT; ++j) {
+        double piv = Lo[j * 32 + j];
+        if (!(piv > 0.0) || !isfinite(piv)) {
+          bd = 1;
+          piv = 1.0;
+        }
+        const double rj = rsqrt(piv);
+        if (lane == 0) rsd[j] = rj;
+        const double aj = Lo[lane * 32 + j];
+        const double lij = lane > j ? aj * rj : (lane == j ? piv * rj : 0.0);
+        __syncwarp();
+        if (lane < WT) Lo[lane * 32 + j] = lij;
+        __syncwarp();
+#pragma unroll 4
+        for (int k = j + 1; k < WT; ++k) {
+          const double lkj = Lo[k * 32 + j];
+          if (lane >= k && lane < WT) Lo[lane * 32 + k] = fma(-lij, lkj, Lo[lane * 32 + k]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0 && bd) bad = 1;
+      // column `lane` of L^{-1} by forward substitution (x[m] kept in Xs);
+      // 1/l_ii = rsd[i] from the factorisation
+#pragma unroll 1
+      for (int i = 0; i < WT; ++i) {
+        double v = (i == lane) ? 1.0 : 0.0;
+#pragma unroll 4
+        for (int m = 0; m < i; ++m) v = fma(-Lo[i * 32 + m], Xs[m * 33 + lane], v);
         Xs[i * 33 + lane] = (i >= lane) ? v * rsd[i] : 0.0;
       }
     }
