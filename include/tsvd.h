@@ -168,6 +168,18 @@ tsvd_status tsvd_set_start(tsvd_t h, const double* block, int64_t rows,
  * reading R12) or maxit cycles.  r >= 1 wanted triplets, b >= 1 block size,
  * tol > 0, maxit >= 1. */
 tsvd_status tsvd_block_lanczos(tsvd_t h, int r, int b, double tol, int maxit);
+/* tsvd_block_lanczos_threshold (Eq. 3): the rank r
+ * is set by the threshold ||A - U_r S_r V_r^T||_2 = sigma_{r+1} <= tau *
+ * sigma_1.  Reading R33: tsvd_block_lanczos is run for r + 1
+ * wanted triplets (r = b first, then doubled up to r_max, each solve from a
+ * fresh start with the handle's Krylov dimension or the default for r + 1);
+ * the result is the smallest r whose sigma_{r+1} <= tau * sigma_1 with
+ * triplets 1..r+1 converged (rho <= tol).  *r_out (may be NULL) receives r;
+ * tsvd_get then returns r columns.  0 < tau < 1, b >= 1, r_max >= 1 (capped
+ * at n - 1), else TSVD_EINVAL.  Not found by r_max: TSVD_WARN_NOTCONV with
+ * r = r_max triplets retrievable. */
+tsvd_status tsvd_block_lanczos_threshold(tsvd_t h, double tau, int b, double tol, int maxit,
+                                         int r_max, int* r_out);
 /* tsvd_rsvd: Alg. 1 with l = r + p columns (p = oversampling) and q power
  * iterations, i.e. q + 1 passes of S1-S4 (paper p = q + 1, reading R6); QR by
  * CGS-QR (Alg. 3) with panels of b_qr columns. */

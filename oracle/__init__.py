@@ -26,6 +26,6 @@ from .core import (  # noqa: F401
     Operator, DrawCtx, chol, trsm_right_lt, cholqr2, cgs_cqr2, cgs2, cgs_qr,
     small_svd, sign_normalize,
 )
-from .lancsvd import lancsvd  # noqa: F401
+from .lancsvd import lancsvd, lancsvd_threshold  # noqa: F401
 from .randsvd import randsvd  # noqa: F401
 from .residual import residuals, eckart_young_2norm  # noqa: F401

@@ -113,3 +113,41 @@ def lancsvd(op, r: int, b: int, d: int, tol: float, maxit: int, seed: int,
                    Ub=Ub, Vb=Vb, S_all=S)
     return LancResult(U=U, S=S[:r].copy(), V=V, rho=rho[:r].copy(), cycles=cycle,
                       nconv=int(np.sum(ok)), converged=converged, debug=dbg)
+
+
+def default_krylov_dim(r: int, b: int, n: int) -> int:
+    """d when none is given: min(n, max(4 r, 2 b)) rounded down to a multiple
+    of b (include/tsvd.h, tsvd_set_krylov_dim)."""
+    d = min(max(4 * r, 2 * b), n)
+    return d - d % b
+
+
+def lancsvd_threshold(op, tau: float, b: int, tol: float, maxit: int, r_max: int, seed: int,
+                      d: int | None = None):
+    """the rank set by the threshold of Eq. 3,
+    ||A - U_r S_r V_r^T||_2 = sigma_{r+1} <= tau * sigma_1.  Reading R33:
+    LancSVD is run for r + 1 wanted triplets (r = b first, then doubled up to
+    r_max, each run from the same fresh start); the answer is the smallest r
+    with sigma_{r+1} <= tau * sigma_1 whose triplets 1..r+1 converged
+    (rho <= tol * sigma_1).  Returns (LancResult trimmed to r, r, found)."""
+    r_max = min(r_max, op.n - 1)
+    req = min(b, r_max)
+    while True:
+        want = req + 1
+        dd = d if d else default_krylov_dim(want, b, op.n)
+        res = lancsvd(op, want, b, dd, tol, maxit, seed)
+        conv = res.rho <= tol * res.S[0]
+        found = None
+        for r in range(1, want):
+            if not (conv[r - 1] and conv[r]):
+                break
+            if res.S[r] <= tau * res.S[0]:
+                found = r
+                break
+        if found is not None or req >= r_max:
+            r = found if found is not None else req
+            out = LancResult(U=res.U[:, :r].copy(), S=res.S[:r].copy(), V=res.V[:, :r].copy(),
+                             rho=res.rho[:r].copy(), cycles=res.cycles,
+                             nconv=int(np.sum(conv[:r])), converged=found is not None)
+            return out, r, found is not None
+        req = min(2 * req, r_max)

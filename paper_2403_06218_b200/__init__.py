@@ -30,7 +30,7 @@ TSVD_OUT_AUTO, TSVD_OUT_SEPARATE, TSVD_OUT_INPLACE = 0, 1, 2
 # every symbol include/tsvd.h declares (tests check the .so exports them)
 EXPORTS = [
     "tsvd_create_csr", "tsvd_create_dense", "tsvd_set_stream", "tsvd_set_seed",
-    "tsvd_set_krylov_dim", "tsvd_set_thick_restart", "tsvd_set_output_mode", "tsvd_trim_memory", "tsvd_set_qr_block", "tsvd_set_start", "tsvd_block_lanczos",
+    "tsvd_set_krylov_dim", "tsvd_set_thick_restart", "tsvd_set_output_mode", "tsvd_trim_memory", "tsvd_set_qr_block", "tsvd_set_start", "tsvd_block_lanczos", "tsvd_block_lanczos_threshold",
     "tsvd_rsvd", "tsvd_get", "tsvd_get_info", "tsvd_get_rho", "tsvd_destroy",
     "tsvd_strerror", "tsvd_last_error", "tsvd_dbg_philox", "tsvd_dbg_philox_words",
     "tsvd_dbg_apply", "tsvd_dbg_cholqr2", "tsvd_dbg_cgs_cqr2", "tsvd_dbg_cgs_qr",
@@ -86,6 +86,7 @@ _SIGS = {
     "tsvd_set_start": [vp, vp, i64, i64, i64, i32],
     "tsvd_block_lanczos": [vp, i32, i32, dbl, i32],
     "tsvd_rsvd": [vp, i32, i32, i32],
+    "tsvd_block_lanczos_threshold": [vp, dbl, i32, dbl, i32, i32, C.POINTER(C.c_int)],
     "tsvd_get": [vp, vp, i64, vp, vp, i64, i32],
     "tsvd_get_info": [vp, C.POINTER(TsvdInfo)],
     "tsvd_get_rho": [vp, vp],
@@ -292,6 +293,19 @@ class TruncatedSVD:
                     "tsvd_block_lanczos", allow_warn=True)
         self.r = int(r)
         return st
+
+    def block_lanczos_threshold(self, tau: float, b: int, tol: float, maxit: int, r_max: int,
+                                d: int | None = None):
+        """Rank by threshold sigma_{r+1} <= tau sigma_1 (Eq. 3).
+        Returns (status, r)."""
+        if d is not None:
+            self.set_krylov_dim(d)
+        r = C.c_int(0)
+        st = _check(lib().tsvd_block_lanczos_threshold(self._h, float(tau), int(b), float(tol),
+                                                       int(maxit), int(r_max), C.byref(r)),
+                    "tsvd_block_lanczos_threshold", allow_warn=True)
+        self.r = int(r.value)
+        return st, self.r
 
     def rsvd(self, r: int, p: int, q: int) -> int:
         st = _check(lib().tsvd_rsvd(self._h, int(r), int(p), int(q)), "tsvd_rsvd")

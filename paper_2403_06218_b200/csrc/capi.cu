@@ -374,6 +374,14 @@ tsvd_status tsvd_block_lanczos(tsvd_t h, int r, int b, double tol, int maxit) {
   TSVD_API_END
 }
 
+tsvd_status tsvd_block_lanczos_threshold(tsvd_t h, double tau, int b, double tol, int maxit,
+                                         int r_max, int* r_out) {
+  if (!h) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  return lanczos_threshold(*h, tau, b, tol, maxit, r_max, r_out);
+  TSVD_API_END
+}
+
 tsvd_status tsvd_rsvd(tsvd_t h, int r, int p, int q) {
   if (!h) return TSVD_EINVAL;
   TSVD_API_BEGIN

@@ -116,4 +116,6 @@ void all_gather(Ctx& c, const double* send, double* recv, size_t send_count);
 // solvers (solvers.cu)
 tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit);
 tsvd_status rsvd_solve(Ctx& c, int r, int p, int q);
+tsvd_status lanczos_threshold(Ctx& c, double tau, int b, double tol, int maxit, int r_max,
+                              int* r_out);
 }  // namespace tsvd

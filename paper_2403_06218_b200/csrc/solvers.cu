@@ -302,6 +302,49 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   return conv ? TSVD_OK : TSVD_WARN_NOTCONV;
 }
 
+// SURVEY 8(f) N4 (Eq. 3): the rank is not known in advance but set
+// by a threshold on ||A - U_r S_r V_r^T||_2 = sigma_{r+1}.  Reading R33:
+// request r + 1 triplets (r = b first), take the smallest r with
+// sigma_{r+1} <= tau * sigma_1 whose triplets 1..r+1 all converged
+// (rho <= tol); otherwise double r (at most r_max) and solve again from a
+// fresh start.  The Krylov dimension is the user's (tsvd_set_krylov_dim) or
+// the default for the current request.  Driver-level only: every solve is
+// lanczos_solve on the same kernels.
+tsvd_status lanczos_threshold(Ctx& c, double tau, int b, double tol, int maxit, int r_max,
+                              int* r_out) {
+  if (!(tau > 0.0) || tau >= 1.0 || b < 1 || r_max < 1) return TSVD_EINVAL;
+  r_max = (int)std::min<int64_t>(r_max, c.ng - 1);
+  if (r_max < 1) return TSVD_ESHAPE;
+  int req = std::min(b, r_max);
+  std::vector<double> hs;
+  for (;;) {
+    const int want = req + 1;
+    const tsvd_status st = lanczos_solve(c, want, b, tol, maxit);
+    if (st < 0) return st;
+    hs.resize(want);
+    TSVD_CUDA(cudaMemcpyAsync(hs.data(), c.S, want * sizeof(double), cudaMemcpyDeviceToHost,
+                              c.st));
+    TSVD_CUDA(cudaStreamSynchronize(c.st));
+    int found = -1;
+    for (int r = 1; r < want && c.rho[r - 1] <= tol; ++r) {
+      if (c.rho[r] > tol) break;                      // sigma_{r+1} itself not converged
+      if (hs[r] <= tau * hs[0]) {
+        found = r;
+        break;
+      }
+    }
+    if (found > 0 || req >= r_max) {
+      const int r = found > 0 ? found : req;
+      c.r = r;                                          // tsvd_get: first r columns
+      c.info.r = r;
+      c.rho.resize(r);
+      if (r_out) *r_out = r;
+      return found > 0 ? TSVD_OK : TSVD_WARN_NOTCONV;
+    }
+    req = std::min(2 * req, r_max);
+  }
+}
+
 tsvd_status rsvd_solve(Ctx& c, int r, int p, int q) {
   const int64_t m = c.m, n = c.n;  // this rank's rows (single GPU: all)
   if (r < 1 || p < 0 || q < 0) return TSVD_EINVAL;

@@ -304,3 +304,37 @@ def test_output_mode_errors():
         for bad in (-1, 3):
             with pytest.raises(T.TsvdError):
                 h.set_output_mode(bad)
+
+
+# ---- N4: rank by threshold (Eq. 3), tsvd_block_lanczos_threshold ----------
+@pytest.mark.parametrize("tau,r_expect", [(1.5e-3, 10), (2e-3, 9)])
+def test_threshold_rank_parity(tau, r_expect):
+    A, s = _c1()
+    op = oracle.Operator(dense=A)
+    seed = SEEDS["C1"]
+    ro, r_o, found = oracle.lancsvd_threshold(op, tau=tau, b=4, tol=1e-12, maxit=8, r_max=40,
+                                              seed=seed)
+    with T.TruncatedSVD(A) as h:
+        h.set_seed(seed)
+        st, r = h.block_lanczos_threshold(tau, b=4, tol=1e-12, maxit=8, r_max=40)
+        Ug, Sg, Vg = h.get()
+        info = h.info()
+    assert found and st == T.TSVD_OK
+    assert r == r_o == r_expect and Ug.shape == (200, r) and info["r"] == r
+    _accept(op, Ug, Sg, Vg, ro.S)
+    assert np.abs(Sg - s[:r]).max() / s[0] <= 1e-10                 # closed form
+    ey = oracle.eckart_young_2norm(op, Ug, Sg, Vg)                   # Eq. 3
+    assert ey == pytest.approx(s[r], rel=1e-6) and ey <= tau * s[0]
+
+
+def test_threshold_rank_rmax_and_errors():
+    A, s = _c1()
+    with T.TruncatedSVD(A) as h:
+        h.set_seed(SEEDS["C1"])
+        st, r = h.block_lanczos_threshold(1e-6, b=4, tol=1e-12, maxit=8, r_max=6)
+        _, Sg, _ = h.get()
+        assert st == T.TSVD_WARN_NOTCONV and r == 6 and len(Sg) == 6
+        assert np.abs(Sg - s[:6]).max() / s[0] <= 1e-10
+        for bad in (0.0, -1.0, 1.0):
+            with pytest.raises(T.TsvdError):
+                h.block_lanczos_threshold(bad, b=4, tol=1e-12, maxit=8, r_max=6)

@@ -279,3 +279,34 @@ def test_thick_restart_slow_decay_closed_form():
     paper = oracle.lancsvd(op, r=4, b=4, d=16, tol=1e-10, maxit=60, seed=5)
     assert res.converged and res.cycles < paper.cycles
     assert np.abs(res.S - s[:4]).max() <= 1e-10 * s[0]
+
+
+# ---- N4: rank by threshold (Eq. 3), reading R33 ---------------------------
+def test_threshold_rank_closed_form():
+    """C1 (Eq. 16 set reading, n = 100): sigma_i = 10^(1 - 0.3 (i - 1)), so
+    with tau = 1.5e-3 the smallest r with sigma_{r+1} <= tau sigma_1 = 0.015
+    is r = 10 (sigma_10 = 0.01995 > 0.015 >= sigma_11 = 0.01): found after
+    the requests r = 4, 8, 16; sigma and Eckart-Young (Eq. 3) pinned by the
+    prescribed spectrum."""
+    op, s = _c1()
+    i = np.arange(1, 12)
+    assert np.allclose(s[:11], 10.0 ** (1 - 0.3 * (i - 1)), rtol=1e-14)
+    res, r, found = oracle.lancsvd_threshold(op, tau=1.5e-3, b=4, tol=1e-12, maxit=8,
+                                             r_max=40, seed=SEEDS["C1"])
+    assert found and r == 10
+    assert np.abs(res.S - s[:10]).max() / s[0] <= 1e-10
+    ey = oracle.eckart_young_2norm(op, res.U, res.S, res.V)
+    assert ey == pytest.approx(s[10], rel=1e-6)
+    assert ey <= 1.5e-3 * s[0]
+    # one step coarser threshold: sigma_10 <= 0.02 -> r = 9
+    _, r2, found2 = oracle.lancsvd_threshold(op, tau=2e-3, b=4, tol=1e-12, maxit=8, r_max=40,
+                                             seed=SEEDS["C1"])
+    assert found2 and r2 == 9
+
+
+def test_threshold_rank_not_found_by_rmax():
+    op, s = _c1()
+    res, r, found = oracle.lancsvd_threshold(op, tau=1e-6, b=4, tol=1e-12, maxit=8, r_max=6,
+                                             seed=SEEDS["C1"])
+    assert not found and r == 6 and len(res.S) == 6
+    assert np.abs(res.S - s[:6]).max() / s[0] <= 1e-10
