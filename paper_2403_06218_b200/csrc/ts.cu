@@ -939,11 +939,12 @@ __global__ void __launch_bounds__(288, NYB == 1 ? 2 : 1) gemm_nn_tma_kernel(
   // takes K chunks [nk_all y / Y, nk_all (y+1) / Y) and writes its partial
   // product to Z + y zsplit; the caller sums the partials in a fixed order.
   using CF = NnTmaCfg<KC, S, NYB>;
-  constexpr int WP = CF::WP, NT = 2 * NYB, OP = CF::OP, TP = CF::TP, NPAIR = NT * NT;
-  // Gram: NPAIR 8x8 output tiles over 8 warps (KSPLIT warps share a tile and
-  // split its rows when NPAIR < 8; PPW tiles per warp when NPAIR > 8)
-  constexpr int KSPLIT = NPAIR >= 8 ? 1 : 8 / NPAIR, PPW = NPAIR >= 8 ? NPAIR / 8 : 1;
-  constexpr int KSTEPS = NT_R / 4 / KSPLIT;
+  constexpr int WP = CF::WP, NT = 2 * NYB, OP = CF::OP, TP = CF::TP;
+  // Gram: each warp accumulates W = Z^T Z over ITS OWN 16 rows of every tile
+  // for the NGP upper-triangular 8 x 8 tile pairs (mi <= ni; W is symmetric),
+  // so the tile epilogue needs no CTA barrier: Z is stored from the
+  // fragments and a warp's out-tile rows are read back only by that warp
+  constexpr int NGP = NT * (NT + 1) / 2;
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
   const double* Ys = (const double*)(sm + CF::y_off);
@@ -1007,9 +1008,11 @@ __global__ void __launch_bounds__(288, NYB == 1 ? 2 : 1) gemm_nn_tma_kernel(
     }
     return;
   }
-  double g[PPW][2][2];
+  double gw[NGP][2];
 #pragma unroll
-  for (int p = 0; p < PPW; ++p) g[p][0][0] = g[p][0][1] = g[p][1][0] = g[p][1][1] = 0.0;
+  for (int p = 0; p < NGP; ++p) gw[p][0] = gw[p][1] = 0.0;
+  const bool zal = Z && ((((uintptr_t)Z) | (uintptr_t)(ldz * 8)) & 15) == 0;
+  double* Ow = Os + warp * 16 * OP;  // this warp's rows of the out tile
   double acc[2][2][NT][2];
   for (int64_t j = 0; j < nsteps; ++j) {
     const int st = (int)(j % S);
@@ -1102,61 +1105,79 @@ __global__ void __launch_bounds__(288, NYB == 1 ? 2 : 1) gemm_nn_tma_kernel(
         __syncwarp();
         if (lane == 0) mbar_arrive(yempty);
       }
+      // warp-private epilogue (no CTA barrier): Z rows of this warp stored
+      // straight from the fragments (16-byte pieces of 64-byte row segments),
+      // and the warp's Gram contribution from its own rows of the out tile
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < NT; ++ni)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int r = warp * 16 + mi * 8 + prow, c = ni * 8 + 2 * tig + e;
-            const double z = alpha * (acc[0][mi][ni][e] + acc[1][mi][ni][e]) + beta * yt[mi][ni][e];
-            Os[r * OP + c] = (c < w && r0 + r < q) ? z : 0.0;
+        for (int ni = 0; ni < NT; ++ni) {
+          const int rl = mi * 8 + prow, c = ni * 8 + 2 * tig;
+          const int64_t row = r0 + warp * 16 + rl;
+          const bool rv = row < q;
+          double z0 = alpha * (acc[0][mi][ni][0] + acc[1][mi][ni][0]) + beta * yt[mi][ni][0];
+          double z1 = alpha * (acc[0][mi][ni][1] + acc[1][mi][ni][1]) + beta * yt[mi][ni][1];
+          z0 = (c < w && rv) ? z0 : 0.0;
+          z1 = (c + 1 < w && rv) ? z1 : 0.0;
+          if (gram) {
+            Ow[rl * OP + c] = z0;
+            Ow[rl * OP + c + 1] = z1;
           }
+          if (Z && rv) {
+            double* zp = Z + row * ldz + c;
+            if (zal && c + 1 < w) {
+              *reinterpret_cast<double2*>(zp) = make_double2(z0, z1);
+            } else {
+              if (c < w) zp[0] = z0;
+              if (c + 1 < w) zp[1] = z1;
+            }
+          }
+        }
       if (use_y && !T) {
         __syncwarp();
         if (lane == 0) mbar_arrive(yempty);
       }
-      bar_consumers();
-      if (Z) {
-        for (int idx = tid; idx < NT_R * WP; idx += 256) {
-          const int r = idx / WP, c = idx % WP;
-          const int64_t row = r0 + r;
-          if (row < q && c < w) Z[row * ldz + c] = Os[r * OP + c];
-        }
-      }
       if (gram) {
+        __syncwarp();
 #pragma unroll
-        for (int p = 0; p < PPW; ++p) {
-          const int pair = (KSPLIT > 1) ? (warp % NPAIR) : (warp + 8 * p);
-          const int k0 = (KSPLIT > 1) ? (warp / NPAIR) * KSTEPS : 0;
-          const int mi = pair / NT, ni = pair % NT;
-#pragma unroll 8
-          for (int kk = 0; kk < KSTEPS; ++kk) {
-            const int kr = (k0 + kk) * 4 + tig;
-            const double a = Os[kr * OP + mi * 8 + gid];
-            const double b = Os[kr * OP + ni * 8 + gid];
-            dmma884(g[p][kk & 1][0], g[p][kk & 1][1], a, b);
-          }
-        }
+        for (int mi = 0, p = 0; mi < NT; ++mi)
+#pragma unroll
+          for (int ni = mi; ni < NT; ++ni, ++p)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const int kr = kk * 4 + tig;
+              dmma884(gw[p][0], gw[p][1], Ow[kr * OP + mi * 8 + gid], Ow[kr * OP + ni * 8 + gid]);
+            }
+        __syncwarp();  // the next tile overwrites Ow
       }
-      bar_consumers();
     }
   }
   if (gram) {
-    double* red = Os;  // free now: every consumer passed the last barrier
-    // 8 warps x PPW tiles x 64 values; tile (pair) of KSPLIT group k at slot k*NPAIR+pair
-#pragma unroll
-    for (int p = 0; p < PPW; ++p)
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-        red[(warp + 8 * p) * 64 + gid * 8 + 2 * tig + e] = g[p][0][e] + g[p][1][e];
+    // the TMA ring is idle now (every stage consumed): 8 warps x NGP x 64
+    // partials there, summed over the warps in a fixed order and mirrored
+    double* red = (double*)sm;
     bar_consumers();
-    for (int idx = tid; idx < NPAIR * 64; idx += 256) {
-      const int pair = idx / 64, ii = (idx % 64) / 8, jj = idx % 8;
+#pragma unroll
+    for (int p = 0; p < NGP; ++p)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) red[(warp * NGP + p) * 64 + gid * 8 + 2 * tig + e] = gw[p][e];
+    bar_consumers();
+    for (int idx = tid; idx < NGP * 64; idx += 256) {
+      const int p = idx / 64, ii = (idx % 64) / 8, jj = idx % 8;
+      int mi = 0, base = 0;
+      while (p >= base + (NT - mi)) {
+        base += NT - mi;
+        ++mi;
+      }
+      const int ni = mi + (p - base);
       double sum = 0.0;
-      for (int k = 0; k < KSPLIT; ++k) sum += red[(k * NPAIR + pair) * 64 + ii * 8 + jj];
-      const int i = (pair / NT) * 8 + ii, jc = (pair % NT) * 8 + jj;
-      if (i < w && jc < w) gram[(int64_t)blockIdx.x * w * w + i * w + jc] = sum;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum += red[(k * NGP + p) * 64 + ii * 8 + jj];
+      const int i = mi * 8 + ii, jc = ni * 8 + jj;
+      if (i < w && jc < w) {
+        gram[(int64_t)blockIdx.x * w * w + i * w + jc] = sum;
+        gram[(int64_t)blockIdx.x * w * w + jc * w + i] = sum;
+      }
     }
   }
 }
