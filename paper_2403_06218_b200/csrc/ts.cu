@@ -791,7 +791,9 @@ __global__ void __launch_bounds__(256) rowT_kernel(const double* Y, int64_t ldy,
                                                    const double* __restrict__ T, double* Z,
                                                    int64_t ldz, int64_t q, int w, double beta,
                                                    double* __restrict__ gram) {
-  constexpr int NT = WP / 8, KY = WP / 4, NPAIR = NT * NT, ZP = WP + 4;
+  // Gram: only the NPAIR upper-triangular 8 x 8 tile pairs (mi <= ni) are
+  // accumulated (W is symmetric; mirrored when written)
+  constexpr int NT = WP / 8, KY = WP / 4, NPAIR = NT * (NT + 1) / 2, ZP = WP + 4;
   constexpr int GCH = NPAIR < 4 ? NPAIR : 4;  // Gram tiles reduced per chunk (static smem)
   __shared__ double zs[8][8 * ZP];
   __shared__ double gred[8][GCH * 64];
@@ -864,12 +866,12 @@ __global__ void __launch_bounds__(256) rowT_kernel(const double* Y, int64_t ldy,
 #pragma unroll
       for (int k2 = 0; k2 < 2; ++k2)
 #pragma unroll
-        for (int mi = 0; mi < NT; ++mi) {
+        for (int mi = 0, p = 0; mi < NT; ++mi) {
           const double a = zw[(k2 * 4 + tig) * ZP + mi * 8 + gid];
 #pragma unroll
-          for (int ni = 0; ni < NT; ++ni) {
+          for (int ni = mi; ni < NT; ++ni, ++p) {
             const double b = zw[(k2 * 4 + tig) * ZP + ni * 8 + gid];
-            dmma884(g[mi * NT + ni][0], g[mi * NT + ni][1], a, b);
+            dmma884(g[p][0], g[p][1], a, b);
           }
         }
       __syncwarp();
@@ -883,15 +885,26 @@ __global__ void __launch_bounds__(256) rowT_kernel(const double* Y, int64_t ldy,
 #pragma unroll
       for (int p = 0; p < GCH; ++p)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) gred[warp][p * 64 + gid * 8 + 2 * tig + e] = g[p0 + p][e];
+        for (int e = 0; e < 2; ++e)
+          if (p0 + p < NPAIR) gred[warp][p * 64 + gid * 8 + 2 * tig + e] = g[p0 + p][e];
       __syncthreads();
       for (int idx = tid; idx < GCH * 64; idx += 256) {
+        const int p = p0 + idx / 64, ii = (idx % 64) / 8, jj = idx % 8;
+        if (p >= NPAIR) break;
         double sum = 0.0;
 #pragma unroll
         for (int k = 0; k < 8; ++k) sum += gred[k][idx];
-        const int p = p0 + idx / 64, ii = (idx % 64) / 8, jj = idx % 8;
-        const int i = (p / NT) * 8 + ii, j = (p % NT) * 8 + jj;
-        if (i < w && j < w) gram[(int64_t)blockIdx.x * w * w + i * w + j] = sum;
+        int mi = 0, base = 0;
+        while (p >= base + (NT - mi)) {
+          base += NT - mi;
+          ++mi;
+        }
+        const int ni = mi + (p - base);
+        const int i = mi * 8 + ii, j = ni * 8 + jj;
+        if (i < w && j < w) {
+          gram[(int64_t)blockIdx.x * w * w + i * w + j] = sum;
+          gram[(int64_t)blockIdx.x * w * w + j * w + i] = sum;
+        }
       }
     }
   }
