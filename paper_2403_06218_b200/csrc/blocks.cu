@@ -403,7 +403,7 @@ static void apply_local(Ctx& c, bool trans, const double* X, int64_t ldx, double
   } else {
     const Csr& A = trans ? c.AT : c.A;
     double* part = dbuf(c, trans ? "spmm_part_t" : "spmm_part",
-                        (size_t)std::max<int64_t>(1, A.nslots) * 32);
+                        (size_t)std::max<int64_t>(1, A.nslots) * 64);
     launch_spmm_wide(A, X, ldx, Y, ldy, w, part, c.st);
   }
 }

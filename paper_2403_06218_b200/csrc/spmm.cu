@@ -23,6 +23,7 @@ namespace tsvd {
 constexpr int kLongRow = 64;   // rows up to this length: sub-warp groups (sorted)
 constexpr int kMedRow = 512;   // rows up to this length: one warp each (sorted)
 constexpr int kSeg = 2048;     // longer rows: CTA segments of this many nonzeros
+constexpr int kPartW = 64;     // columns per partial slot of a split long row (w <= 64)
 
 template <int VEC>
 __device__ __forceinline__ void ldx_vec(const double* p, double (&x)[VEC]) {
@@ -217,7 +218,7 @@ __device__ __forceinline__ void spmm_long_dev(
     if (slot < 0)
       Y[seg_row[s] * ldy + threadIdx.x] = sum;
     else
-      part[(int64_t)slot * 32 + threadIdx.x] = sum;
+      part[(int64_t)slot * kPartW + threadIdx.x] = sum;
   }
 }
 
@@ -248,12 +249,12 @@ __global__ void spmm_fixup_kernel(const int64_t* __restrict__ split_row,
                                   const double* __restrict__ part, double* __restrict__ Y,
                                   int64_t ldy, int w, int64_t nsplit) {
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t r = t / 32;
-  const int c = (int)(t % 32);
+  const int64_t r = t / kPartW;
+  const int c = (int)(t % kPartW);
   if (r >= nsplit || c >= w) return;
   const int first = split_first[r], cnt = split_count[r];
   double sum = 0.0;
-  for (int j = 0; j < cnt; ++j) sum += part[(int64_t)(first + j) * 32 + c];
+  for (int j = 0; j < cnt; ++j) sum += part[(int64_t)(first + j) * kPartW + c];
   Y[split_row[r] * ldy + c] = sum;
 }
 
@@ -272,7 +273,7 @@ static void spmm_dispatch(const Csr& A, const double* X, int64_t ldx, double* Y,
     TSVD_CHECK_LAUNCH();
   }
   if (A.nsplit > 0) {
-    const int64_t thr = A.nsplit * 32;
+    const int64_t thr = A.nsplit * kPartW;
     spmm_fixup_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(
         A.split_row, A.split_first, A.split_count, part, Y, ldy, w, A.nsplit);
     TSVD_CHECK_LAUNCH();
@@ -292,9 +293,12 @@ void launch_spmm(const Csr& A, const double* X, int64_t ldx, double* Y, int64_t 
       spmm_dispatch<4, 2>(A, X, ldx, Y, ldy, w, part, st);
     else if (w <= 16)
       spmm_dispatch<8, 2>(A, X, ldx, Y, ldy, w, part, st);
-    else
+    else if (w <= 32)
       spmm_dispatch<16, 2>(A, X, ldx, Y, ldy, w, part, st);
+    else  // 32 < w <= 64 (wide RandSVD blocks): a whole warp per short row
+      spmm_dispatch<32, 2>(A, X, ldx, Y, ldy, w, part, st);
   } else {
+    if (w > 32) throw Error{TSVD_EINVAL, "launch_spmm: w > 32 needs 16-byte aligned operands"};
     if (w <= 4)
       spmm_dispatch<4, 1>(A, X, ldx, Y, ldy, w, part, st);
     else if (w <= 8)
@@ -308,8 +312,13 @@ void launch_spmm(const Csr& A, const double* X, int64_t ldx, double* Y, int64_t 
 
 void launch_spmm_wide(const Csr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
                       int w, double* part, cudaStream_t st) {
-  for (int c0 = 0; c0 < w; c0 += 32) {
-    const int wc = w - c0 < 32 ? w - c0 : 32;
+  // 64-column launches when the double2 path applies (A is read once per 64
+  // columns of X instead of once per 32), else 32
+  const bool v2 = (ldx % 2 == 0) && (ldy % 2 == 0) && ((uintptr_t)X % 16 == 0) &&
+                  ((uintptr_t)Y % 16 == 0);
+  const int cw = v2 ? 64 : 32;
+  for (int c0 = 0; c0 < w; c0 += cw) {
+    const int wc = w - c0 < cw ? w - c0 : cw;
     launch_spmm(A, X + c0, ldx, Y + c0, ldy, wc, part, st);
   }
 }
