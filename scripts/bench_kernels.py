@@ -149,7 +149,7 @@ def spmm_bench():
             ms = timeit(lambda: T.dbg_apply(h, tr, X, Y))
             rows, cols = (n, m) if tr else (m, n)
             gb = (12.0 * nnz + 8 * (rows + 1) + 8.0 * w * (rows + cols)) / (ms * 1e-3) / 1e9
-            print(f"spmm {cfgn} w={w} trans={tr} slice={os.environ.get('TSVD_SPMM_SLICE', '0')}: "
+            print(f"spmm {cfgn} w={w} trans={tr}: "
                   f"{ms:.3f} ms  {gb:.0f} GB/s compulsory ({gb / HBM:.2f} of HBM)", flush=True)
         h.close()
         del Pb, P
