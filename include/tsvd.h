@@ -49,6 +49,9 @@ enum {
   TSVD_WARN_NOTCONV = 1, /* maxit reached before max_{i<=r} rho_i <= tol*sigma_1 */
   TSVD_WARN_FALLBACK = 2, /* tsvd_dbg_cholqr2 / _cgs_cqr2 only: the Cholesky breakdown
                              test fired and the CGS2 fallback gave the result */
+  TSVD_WARN_SVD = 3,     /* the device Jacobi SVD of B_k / R_p (reading R20) hit its
+                            sweep cap (30) before every column pair passed the
+                            rotation test; results retrievable, tsvd_info counts it */
   TSVD_EINVAL = -1,      /* bad argument (NULL, non-canonical CSR, tol <= 0 ...) */
   TSVD_ESHAPE = -2,      /* m < n, r > n, d % b != 0, r > d, r + p > n ...     */
   TSVD_ENOMEM = -3,      /* device allocation failed                            */
@@ -62,12 +65,15 @@ enum { TSVD_ROW_MAJOR = 0, TSVD_COL_MAJOR = 1 };
 
 /* ---- creation ----------------------------------------------------------
  * tsvd_create_csr: A as CSR.  rowptr[m+1] (rowptr[0] = 0,
- * non-decreasing, rowptr[m] = nnz), colidx[nnz] in [0, n) strictly increasing
- * within each row (canonical: sorted, no duplicates), vals[nnz].  The library
- * builds CSR(A^T) on the device (counting sort by column, stable) so that
- * A^T.X needs no atomics (north_star; P:460 discusses the transposed product).
+ * non-decreasing, rowptr[m] = nnz), colidx[nnz] in [0, n), vals[nnz].  The
+ * columns of a row may be unsorted and may repeat: the library's copy is
+ * canonicalised on the device (columns sorted within each row, duplicate
+ * entries summed in their input order).  The library builds
+ * CSR(A^T) on the device (radix sort by column, stable) so that A^T.X needs
+ * no atomics (north_star; P:460 discusses the transposed product).
  * Returns TSVD_ESHAPE if m < n ("otherwise target the transpose"),
- * TSVD_EINVAL if the CSR is not canonical. */
+ * TSVD_EINVAL if the row pointer is malformed or a column index is out of
+ * range. */
 tsvd_status tsvd_create_csr(tsvd_t* h, int64_t m, int64_t n, int64_t nnz,
                             const int64_t* rowptr, const int32_t* colidx,
                             const double* vals, int mem_kind);
@@ -118,8 +124,9 @@ tsvd_status tsvd_set_stream(tsvd_t h, void* cuda_stream);
  * replacement columns (draws 1, 2, ...).  P:406, reading R9. */
 tsvd_status tsvd_set_seed(tsvd_t h, uint64_t seed);
 /* Krylov dimension d of LancSVD (the paper's "r"); must be a
- * multiple of b with r <= d <= n.  0 => default min(n, max(4r, 2b)) rounded
- * down to a multiple of b. */
+ * multiple of b with r <= d <= n and d <= 1536 (the largest B_k the device
+ * Jacobi SVD takes; checked when the solve starts: TSVD_ESHAPE).  0 =>
+ * default min(n, max(4r, 2b), 1536) rounded down to a multiple of b. */
 tsvd_status tsvd_set_krylov_dim(tsvd_t h, int d);
 /* Restart of LancSVD.  keep = 0 (default): the paper's restart, Alg. 2 S7
  * (P:200-203): the next cycle starts from the first b left Ritz vectors.
@@ -140,6 +147,19 @@ tsvd_status tsvd_set_thick_restart(tsvd_t h, int keep);
  * returns reserved-but-unused pool memory above keep_bytes to the system.
  * Returns TSVD_ECUDA without a usable device. */
 tsvd_status tsvd_trim_memory(size_t keep_bytes);
+/* Device memory from the caller instead (e.g. PyTorch's caching
+ * allocator).  Process-wide: every later library allocation (create, solver
+ * workspaces) calls alloc(bytes, stream, ctx) with the handle's cudaStream_t
+ * and must get device memory usable in stream order on that stream, or NULL
+ * (=> TSVD_ENOMEM); such blocks are returned with free_(ptr, stream, ctx)
+ * (stream-ordered: work already enqueued on `stream` may still use the block
+ * until it completes).  Blocks obtained before a change go back to the
+ * allocator that produced them.  alloc = NULL restores the default pool.
+ * Both callbacks must be thread-safe if handles are used from several threads;
+ * they are never called with a lock of the library held. */
+typedef void* (*tsvd_alloc_fn)(size_t bytes, void* stream, void* ctx);
+typedef void (*tsvd_free_fn)(void* ptr, void* stream, void* ctx);
+tsvd_status tsvd_set_allocator(tsvd_alloc_fn alloc, tsvd_free_fn free_, void* ctx);
 /* Where the outputs U_r = Pbar_k Ubar[:, :r], V_r = P_k Vbar[:, :r] (Eq. 12;
  * RandSVD Alg. 1 S6/S7) are formed.  TSVD_OUT_AUTO (default): in separate
  * result buffers when (m + n) r doubles fit in the free device memory, else
@@ -182,7 +202,9 @@ tsvd_status tsvd_block_lanczos_threshold(tsvd_t h, double tau, int b, double tol
                                          int r_max, int* r_out);
 /* tsvd_rsvd: Alg. 1 with l = r + p columns (p = oversampling) and q power
  * iterations, i.e. q + 1 passes of S1-S4 (paper p = q + 1, reading R6); QR by
- * CGS-QR (Alg. 3) with panels of b_qr columns. */
+ * CGS-QR (Alg. 3) with panels of b_qr columns.  l <= min(n, 1536) (the
+ * l x l R_p goes through the device Jacobi SVD), else TSVD_ESHAPE before any
+ * work is done. */
 tsvd_status tsvd_rsvd(tsvd_t h, int r, int p, int q);
 
 /* ---- results ------------------------------------------------------------
@@ -204,6 +226,8 @@ typedef struct {
   int64_t launches; /* kernels launched by the last solve                 */
   int replaced;     /* dependent columns the fallback replaced by Philox
                        draws (reading R16)                                */
+  int svd_sweeps;   /* largest Jacobi sweep count of the solve's SVDs     */
+  int svd_unconverged; /* SVDs that hit the sweep cap (=> TSVD_WARN_SVD)  */
 } tsvd_info;
 tsvd_status tsvd_get_info(tsvd_t h, tsvd_info* out);
 /* rho_i / sigma_1 for i < r of the last LancSVD cycle (host buffer). */

@@ -116,9 +116,10 @@ def lancsvd(op, r: int, b: int, d: int, tol: float, maxit: int, seed: int,
 
 
 def default_krylov_dim(r: int, b: int, n: int) -> int:
-    """d when none is given: min(n, max(4 r, 2 b)) rounded down to a multiple
-    of b (include/tsvd.h, tsvd_set_krylov_dim)."""
-    d = min(max(4 * r, 2 * b), n)
+    """d when none is given: min(n, max(4 r, 2 b), 1536) rounded down to a
+    multiple of b (include/tsvd.h, tsvd_set_krylov_dim; 1536 = the largest
+    B_k the library's device SVD takes)."""
+    d = min(max(4 * r, 2 * b), n, 1536)
     return d - d % b
 
 

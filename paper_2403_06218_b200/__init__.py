@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # TSVD_LIB: an alternative build of the same library (development A/B runs)
 LIB_PATH = os.environ.get("TSVD_LIB") or os.path.join(_HERE, "libtsvd.so")
 
-TSVD_OK, TSVD_WARN_NOTCONV, TSVD_WARN_FALLBACK = 0, 1, 2
+TSVD_OK, TSVD_WARN_NOTCONV, TSVD_WARN_FALLBACK, TSVD_WARN_SVD = 0, 1, 2, 3
 TSVD_EINVAL, TSVD_ESHAPE, TSVD_ENOMEM, TSVD_ECUDA, TSVD_ENCCL, TSVD_ESTATE = -1, -2, -3, -4, -5, -6
 TSVD_HOST, TSVD_DEVICE = 0, 1
 TSVD_ROW_MAJOR, TSVD_COL_MAJOR = 0, 1
@@ -37,7 +37,7 @@ EXPORTS = [
     "tsvd_dbg_small_svd", "tsvd_dbg_gemm_tn", "tsvd_dbg_gemm_nn",
     "tsvd_set_profiling", "tsvd_get_profile", "tsvd_reset_profile",
     "tsvd_create_csr_dist", "tsvd_create_dense_dist", "tsvd_nccl_unique_id",
-    "tsvd_partition_rows",
+    "tsvd_partition_rows", "tsvd_set_allocator",
 ]
 
 
@@ -45,7 +45,7 @@ class TsvdInfo(C.Structure):
     _fields_ = [("cycles", C.c_int), ("nconv", C.c_int), ("r", C.c_int), ("d", C.c_int),
                 ("b", C.c_int), ("breakdowns", C.c_int), ("rho_max", C.c_double),
                 ("sigma1", C.c_double), ("ms_total", C.c_double), ("launches", C.c_int64),
-                ("replaced", C.c_int)]
+                ("replaced", C.c_int), ("svd_sweeps", C.c_int), ("svd_unconverged", C.c_int)]
 
 
 class TsvdDist(C.Structure):
@@ -107,6 +107,7 @@ _SIGS = {
     "tsvd_create_dense_dist": [C.POINTER(vp), C.POINTER(TsvdDist), vp, i64, i32],
     "tsvd_nccl_unique_id": [vp],
     "tsvd_partition_rows": [vp, i64, i32, vp],
+    "tsvd_set_allocator": [vp, vp, vp],
 }
 
 
@@ -308,7 +309,8 @@ class TruncatedSVD:
         return st, self.r
 
     def rsvd(self, r: int, p: int, q: int) -> int:
-        st = _check(lib().tsvd_rsvd(self._h, int(r), int(p), int(q)), "tsvd_rsvd")
+        st = _check(lib().tsvd_rsvd(self._h, int(r), int(p), int(q)), "tsvd_rsvd",
+                    allow_warn=True)
         self.r = int(r)
         return st
 
@@ -384,6 +386,36 @@ class TruncatedSVD:
         self.close()
 
 
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+_ALLOC_KEEP = []  # every thunk ever registered (blocks may outlive a re-registration)
+
+
+def use_torch_allocator(on: bool = True):
+    """Back every later library allocation with PyTorch's caching allocator
+    (tsvd_set_allocator, process-wide), on the handle's stream; on=False
+    restores the library's default stream-ordered pool."""
+    if not on:
+        _check(lib().tsvd_set_allocator(None, None, None), "tsvd_set_allocator")
+        return
+    import torch
+
+    def _alloc(nbytes, stream, ctx):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), torch.cuda.current_device(),
+                                                      int(stream or 0))
+        except Exception:  # out of memory -> NULL -> TSVD_ENOMEM
+            return None
+
+    def _free(ptr, stream, ctx):
+        torch.cuda.caching_allocator_delete(int(ptr))
+
+    cbs = (_ALLOC_FN(_alloc), _FREE_FN(_free))
+    _check(lib().tsvd_set_allocator(C.cast(cbs[0], vp), C.cast(cbs[1], vp), None),
+           "tsvd_set_allocator")
+    _ALLOC_KEEP.append(cbs)  # the C side keeps raw pointers to these thunks
+
+
 def trim_memory(keep_bytes: int = 0):
     """Return the library's reserved-but-unused device pool memory (tsvd_trim_memory)."""
     _check(lib().tsvd_trim_memory(int(keep_bytes)), "tsvd_trim_memory")
@@ -453,11 +485,12 @@ def dbg_cgs_qr(Y, bq: int, R, seed: int = 0, stream=None):
 
 
 def dbg_small_svd(B, Ub, S, Vb, stream=None) -> int:
-    """Returns the number of Jacobi sweeps used."""
+    """Returns the number of Jacobi sweeps used (== the cap, 30, with status
+    TSVD_WARN_SVD when the rotation test did not pass)."""
     d = B.shape[0]
     sw = C.c_int(0)
     _check(lib().tsvd_dbg_small_svd(_dp(B), d, _dp(Ub), _dp(S), _dp(Vb), C.byref(sw),
-                                    _stream_ptr(stream)), "tsvd_dbg_small_svd")
+                                    _stream_ptr(stream)), "tsvd_dbg_small_svd", allow_warn=True)
     return sw.value
 
 

@@ -15,6 +15,9 @@
 // Y itself is only overwritten by pass 5, after the host has seen both
 // breakdown flags, so the CGS2 fallback always restarts from the original Y
 // exactly as in the oracle (one stream sync per orthogonalisation).
+#include <mutex>
+#include <unordered_map>
+
 #include "ctx.h"
 
 namespace tsvd {
@@ -32,7 +35,37 @@ static void pool_init() {
   done = true;
 }
 
+// Caller-registered allocator (tsvd_set_allocator), process-wide.  Blocks it
+// returned are remembered so that they go back to it (and blocks from the
+// default pool back to the pool) whatever is registered when they are freed.
+static std::mutex g_alloc_mu;
+static tsvd_alloc_fn g_alloc = nullptr;
+static tsvd_free_fn g_free = nullptr;
+static void* g_alloc_ctx = nullptr;
+static std::unordered_map<void*, std::pair<tsvd_free_fn, void*>> g_user_blocks;
+
+void set_allocator(tsvd_alloc_fn a, tsvd_free_fn f, void* ctx) {
+  std::lock_guard<std::mutex> lk(g_alloc_mu);
+  g_alloc = a;
+  g_free = f;
+  g_alloc_ctx = ctx;
+}
+
 void* dmalloc(size_t bytes, cudaStream_t st) {
+  {
+    std::unique_lock<std::mutex> lk(g_alloc_mu);
+    if (g_alloc) {
+      tsvd_alloc_fn a = g_alloc;
+      tsvd_free_fn f = g_free;
+      void* ctx = g_alloc_ctx;
+      lk.unlock();
+      void* p = a(bytes ? bytes : 8, (void*)st, ctx);
+      if (!p) throw Error{TSVD_ENOMEM, "registered allocator returned NULL"};
+      lk.lock();
+      g_user_blocks[p] = {f, ctx};
+      return p;
+    }
+  }
   pool_init();
   void* p = nullptr;
   cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 8, st);
@@ -54,7 +87,19 @@ void* dmalloc(size_t bytes, cudaStream_t st) {
 }
 
 void dfree(void* p, cudaStream_t st) {
-  if (p) cudaFreeAsync(p, st);
+  if (!p) return;
+  {
+    std::unique_lock<std::mutex> lk(g_alloc_mu);
+    auto it = g_user_blocks.find(p);
+    if (it != g_user_blocks.end()) {
+      auto fc = it->second;
+      g_user_blocks.erase(it);
+      lk.unlock();
+      fc.first(p, (void*)st, fc.second);
+      return;
+    }
+  }
+  cudaFreeAsync(p, st);
 }
 
 void* buf(Ctx& c, const std::string& name, size_t bytes) {

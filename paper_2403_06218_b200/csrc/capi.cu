@@ -35,7 +35,7 @@ static tsvd_status init_ctx(tsvd_ctx* c) {
   TSVD_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
   c->own_stream = true;
   TSVD_CUDA(cudaMalloc(&c->dflags, 4 * sizeof(int)));
-  TSVD_CUDA(cudaMallocHost(&c->hflags, 4 * sizeof(int)));
+  TSVD_CUDA(cudaMallocHost(&c->hflags, 8 * sizeof(int)));
   return TSVD_OK;
 }
 
@@ -61,6 +61,7 @@ const char* tsvd_strerror(tsvd_status s) {
     case TSVD_OK: return "ok";
     case TSVD_WARN_NOTCONV: return "not converged within maxit (results retrievable)";
     case TSVD_WARN_FALLBACK: return "Cholesky breakdown: CGS2 fallback used (P:275)";
+    case TSVD_WARN_SVD: return "device Jacobi SVD hit its sweep cap (results retrievable)";
     case TSVD_EINVAL: return "invalid argument";
     case TSVD_ESHAPE: return "invalid shape";
     case TSVD_ENOMEM: return "device out of memory";
@@ -103,7 +104,12 @@ static tsvd_status setup_csr(tsvd_ctx* c, int64_t nnz, const int64_t* rowptr,
     TSVD_CUDA(cudaMemcpyAsync(A.vals, vals, nnz * sizeof(double), kind, c->st));
   }
   TSVD_CUDA(cudaStreamSynchronize(c->st));
-  if (csr_validate_device(A, c->st) != 0) return TSVD_EINVAL;  // warp per row, exact
+  const int bad = csr_validate_device(A, c->st);  // warp per row, exact
+  if (bad & ~2) return TSVD_EINVAL;               // bounds / out-of-range columns
+  if (bad & 2) {                                  // unsorted or duplicates: canonicalise
+    csr_canonicalize(A, c->st);
+    TSVD_CUDA(cudaMemcpy(hrp.data(), A.rowptr, (m + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  }
   csr_transpose(A, c->AT, c->st);
   csr_build_plan(A, hrp.data(), c->st);
   std::vector<int64_t> hrpt(n + 1);
@@ -328,6 +334,12 @@ tsvd_status tsvd_trim_memory(size_t keep_bytes) {
   return TSVD_OK;
 }
 
+tsvd_status tsvd_set_allocator(tsvd_alloc_fn alloc, tsvd_free_fn free_, void* ctx) {
+  if ((alloc == nullptr) != (free_ == nullptr)) return TSVD_EINVAL;
+  set_allocator(alloc, free_, ctx);
+  return TSVD_OK;
+}
+
 tsvd_status tsvd_set_thick_restart(tsvd_t h, int keep) {
   if (!h || keep < 0) return TSVD_EINVAL;
   h->thick_keep = keep;
@@ -465,7 +477,7 @@ static tsvd_ctx* dbg_ctx(void* stream) {
   if (!c) {
     c = new tsvd_ctx();
     TSVD_CUDA(cudaMalloc(&c->dflags, 4 * sizeof(int)));
-    TSVD_CUDA(cudaMallocHost(&c->hflags, 4 * sizeof(int)));
+    TSVD_CUDA(cudaMallocHost(&c->hflags, 8 * sizeof(int)));
   }
   c->st = (cudaStream_t)stream;
   c->own_stream = false;
@@ -550,8 +562,9 @@ tsvd_status tsvd_dbg_small_svd(const double* B, int d, double* Ub, double* S, do
   double* work = dbuf(*c, "jacobi_work", small_svd_work(d));
   small_svd(B, d, Ub, S, Vb, work, c->st);
   TSVD_CUDA(cudaStreamSynchronize(c->st));
-  if (sweeps) *sweeps = small_svd_sweeps(work, d);
-  return TSVD_OK;
+  const int sw = small_svd_sweeps(work, d);
+  if (sweeps) *sweeps = sw;
+  return sw >= small_svd_max_sweeps() ? TSVD_WARN_SVD : TSVD_OK;
   TSVD_API_END
 }
 

@@ -52,7 +52,7 @@ struct tsvd_ctx {
   bool deferred = false;
   int* flag_log = nullptr;
   int flag_slot = 0;
-  int* hflags = nullptr;      // pinned host mirror
+  int* hflags = nullptr;      // pinned host mirror (8 ints: [0,4) flags, [4] SVD sweeps)
   // results of the last solve
   double *U = nullptr, *S = nullptr, *V = nullptr;
   int64_t ldU = 0, ldV = 0;   // row pitch of U / V (r, or the basis ld in place)

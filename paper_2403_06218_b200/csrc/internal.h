@@ -93,6 +93,7 @@ void launch_spmm_wide(const Csr& A, const double* X, int64_t ldx, double* Y, int
 // use so blocks freed by one handle are reused by the next (no cudaMalloc /
 // OS round trip per handle); tsvd_trim_memory() returns them.
 void* dmalloc(size_t bytes, cudaStream_t st);
+void set_allocator(tsvd_alloc_fn a, tsvd_free_fn f, void* ctx);  // tsvd_set_allocator
 void dfree(void* p, cudaStream_t st);
 template <class T> inline void dmalloc_t(T** p, size_t count, cudaStream_t st) {
   *p = (T*)dmalloc(count * sizeof(T), st);
@@ -100,8 +101,13 @@ template <class T> inline void dmalloc_t(T** p, size_t count, cudaStream_t st) {
 void csr_transpose(const Csr& A, Csr& T, cudaStream_t st);
 void csr_build_plan(Csr& A, const int64_t* host_rowptr, cudaStream_t st);
 void csr_free(Csr& A, cudaStream_t st);
-// device validation of a CSR: returns 0 if canonical
+// device validation of a CSR: 0 if canonical; bits: 1 bad row bounds, 2
+// unsorted or duplicate columns in a row (canonicalisable), 4 rowptr[0] != 0
+// or rowptr[rows] != nnz, 8 column index out of range
 int csr_validate_device(const Csr& A, cudaStream_t st);
+// sort each row's columns and sum duplicates (stable order), in place; the
+// row pointer is rewritten, nnz may shrink
+void csr_canonicalize(Csr& A, cudaStream_t st);
 
 // -------------------------------------------------- tall-skinny products --
 // gemm_tn: C (s x w, ldc) = X^T Y  (X: q x s, Y: q x w, both row-major).
@@ -153,6 +159,12 @@ void small_svd(const double* B, int d, double* Ub, double* S, double* Vb, double
                cudaStream_t st);
 size_t small_svd_work(int d);
 int small_svd_sweeps(const double* work, int d);  // sweeps of the last small_svd (syncs)
+// device word holding the sweep count of the last small_svd (read together
+// with rho once per cycle); a count equal to small_svd_max_sweeps() means the
+// sweep cap was hit before the rotation test passed (not converged)
+const unsigned* small_svd_sweeps_dev(const double* work, int d);
+int small_svd_max_sweeps();
+constexpr int kSmallSvdMaxD = 1536;  // largest d the device Jacobi SVD takes
 
 // rho_i = || Rbar * Vb[(k-1)b:kb, i] || / S[0] for i < cnt
 void lanczos_rho(const double* Rbar, int b, const double* Vb, int d, const double* S, int cnt,

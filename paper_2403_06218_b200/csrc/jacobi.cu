@@ -36,7 +36,7 @@ constexpr int JW = 2 * JC;   // columns per block pair
 constexpr int JP = JW + 1;   // padded smem row
 constexpr int kMaxSweeps = 30;
 constexpr int kInnerSweeps = 1;
-constexpr int kJacobiMaxD = 1536;
+constexpr int kJacobiMaxD = kSmallSvdMaxD;
 
 static int jac_nb(int d) {
   int nb = (d + JC - 1) / JC;
@@ -693,6 +693,11 @@ extern "C" int tsvd_dev_jacobi_timing_reset() {
   return (int)cudaMemcpyToSymbol(g_jac_t, z, sizeof(z));
 }
 #endif
+
+const unsigned* small_svd_sweeps_dev(const double* work, int d) {
+  return jac_ctl(const_cast<double*>(work), d) + 4;
+}
+int small_svd_max_sweeps() { return kMaxSweeps; }
 
 int small_svd_sweeps(const double* work, int d) {
   const unsigned* ctl = jac_ctl(const_cast<double*>(work), d);

@@ -112,8 +112,33 @@ struct EventTimer {
   }
 };
 
+// Deferred breakdown checks (tsvd_ctx::deferred) must never outlive the
+// solve that set them: an exception leaving the block-step loop (ENOMEM, a
+// CUDA or NCCL error) would otherwise leave a later solve on this handle
+// skipping its breakdown test and writing into a stale flag log.
+struct DeferredGuard {
+  Ctx& c;
+  explicit DeferredGuard(Ctx& c_) : c(c_) { reset(); }
+  ~DeferredGuard() { reset(); }
+  void reset() {
+    c.deferred = false;
+    c.flag_log = nullptr;
+    c.flag_slot = 0;
+  }
+};
+
+// Sweep count of the SVD just enqueued, read with the cycle's other scalars.
+struct SvdWatch {
+  int max_sweeps = 0, unconverged = 0;
+  void add(unsigned sweeps) {
+    max_sweeps = std::max(max_sweeps, (int)sweeps);
+    if ((int)sweeps >= small_svd_max_sweeps()) ++unconverged;
+  }
+};
+
 tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   const int64_t m = c.m, n = c.n;  // this rank's rows (single GPU: all)
+  DeferredGuard guard(c);
   if (r < 1 || b < 1 || !(tol > 0.0) || maxit < 1) return TSVD_EINVAL;
   if (b > 32) return TSVD_EINVAL;  // kernel tile limit
   if (r > c.ng) return TSVD_ESHAPE;
@@ -121,9 +146,10 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   if (d == 0) {
     d = std::max(4 * r, 2 * b);
     d = (int)std::min<int64_t>(d, c.ng);
+    d = std::min(d, kSmallSvdMaxD);
     d -= d % b;
   }
-  if (d % b != 0 || d < r || d > c.ng || d < b) return TSVD_ESHAPE;
+  if (d % b != 0 || d < r || d > c.ng || d < b || d > kSmallSvdMaxD) return TSVD_ESHAPE;
   if (!c.start.empty() && (c.start_rows != m || c.start_cols != b)) return TSVD_ESHAPE;
   const int keep = c.thick_keep;  // N1 thick restart (0: Alg. 2 S7)
   if (keep && (keep % b != 0 || keep < r || keep >= d)) return TSVD_ESHAPE;
@@ -164,6 +190,8 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   cholqr2(c, Pb, m, b, ldb, R);
 
   std::vector<double> hrho(r), hs(1);
+  unsigned* hsw = reinterpret_cast<unsigned*>(c.hflags + 4);  // pinned word
+  SvdWatch svdw;
   int cycle = 0, nconv = 0;
   bool conv = false;
   double rho_max = 0.0;
@@ -223,7 +251,10 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
     }
     TSVD_CUDA(cudaMemcpyAsync(hrho.data(), rho, r * sizeof(double), cudaMemcpyDeviceToHost, c.st));
     TSVD_CUDA(cudaMemcpyAsync(hs.data(), Sg, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+    TSVD_CUDA(cudaMemcpyAsync(hsw, small_svd_sweeps_dev(jw, d), sizeof(unsigned),
+                              cudaMemcpyDeviceToHost, c.st));
     TSVD_CUDA(cudaStreamSynchronize(c.st));
+    svdw.add(*hsw);
     nconv = 0;
     rho_max = 0.0;
     for (int i = 0; i < r; ++i) {
@@ -299,7 +330,10 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   c.info.sigma1 = hs[0];
   c.info.ms_total = ms;
   c.info.launches = g_launches.load() - launches0;
-  return conv ? TSVD_OK : TSVD_WARN_NOTCONV;
+  c.info.svd_sweeps = svdw.max_sweeps;
+  c.info.svd_unconverged = svdw.unconverged;
+  if (!conv) return TSVD_WARN_NOTCONV;
+  return svdw.unconverged ? TSVD_WARN_SVD : TSVD_OK;
 }
 
 // SURVEY 8(f) N4 (Eq. 3): the rank is not known in advance but set
@@ -347,9 +381,10 @@ tsvd_status lanczos_threshold(Ctx& c, double tau, int b, double tol, int maxit, 
 
 tsvd_status rsvd_solve(Ctx& c, int r, int p, int q) {
   const int64_t m = c.m, n = c.n;  // this rank's rows (single GPU: all)
+  DeferredGuard guard(c);
   if (r < 1 || p < 0 || q < 0) return TSVD_EINVAL;
   const int l = r + p;
-  if (l > c.ng) return TSVD_ESHAPE;
+  if (l > c.ng || l > kSmallSvdMaxD) return TSVD_ESHAPE;
   if (!c.start.empty() && (c.start_rows != n || c.start_cols != l)) return TSVD_ESHAPE;
   const int bq = std::min(std::max(1, c.b_qr), 32);
   c.have = false;
@@ -401,8 +436,13 @@ tsvd_status rsvd_solve(Ctx& c, int r, int p, int q) {
     TSVD_CUDA(cudaMemcpyAsync(c.S, Sg, r * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
   }
   double s1 = 0.0;
+  unsigned* hsw = reinterpret_cast<unsigned*>(c.hflags + 4);
   TSVD_CUDA(cudaMemcpyAsync(&s1, Sg, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+  TSVD_CUDA(cudaMemcpyAsync(hsw, small_svd_sweeps_dev(jw, l), sizeof(unsigned),
+                            cudaMemcpyDeviceToHost, c.st));
   const double ms = timer.stop();
+  SvdWatch svdw;
+  svdw.add(*hsw);
   prof_harvest(c);
   c.rho.clear();
   c.have = true;
@@ -416,7 +456,9 @@ tsvd_status rsvd_solve(Ctx& c, int r, int p, int q) {
   c.info.sigma1 = s1;
   c.info.ms_total = ms;
   c.info.launches = g_launches.load() - launches0;
-  return TSVD_OK;
+  c.info.svd_sweeps = svdw.max_sweeps;
+  c.info.svd_unconverged = svdw.unconverged;
+  return svdw.unconverged ? TSVD_WARN_SVD : TSVD_OK;
 }
 
 }  // namespace tsvd

@@ -15,6 +15,7 @@
 #include <algorithm>
 
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include "internal.h"
 
@@ -555,16 +556,116 @@ __global__ void csr_validate_kernel(const int64_t* __restrict__ rowptr,
       if (lane == 0) atomicOr(bad, 1);
       continue;
     }
-    bool ok = true;
+    bool ok = true, inrange = true;
     for (int64_t k = b + lane; k < e; k += 32) {
       const int64_t c = colidx[k];
-      if (c < 0 || c >= cols || (k > b && colidx[k - 1] >= c)) ok = false;
+      if (c < 0 || c >= cols) inrange = false;
+      else if (k > b && colidx[k - 1] >= c) ok = false;
     }
+    if (!__all_sync(0xffffffffu, inrange) && lane == 0) atomicOr(bad, 8);
     if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicOr(bad, 2);
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (rowptr[0] != 0 || rowptr[rows] != nnz) atomicOr(bad, 4);
   }
+}
+
+// ---------------------------------------------------------- canonicalise --
+// unsorted column indices and duplicate entries are accepted and
+// canonicalised on the device: a stable radix sort by (row, column) keeps the
+// input order among duplicates, and each run of equal (row, column) is summed
+// sequentially in that order by the thread owning its first entry, so the
+// result does not depend on the launch configuration.
+__global__ void csr_keys_kernel(const int32_t* __restrict__ row_of,
+                                const int32_t* __restrict__ colidx, int64_t cols, int64_t nnz,
+                                int64_t* __restrict__ key) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x)
+    key[k] = (int64_t)row_of[k] * cols + colidx[k];
+}
+
+__global__ void csr_run_heads_kernel(const int64_t* __restrict__ key, int64_t nnz,
+                                     int32_t* __restrict__ head) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x)
+    head[k] = (k == 0 || key[k] != key[k - 1]) ? 1 : 0;
+}
+
+__global__ void csr_sum_runs_kernel(const int64_t* __restrict__ key,
+                                    const int32_t* __restrict__ src,
+                                    const double* __restrict__ vals,
+                                    const int32_t* __restrict__ head,
+                                    const int32_t* __restrict__ pos, int64_t cols, int64_t nnz,
+                                    int32_t* __restrict__ out_row, int32_t* __restrict__ out_col,
+                                    double* __restrict__ out_val) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    if (!head[k]) continue;
+    double v = vals[src[k]];
+    for (int64_t j = k + 1; j < nnz && key[j] == key[k]; ++j) v += vals[src[j]];
+    const int32_t p = pos[k];
+    out_row[p] = (int32_t)(key[k] / cols);
+    out_col[p] = (int32_t)(key[k] % cols);
+    out_val[p] = v;
+  }
+}
+
+void csr_canonicalize(Csr& A, cudaStream_t st) {
+  if (A.nnz >= (int64_t)INT32_MAX) throw Error{TSVD_EINVAL, "nnz >= 2^31 per shard"};
+  const int nnz = (int)A.nnz;
+  if (nnz == 0) return;
+  const unsigned grid = 148 * 8;
+  int32_t *row_of, *idx_in, *idx_out, *head, *pos;
+  int64_t *key_in, *key_out;
+  dmalloc_t(&row_of, nnz, st);
+  dmalloc_t(&idx_in, nnz, st);
+  dmalloc_t(&idx_out, nnz, st);
+  dmalloc_t(&head, nnz, st);
+  dmalloc_t(&pos, nnz, st);
+  dmalloc_t(&key_in, nnz, st);
+  dmalloc_t(&key_out, nnz, st);
+  row_of_nz_kernel<<<grid, 256, 0, st>>>(A.rowptr, A.rows, A.nnz, row_of);
+  iota_kernel<<<grid, 256, 0, st>>>(idx_in, A.nnz);
+  csr_keys_kernel<<<grid, 256, 0, st>>>(row_of, A.colidx, A.cols, A.nnz, key_in);
+  TSVD_CHECK_LAUNCH();
+  int end_bit = 1;
+  const unsigned long long kmax = (unsigned long long)A.rows * (unsigned long long)A.cols;
+  while (end_bit < 63 && (1ULL << end_bit) < kmax) ++end_bit;
+  size_t tmp_bytes = 0, scan_bytes = 0;
+  TSVD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, key_in, key_out, idx_in, idx_out,
+                                            nnz, 0, end_bit, st));
+  TSVD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, head, pos, nnz, st));
+  void* tmp = dmalloc(std::max(tmp_bytes, scan_bytes), st);
+  TSVD_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key_in, key_out, idx_in, idx_out, nnz,
+                                            0, end_bit, st));
+  csr_run_heads_kernel<<<grid, 256, 0, st>>>(key_out, A.nnz, head);
+  TSVD_CHECK_LAUNCH();
+  TSVD_CUDA(cub::DeviceScan::ExclusiveSum(tmp, scan_bytes, head, pos, nnz, st));
+  int last_pos = 0, last_head = 0;
+  TSVD_CUDA(cudaMemcpyAsync(&last_pos, pos + nnz - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  TSVD_CUDA(cudaMemcpyAsync(&last_head, head + nnz - 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+  TSVD_CUDA(cudaStreamSynchronize(st));
+  const int64_t nnz2 = (int64_t)last_pos + last_head;
+  int32_t *new_row, *new_col;
+  double* new_val;
+  dmalloc_t(&new_row, nnz2, st);
+  dmalloc_t(&new_col, nnz2, st);
+  dmalloc_t(&new_val, nnz2, st);
+  csr_sum_runs_kernel<<<grid, 256, 0, st>>>(key_out, idx_out, A.vals, head, pos, A.cols, A.nnz,
+                                            new_row, new_col, new_val);
+  TSVD_CHECK_LAUNCH();
+  // row pointer: first position of each row in the sorted, deduplicated rows
+  t_rowptr_kernel<<<grid, 256, 0, st>>>(new_row, nnz2, A.rows, A.rowptr);
+  TSVD_CHECK_LAUNCH();
+  TSVD_CUDA(cudaStreamSynchronize(st));
+  for (void* p : {(void*)row_of, (void*)idx_in, (void*)idx_out, (void*)head, (void*)pos,
+                  (void*)key_in, (void*)key_out, tmp, (void*)new_row})
+    dfree(p, st);
+  dfree(A.colidx, st);
+  dfree(A.vals, st);
+  A.colidx = new_col;
+  A.vals = new_val;
+  A.nnz = nnz2;
 }
 
 int csr_validate_device(const Csr& A, cudaStream_t st) {

@@ -1464,7 +1464,14 @@ void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const d
              int64_t ldy, const double* T, double* Z, int64_t ldz, int64_t q, int s, int w,
              double alpha, double beta, double* gram, cudaStream_t st, double* part,
              size_t part_cap) {
-  if (w <= 0 || q <= 0) return;
+  if (w <= 0) return;
+  if (q <= 0) {
+    // empty row range (a rank whose row slice or n-shard is empty): the
+    // caller still reduces nn_ctas(0, w) = 1 Gram partial, so it must be the
+    // zero matrix, not whatever an earlier pass left in the buffer
+    if (gram) TSVD_CUDA(cudaMemsetAsync(gram, 0, sizeof(double) * nn_ctas(0, w) * w * w, st));
+    return;
+  }
   if (w > 32) {
     if (T || gram) throw Error{TSVD_EINVAL, "gemm_nn: T/gram need w <= 32"};
     if (beta == 0.0 && s > 0 && g_nn_tma && aligned16(X, ldx) && aligned16(H, ldh)) {

@@ -193,9 +193,61 @@ def test_errors():
     with pytest.raises(T.TsvdError):
         T.TruncatedSVD(csr=(np.array([0, 2, 1], np.int64), np.array([0, 1], np.int32),
                             np.ones(2)), shape=(2, 2))
-    with pytest.raises(T.TsvdError):   # unsorted columns
-        T.TruncatedSVD(csr=(np.array([0, 2, 2], np.int64), np.array([1, 0], np.int32),
+    with pytest.raises(T.TsvdError):   # column index out of range
+        T.TruncatedSVD(csr=(np.array([0, 2, 2], np.int64), np.array([1, 2], np.int32),
                             np.ones(2)), shape=(2, 2))
+    with T.TruncatedSVD(A) as h:       # d above the device Jacobi's 1536 limit
+        with pytest.raises(T.TsvdError):
+            h.rsvd(r=1, p=1536, q=0)
+
+
+def _noncanonical(csr, seed):
+    """The same matrix with every row's entries shuffled and about a third
+    of them split into two duplicates v/2 + v/2 (= v exactly)."""
+    rp, ci, va = csr
+    rng = np.random.default_rng(seed)
+    rows, cols, vals = [], [], []
+    for i in range(len(rp) - 1):
+        c, v = ci[rp[i]:rp[i + 1]], va[rp[i]:rp[i + 1]]
+        split = rng.random(len(c)) < 0.35
+        cc = np.concatenate([c, c[split]])
+        vv = np.concatenate([np.where(split, v * 0.5, v), v[split] * 0.5])
+        p = rng.permutation(len(cc))
+        rows.append(np.full(len(cc), i))
+        cols.append(cc[p])
+        vals.append(vv[p])
+    lens = np.array([len(x) for x in cols])
+    rp2 = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    return rp2, np.concatenate(cols).astype(np.int32), np.concatenate(vals)
+
+
+def test_noncanonical_csr_is_canonicalised():
+    """unsorted / duplicate entries are canonicalised on the
+    device (sorted, duplicates summed).  The products and a solve equal those
+    of the canonical matrix (scipy's CSR, the oracle's operator, sums the
+    duplicates too)."""
+    m, n = 20000, 8000
+    csr = powerlaw_csr(m, n, 200000, 2.5, seed=17)
+    nc = _noncanonical(csr, 5)
+    op = oracle.Operator(csr=nc, shape=(m, n))
+    rng = np.random.default_rng(2)
+    X = torch.from_numpy(rng.standard_normal((n, 16))).cuda()
+    Xt = torch.from_numpy(rng.standard_normal((m, 16))).cuda()
+    outs = []
+    for c in (csr, nc):
+        with T.TruncatedSVD(csr=c, shape=(m, n)) as h:
+            Y = torch.empty((m, 16), dtype=torch.float64, device="cuda")
+            Z = torch.empty((n, 16), dtype=torch.float64, device="cuda")
+            T.dbg_apply(h, False, X, Y)
+            T.dbg_apply(h, True, Xt, Z)
+            h.set_seed(9)
+            h.block_lanczos(r=8, b=8, tol=1e-10, maxit=8, d=64)
+            outs.append((Y.cpu().numpy(), Z.cpu().numpy(), *h.get()))
+    # v/2 + v/2 == v exactly, so the canonical form is bit-identical
+    for a, b in zip(outs[0], outs[1]):
+        assert np.array_equal(a, b)
+    ref = op.matmul(X.cpu().numpy())
+    assert np.abs(outs[1][0] - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
 # ---- N1 thick restart (tsvd_set_thick_restart; oracle/lancsvd.py keep=l) ---
