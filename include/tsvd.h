@@ -214,6 +214,18 @@ tsvd_status tsvd_rsvd(tsvd_t h, int r, int p, int q);
 tsvd_status tsvd_get(tsvd_t h, double* U, int64_t ldu, double* S, double* V,
                      int64_t ldv, int mem_kind);
 
+/* Explicit residuals of the last solve's r triplets (Eq. 14,
+ * P:408-410, as corrected by DESIGN.md reading R13: the printed
+ * ||A u_i - sigma_i v_i|| is dimensionally inconsistent):
+ *   e[i] = ||A v_i - sigma_i u_i||_2 / sigma_1   (north_star's measure)
+ *   rel[i] = ||A v_i - sigma_i u_i||_2 / sigma_i (the paper's R_i)
+ * computed on the device with the library's own A.X product and a
+ * fixed-order column-norm reduction (multi-GPU: row-sharded sums
+ * all-reduced; every rank gets all r values).  e, rel: host arrays of r
+ * doubles, either may be NULL.  Collective on multi-GPU handles.
+ * TSVD_ESTATE before a successful solve. */
+tsvd_status tsvd_residuals(tsvd_t h, double* e, double* rel);
+
 typedef struct {
   int cycles;       /* LancSVD restart cycles run (RandSVD: q + 1)        */
   int nconv;        /* i < r with rho_i <= tol*sigma_1 (LancSVD)          */

@@ -37,7 +37,7 @@ EXPORTS = [
     "tsvd_dbg_small_svd", "tsvd_dbg_gemm_tn", "tsvd_dbg_gemm_nn",
     "tsvd_set_profiling", "tsvd_get_profile", "tsvd_reset_profile",
     "tsvd_create_csr_dist", "tsvd_create_dense_dist", "tsvd_nccl_unique_id",
-    "tsvd_partition_rows", "tsvd_set_allocator",
+    "tsvd_partition_rows", "tsvd_set_allocator", "tsvd_residuals",
 ]
 
 
@@ -108,6 +108,7 @@ _SIGS = {
     "tsvd_nccl_unique_id": [vp],
     "tsvd_partition_rows": [vp, i64, i32, vp],
     "tsvd_set_allocator": [vp, vp, vp],
+    "tsvd_residuals": [vp, vp, vp],
 }
 
 
@@ -344,6 +345,14 @@ class TruncatedSVD:
         kind = kinds.pop() if kinds else TSVD_HOST
         _check(lib().tsvd_get(self._h, ps[0][0], self.r, ps[1][0], ps[2][0], self.r, kind),
                "tsvd_get")
+
+    def residuals(self):
+        """(e, R): e_i = ||A v_i - s_i u_i|| / s_1 and R_i = ... / s_i of the
+        last solve, computed on the device by the library (tsvd_residuals)."""
+        e = np.empty(self.r)
+        R = np.empty(self.r)
+        _check(lib().tsvd_residuals(self._h, e.ctypes.data, R.ctypes.data), "tsvd_residuals")
+        return e, R
 
     def info(self) -> dict:
         inf = TsvdInfo()

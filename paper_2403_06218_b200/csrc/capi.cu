@@ -422,6 +422,15 @@ tsvd_status tsvd_get(tsvd_t h, double* U, int64_t ldu, double* S, double* V, int
   TSVD_API_END
 }
 
+tsvd_status tsvd_residuals(tsvd_t h, double* e, double* rel) {
+  if (!h) return TSVD_EINVAL;
+  if (!h->have) return TSVD_ESTATE;
+  TSVD_API_BEGIN
+  residuals(*h, e, rel);
+  return TSVD_OK;
+  TSVD_API_END
+}
+
 tsvd_status tsvd_get_info(tsvd_t h, tsvd_info* out) {
   if (!h || !out) return TSVD_EINVAL;
   *out = h->info;

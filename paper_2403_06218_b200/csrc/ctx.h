@@ -113,6 +113,10 @@ void allreduce_sum(Ctx& c, double* buf, size_t count);
 void reduce_scatter_sum(Ctx& c, const double* send, double* recv, size_t recv_count);
 void all_gather(Ctx& c, const double* send, double* recv, size_t send_count);
 
+// explicit residuals of the last solve (residual.cu):
+// e[i] = ||A v_i - s_i u_i|| / s_1, rel[i] = ... / s_i (host arrays, may be NULL)
+void residuals(Ctx& c, double* e_host, double* rel_host);
+
 // solvers (solvers.cu)
 tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit);
 tsvd_status rsvd_solve(Ctx& c, int r, int p, int q);

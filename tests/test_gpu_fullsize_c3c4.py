@@ -96,8 +96,8 @@ def test_c3_lanczos_properties(c3):
         Ug, Sg, Vg = h.get()
         rho = h.rho()
     conv = rho <= cfg["tol"]
-    assert st in (T.TSVD_OK, T.TSVD_WARN_NOTCONV)
-    assert conv.sum() >= cfg["b"]  # at least the kept block converges
+    assert st == T.TSVD_OK          # all r = 100 converge (2 cycles at d = 640)
+    assert conv.all()
     e, _ = oracle.residuals(op, Ug, Sg, Vg)
     assert e[conv].max() <= 1e-8
     assert np.abs(rho - e).max() <= 1e-12
@@ -120,8 +120,14 @@ def test_c3_rsvd_properties(c3):
     ATU = op.rmatmul(Ug)
     f = np.linalg.norm(ATU - Vg * Sg, axis=0) / Sg[0]
     assert f.max() <= 1e-11
+    # Rayleigh-Ritz: U^T A V = Sigma (Alg. 1 S5-S7: U = Qbar Vbar, V = Q Ubar,
+    # Qbar^T A Q = R_p^T), so sigma_i = u_i^T A v_i to rounding
+    AV = op.matmul(Vg)
+    assert np.abs(np.einsum("ij,ij->j", Ug, AV) - Sg).max() / Sg[0] <= 1e-12
+    # residuals: ||A v - s u|| <= ||A v|| <= s_1 (parity with the oracle's
+    # iterate: tests/test_gpu_oracle_fullsize.py::test_c3_rsvd_vs_oracle)
     e, _ = oracle.residuals(op, Ug, Sg, Vg)
-    assert np.all(np.isfinite(e))
+    assert np.all(np.isfinite(e)) and e.max() <= 1.0 + 1e-12
 
 
 def test_c4_products_sampled(c4):

@@ -255,15 +255,41 @@ def test_cgs_qr_parity(q, l, bq):
     assert np.abs(Q - Qo).max() <= 1e-9
 
 
-@pytest.mark.parametrize("d", [1, 5, 28, 64, 97, 200, 384, 513])
-def test_small_svd_parity(d):
+def _lanczos_like_B(d, b, rng):
+    """Lower block-bidiagonal d x d with b x b blocks (Eq. 8) whose values
+    follow a Lanczos B_k's: lower-triangular diagonal blocks L_i and upper
+    triangular subdiagonal blocks Rbar_i with geometrically decaying norms."""
+    B = np.zeros((d, d))
+    k = d // b
+    for i in range(k):
+        sc = 100.0 * 0.97 ** i
+        B[i * b:(i + 1) * b, i * b:(i + 1) * b] = sc * np.tril(rng.standard_normal((b, b)))
+        if i + 1 < k:
+            B[(i + 1) * b:(i + 2) * b, i * b:(i + 1) * b] = 0.3 * sc * np.triu(
+                rng.standard_normal((b, b)))
+    return B
+
+
+@pytest.mark.parametrize("d,kind", [(1, "tri"), (5, "tri"), (28, "tri"), (64, "tri"),
+                                    (97, "tri"), (200, "tri"), (384, "tri"), (513, "tri"),
+                                    (384, "lanczos16"), (640, "lanczos32"),
+                                    (704, "lanczos32"), (768, "tri"), (1024, "lanczos32"),
+                                    (1536, "tri"), (1536, "lanczos32")])
+def test_small_svd_parity(d, kind):
+    """Device Jacobi vs LAPACK gesvd up to the largest d the library takes
+    (C3: 640, C4: 704, limit 1536), on random lower-triangular B and on
+    Lanczos-shaped block-bidiagonal B; the sweep cap is never hit."""
     rng = np.random.default_rng(d)
-    B = np.tril(rng.standard_normal((d, d))) - np.tril(rng.standard_normal((d, d)), -5)
+    if kind == "tri":
+        B = np.tril(rng.standard_normal((d, d))) - np.tril(rng.standard_normal((d, d)), -5)
+    else:
+        B = _lanczos_like_B(d, int(kind[7:]), rng)
     Uo, So, Vo = oracle.small_svd(B)
     Ub = torch.zeros((d, d), dtype=torch.float64, device="cuda")
     Vb = torch.zeros((d, d), dtype=torch.float64, device="cuda")
     S = torch.zeros(d, dtype=torch.float64, device="cuda")
-    T.dbg_small_svd(cu(B), Ub, S, Vb)
+    sweeps = T.dbg_small_svd(cu(B), Ub, S, Vb)
+    assert sweeps < 30
     Ug, Sg, Vg = Ub.cpu().numpy(), S.cpu().numpy(), Vb.cpu().numpy()
     tol = 10 * d * U * So[0]
     assert np.abs(Sg - So).max() <= tol

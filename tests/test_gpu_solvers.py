@@ -390,3 +390,41 @@ def test_threshold_rank_rmax_and_errors():
         for bad in (0.0, -1.0, 1.0):
             with pytest.raises(T.TsvdError):
                 h.block_lanczos_threshold(bad, b=4, tol=1e-12, maxit=8, r_max=6)
+
+
+# ---- a17: explicit residuals inside the library (tsvd_residuals) -----------
+@pytest.mark.parametrize("case", ["dense", "sparse", "sparse_wide", "inplace"])
+def test_residuals_parity(case):
+    """tsvd_residuals (device: the library's A.X + fixed-order column norms)
+    vs oracle.residuals (scipy/numpy) on the same returned triplets: e_i and
+    R_i = e_i s_1 / s_i (Eq. 14 corrected, reading R13).  The residual is a
+    difference of nearly equal vectors, so the comparison is absolute in
+    units of s_1: | ||z|| - ||z^o|| | <= ||z - z^o|| <= ||b|| with the
+    element-wise forward-error bound b = 2 (K + 2) u (|A| |v| + s |u|)
+    of both sides' products (K = row length)."""
+    if case == "dense":
+        A, _ = _c1()
+        op, kw, r = oracle.Operator(dense=A), dict(A=A), 10
+    else:
+        m, n = (30000, 12000) if case != "sparse_wide" else (20000, 9000)
+        csr = powerlaw_csr(m, n, 300000, 2.5, seed=23)
+        op, kw, r = oracle.Operator(csr=csr, shape=(m, n)), dict(csr=csr, shape=(m, n)), 40
+        if case == "sparse_wide":
+            r = 70                       # > 64: two chunks of the column loop
+    with T.TruncatedSVD(**kw) as h:
+        if case == "inplace":
+            h.set_output_mode(T.TSVD_OUT_INPLACE)
+        h.set_seed(11)
+        if case == "sparse_wide":
+            h.rsvd(r, 10, 1)
+        else:
+            h.block_lanczos(r, 8, 1e-10, 4, d=min(4 * r, 160))
+        Ug, Sg, Vg = h.get()
+        e, R = h.residuals()
+    eo, Ro = oracle.residuals(op, Ug, Sg, Vg)
+    absA = np.abs(op.A) if op.kind == "dense" else abs(op.A)
+    K = op.n if op.kind == "dense" else np.diff(op.A.indptr)
+    b = 2 * (np.asarray(K)[..., None] + 2) * U * (np.asarray(absA @ np.abs(Vg)) + np.abs(Ug) * Sg)
+    tol = 2 * np.linalg.norm(b, axis=0) / Sg[0] + 1e-300
+    assert np.all(np.abs(e - eo) <= tol)
+    assert np.allclose(R * Sg, e * Sg[0], rtol=1e-14, atol=0)
