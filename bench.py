@@ -109,10 +109,15 @@ def shard_workload(work, rank, world, T):
     if "csr" in work:
         rp, ci, va = work["csr"]
         m, n = work["shape"]
-        b = T.partition_rows(rp, world)
+        rp_h = rp.cpu().numpy() if hasattr(rp, "cpu") else rp
+        b = T.partition_rows(rp_h, world)
         r0, r1 = int(b[rank]), int(b[rank + 1])
-        lo, hi = int(rp[r0]), int(rp[r1])
-        local = dict(csr=(np.ascontiguousarray(rp[r0:r1 + 1] - lo), ci[lo:hi], va[lo:hi]))
+        lo, hi = int(rp_h[r0]), int(rp_h[r1])
+        if hasattr(rp, "cpu"):  # device-generated (C5): every rank built the same bytes
+            local = dict(csr=((rp[r0:r1 + 1] - lo).contiguous(), ci[lo:hi].clone(),
+                              va[lo:hi].clone()))
+        else:
+            local = dict(csr=(np.ascontiguousarray(rp[r0:r1 + 1] - lo), ci[lo:hi], va[lo:hi]))
     else:
         A = work["A"]
         m, n = A.shape
@@ -457,6 +462,7 @@ def main():
             dist.broadcast(idt, 0)
         return dict(rank=rank, world=world, nccl_id=bytes(idt.cpu().numpy()), **geo)
 
+    lwork = None
     if use_dist:
         lwork, geo = shard_workload(work, rank, world, T)
         dist_kw = fresh_dist_kw(geo)
@@ -483,8 +489,7 @@ def main():
         # C5: the library holds its own copies of A and CSR(A^T); free the
         # generator's so the d = 160 bases (141 GB) fit, and let the outputs be
         # formed in place (tsvd_set_output_mode AUTO)
-        del dwork, work, hwork
-        dwork = work = hwork = None
+        dwork = work = hwork = lwork = None
         torch.cuda.empty_cache()
         T.trim_memory(0)
         free, total = torch.cuda.mem_get_info()

@@ -50,7 +50,7 @@ enum {
   TSVD_WARN_FALLBACK = 2, /* tsvd_dbg_cholqr2 / _cgs_cqr2 only: the Cholesky breakdown
                              test fired and the CGS2 fallback gave the result */
   TSVD_WARN_SVD = 3,     /* the device Jacobi SVD of B_k / R_p (reading R20) hit its
-                            sweep cap (30) before every column pair passed the
+                            sweep cap (60) before every column pair passed the
                             rotation test; results retrievable, tsvd_info counts it */
   TSVD_EINVAL = -1,      /* bad argument (NULL, non-canonical CSR, tol <= 0 ...) */
   TSVD_ESHAPE = -2,      /* m < n, r > n, d % b != 0, r > d, r + p > n ...     */
@@ -100,6 +100,8 @@ typedef struct {
   const void* nccl_id;        /* 128 bytes, identical on all ranks */
   int64_t m_global, n_global; /* sizes of the whole A, m >= n */
   int64_t row_begin, row_end; /* this rank's rows of A */
+  void* loopback;             /* NULL (NCCL), or a tsvd_loopback_create group:
+                                 then nccl_id may be NULL (test-only, below) */
 } tsvd_dist;
 /* rowptr/colidx/vals: this rank's rows only (local rowptr starting at 0,
  * GLOBAL column indices). */
@@ -111,6 +113,15 @@ tsvd_status tsvd_create_dense_dist(tsvd_t* h, const tsvd_dist* dist, const doubl
                                    int64_t lda, int mem_kind);
 /* Fill out128 with a fresh ncclUniqueId (TSVD_ENCCL if NCCL is unavailable). */
 tsvd_status tsvd_nccl_unique_id(void* out128);
+/* TEST-ONLY in-process communicator: `world` (1..8) handles on ONE device,
+ * each driven from its own host thread, exchange through device memory
+ * instead of NCCL (rank-ordered sums), so the library's complete
+ * row-partitioned code path runs at world > 1 on a single GPU.  Pass the
+ * group as tsvd_dist.loopback to every rank's create call; destroy it after
+ * all its handles.  Collectives block the calling thread until all ranks
+ * reach them (like NCCL's), so the ranks MUST run on separate threads. */
+tsvd_status tsvd_loopback_create(int world, void** group);
+tsvd_status tsvd_loopback_destroy(void* group);
 /* Row split of a CSR row pointer (host) into `world` contiguous ranges with
  * (nearly) equal nonzeros: bounds[0] = 0 ... bounds[world] = m. */
 tsvd_status tsvd_partition_rows(const int64_t* rowptr, int64_t m, int world, int64_t* bounds);

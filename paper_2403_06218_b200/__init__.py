@@ -37,7 +37,8 @@ EXPORTS = [
     "tsvd_dbg_small_svd", "tsvd_dbg_gemm_tn", "tsvd_dbg_gemm_nn",
     "tsvd_set_profiling", "tsvd_get_profile", "tsvd_reset_profile",
     "tsvd_create_csr_dist", "tsvd_create_dense_dist", "tsvd_nccl_unique_id",
-    "tsvd_partition_rows", "tsvd_set_allocator", "tsvd_residuals",
+    "tsvd_partition_rows", "tsvd_set_allocator", "tsvd_residuals", "tsvd_loopback_create",
+    "tsvd_loopback_destroy",
 ]
 
 
@@ -51,7 +52,7 @@ class TsvdInfo(C.Structure):
 class TsvdDist(C.Structure):
     _fields_ = [("rank", C.c_int), ("world", C.c_int), ("nccl_id", C.c_void_p),
                 ("m_global", C.c_int64), ("n_global", C.c_int64),
-                ("row_begin", C.c_int64), ("row_end", C.c_int64)]
+                ("row_begin", C.c_int64), ("row_end", C.c_int64), ("loopback", C.c_void_p)]
 
 
 class TsvdProfEntry(C.Structure):
@@ -109,6 +110,8 @@ _SIGS = {
     "tsvd_partition_rows": [vp, i64, i32, vp],
     "tsvd_set_allocator": [vp, vp, vp],
     "tsvd_residuals": [vp, vp, vp],
+    "tsvd_loopback_create": [i32, C.POINTER(vp)],
+    "tsvd_loopback_destroy": [vp],
 }
 
 
@@ -194,10 +197,13 @@ class TruncatedSVD:
         L = lib()
         h = vp()
         if dist is not None:
-            self._id_buf = C.create_string_buffer(bytes(dist["nccl_id"]), 128)
+            nid = dist.get("nccl_id")
+            self._id_buf = C.create_string_buffer(bytes(nid), 128) if nid else None
+            lb = dist.get("loopback")
             dd = TsvdDist(int(dist["rank"]), int(dist["world"]),
-                          C.cast(self._id_buf, C.c_void_p).value, int(dist["m_global"]),
-                          int(dist["n_global"]), int(dist["row_begin"]), int(dist["row_end"]))
+                          C.cast(self._id_buf, C.c_void_p).value if nid else None,
+                          int(dist["m_global"]), int(dist["n_global"]), int(dist["row_begin"]),
+                          int(dist["row_end"]), lb.ptr if lb is not None else None)
             mloc = int(dist["row_end"]) - int(dist["row_begin"])
             ng = int(dist["n_global"])
             nsh = -(-ng // int(dist["world"]))
@@ -437,6 +443,21 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+class LoopbackGroup:
+    """TEST-ONLY in-process communicator (tsvd_loopback_create): `world`
+    handles on one GPU, one host thread per rank; pass as dist["loopback"]."""
+
+    def __init__(self, world: int):
+        g = vp()
+        _check(lib().tsvd_loopback_create(int(world), C.byref(g)), "tsvd_loopback_create")
+        self.ptr, self.world = g.value, int(world)
+
+    def close(self):
+        if self.ptr:
+            lib().tsvd_loopback_destroy(self.ptr)
+            self.ptr = None
+
+
 def partition_rows(rowptr, world: int) -> np.ndarray:
     """nnz-balanced contiguous row split (tsvd_partition_rows): bounds[world+1]."""
     rp = np.ascontiguousarray(rowptr, dtype=np.int64)
@@ -494,7 +515,7 @@ def dbg_cgs_qr(Y, bq: int, R, seed: int = 0, stream=None):
 
 
 def dbg_small_svd(B, Ub, S, Vb, stream=None) -> int:
-    """Returns the number of Jacobi sweeps used (== the cap, 30, with status
+    """Returns the number of Jacobi sweeps used (== the cap, 60, with status
     TSVD_WARN_SVD when the rotation test did not pass)."""
     d = B.shape[0]
     sw = C.c_int(0)

@@ -154,7 +154,8 @@ static void set_single(tsvd_ctx* c, int64_t m, int64_t n) {
 }
 
 static tsvd_status set_dist(tsvd_ctx* c, const tsvd_dist* d) {
-  if (!d || d->world < 1 || d->rank < 0 || d->rank >= d->world || !d->nccl_id) return TSVD_EINVAL;
+  if (!d || d->world < 1 || d->rank < 0 || d->rank >= d->world || (!d->nccl_id && !d->loopback))
+    return TSVD_EINVAL;
   if (d->m_global < d->n_global) return TSVD_ESHAPE;
   if (d->row_begin < 0 || d->row_end < d->row_begin || d->row_end > d->m_global)
     return TSVD_EINVAL;
@@ -231,6 +232,27 @@ tsvd_status tsvd_create_dense(tsvd_t* h, int64_t m, int64_t n, const double* Ain
   TSVD_CREATE_CATCH
 }
 
+static void join_comm(tsvd_ctx* c, const tsvd_dist* d) {
+  if (d->loopback)
+    loop_join(*c, static_cast<LoopGroup*>(d->loopback), d->rank);
+  else
+    comm_init(*c, d->nccl_id, d->rank, d->world);
+}
+
+tsvd_status tsvd_loopback_create(int world, void** group) {
+  if (!group || world < 1 || world > kLoopMaxWorld) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  *group = loop_group_create(world);
+  return TSVD_OK;
+  TSVD_API_END
+}
+
+tsvd_status tsvd_loopback_destroy(void* group) {
+  if (!group) return TSVD_EINVAL;
+  loop_group_destroy(static_cast<LoopGroup*>(group));
+  return TSVD_OK;
+}
+
 tsvd_status tsvd_create_csr_dist(tsvd_t* h, const tsvd_dist* dist, int64_t nnz,
                                  const int64_t* rowptr, const int32_t* colidx,
                                  const double* vals, int mem_kind) {
@@ -241,7 +263,7 @@ tsvd_status tsvd_create_csr_dist(tsvd_t* h, const tsvd_dist* dist, int64_t nnz,
     tsvd_status s = init_ctx(c);
     if (s == TSVD_OK) s = set_dist(c, dist);
     if (s == TSVD_OK) s = setup_csr(c, nnz, rowptr, colidx, vals, mem_kind);
-    if (s == TSVD_OK) comm_init(*c, dist->nccl_id, dist->rank, dist->world);
+    if (s == TSVD_OK) join_comm(c, dist);
     if (s != TSVD_OK) {
       destroy_ctx(c);
       return s;
@@ -262,7 +284,7 @@ tsvd_status tsvd_create_dense_dist(tsvd_t* h, const tsvd_dist* dist, const doubl
     if (s == TSVD_OK) s = set_dist(c, dist);
     if (s == TSVD_OK && (c->m > 0 && (!Ain || lda < c->ng))) s = TSVD_EINVAL;
     if (s == TSVD_OK) s = setup_dense(c, Ain, lda, TSVD_ROW_MAJOR, mem_kind);
-    if (s == TSVD_OK) comm_init(*c, dist->nccl_id, dist->rank, dist->world);
+    if (s == TSVD_OK) join_comm(c, dist);
     if (s != TSVD_OK) {
       destroy_ctx(c);
       return s;

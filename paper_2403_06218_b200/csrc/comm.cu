@@ -12,6 +12,10 @@
 // B_k, the Jacobi SVD, rho and the restart decision are replicated on every
 // rank from bitwise-identical all-reduced inputs.
 #include <dlfcn.h>
+
+#include <algorithm>
+#include <condition_variable>
+#include <mutex>
 #include <nccl.h>
 
 #include "ctx.h"
@@ -81,20 +85,147 @@ void comm_init(Ctx& c, const void* id128, int rank, int world) {
 }
 
 void comm_destroy(Ctx& c) {
+  if (c.loop) {  // the group belongs to the caller (tsvd_loopback_destroy)
+    c.loop = nullptr;
+    c.comm = nullptr;
+    return;
+  }
   if (c.comm && api().ok) api().CommDestroy((ncclComm_t)c.comm);
   c.comm = nullptr;
+}
+
+// ------------------------------------------------------------- loopback --
+// In-process communicator for tests: `world` handles on ONE device, driven
+// from `world` host threads, exchange through device memory instead of NCCL.
+// It runs the library's complete multi-GPU code path (row shards, n-shard
+// padding, Philox row offsets, all-reduced Grams, gathered sign rule) at
+// world > 1 on a single GPU.  Every collective is two host barriers and
+// cross-stream events: ranks publish their buffers and a "ready" event,
+// each rank's stream waits for all ready events, a kernel on its stream
+// reads every rank's buffer (plain device pointers: same GPU) and writes its
+// own result, and a second barrier + "done" events keep every send buffer
+// alive until all ranks have read it.  Sums run over ranks in rank order.
+struct LoopGroup {
+  int world = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int count = 0;
+  uint64_t gen = 0;
+  std::vector<const double*> send;
+  std::vector<cudaEvent_t> ready, done;
+};
+
+LoopGroup* loop_group_create(int world) {
+  if (world < 1 || world > kLoopMaxWorld) throw Error{TSVD_EINVAL, "loopback world out of range"};
+  auto* g = new LoopGroup();
+  g->world = world;
+  g->send.assign(world, nullptr);
+  g->ready.assign(world, nullptr);
+  g->done.assign(world, nullptr);
+  for (int r = 0; r < world; ++r) {
+    TSVD_CUDA(cudaEventCreateWithFlags(&g->ready[r], cudaEventDisableTiming));
+    TSVD_CUDA(cudaEventCreateWithFlags(&g->done[r], cudaEventDisableTiming));
+  }
+  return g;
+}
+
+void loop_group_destroy(LoopGroup* g) {
+  if (!g) return;
+  for (auto e : g->ready) if (e) cudaEventDestroy(e);
+  for (auto e : g->done) if (e) cudaEventDestroy(e);
+  delete g;
+}
+
+static void loop_barrier(LoopGroup& g) {
+  std::unique_lock<std::mutex> lk(g.mu);
+  const uint64_t my = g.gen;
+  if (++g.count == g.world) {
+    g.count = 0;
+    ++g.gen;
+    g.cv.notify_all();
+  } else {
+    g.cv.wait(lk, [&] { return g.gen != my; });
+  }
+}
+
+struct LoopPtrs {
+  const double* p[kLoopMaxWorld];
+};
+
+// out[i] = sum_k src_k[off + i] (k in rank order)
+__global__ void loop_sum_kernel(LoopPtrs src, int world, size_t off, size_t count,
+                                double* __restrict__ out) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x) {
+    double s = src.p[0][off + i];
+    for (int k = 1; k < world; ++k) s += src.p[k][off + i];
+    out[i] = s;
+  }
+}
+
+// out[k * count + i] = src_k[i]
+__global__ void loop_gather_kernel(LoopPtrs src, int world, size_t count, double* __restrict__ out) {
+  const size_t total = (size_t)world * count;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
+       t += (size_t)gridDim.x * blockDim.x)
+    out[t] = src.p[t / count][t % count];
+}
+
+template <class F>
+static void loop_collective(Ctx& c, const double* send, F&& body) {
+  LoopGroup& g = *c.loop;
+  const int r = c.rank;
+  g.send[r] = send;
+  TSVD_CUDA(cudaEventRecord(g.ready[r], c.st));
+  loop_barrier(g);
+  for (int k = 0; k < g.world; ++k)
+    if (k != r) TSVD_CUDA(cudaStreamWaitEvent(c.st, g.ready[k], 0));
+  LoopPtrs ptrs{};
+  for (int k = 0; k < g.world; ++k) ptrs.p[k] = g.send[k];
+  body(ptrs);
+  TSVD_CUDA(cudaEventRecord(g.done[r], c.st));
+  loop_barrier(g);  // every rank has read every send buffer (on its stream)
+  for (int k = 0; k < g.world; ++k)
+    if (k != r) TSVD_CUDA(cudaStreamWaitEvent(c.st, g.done[k], 0));
+}
+
+static unsigned loop_grid(size_t n) {
+  return (unsigned)std::max<size_t>(1, std::min<size_t>((n + 255) / 256, 148 * 8));
+}
+
+void loop_join(Ctx& c, LoopGroup* g, int rank) {
+  c.loop = g;
+  c.comm = g;  // non-null: the handle takes the multi-GPU code path
 }
 
 // Handles created through tsvd_create_*_dist always run the collectives (also
 // with a single rank, which exercises the multi-GPU path on one GPU).
 void allreduce_sum(Ctx& c, double* buf, size_t count) {
   if (!c.comm || count == 0) return;
+  if (c.loop) {
+    // in place: sum into a private buffer, copy back after every rank has read
+    double* tmp = dbuf(c, "loop_tmp", count);
+    loop_collective(c, buf, [&](const LoopPtrs& p) {
+      loop_sum_kernel<<<loop_grid(count), 256, 0, c.st>>>(p, c.loop->world, 0, count, tmp);
+      TSVD_CHECK_LAUNCH();
+    });
+    TSVD_CUDA(cudaMemcpyAsync(buf, tmp, count * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+    return;
+  }
   check(api().AllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)c.comm, c.st),
         "ncclAllReduce");
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 
 void reduce_scatter_sum(Ctx& c, const double* send, double* recv, size_t recv_count) {
+  if (c.loop) {
+    loop_collective(c, send, [&](const LoopPtrs& p) {
+      loop_sum_kernel<<<loop_grid(recv_count), 256, 0, c.st>>>(
+          p, c.loop->world, (size_t)c.rank * recv_count, recv_count, recv);
+      TSVD_CHECK_LAUNCH();
+    });
+    return;
+  }
   check(api().ReduceScatter(send, recv, recv_count, ncclFloat64, ncclSum, (ncclComm_t)c.comm,
                             c.st),
         "ncclReduceScatter");
@@ -102,6 +233,14 @@ void reduce_scatter_sum(Ctx& c, const double* send, double* recv, size_t recv_co
 }
 
 void all_gather(Ctx& c, const double* send, double* recv, size_t send_count) {
+  if (c.loop) {
+    loop_collective(c, send, [&](const LoopPtrs& p) {
+      loop_gather_kernel<<<loop_grid(send_count * c.loop->world), 256, 0, c.st>>>(
+          p, c.loop->world, send_count, recv);
+      TSVD_CHECK_LAUNCH();
+    });
+    return;
+  }
   check(api().AllGather(send, recv, send_count, ncclFloat64, (ncclComm_t)c.comm, c.st),
         "ncclAllGather");
   g_launches.fetch_add(1, std::memory_order_relaxed);

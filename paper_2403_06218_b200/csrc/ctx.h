@@ -8,6 +8,8 @@
 #include "internal.h"
 
 namespace tsvd {
+struct LoopGroup;
+constexpr int kLoopMaxWorld = 8;
 // P_ROWT: the s = 0 passes (Gram of Y, TRSM-as-multiply S T) - rowT_kernel
 enum ProfCat { P_APPLY_A = 0, P_APPLY_AT, P_TN, P_NN, P_SMALL, P_SVD, P_RESTART, P_OTHER, P_ROWT };
 struct ProfRec {
@@ -24,7 +26,8 @@ struct tsvd_ctx {
   int64_t m = 0, n = 0;
   // multi-GPU; world == 1: mg = m, ng = n, offsets 0, nsh = n
   int world = 1, rank = 0;
-  void* comm = nullptr;        // ncclComm_t
+  void* comm = nullptr;        // ncclComm_t (or the loopback group)
+  tsvd::LoopGroup* loop = nullptr;  // test-only in-process communicator (comm.cu)
   int64_t mg = 0, ng = 0;      // global sizes
   int64_t m0 = 0, n0 = 0;      // global offsets of the local rows / n-shard
   int64_t nsh = 0;             // uniform n-shard size (ceil(ng / world))
@@ -112,6 +115,9 @@ void comm_destroy(Ctx& c);
 void allreduce_sum(Ctx& c, double* buf, size_t count);
 void reduce_scatter_sum(Ctx& c, const double* send, double* recv, size_t recv_count);
 void all_gather(Ctx& c, const double* send, double* recv, size_t send_count);
+LoopGroup* loop_group_create(int world);
+void loop_group_destroy(LoopGroup* g);
+void loop_join(Ctx& c, LoopGroup* g, int rank);
 
 // explicit residuals of the last solve (residual.cu):
 // e[i] = ||A v_i - s_i u_i|| / s_1, rel[i] = ... / s_i (host arrays, may be NULL)

@@ -69,6 +69,17 @@ struct Csr {  // device CSR (canonical)
   int64_t nshort = 0;            // rows with <= kLongRow nonzeros
   int64_t nmed = 0;              // rows with kLongRow < len <= kMedRow
   int32_t* perm = nullptr;       // output row of each position
+  // staged SpMM (spmm.cu, spmm_staged_kernel): rows of equal length L form
+  // a bin of consecutive positions (bins in increasing L, L <= kMedRow);
+  // per bin: L, row count, first position, first nonzero; and for each of
+  // the three chunk sizes NZC = 256 / 128 / 64 (lane groups of 8 / 16 / 32
+  // for w <= 16 / 32 / 64) the prefix of chunks over the bins with L <= NZC
+  int nbins = 0;
+  int64_t* bins = nullptr;       // [nbins][4]: L, count, pos0, nz0
+  int64_t* bin_chunk0[3] = {nullptr, nullptr, nullptr};  // [nbins_v + 1]
+  int nbins_v[3] = {0, 0, 0};    // bins with L <= NZC_v (a prefix)
+  int64_t nchunks[3] = {0, 0, 0};
+  int64_t med_gt[3] = {0, 0, 0}; // medium rows longer than NZC_v (warp-per-row path)
 };
 
 

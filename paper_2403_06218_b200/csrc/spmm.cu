@@ -13,11 +13,14 @@
 //    rows with several segments write partials that a fix-up kernel sums in
 //    segment order.  Deterministic: no floating-point atomics anywhere.
 #include <algorithm>
+#include <array>
+#include <cstdlib>
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace tsvd {
 
@@ -230,16 +233,17 @@ template <int L, int VEC>
 __global__ void __launch_bounds__(256) spmm_kernel(Csr A, const double* __restrict__ X,
                                                    int64_t ldx, double* __restrict__ Y,
                                                    int64_t ldy, int w, double* __restrict__ part,
-                                                   int64_t nb_long, int64_t nb_med) {
+                                                   int64_t nb_long, int64_t nb_med,
+                                                   int64_t nmed_run, int64_t nshort_run) {
   const int64_t b = blockIdx.x;
   if (b < nb_long) {
     spmm_long_dev<L, VEC>(A.seg_row, A.seg_beg, A.seg_end, A.seg_slot, A.colidx, A.vals, X, ldx,
                           Y, ldy, w, part, b);
   } else if (b < nb_long + nb_med) {
     spmm_medium_dev<L, VEC>(A.rowptr + A.nshort, A.colidx, A.vals, X, ldx, Y, ldy,
-                            A.perm + A.nshort, A.nmed, w, b - nb_long);
+                            A.perm + A.nshort, nmed_run, w, b - nb_long);
   } else {
-    spmm_short_dev<L, VEC>(A.rowptr, A.colidx, A.vals, X, ldx, Y, ldy, A.perm, A.nshort, w,
+    spmm_short_dev<L, VEC>(A.rowptr, A.colidx, A.vals, X, ldx, Y, ldy, A.perm, nshort_run, w,
                            b - nb_long - nb_med);
   }
 }
@@ -259,18 +263,294 @@ __global__ void spmm_fixup_kernel(const int64_t* __restrict__ split_row,
   Y[split_row[r] * ldy + c] = sum;
 }
 
+// nmed_run / nshort_run: how many medium / short rows this launch covers
+// (the first ones of each section; -1 = all).  With the staged kernel only
+// the medium rows longer than its chunk go here.
 template <int L, int VEC>
 static void spmm_dispatch(const Csr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
-                          int w, double* part, cudaStream_t st) {
+                          int w, double* part, cudaStream_t st, int64_t nmed_run = -1,
+                          int64_t nshort_run = -1, bool fixup = true) {
   constexpr int RPW = 32 / L;
+  if (nmed_run < 0) nmed_run = A.nmed;
+  if (nshort_run < 0) nshort_run = A.nshort;
   const int64_t rows_per_block = 8 * RPW;
-  const int64_t nb_short = (A.nshort + rows_per_block - 1) / rows_per_block;
-  const int64_t nb_med = (A.nmed + 7) / 8;
+  const int64_t nb_short = (nshort_run + rows_per_block - 1) / rows_per_block;
+  const int64_t nb_med = (nmed_run + 7) / 8;
   const int64_t nb_long = A.nseg;
   const int64_t blocks = nb_short + nb_med + nb_long;
   if (blocks > 0) {
     spmm_kernel<L, VEC><<<(unsigned)blocks, 256, 0, st>>>(A, X, ldx, Y, ldy, w, part, nb_long,
-                                                           nb_med);
+                                                           nb_med, nmed_run, nshort_run);
+    TSVD_CHECK_LAUNCH();
+  }
+  if (fixup && A.nsplit > 0) {
+    const int64_t thr = A.nsplit * kPartW;
+    spmm_fixup_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(
+        A.split_row, A.split_first, A.split_count, part, Y, ldy, w, A.nsplit);
+    TSVD_CHECK_LAUNCH();
+  }
+}
+
+
+// ------------------------------------------------------- staged SpMM ---
+// Rows of length L <= NZC (nonzeros per chunk) go in chunks of R = NZC / L
+// rows of one length bin (ELL-like: the row pointer is never read; a
+// chunk's nonzeros are one contiguous range of the row-sorted arrays).
+// Persistent CTAs = 8 consumer warps + 1 producer warp, two mbarrier rings
+// in shared memory:
+//   * index ring (NIS stages): a chunk's colidx, vals and output rows arrive
+//     by three 1-D bulk copies (TMA engine, SASS UBLKCP), NIS - 1 chunks
+//     ahead of the gathers that need them;
+//   * gather ring (NXS stages): the producer warp gathers the X row of every
+//     nonzero (2 LPR doubles) with TMA tile::gather4 (4 rows per
+//     instruction, SASS UTMALDG), NXS - 1 chunks ahead of the consumers.
+// So no register holds an in-flight gather, no gather waits behind an index
+// load in the same thread, and the number of gathers in flight is bounded by
+// shared memory (3 x 32 KB per SM).  Consumers multiply from shared memory:
+// groups of LPR lanes own a row (or, for long rows, S = 2^k consecutive
+// slices of it whose partials are summed in slice order).  Deterministic,
+// no atomics.
+template <int LPR>
+struct StagedCfg {
+  static constexpr int NZC = 2048 / LPR;          // nonzeros per chunk (256 / 128 / 64)
+  static constexpr int G = 256 / LPR;             // lane groups of the 8 consumer warps
+  static constexpr int NXS = 4;                   // gather stages
+  static constexpr int NIS = 8;                   // index stages
+  static constexpr int XROWS = NZC + 4;           // gather4 pads the last group of 4
+  static constexpr int XD = XROWS * LPR * 2;      // doubles per gather stage (~32 KB)
+  static constexpr int CI = NZC + 4, VI = NZC + 2, PI = NZC + 4;  // index stage sizes
+  static constexpr int IDXB = ((CI * 4 + VI * 8 + PI * 4) + 15) / 16 * 16;
+  static constexpr int MAXB = 260;                // bins with L <= NZC (L = 0..256)
+  static constexpr size_t x_off = 0;
+  static constexpr size_t i_off = x_off + (size_t)NXS * XD * 8;
+  static constexpr size_t r_off = i_off + (size_t)NIS * IDXB;
+  static constexpr size_t b_off = r_off + (size_t)G * LPR * 16;
+  static constexpr size_t bar_off = b_off + (size_t)MAXB * 40;
+  static constexpr size_t bytes = bar_off + (size_t)(2 * NIS + 2 * NXS) * 8 + 128;
+};
+
+struct ChunkGeo {
+  int L, nr;          // row length, rows in this chunk
+  int64_t pos, nz;    // first position, first nonzero
+};
+
+__device__ __forceinline__ ChunkGeo chunk_geo(int64_t c, int nb, int nzc, const int* sL,
+                                              const int64_t* sCnt, const int64_t* sPos,
+                                              const int64_t* sNz, const int64_t* sC0) {
+  int lo = 0, hi = nb;  // last bin with sC0[bin] <= c
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (sC0[mid] <= c) lo = mid; else hi = mid;
+  }
+  ChunkGeo g;
+  g.L = sL[lo];
+  const int64_t R = g.L ? max(1, nzc / g.L) : nzc;
+  const int64_t j = c - sC0[lo];
+  g.pos = sPos[lo] + j * R;
+  g.nr = (int)min(R, sCnt[lo] - j * R);
+  g.nz = sNz[lo] + j * R * g.L;
+  return g;
+}
+
+template <int LPR>
+__global__ void __launch_bounds__(288, 1) spmm_staged_kernel(
+    const __grid_constant__ CUtensorMap xmap, const int32_t* __restrict__ colidx,
+    const double* __restrict__ vals, const int32_t* __restrict__ perm,
+    const int64_t* __restrict__ bins, const int64_t* __restrict__ chunk0, int nb,
+    int64_t nchunks, double* __restrict__ Y, int64_t ldy, int w) {
+  using C = StagedCfg<LPR>;
+  constexpr int NZC = C::NZC, G = C::G, NXS = C::NXS, NIS = C::NIS, XW = 2 * LPR;
+  extern __shared__ __align__(128) unsigned char smraw[];
+  double* xs = reinterpret_cast<double*>(smraw + C::x_off);
+  unsigned char* idx = smraw + C::i_off;
+  double2* red = reinterpret_cast<double2*>(smraw + C::r_off);
+  int64_t* sCnt = reinterpret_cast<int64_t*>(smraw + C::b_off);
+  int64_t* sPos = sCnt + C::MAXB;
+  int64_t* sNz = sPos + C::MAXB;
+  int64_t* sC0 = sNz + C::MAXB;
+  int* sL = reinterpret_cast<int*>(sC0 + C::MAXB);
+  uint64_t* ifull = reinterpret_cast<uint64_t*>(smraw + C::bar_off);
+  uint64_t* iempty = ifull + NIS;
+  uint64_t* xfull = iempty + NIS;
+  uint64_t* xempty = xfull + NXS;
+  // per index stage: offsets of colidx / vals / perm inside it, L, rows
+  __shared__ int sMeta[NIS][5];
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  for (int b = tid; b < nb; b += 288) {
+    sL[b] = (int)bins[4 * b];
+    sCnt[b] = bins[4 * b + 1];
+    sPos[b] = bins[4 * b + 2];
+    sNz[b] = bins[4 * b + 3];
+    sC0[b] = chunk0[b];
+  }
+  if (tid == 0) {
+    for (int i = 0; i < NIS; ++i) {
+      mbar_init(&ifull[i], 1);
+      mbar_init(&iempty[i], 8);
+    }
+    for (int i = 0; i < NXS; ++i) {
+      mbar_init(&xfull[i], 1);
+      mbar_init(&xempty[i], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t c0 = blockIdx.x, cs = gridDim.x;
+  const int64_t nmine = c0 < nchunks ? (nchunks - 1 - c0) / cs + 1 : 0;
+  auto stage_ci = [&](int s) { return reinterpret_cast<int32_t*>(idx + (size_t)s * C::IDXB); };
+  auto stage_va = [&](int s) {
+    return reinterpret_cast<double*>(idx + (size_t)s * C::IDXB + C::CI * 4);
+  };
+  auto stage_pm = [&](int s) {
+    return reinterpret_cast<int32_t*>(idx + (size_t)s * C::IDXB + C::CI * 4 + C::VI * 8);
+  };
+
+  if (warp == 8) {
+    // ---------------------------------------------------------- producer --
+    auto issue_idx = [&](int64_t i) {  // lane 0: bulk-copy chunk i's index data
+      const int s = (int)(i % NIS);
+      if (i >= NIS) mbar_wait(&iempty[s], (unsigned)((i / NIS - 1) & 1));
+      const ChunkGeo cg = chunk_geo(c0 + i * cs, nb, NZC, sL, sCnt, sPos, sNz, sC0);
+      const int64_t n = (int64_t)cg.nr * cg.L;
+      const int64_t ca0 = cg.nz & ~3LL, ca1 = (cg.nz + n + 3) & ~3LL;
+      const int64_t va0 = cg.nz & ~1LL, va1 = (cg.nz + n + 1) & ~1LL;
+      const int64_t pa0 = cg.pos & ~3LL, pa1 = (cg.pos + cg.nr + 3) & ~3LL;
+      const unsigned cb = n ? (unsigned)(ca1 - ca0) * 4 : 0;
+      const unsigned vb = n ? (unsigned)(va1 - va0) * 8 : 0;
+      const unsigned pb = (unsigned)(pa1 - pa0) * 4;
+      sMeta[s][0] = (int)(cg.nz - ca0);
+      sMeta[s][1] = (int)(cg.nz - va0);
+      sMeta[s][2] = (int)(cg.pos - pa0);
+      sMeta[s][3] = cg.L;
+      sMeta[s][4] = cg.nr;
+      mbar_expect_tx(&ifull[s], cb + vb + pb);  // release: sMeta visible to waiters
+      if (cb) bulk_load(stage_ci(s), colidx + ca0, cb, &ifull[s]);
+      if (vb) bulk_load(stage_va(s), vals + va0, vb, &ifull[s]);
+      bulk_load(stage_pm(s), perm + pa0, pb, &ifull[s]);
+    };
+    if (lane == 0)
+      for (int64_t i = 0; i < NIS - 1 && i < nmine; ++i) issue_idx(i);
+    for (int64_t i = 0; i < nmine; ++i) {
+      if (lane == 0 && i + NIS - 1 < nmine) issue_idx(i + NIS - 1);
+      const int s = (int)(i % NIS), xsl = (int)(i % NXS);
+      mbar_wait(&ifull[s], (unsigned)((i / NIS) & 1));
+      if (i >= NXS) mbar_wait(&xempty[xsl], (unsigned)((i / NXS - 1) & 1));
+      const int n = sMeta[s][3] * sMeta[s][4];
+      const int n4 = (n + 3) >> 2;
+      if (lane == 0) mbar_expect_tx(&xfull[xsl], (unsigned)n4 * 4 * XW * 8);
+      __syncwarp();
+      const int32_t* ci = stage_ci(s) + sMeta[s][0];
+      double* xd = xs + (size_t)xsl * C::XD;
+      for (int k4 = lane; k4 < n4; k4 += 32) {
+        const int k = 4 * k4;
+        const int r0 = ci[k];
+        const int r1 = k + 1 < n ? ci[k + 1] : r0;
+        const int r2 = k + 2 < n ? ci[k + 2] : r0;
+        const int r3 = k + 3 < n ? ci[k + 3] : r0;
+        tma_gather4(xd + (size_t)k * XW, &xmap, 0, r0, r1, r2, r3, &xfull[xsl]);
+      }
+    }
+    return;
+  }
+  // ------------------------------------------------------------ consumers --
+  const int g = tid / LPR, ln = tid % LPR;
+  const bool lane_on = 2 * ln < w;
+  for (int64_t i = 0; i < nmine; ++i) {
+    const int s = (int)(i % NIS), xsl = (int)(i % NXS);
+    mbar_wait(&xfull[xsl], (unsigned)((i / NXS) & 1));
+    mbar_wait(&ifull[s], (unsigned)((i / NIS) & 1));  // long complete (gathers need it)
+    const double* va = stage_va(s) + sMeta[s][1];
+    const int32_t* pm = stage_pm(s) + sMeta[s][2];
+    const double2* xd = reinterpret_cast<const double2*>(xs + (size_t)xsl * C::XD);
+    const int L = sMeta[s][3], nr = sMeta[s][4];
+    const int R = L ? max(1, NZC / L) : NZC;
+    // slices per row: the largest power of two <= G / R (1 if R >= G)
+    int lgS = 0;
+    while (R < G && (2 << lgS) * R <= G) ++lgS;
+    const int S = 1 << lgS;
+    for (int task = g; task < (nr << lgS); task += G) {
+      const int r = task >> lgS, sl = task & (S - 1);
+      const int k0 = r * L + ((sl * L) >> lgS), k1 = r * L + (((sl + 1) * L) >> lgS);
+      double a0 = 0.0, a1 = 0.0;
+      for (int k = k0; k < k1; ++k) {
+        const double v = va[k];
+        const double2 x = xd[k * LPR + ln];
+        a0 = fma(v, x.x, a0);
+        a1 = fma(v, x.y, a1);
+      }
+      if (S == 1) {
+        if (lane_on)
+          *reinterpret_cast<double2*>(Y + (int64_t)pm[r] * ldy + 2 * ln) = make_double2(a0, a1);
+      } else {
+        red[task * LPR + ln] = make_double2(a0, a1);
+      }
+    }
+    if (S > 1) {
+      bar_consumers();
+      for (int t = tid; t < nr * LPR; t += 256) {
+        const int r = t / LPR, l2 = t % LPR;
+        double a0 = 0.0, a1 = 0.0;
+        for (int sl = 0; sl < S; ++sl) {
+          const double2 p = red[((r << lgS) + sl) * LPR + l2];
+          a0 += p.x;
+          a1 += p.y;
+        }
+        if (2 * l2 < w)
+          *reinterpret_cast<double2*>(Y + (int64_t)pm[r] * ldy + 2 * l2) = make_double2(a0, a1);
+      }
+      bar_consumers();  // red is reused by the next chunk
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&xempty[xsl]);
+      mbar_arrive(&iempty[s]);
+    }
+  }
+}
+
+static bool g_spmm_staged = [] {
+  const char* e = getenv("TSVD_SPMM_STAGED");
+  return !(e && e[0] == '0');
+}();
+
+// X (rows x w, ld) as a 2-D tensor for tile::gather4: box = {2 LPR, 1}
+// (columns >= w are zero-filled by the copy engine)
+static bool gather_map(CUtensorMap* m, const double* X, int64_t rows, int w, int64_t ldx,
+                       int box_cols) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || rows < 1 || rows > ((int64_t)1 << 31) || ((uintptr_t)X & 15) || (ldx & 1))
+    return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)w, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldx * 8};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, 1};
+  const cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)X, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int LPR>
+static bool staged_launch(const Csr& A, const double* X, int64_t ldx, double* Y, int64_t ldy,
+                          int w, double* part, int v, cudaStream_t st) {
+  using C = StagedCfg<LPR>;
+  constexpr int VL = LPR == 8 ? 8 : LPR == 16 ? 16 : 32;  // spmm_kernel lane-group width
+  CUtensorMap xmap;
+  if (A.nchunks[v] > 0 && !gather_map(&xmap, X, A.cols, w, ldx, 2 * LPR)) return false;
+  // medium rows longer than a chunk + long-row segments: warp / CTA path
+  spmm_dispatch<VL, 2>(A, X, ldx, Y, ldy, w, part, st, A.med_gt[v], 0, false);
+  if (A.nchunks[v] > 0) {
+    static bool attr = false;
+    if (!attr) {
+      TSVD_CUDA(cudaFuncSetAttribute(spmm_staged_kernel<LPR>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::bytes));
+      attr = true;
+    }
+    const unsigned grid = (unsigned)std::min<int64_t>(A.nchunks[v], 148);
+    spmm_staged_kernel<LPR><<<grid, 288, C::bytes, st>>>(xmap, A.colidx, A.vals, A.perm, A.bins,
+                                                         A.bin_chunk0[v], A.nbins_v[v],
+                                                         A.nchunks[v], Y, ldy, w);
     TSVD_CHECK_LAUNCH();
   }
   if (A.nsplit > 0) {
@@ -279,12 +559,19 @@ static void spmm_dispatch(const Csr& A, const double* X, int64_t ldx, double* Y,
         A.split_row, A.split_first, A.split_count, part, Y, ldy, w, A.nsplit);
     TSVD_CHECK_LAUNCH();
   }
+  return true;
 }
 
 void launch_spmm(const Csr& A, const double* X, int64_t ldx, double* Y, int64_t ldy, int w,
                  double* part, cudaStream_t st) {
   const bool v2 = (w % 2 == 0) && (ldx % 2 == 0) && (ldy % 2 == 0) &&
                   ((uintptr_t)X % 16 == 0) && ((uintptr_t)Y % 16 == 0);
+  if (v2 && g_spmm_staged && A.bins && w > 4) {
+    if (w <= 16 ? staged_launch<8>(A, X, ldx, Y, ldy, w, part, 0, st)
+                : w <= 32 ? staged_launch<16>(A, X, ldx, Y, ldy, w, part, 1, st)
+                          : staged_launch<32>(A, X, ldx, Y, ldy, w, part, 2, st))
+      return;
+  }
   if (v2) {
     if (w <= 2)
       spmm_dispatch<1, 2>(A, X, ldx, Y, ldy, w, part, st);
@@ -417,6 +704,43 @@ void csr_build_plan(Csr& A, const int64_t* hrp, cudaStream_t st) {
   up64(sprow, &A.split_row);
   up32(spfirst, &A.split_first);
   up32(spcnt, &A.split_count);
+  // staged SpMM bins: runs of equal length among the rows <= kMedRow (the
+  // sorted sections make every length one contiguous run of positions)
+  {
+    std::vector<std::array<int64_t, 4>> bins;  // L, count, pos0, nz0
+    for (int64_t q = 0; q < nshort + nmed;) {
+      const int64_t L = len_of(perm[q]);
+      int64_t e = q + 1;
+      while (e < nshort + nmed && len_of(perm[e]) == L) ++e;
+      bins.push_back({L, e - q, q, nrp[q]});
+      q = e;
+    }
+    std::stable_sort(bins.begin(), bins.end(),
+                     [](const auto& a, const auto& b) { return a[0] < b[0]; });
+    A.nbins = (int)bins.size();
+    std::vector<int64_t> flat;
+    for (auto& b : bins) flat.insert(flat.end(), b.begin(), b.end());
+    if (!flat.empty()) up64(flat, &A.bins);
+    const int nzc[3] = {256, 128, 64};
+    for (int v = 0; v < 3; ++v) {
+      std::vector<int64_t> c0(1, 0);
+      int nb = 0;
+      for (auto& b : bins) {
+        if (b[0] > nzc[v]) break;
+        const int64_t R = b[0] ? std::max<int64_t>(1, nzc[v] / b[0]) : nzc[v];
+        c0.push_back(c0.back() + (b[1] + R - 1) / R);
+        ++nb;
+      }
+      A.nbins_v[v] = nb;
+      A.nchunks[v] = c0.back();
+      int64_t gt = 0;
+      for (int64_t q = nshort; q < nshort + nmed; ++q)
+        if (len_of(perm[q]) > nzc[v]) ++gt;
+      A.med_gt[v] = gt;
+      up64(c0, &A.bin_chunk0[v]);
+    }
+  }
+  perm.resize(A.rows + 4, 0);  // bulk copies read whole 16-byte pieces
   up32(perm, &A.perm);
   // move the nonzeros into the permuted layout
   int64_t* new_rp = nullptr;
@@ -424,8 +748,8 @@ void csr_build_plan(Csr& A, const int64_t* hrp, cudaStream_t st) {
   if (A.rows > 0 && A.nnz > 0) {
     int32_t* nci;
     double* nva;
-    dmalloc_t(&nci, A.nnz, st);
-    dmalloc_t(&nva, A.nnz, st);
+    dmalloc_t(&nci, A.nnz + 4, st);  // +padding: bulk copies read whole 16-byte pieces
+    dmalloc_t(&nva, A.nnz + 2, st);
     // one warp per row, up to 64 CTAs per SM in flight (latency-bound)
     const unsigned pg = (unsigned)std::min<int64_t>((A.rows + 7) / 8, 148 * 64);
     csr_permute_kernel<<<pg, 256, 0, st>>>(A.rowptr, A.colidx, A.vals, A.perm, new_rp,
@@ -453,6 +777,8 @@ void csr_free(Csr& A, cudaStream_t st) {
   dfree(A.split_first, st);
   dfree(A.split_count, st);
   dfree(A.perm, st);
+  dfree(A.bins, st);
+  for (auto& p : A.bin_chunk0) dfree(p, st);
   A = Csr{};
 }
 

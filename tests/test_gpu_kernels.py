@@ -289,7 +289,7 @@ def test_small_svd_parity(d, kind):
     Vb = torch.zeros((d, d), dtype=torch.float64, device="cuda")
     S = torch.zeros(d, dtype=torch.float64, device="cuda")
     sweeps = T.dbg_small_svd(cu(B), Ub, S, Vb)
-    assert sweeps < 30
+    assert sweeps < 60
     Ug, Sg, Vg = Ub.cpu().numpy(), S.cpu().numpy(), Vb.cpu().numpy()
     tol = 10 * d * U * So[0]
     assert np.abs(Sg - So).max() <= tol
