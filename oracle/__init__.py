@@ -23,7 +23,7 @@ breakdown branch near its threshold.
 """
 from .philox import gaussian_block, philox4x32_10  # noqa: F401
 from .core import (  # noqa: F401
-    Operator, DrawCtx, chol, trsm_right_lt, cholqr2, cgs_cqr2, cgs2, cgs_qr,
+    Operator, DrawCtx, chol, trsm_right_lt, cholqr2, cgs_cqr2, bcgs_pip2, cgs2, cgs_qr,
     small_svd, sign_normalize,
 )
 from .lancsvd import lancsvd, lancsvd_threshold  # noqa: F401

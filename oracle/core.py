@@ -165,6 +165,44 @@ def cgs_cqr2(Y, P, ctx: DrawCtx):
     return Q, H, R
 
 
+def bcgs_pip2(Y, P, ctx: DrawCtx):
+    """BCGS-PIP+ (reading R34): block classical Gram-Schmidt
+    with the Pythagorean inner product, run twice (reorthogonalisation).
+    NOT in the paper: the communication-reducing alternative to Alg. 5
+    (CGS-CQR2) whose every pass needs ONE reduction, [P Y]^T Y, instead of
+    two (P^T Y, then the Gram of the projected block), and no separate pass
+    for the TRSM.  Written from its definition (block Gram-Schmidt with the
+    Pythagorean Cholesky; Barlow 2019, Carson et al. 2022):
+      pass(Y):  H = P^T Y,  W = Y^T Y          (one reduction)
+                L = chol(W - H^T H)            (Pythagorean: = Y'^T Y', Y' = Y - P H)
+                Q = (Y - P H) L^{-T},  R = L^T
+      Q1, H1, R1 = pass(Y);  Q, H2, R2 = pass(Q1)
+      H = H1 + H2 R1,  R = R2 R1               (Y = P H + Q R)
+    Breakdown (a pivot <= 0 or non-finite in either pass) -> the same CGS2
+    fallback as Alg. 5 (reading R16).  Returns (Q, H, R)."""
+    if P is None or P.shape[1] == 0:
+        Q, R = cholqr2(Y, ctx)
+        return Q, np.zeros((0, Y.shape[1])), R
+
+    def one_pass(Z):
+        H = P.T @ Z
+        W = Z.T @ Z
+        L = chol(W - H.T @ H)
+        if L is None:
+            return None
+        return trsm_right_lt(Z - P @ H, L), H, L.T
+
+    p1 = one_pass(Y)
+    if p1 is None:
+        return cgs2(Y, P, ctx)
+    Q1, H1, R1 = p1
+    p2 = one_pass(Q1)
+    if p2 is None:
+        return cgs2(Y, P, ctx)
+    Q, H2, R2 = p2
+    return Q, H1 + H2 @ R1, R2 @ R1
+
+
 def cgs_qr(Y, bq: int, ctx: DrawCtx):
     """Alg. 3 CGS-QR with panels of bq columns; the last panel
     may be narrower (reading R8).  Returns (Q, R), R block upper triangular

@@ -38,7 +38,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .core import DrawCtx, cholqr2, cgs_cqr2, small_svd, sign_normalize
+from .core import DrawCtx, bcgs_pip2, cholqr2, cgs_cqr2, small_svd, sign_normalize
 from .philox import gaussian_block
 
 
@@ -55,8 +55,12 @@ class LancResult:
 
 
 def lancsvd(op, r: int, b: int, d: int, tol: float, maxit: int, seed: int,
-            start=None, debug: bool = False, keep: int = 0) -> LancResult:
+            start=None, debug: bool = False, keep: int = 0,
+            ortho: str = "cgs_cqr2") -> LancResult:
+    """ortho: the block orthogonalisation of S3b / S5 -- "cgs_cqr2" (the
+    paper's Alg. 5) or "bcgs_pip2" (SURVEY 8(f) N2 ablation, core.bcgs_pip2)."""
     m, n = op.m, op.n
+    orth = {"cgs_cqr2": cgs_cqr2, "bcgs_pip2": bcgs_pip2}[ortho]
     assert m >= n and 1 <= r <= d <= n and d % b == 0 and maxit >= 1
     assert keep == 0 or (keep % b == 0 and r <= keep < d)
     ctx = DrawCtx(seed)
@@ -86,11 +90,11 @@ def lancsvd(op, r: int, b: int, d: int, tol: float, maxit: int, seed: int,
             if lo == 0:
                 Q, R = cholqr2(Y, ctx)                           # S3a
             else:
-                Q, _, R = cgs_cqr2(Y, P[:, :lo], ctx)            # S3b
+                Q, _, R = orth(Y, P[:, :lo], ctx)                # S3b
             P[:, lo:hi] = Q
             B[lo:hi, lo:hi] = R.T                                # L_i
             Z = op.matmul(Q)                                     # S4
-            Qb, _, Rb = cgs_cqr2(Z, Pbar[:, :hi], ctx)           # S5
+            Qb, _, Rb = orth(Z, Pbar[:, :hi], ctx)               # S5
             Pbar[:, hi:hi + b] = Qb
             if i < k - 1:
                 B[hi:hi + b, lo:hi] = Rb                         # Rbar_i

@@ -316,6 +316,9 @@ struct StagedCfg {
   static constexpr int G = 256 / LPR;             // lane groups of the 8 consumer warps
   static constexpr int NXS = 4;                   // gather stages
   static constexpr int NIS = 8;                   // index stages
+  static constexpr int NPW = 4;                   // producer warps (gather4 issue is per
+                                                  // lane-serialised: one warp per SMSP)
+  static constexpr int NTHR = 256 + 32 * NPW;
   static constexpr int XROWS = NZC + 4;           // gather4 pads the last group of 4
   static constexpr int XD = XROWS * LPR * 2;      // doubles per gather stage (~32 KB)
   static constexpr int CI = NZC + 4, VI = NZC + 2, PI = NZC + 4;  // index stage sizes
@@ -353,7 +356,7 @@ __device__ __forceinline__ ChunkGeo chunk_geo(int64_t c, int nb, int nzc, const 
 }
 
 template <int LPR>
-__global__ void __launch_bounds__(288, 1) spmm_staged_kernel(
+__global__ void __launch_bounds__(StagedCfg<LPR>::NTHR, 1) spmm_staged_kernel(
     const __grid_constant__ CUtensorMap xmap, const int32_t* __restrict__ colidx,
     const double* __restrict__ vals, const int32_t* __restrict__ perm,
     const int64_t* __restrict__ bins, const int64_t* __restrict__ chunk0, int nb,
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(288, 1) spmm_staged_kernel(
   __shared__ int sMeta[NIS][5];
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int b = tid; b < nb; b += 288) {
+  for (int b = tid; b < nb; b += C::NTHR) {
     sL[b] = (int)bins[4 * b];
     sCnt[b] = bins[4 * b + 1];
     sPos[b] = bins[4 * b + 2];
@@ -407,8 +410,13 @@ __global__ void __launch_bounds__(288, 1) spmm_staged_kernel(
     return reinterpret_cast<int32_t*>(idx + (size_t)s * C::IDXB + C::CI * 4 + C::VI * 8);
   };
 
-  if (warp == 8) {
-    // ---------------------------------------------------------- producer --
+  if (warp >= 8) {
+    // --------------------------------------------------------- producers --
+    // warp 8 lane 0 also streams the index data; all producer warps split a
+    // chunk's gather4s (the first expect_tx may trail some complete_tx: the
+    // transaction count may go transiently negative, the phase cannot
+    // complete before the arrival)
+    const int pw = warp - 8;
     auto issue_idx = [&](int64_t i) {  // lane 0: bulk-copy chunk i's index data
       const int s = (int)(i % NIS);
       if (i >= NIS) mbar_wait(&iempty[s], (unsigned)((i / NIS - 1) & 1));
@@ -430,20 +438,19 @@ __global__ void __launch_bounds__(288, 1) spmm_staged_kernel(
       if (vb) bulk_load(stage_va(s), vals + va0, vb, &ifull[s]);
       bulk_load(stage_pm(s), perm + pa0, pb, &ifull[s]);
     };
-    if (lane == 0)
+    if (pw == 0 && lane == 0)
       for (int64_t i = 0; i < NIS - 1 && i < nmine; ++i) issue_idx(i);
     for (int64_t i = 0; i < nmine; ++i) {
-      if (lane == 0 && i + NIS - 1 < nmine) issue_idx(i + NIS - 1);
+      if (pw == 0 && lane == 0 && i + NIS - 1 < nmine) issue_idx(i + NIS - 1);
       const int s = (int)(i % NIS), xsl = (int)(i % NXS);
       mbar_wait(&ifull[s], (unsigned)((i / NIS) & 1));
       if (i >= NXS) mbar_wait(&xempty[xsl], (unsigned)((i / NXS - 1) & 1));
       const int n = sMeta[s][3] * sMeta[s][4];
       const int n4 = (n + 3) >> 2;
-      if (lane == 0) mbar_expect_tx(&xfull[xsl], (unsigned)n4 * 4 * XW * 8);
-      __syncwarp();
+      if (pw == 0 && lane == 0) mbar_expect_tx(&xfull[xsl], (unsigned)n4 * 4 * XW * 8);
       const int32_t* ci = stage_ci(s) + sMeta[s][0];
       double* xd = xs + (size_t)xsl * C::XD;
-      for (int k4 = lane; k4 < n4; k4 += 32) {
+      for (int k4 = pw * 32 + lane; k4 < n4; k4 += 32 * C::NPW) {
         const int k = 4 * k4;
         const int r0 = ci[k];
         const int r1 = k + 1 < n ? ci[k + 1] : r0;
@@ -548,7 +555,7 @@ static bool staged_launch(const Csr& A, const double* X, int64_t ldx, double* Y,
       attr = true;
     }
     const unsigned grid = (unsigned)std::min<int64_t>(A.nchunks[v], 148);
-    spmm_staged_kernel<LPR><<<grid, 288, C::bytes, st>>>(xmap, A.colidx, A.vals, A.perm, A.bins,
+    spmm_staged_kernel<LPR><<<grid, C::NTHR, C::bytes, st>>>(xmap, A.colidx, A.vals, A.perm, A.bins,
                                                          A.bin_chunk0[v], A.nbins_v[v],
                                                          A.nchunks[v], Y, ldy, w);
     TSVD_CHECK_LAUNCH();

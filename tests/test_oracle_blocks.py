@@ -11,7 +11,8 @@ import numpy as np
 import pytest
 
 import oracle
-from oracle.core import DrawCtx, chol, trsm_right_lt, cholqr2, cgs_cqr2, cgs2, cgs_qr, small_svd
+from oracle.core import (DrawCtx, chol, trsm_right_lt, cholqr2, cgs_cqr2, bcgs_pip2, cgs2, cgs_qr,
+                         small_svd)
 from oracle.philox import philox4x32_10, gaussian_from_words, gaussian_block
 
 U = 2.0 ** -53
@@ -128,6 +129,46 @@ def test_cgs_cqr2_invariants(kappa):
     # of [P | Y] itself
     cond = np.linalg.cond(np.hstack([P, Y]))
     assert np.abs(Q - Qlast).max() <= 1e-14 * cond
+
+
+@pytest.mark.parametrize("kappa", [1.0, 1e3, 1e6])
+def test_bcgs_pip2_invariants(kappa):
+    """BCGS-PIP+ (reading R34) pinned by what fixes a block QR:
+    Q^T Q = I, P^T Q = 0, Y = P H + Q R with R upper triangular and positive
+    diagonal -- so Q equals the last block of the Householder Q of [P | Y]
+    and (Q, H, R) equal CGS-CQR2's (the QR with positive diagonal is
+    unique) to O(u cond).  A dropped R1 in H = H1 + H2 R1, or R1 R2 for
+    R2 R1, breaks Y = P H + Q R here (the second pass is not a no-op in
+    floating point, and R1 is far from I)."""
+    rng = np.random.default_rng(7)
+    q, s, w = 600, 32, 8
+    P, _ = np.linalg.qr(rng.standard_normal((q, s)))
+    Y = 0.5 * P @ rng.standard_normal((s, w)) + _cond_matrix(q, w, kappa, rng, 3.0)
+    Q, H, R = bcgs_pip2(Y, P, DrawCtx(0))
+    assert np.abs(P.T @ Q).max() <= 100 * U
+    assert np.abs(Q.T @ Q - np.eye(w)).max() <= 10 * w * U
+    assert np.linalg.norm(Y - P @ H - Q @ R) / np.linalg.norm(Y) <= 100 * U
+    assert np.allclose(np.tril(R, -1), 0.0) and np.all(np.diag(R) > 0)
+    cond = np.linalg.cond(np.hstack([P, Y]))
+    Qh, Rh = _householder_posdiag(np.hstack([P, Y]))
+    assert np.abs(Q - Qh[:, s:]).max() <= 1e-14 * cond
+    Qc, Hc, Rc = cgs_cqr2(Y, P, DrawCtx(0))
+    assert np.abs(Q - Qc).max() <= 1e-14 * cond
+    assert np.abs(R - Rc).max() <= 1e-14 * cond * np.abs(Rc).max()
+    assert np.abs(H - Hc).max() <= 1e-14 * cond * np.abs(Hc).max()
+
+
+def test_bcgs_pip2_breakdown_falls_back_to_cgs2():
+    """A column inside span(P) makes W - H^T H singular (the Pythagorean
+    Cholesky breaks down): the P:275 fallback gives exactly cgs2's result."""
+    rng = np.random.default_rng(4)
+    q = 60
+    P, _ = np.linalg.qr(rng.standard_normal((q, 5)))
+    Y = np.stack([rng.standard_normal(q), P[:, 0] * 3.0, rng.standard_normal(q)], axis=1)
+    Q, H, R = bcgs_pip2(Y, P, DrawCtx(11))
+    Qd, Hd, Rd = cgs2(Y, P, DrawCtx(11))
+    assert np.array_equal(Q, Qd) and np.array_equal(R, Rd) and np.array_equal(H, Hd)
+    assert R[1, 1] == 0.0
 
 
 def test_cgs_cqr2_with_empty_basis_is_cholqr2():

@@ -66,9 +66,11 @@ def test_blockdiag_csr_spectrum_closed_form():
     assert np.allclose(sig[:20], top)
 
 
-def test_lancsvd_c1_closed_form():
+@pytest.mark.parametrize("ortho", ["cgs_cqr2", "bcgs_pip2"])
+def test_lancsvd_c1_closed_form(ortho):
     op, s = _c1()
-    res = oracle.lancsvd(op, r=10, b=4, d=28, tol=1e-12, maxit=8, seed=SEEDS["C1"], debug=True)
+    res = oracle.lancsvd(op, r=10, b=4, d=28, tol=1e-12, maxit=8, seed=SEEDS["C1"], debug=True,
+                         ortho=ortho)
     assert res.converged
     assert np.abs(res.S - s[:10]).max() / s[0] <= 1e-10
     e, _ = oracle.residuals(op, res.U, res.S, res.V)
@@ -96,11 +98,12 @@ def _lanczos_relations(op, res, b):
     return r1, r2, o1, o2
 
 
+@pytest.mark.parametrize("ortho", ["cgs_cqr2", "bcgs_pip2"])
 @pytest.mark.parametrize("b,d", [(4, 28), (1, 12), (3, 24), (5, 100)])
-def test_lancsvd_relations(b, d):
+def test_lancsvd_relations(b, d, ortho):
     op, s = _c1()
     res = oracle.lancsvd(op, r=min(10, d), b=b, d=d, tol=1e-30, maxit=1,
-                         seed=SEEDS["C1"] + b, debug=True)
+                         seed=SEEDS["C1"] + b, debug=True, ortho=ortho)
     r1, r2, o1, o2 = _lanczos_relations(op, res, b)
     assert r1 <= 1e-13 and r2 <= 1e-12 and o1 <= 1e-13 and o2 <= 1e-13
     B = res.debug["B"]
