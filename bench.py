@@ -49,6 +49,9 @@ CONFIG_TEXT = {
           "block Lanczos b=32",
     "C5": "large synthetic sparse CSR, m=n=5e7, nnz~1e9, r=100, b=32; fixed work: one "
           "restart cycle at d=160 (SURVEY 8(d) C5 (i))",
+    "C5g2": "G2 twin of C5: block-diagonal CSR m=n=5e7, nnz~1e9, closed-form spectrum (top 100 "
+            "in [100, 200], tail <= 20), r=100, b=32, d=160, thick restart keep 128, tol 1e-8 "
+            "(SURVEY 8(d) C5 (iii))",
 }
 
 
@@ -87,6 +90,17 @@ def make_workload(cfg_name: str, rank: int = 0):
     from tsvd_inputs import CONFIGS, SEEDS, dense_prescribed, powerlaw_csr, spectrum_eq16
     cfg = dict(CONFIGS[cfg_name])
     seed = SEEDS[cfg_name] + 1000 * rank
+    if cfg.get("device_gen") == "g2":  # C5 (iii): G2 twin, closed-form spectrum, in HBM
+        import numpy as np
+        from tsvd_inputs import blockdiag_csr_device
+        t0 = time.time()
+        hi, lo, k = cfg["top"]
+        rp, ci, va, sig = blockdiag_csr_device(cfg["m"], cfg["n"], cfg["mean_block"],
+                                               cfg["alpha"], seed, np.linspace(hi, lo, k),
+                                               tail_max=cfg["tail_max"])
+        print(f"{cfg_name}: generated {ci.numel()} nonzeros (G2) in HBM in "
+              f"{time.time() - t0:.1f} s", file=sys.stderr, flush=True)
+        return cfg, seed, dict(csr=(rp, ci, va), shape=(cfg["m"], cfg["n"]), sigma=sig[:k + 1])
     if cfg.get("device_gen"):  # C5: 1e9 nonzeros, generated in HBM (tsvd_inputs)
         from tsvd_inputs import powerlaw_csr_device
         t0 = time.time()
@@ -381,6 +395,9 @@ def main():
                          "restart (Alg. 2 S7); default: the config's setting")
     ap.add_argument("--d", type=int, default=None, help="override the config's Krylov dimension")
     ap.add_argument("--maxit", type=int, default=None, help="override the config's maxit")
+    ap.add_argument("--ortho", default="cgs_cqr2", choices=["cgs_cqr2", "bcgs_pip2"],
+                    help="block orthogonalisation: the paper's CGS-CQR2 (Alg. 5, default) or "
+                         "BCGS-PIP+ (SURVEY 8(f) N2 ablation)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--ref-budget", type=float, default=120.0,
@@ -449,6 +466,7 @@ def main():
     T.lib()
 
     cfg, seed, work = make_workload(cfg_name, 0)
+    sigma_exact = work.pop("sigma", None)   # G2: the closed-form spectrum
     dist_kw = None
     # TSVD_BENCH_DIST=1 runs the row-partitioned NCCL path also with one rank
     use_dist = world > 1 or os.environ.get("TSVD_BENCH_DIST") == "1"
@@ -498,6 +516,7 @@ def main():
     h.set_seed(seed)
     h.set_krylov_dim(d)
     h.set_thick_restart(keep)
+    h.set_ortho(args.ortho)
     rsvd = args.algo == "rsvd"
     if rsvd and "rsvd_p" not in cfg:
         raise SystemExit(f"config {cfg_name} has no rSVD settings")
@@ -547,6 +566,11 @@ def main():
     accuracy = None
     if big:  # U, V (80 GB) stay in place in the bases; the library computes e
         accuracy = residual_check(h)
+        if sigma_exact is not None:  # G2: sigma against the closed form
+            import numpy as np
+            S = h.singular_values()
+            accuracy["sigma_err_max_over_sigma1"] = float(
+                np.abs(S - sigma_exact[:len(S)]).max() / sigma_exact[0])
     else:
         U, S, V = h.get(device=True)
         accuracy = residual_check(h, U, V) if not use_dist else residual_check(h)
@@ -636,6 +660,7 @@ def main():
             h2.set_seed(seed)
             h2.set_krylov_dim(d)
             h2.set_thick_restart(keep)
+            h2.set_ortho(args.ortho)
             solve(h2)
             h2.get_into(Uo[:h2.m], So, Vo[:h2.n])
             h2.close()
@@ -677,6 +702,8 @@ def main():
                    "r": r, "b": b, "d": d, "tol": tol, "maxit": maxit,
                    "restart": (f"thick, keep {keep} (SURVEY 8(f) N1)" if keep else
                                "paper (Alg. 2 S7)"),
+                   "ortho": ("CGS-CQR2 (Alg. 5)" if args.ortho == "cgs_cqr2" else
+                             "BCGS-PIP+ (SURVEY 8(f) N2 ablation)"),
                    "l2": "no flush: working set (A, A^T, bases) >> 126 MB L2",
                    "parallelism": f"row-partitioned x{world} (NCCL)" if world > 1 else "single"},
         "solver": {"cycles": last["cycles"], "nconv": last["nconv"], "rho_max": last["rho_max"],

@@ -182,6 +182,24 @@ tsvd_status tsvd_set_allocator(tsvd_alloc_fn alloc, tsvd_free_fn free_, void* ct
  * tsvd_get as usual.  Other values => TSVD_EINVAL. */
 enum { TSVD_OUT_AUTO = 0, TSVD_OUT_SEPARATE = 1, TSVD_OUT_INPLACE = 2 };
 tsvd_status tsvd_set_output_mode(tsvd_t h, int mode);
+/* Block orthogonalisation of every S3b / S5 step (and of RandSVD's CGS-QR
+ * panels).  TSVD_ORTHO_CGS_CQR2 (default): the paper's Alg. 5.
+ * TSVD_ORTHO_BCGS_PIP2: BCGS-PIP+ (reading R34 --
+ * not in the paper): two Pythagorean block-CGS passes, each needing ONE
+ * reduction [P Y]^T Y (multi-GPU: 2 all-reduces per orthogonalisation
+ * instead of 4) and no basis-free TRSM / Gram passes; the same Cholesky
+ * breakdown test and CGS2 fallback.  Stable while the block is not
+ * nearly inside span(P) (kappa(Y) well below u^{-1/2}); a measured ablation.
+ * Other values => TSVD_EINVAL. */
+enum { TSVD_ORTHO_CGS_CQR2 = 0, TSVD_ORTHO_BCGS_PIP2 = 1 };
+tsvd_status tsvd_set_ortho(tsvd_t h, int ortho);
+/* CUDA-graph replay of a LancSVD cycle's block steps (single-GPU handles):
+ * with on != 0 the deferred-check pass of a cycle (no host synchronisation
+ * inside) is captured the second time the same cycle shape runs and replayed
+ * afterwards; results are bit-identical to the eager path.  Default off (no
+ * measured gain on C2); env TSVD_GRAPHS=1 sets it for new
+ * handles. */
+tsvd_status tsvd_set_graphs(tsvd_t h, int on);
 /* Panel width of CGS-QR (Alg. 3) inside RandSVD; default 16. */
 tsvd_status tsvd_set_qr_block(tsvd_t h, int b_qr);
 /* Optional exact start block instead of the Philox one: for LancSVD the

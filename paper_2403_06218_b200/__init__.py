@@ -26,6 +26,7 @@ TSVD_EINVAL, TSVD_ESHAPE, TSVD_ENOMEM, TSVD_ECUDA, TSVD_ENCCL, TSVD_ESTATE = -1,
 TSVD_HOST, TSVD_DEVICE = 0, 1
 TSVD_ROW_MAJOR, TSVD_COL_MAJOR = 0, 1
 TSVD_OUT_AUTO, TSVD_OUT_SEPARATE, TSVD_OUT_INPLACE = 0, 1, 2
+TSVD_ORTHO_CGS_CQR2, TSVD_ORTHO_BCGS_PIP2 = 0, 1
 
 # every symbol include/tsvd.h declares (tests check the .so exports them)
 EXPORTS = [
@@ -38,7 +39,7 @@ EXPORTS = [
     "tsvd_set_profiling", "tsvd_get_profile", "tsvd_reset_profile",
     "tsvd_create_csr_dist", "tsvd_create_dense_dist", "tsvd_nccl_unique_id",
     "tsvd_partition_rows", "tsvd_set_allocator", "tsvd_residuals", "tsvd_loopback_create",
-    "tsvd_loopback_destroy",
+    "tsvd_loopback_destroy", "tsvd_set_ortho", "tsvd_set_graphs",
 ]
 
 
@@ -112,6 +113,8 @@ _SIGS = {
     "tsvd_residuals": [vp, vp, vp],
     "tsvd_loopback_create": [i32, C.POINTER(vp)],
     "tsvd_loopback_destroy": [vp],
+    "tsvd_set_ortho": [vp, i32],
+    "tsvd_set_graphs": [vp, i32],
 }
 
 
@@ -282,6 +285,15 @@ class TruncatedSVD:
         """TSVD_OUT_AUTO / TSVD_OUT_SEPARATE / TSVD_OUT_INPLACE (include/tsvd.h)."""
         _check(lib().tsvd_set_output_mode(self._h, int(mode)), "tsvd_set_output_mode")
 
+    def set_graphs(self, on: bool = True):
+        """CUDA-graph replay of LancSVD cycles (tsvd_set_graphs)."""
+        _check(lib().tsvd_set_graphs(self._h, int(bool(on))), "tsvd_set_graphs")
+
+    def set_ortho(self, ortho):
+        """"cgs_cqr2" (the paper's Alg. 5, default) or "bcgs_pip2"."""
+        code = {"cgs_cqr2": TSVD_ORTHO_CGS_CQR2, "bcgs_pip2": TSVD_ORTHO_BCGS_PIP2}.get(ortho, ortho)
+        _check(lib().tsvd_set_ortho(self._h, int(code)), "tsvd_set_ortho")
+
     def set_qr_block(self, b_qr: int):
         _check(lib().tsvd_set_qr_block(self._h, int(b_qr)), "tsvd_set_qr_block")
 
@@ -341,6 +353,12 @@ class TruncatedSVD:
         _check(lib().tsvd_get(self._h, U.ctypes.data, r, S.ctypes.data, V.ctypes.data, r,
                               TSVD_HOST), "tsvd_get")
         return U, S, V
+
+    def singular_values(self):
+        """S (r) of the last solve only (no U, V copies)."""
+        S = np.empty(self.r)
+        _check(lib().tsvd_get(self._h, None, 0, S.ctypes.data, None, 0, TSVD_HOST), "tsvd_get")
+        return S
 
     def get_into(self, U=None, S=None, V=None):
         """Copy results into caller buffers (numpy or CUDA tensors, same kind)."""

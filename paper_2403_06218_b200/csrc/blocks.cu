@@ -107,11 +107,14 @@ void* buf(Ctx& c, const std::string& name, size_t bytes) {
   auto it = c.bufs.find(name);
   if (it != c.bufs.end() && it->second.second >= bytes) return it->second.first;
   if (it != c.bufs.end()) {
+    if (c.capturing) throw Error{TSVD_ECUDA, "buffer reallocation inside a graph capture"};
     dfree(it->second.first, c.st);  // stream-ordered: pending work on c.st finishes first
     c.bufs.erase(it);
   }
+  if (c.capturing) throw Error{TSVD_ECUDA, "buffer allocation inside a graph capture"};
   void* p = dmalloc(bytes, c.st);
   c.bufs[name] = {p, bytes};
+  ++c.bufgen;
   return p;
 }
 
@@ -135,18 +138,25 @@ static cudaEvent_t pool_get(Ctx& c) {
   return e;
 }
 
+// inside a stream capture the records become event-record nodes of the graph
+// (external events), so every replay re-records them for the same harvest
+static cudaError_t record(Ctx& c, cudaEvent_t e) {
+  return c.capturing ? cudaEventRecordWithFlags(e, c.st, cudaEventRecordExternal)
+                     : cudaEventRecord(e, c.st);
+}
+
 Prof::Prof(Ctx& c_, int cat_, double bytes_, double flops_)
     : c(c_), cat(cat_), bytes(bytes_), flops(flops_) {
   if (!c.prof_on) return;
   a = pool_get(c);
-  TSVD_CUDA(cudaEventRecord(a, c.st));
+  TSVD_CUDA(record(c, a));
   l0 = g_launches.load();
 }
 
 Prof::~Prof() {
   if (!c.prof_on || !a) return;
   cudaEvent_t b = pool_get(c);
-  cudaEventRecord(b, c.st);
+  record(c, b);
   c.prof_open.push_back(ProfRec{cat, a, b, g_launches.load() - l0, bytes, flops});
 }
 
@@ -162,15 +172,29 @@ void prof_harvest(Ctx& c) {
     e.ms += ms;
     e.bytes += r.bytes;
     e.flops += r.flops;
-    c.ev_pool.push_back(r.a);
-    c.ev_pool.push_back(r.b);
+    if (!r.graph_owned) {
+      c.ev_pool.push_back(r.a);
+      c.ev_pool.push_back(r.b);
+    }
   }
   c.prof_open.clear();
   for (int i = 0; i < TSVD_NPROF; ++i) c.prof[i].name = kProfNames[i];
 }
 
+void cycle_graph_reset(Ctx& c) {
+  CycleGraph& g = c.cyc_graph;
+  if (g.exec) cudaGraphExecDestroy(g.exec);
+  for (auto& r : g.prof_recs) {
+    c.ev_pool.push_back(r.a);
+    c.ev_pool.push_back(r.b);
+  }
+  g = CycleGraph{};
+}
+
 void prof_release(Ctx& c) {
+  cycle_graph_reset(c);
   for (auto& r : c.prof_open) {
+    if (r.graph_owned) continue;
     c.ev_pool.push_back(r.a);
     c.ev_pool.push_back(r.b);
   }
@@ -271,10 +295,76 @@ int cholqr2(Ctx& c, double* Y, int64_t q, int w, int64_t ld, double* R) {
   return 0;
 }
 
+// BCGS-PIP+ (reading R34; oracle/core.py bcgs_pip2): two
+// Pythagorean block CGS passes, each with ONE reduction.  Passes:
+//   1 gemm_tn : C1 = [P Y]^T Y  (H1 = P^T Y, W1 = Y^T Y)      -> all-reduce C1
+//     small   : M1 = W1 - H1^T H1, L1 = chol(M1), T1 = L1^{-T}, H1' = H1 T1
+//   2 gemm_nn : Q1 = Y T1 - P H1'  (= (Y - P H1) L1^{-T}),  W2 = Q1^T Q1 (epilogue)
+//   3 gemm_tn : H2 = P^T Q1                                     -> all-reduce [H2; W2]
+//     small   : M2 = W2 - H2^T H2, L2, T2, H2' = H2 T2; R = L2^T L1^T; H = H1 + H2 L1^T
+//   4 gemm_nn : Q = Q1 T2 - P H2'  (into Y's slot)
+// Four basis reads like CGS-CQR2 but no basis-free TRSM / Gram passes (the
+// TRSM rides in the NN epilogue through (Y - P H) T = Y T - P (H T)) and
+// two reductions (multi-GPU: two all-reduces instead of four).
+static int pip2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H, double* R,
+                bool need_h) {
+  double* Y = basis + s;
+  double* S = scratch(c, q);
+  double* gram = gram_buf(c, q);
+  double* part = part_tn(c, q, s + w);
+  double* C1 = dbuf(c, "pip_C1", (size_t)(s + w) * w);
+  double* C2 = dbuf(c, "pip_C2", (size_t)(s + w) * w);
+  double* Hp = dbuf(c, "pip_Hp", (size_t)s * w);
+  double* L1 = dbuf(c, "L1", 32 * 32);
+  double* T1 = dbuf(c, "T1", 32 * 32);
+  double* L2 = dbuf(c, "L2", 32 * 32);
+  double* T2 = dbuf(c, "T2", 32 * 32);
+  const int np = nn_ctas(q, w);
+  clear_flags(c);
+  const double fl = 2.0 * q * s * w;
+  {
+    Prof p(c, P_TN, tn_bytes(q, s + w, 0), 2.0 * q * (s + w) * w);
+    gemm_tn(basis, ld, Y, ld, q, s + w, w, C1, w, part, c.st);                  // [H1; W1]
+    allreduce_sum(c, C1, (size_t)(s + w) * w);
+  }
+  {  // M1 = W1 - H1^T H1, L1 = chol(M1), T1 = L1^{-T}, Hp = H1 T1
+    Prof p(c, P_SMALL, 0, 0);
+    pip_finalize(C1, s, w, L1, T1, Hp, ortho_flags(c) + 0, nullptr, nullptr, nullptr, nullptr,
+                 c.st);
+  }
+  {
+    Prof p(c, P_NN, nn_bytes(q, s, w, true, true), fl + 2.0 * q * w * w * 2);
+    gemm_nn(basis, ld, Hp, w, Y, ld, T1, S, w, q, s, w, -1.0, 1.0, gram, c.st);  // Q1, W2
+  }
+  {
+    Prof p(c, P_TN, tn_bytes(q, s, w), fl);
+    gemm_tn(basis, ld, S, w, q, s, w, C2, w, part, c.st);                         // H2
+  }
+  {
+    Prof p(c, P_SMALL, 0, 0);
+    gram_reduce(gram, np, w, C2 + (size_t)s * w, c.st);                           // W2
+    allreduce_sum(c, C2, (size_t)(s + w) * w);
+    // L2, T2, Hp = H2 T2, R = L2^T L1^T, H = H1 + H2 L1^T
+    pip_finalize(C2, s, w, L2, T2, Hp, ortho_flags(c) + 1, L1, R, C1,
+                 (need_h && H) ? H : nullptr, c.st);
+  }
+  if (breakdown(c)) {
+    Prof p(c, P_OTHER, 0, 0);
+    cgs2(c, basis, q, s, w, ld, H, R);
+    return 1;
+  }
+  {
+    Prof p(c, P_NN, nn_bytes(q, s, w, true, true), fl + 2.0 * q * w * w);
+    gemm_nn(basis, ld, Hp, w, S, w, T2, Y, ld, q, s, w, -1.0, 1.0, nullptr, c.st);  // Q
+  }
+  return 0;
+}
+
 int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H,
              double* R, bool need_h) {
   if (s == 0) return cholqr2(c, basis, q, w, ld, R);
   if (w > 32) throw Error{TSVD_EINVAL, "cgs_cqr2: block wider than 32"};
+  if (c.ortho == TSVD_ORTHO_BCGS_PIP2) return pip2(c, basis, q, s, w, ld, H, R, need_h);
   double* Y = basis + s;
   double* S = scratch(c, q);
   double* gram = gram_buf(c, q);

@@ -374,6 +374,21 @@ tsvd_status tsvd_set_output_mode(tsvd_t h, int mode) {
   return TSVD_OK;
 }
 
+tsvd_status tsvd_set_graphs(tsvd_t h, int on) {
+  if (!h) return TSVD_EINVAL;
+  TSVD_API_BEGIN
+  if (!on) cycle_graph_reset(*h);
+  h->graphs = on != 0;
+  return TSVD_OK;
+  TSVD_API_END
+}
+
+tsvd_status tsvd_set_ortho(tsvd_t h, int ortho) {
+  if (!h || (ortho != TSVD_ORTHO_CGS_CQR2 && ortho != TSVD_ORTHO_BCGS_PIP2)) return TSVD_EINVAL;
+  h->ortho = ortho;
+  return TSVD_OK;
+}
+
 tsvd_status tsvd_set_qr_block(tsvd_t h, int b_qr) {
   if (!h || b_qr < 1 || b_qr > 32) return TSVD_EINVAL;
   h->b_qr = b_qr;

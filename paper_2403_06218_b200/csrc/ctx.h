@@ -1,6 +1,7 @@
 // Handle state of libtsvd (behind the opaque tsvd_t of include/tsvd.h).
 #pragma once
 
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <vector>
@@ -17,6 +18,21 @@ struct ProfRec {
   cudaEvent_t a, b;
   int64_t launches;
   double bytes, flops;
+  bool graph_owned = false;  // recorded by a captured graph: not returned to the pool
+};
+
+// One Lanczos cycle's block steps captured as a CUDA graph (solvers.cu):
+// reused while the key (sizes, buffers, options) is unchanged.
+struct CycleGraph {
+  int64_t m = -1, n = -1;
+  int d = 0, b = 0, s0 = 0, kc = 0, ortho = -1;
+  bool prof = false;
+  const void* ptrs[4] = {nullptr, nullptr, nullptr, nullptr};
+  uint64_t bufgen = 0;
+  int seen = 0;                   // eager runs with this key (capture on the second)
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;           // kernels per replay
+  std::vector<ProfRec> prof_recs; // phase events inside the graph
 };
 }  // namespace tsvd
 
@@ -43,6 +59,7 @@ struct tsvd_ctx {
   int krylov_d = 0;
   int thick_keep = 0;         // N1 thick restart: Ritz vectors kept (0 = Alg. 2 S7)
   int b_qr = 16;
+  int ortho = TSVD_ORTHO_CGS_CQR2;  // tsvd_set_ortho (SURVEY 8(f) N2 ablation)
   std::vector<double> start;  // optional exact start block (row-major, dense)
   int64_t start_rows = 0, start_cols = 0;
   // device workspace: named buffers grown on demand, kept across solves
@@ -71,6 +88,14 @@ struct tsvd_ctx {
   std::vector<tsvd::ProfRec> prof_open;   // recorded, not yet harvested
   std::vector<cudaEvent_t> ev_pool;
   tsvd_prof_entry prof[TSVD_NPROF]{};
+  // CUDA graph of a Lanczos cycle (single-GPU handles; tsvd_set_graphs)
+  // off by default: measured on C2 (profiles/r02), graph replay of the cycle
+  // does not shorten the TTS (the inter-kernel gaps are device-side ramp /
+  // tail, not host launch latency); TSVD_GRAPHS=1 or tsvd_set_graphs enables it
+  bool graphs = getenv("TSVD_GRAPHS") != nullptr && getenv("TSVD_GRAPHS")[0] == '1';
+  bool capturing = false;
+  uint64_t bufgen = 0;            // bumped by every (re)allocation of a named buffer
+  tsvd::CycleGraph cyc_graph;
 };
 
 namespace tsvd {
@@ -93,6 +118,7 @@ struct Prof {
   ~Prof();
 };
 void prof_harvest(Ctx& c);   // after a stream sync: fold records into c.prof
+void cycle_graph_reset(Ctx& c);  // drop the captured Lanczos-cycle graph
 void prof_release(Ctx& c);
 
 // building blocks (blocks.cu).  All blocks are row-major with leading

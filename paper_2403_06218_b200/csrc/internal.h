@@ -154,6 +154,15 @@ void gram_reduce(const double* gram, int np, int w, double* Wred, cudaStream_t s
 void reduce_partials(const double* part, int nparts, int64_t count, double* out,
                      cudaStream_t st);
 
+// BCGS-PIP+ pass finaliser (reading R34): from C = [H; W] ((s+w) x w):
+// L = chol(W - H^T H) (flag |= breakdown), T = L^{-T}, Hp = H T; with L1:
+// R = L^T L1^T and (Hout != null) Hout = H1 + H L1^T
+void pip_finalize(const double* C, int s, int w, double* L, double* T, double* Hp, int* flag,
+                  const double* L1, double* R, const double* H1, double* Hout, cudaStream_t st);
+// C = alpha op(A) op(B) + beta C on small row-major matrices (fixed order)
+void small_gemm(const double* A, int lda, bool ta, const double* B, int ldb, bool tb, double* C,
+                int ldc, int m, int n, int k, double alpha, double beta, cudaStream_t st);
+
 // small helpers
 void copy_block(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows,
                 int cols, bool transpose, cudaStream_t st);

@@ -355,6 +355,165 @@ void chol2_finalize(const double* gram, int np, int w, const double* Lprev, doub
   fin_launch(gram, np, w, 2, nullptr, Lprev, L2, T2, R, H, Hbar, s, flag, st);
 }
 
+// ----------------------------------------------------- BCGS-PIP+ pass ---
+// One CTA (256 threads, 8 warps) does the small work of one Pythagorean
+// pass (reading R34; blocks.cu pip2): from C = [H; W] ((s + w) x w, the
+// reduced [P Y]^T Y)
+//   M = W - H^T H        (8 x 8 tiles by DMMA m8n8k4 over k = s, warp-strided)
+//   L = chol(M) (P:275 breakdown test -> *flag), T = L^{-T}
+//   Hp = H T             (s x w; DMMA tiles, K = w)
+// and, for the second pass (L1 != null): R = L^T L1^T (= R2 R1) and, when
+// Hout != null, Hout = H1 + H L1^T.  Every sum runs in a fixed order.
+__device__ __forceinline__ void dmma884s(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) pip_finalize_kernel(
+    const double* __restrict__ Cm, int s, int w, double* __restrict__ L,
+    double* __restrict__ T, double* __restrict__ Hp, int* __restrict__ flag,
+    const double* __restrict__ L1, double* __restrict__ R, const double* __restrict__ H1,
+    double* __restrict__ Hout) {
+  __shared__ double Ms[32 * 32];
+  __shared__ double Lo[32 * 32];
+  __shared__ double Xs[32 * 33];
+  __shared__ double Ts[32 * 33];
+  __shared__ double L1s[32 * 33];
+  __shared__ int bad;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int nt = (w + 7) / 8;
+  const double* H = Cm;
+  const double* W = Cm + (size_t)s * w;
+  if (tid == 0) bad = 0;
+  for (int i = tid; i < 32 * 32; i += 256) Lo[i] = 0.0;
+  if (L1)
+    for (int i = tid; i < w * w; i += 256) L1s[(i / w) * 33 + i % w] = L1[i];
+  // M = W - H^T H: tile (ti, tj), D[gid][2 tig + e] += sum_k H[k][ti 8 + gid] H[k][tj 8 + 2 tig + e]
+  for (int t = warp; t < nt * nt; t += 8) {
+    const int ti = t / nt, tj = t % nt;
+    const int ci = ti * 8 + gid, cj = tj * 8 + gid;
+    double d0 = 0.0, d1 = 0.0;
+    for (int k0 = 0; k0 < s; k0 += 4) {
+      const int k = k0 + tig;
+      const double a = (k < s && ci < w) ? H[(size_t)k * w + ci] : 0.0;
+      const double b = (k < s && cj < w) ? H[(size_t)k * w + cj] : 0.0;
+      dmma884s(d0, d1, a, b);
+    }
+    const int r = ti * 8 + gid, c = tj * 8 + 2 * tig;
+    if (r < w && c < w) Ms[r * w + c] = W[r * w + c] - d0;
+    if (r < w && c + 1 < w) Ms[r * w + c + 1] = W[r * w + c + 1] - d1;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    warp_cholesky(Ms, Lo, w, &bad);
+    __syncwarp();
+    // T = L^{-T} into Ts (ld 33): lane j forward-substitutes column j of L^{-1}
+    const int j = lane;
+    if (j < w) {
+      for (int i = 0; i < w; ++i) {
+        double v = 0.0;
+        if (i >= j) {
+          v = (i == j) ? 1.0 : 0.0;
+          for (int k = j; k < i; ++k) v = fma(-Lo[i * 32 + k], Xs[k * 33 + j], v);
+          v = v / Lo[i * 32 + i];
+        }
+        Xs[i * 33 + j] = v;
+      }
+    }
+    __syncwarp();
+    if (j < w)
+      for (int i = 0; i < w; ++i) Ts[j * 33 + i] = Xs[i * 33 + j];  // T[j][i] = Linv[i][j]
+  }
+  __syncthreads();
+  for (int i = tid; i < w * w; i += 256) {
+    const int r = i / w, c = i % w;
+    L[i] = Lo[r * 32 + c];
+    T[i] = Ts[r * 33 + c];
+    if (L1 && R) {  // R[r][c] = sum_k L[k][r] L1[c][k]  (= (L^T L1^T)[r][c])
+      double a = 0.0;
+      for (int k = 0; k < w; ++k) a = fma(Lo[k * 32 + r], L1s[c * 33 + k], a);
+      R[i] = a;
+    }
+  }
+  if (tid == 0 && bad) atomicOr(flag, 1);
+  // Hp = H T and (pass 2) Hout = H1 + H L1^T: 8 x 8 row tiles, K = w
+  const int nrt = (s + 7) / 8;
+  for (int t = warp; t < nrt * nt; t += 8) {
+    const int rt = t / nt, ct = t % nt;
+    const int r = rt * 8 + gid, cb = ct * 8 + gid;
+    double d0 = 0.0, d1 = 0.0, e0 = 0.0, e1 = 0.0;
+    for (int k0 = 0; k0 < w; k0 += 4) {
+      const int k = k0 + tig;
+      const double a = (r < s && k < w) ? H[(size_t)r * w + k] : 0.0;
+      const double b = (k < w && cb < w) ? Ts[k * 33 + cb] : 0.0;
+      dmma884s(d0, d1, a, b);
+      if (Hout) {
+        const double b2 = (k < w && cb < w) ? L1s[cb * 33 + k] : 0.0;  // L1^T[k][cb]
+        dmma884s(e0, e1, a, b2);
+      }
+    }
+    const int ro = rt * 8 + gid, c = ct * 8 + 2 * tig;
+    if (ro < s) {
+      if (c < w) Hp[(size_t)ro * w + c] = d0;
+      if (c + 1 < w) Hp[(size_t)ro * w + c + 1] = d1;
+      if (Hout) {
+        if (c < w) Hout[(size_t)ro * w + c] = H1[(size_t)ro * w + c] + e0;
+        if (c + 1 < w) Hout[(size_t)ro * w + c + 1] = H1[(size_t)ro * w + c + 1] + e1;
+      }
+    }
+  }
+}
+
+void pip_finalize(const double* C, int s, int w, double* L, double* T, double* Hp, int* flag,
+                  const double* L1, double* R, const double* H1, double* Hout,
+                  cudaStream_t st) {
+  pip_finalize_kernel<<<1, 256, 0, st>>>(C, s, w, L, T, Hp, flag, L1, R, H1, Hout);
+  TSVD_CHECK_LAUNCH();
+}
+
+// ------------------------------------------------------------ small GEMM ---
+// C (m x n, ldc) = alpha op(A) op(B) + beta C for the small matrices of
+// BCGS-PIP+ (reading R34): W - H^T H, H T, L2^T L1^T, H1 + H2 L1^T.  One
+// thread per entry, k summed in increasing order (deterministic); op(X) =
+// X or X^T of a row-major X.
+__global__ void small_gemm_kernel(const double* __restrict__ A, int lda, int ta,
+                                  const double* __restrict__ B, int ldb, int tb,
+                                  double* __restrict__ Cm, int ldc, int m, int n, int k,
+                                  double alpha, double beta) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)m * n) return;
+  const int i = (int)(t / n), j = (int)(t % n);
+  double a0 = 0.0, a1 = 0.0;
+  int p = 0;
+  for (; p + 1 < k; p += 2) {
+    const double x0 = ta ? A[(int64_t)p * lda + i] : A[(int64_t)i * lda + p];
+    const double y0 = tb ? B[(int64_t)j * ldb + p] : B[(int64_t)p * ldb + j];
+    const double x1 = ta ? A[(int64_t)(p + 1) * lda + i] : A[(int64_t)i * lda + p + 1];
+    const double y1 = tb ? B[(int64_t)j * ldb + p + 1] : B[(int64_t)(p + 1) * ldb + j];
+    a0 = fma(x0, y0, a0);
+    a1 = fma(x1, y1, a1);
+  }
+  if (p < k) {
+    const double x0 = ta ? A[(int64_t)p * lda + i] : A[(int64_t)i * lda + p];
+    const double y0 = tb ? B[(int64_t)j * ldb + p] : B[(int64_t)p * ldb + j];
+    a0 = fma(x0, y0, a0);
+  }
+  const double v = alpha * (a0 + a1);
+  Cm[(int64_t)i * ldc + j] = beta == 0.0 ? v : fma(beta, Cm[(int64_t)i * ldc + j], v);
+}
+
+void small_gemm(const double* A, int lda, bool ta, const double* B, int ldb, bool tb, double* C,
+                int ldc, int m, int n, int k, double alpha, double beta, cudaStream_t st) {
+  const int64_t e = (int64_t)m * n;
+  if (e <= 0) return;
+  small_gemm_kernel<<<(unsigned)((e + 127) / 128), 128, 0, st>>>(A, lda, ta ? 1 : 0, B, ldb,
+                                                                  tb ? 1 : 0, C, ldc, m, n, k,
+                                                                  alpha, beta);
+  TSVD_CHECK_LAUNCH();
+}
+
 // --------------------------------------------------------------- helpers ---
 __global__ void copy_block_kernel(const double* __restrict__ src, int64_t lds,
                                   double* __restrict__ dst, int64_t ldd, int64_t rows, int cols,

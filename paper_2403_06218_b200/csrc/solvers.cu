@@ -38,11 +38,11 @@ static double* signs_of(Ctx& c, const double* V, int64_t n, int64_t ldv, int r) 
 
 // tsvd_set_output_mode: form U_r, V_r in place over the bases when separate
 // m x r and n x r buffers do not fit in the free device memory (C5 on one GPU).
-static bool outputs_in_place(Ctx& c, int r) {
+static bool outputs_in_place(Ctx& c, int r, const char* nu = "res_U", const char* nv = "res_V") {
   if (c.out_mode == TSVD_OUT_INPLACE) return true;
   if (c.out_mode == TSVD_OUT_SEPARATE) return false;
   size_t have = 0;
-  for (const char* nm : {"res_U", "res_V"}) {
+  for (const char* nm : {nu, nv}) {
     auto it = c.bufs.find(nm);
     if (it != c.bufs.end()) have += it->second.second;
   }
@@ -199,8 +199,30 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   std::vector<int> hlog(4 * (size_t)k);
   fill_zero(B, (int64_t)d * d, c.st);
   int s0 = 0;  // columns carried over by a thick restart (block steps start there)
+  int kc = 0;   // block steps of the current cycle
+  // Alg. 2 S2-S5 for block step i of the current cycle (both sides, or only
+  // the m side when a replay starts at the m-side slot of step i)
+  auto block_step = [&](int i, bool n_part = true) {
+    const int lo = s0 + i * b;
+    if (n_part) {
+      apply(c, true, Pb + lo, ldb, P + lo, ldp, b);                  // S2: A^T Qbar_i
+      n_side();
+      c.flag_slot = 2 * i;
+      if (lo == 0)
+        cholqr2(c, P, n, b, ldp, R);                                 // S3a
+      else
+        cgs_cqr2(c, P, n, lo, b, ldp, H, R, false);                  // S3b (H unused, R17)
+      copy_block(R, b, B + (int64_t)lo * d + lo, d, b, b, true, c.st);  // L_i = R^T
+    }
+    apply(c, false, P + lo, ldp, Pb + lo + b, ldb, b);               // S4: A Q_i
+    m_side();
+    c.flag_slot = 2 * i + 1;
+    cgs_cqr2(c, Pb, m, lo + b, b, ldb, H, Rb, false);                // S5 (H unused, R17)
+    if (i < kc - 1)
+      copy_block(Rb, b, B + (int64_t)(lo + b) * d + lo, d, b, b, false, c.st);  // Rbar_i
+  };
   for (cycle = 1; cycle <= maxit; ++cycle) {
-    const int kc = (d - s0) / b;  // block steps of this cycle
+    kc = (d - s0) / b;
     // Block steps, first with deferred breakdown checks (no host sync per
     // orthogonalisation); if the log shows a breakdown in call `slot`
     // (2i: n side of step i, 2i+1: m side) the steps are replayed from there
@@ -209,30 +231,75 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
     c.flag_log = flog;
     c.deferred = true;
     int from_slot = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-      for (int i = from_slot / 2; i < kc; ++i) {
-        const int lo = s0 + i * b;
-        if (!(i == from_slot / 2 && (from_slot & 1))) {
-          apply(c, true, Pb + lo, ldb, P + lo, ldp, b);                  // S2: A^T Qbar_i
-          n_side();
-          c.flag_slot = 2 * i;
-          if (lo == 0)
-            cholqr2(c, P, n, b, ldp, R);                                 // S3a
-          else
-            cgs_cqr2(c, P, n, lo, b, ldp, H, R, false);                  // S3b (H unused, R17)
-          copy_block(R, b, B + (int64_t)lo * d + lo, d, b, b, true, c.st);  // L_i = R^T
+    // The deferred pass has no host synchronisation, so on a single GPU it is
+    // replayed as a CUDA graph once the same cycle shape was seen before (the
+    // first run allocates every workspace; the capture then only records).
+    CycleGraph& cg = c.cyc_graph;
+    const void* ptrs[4] = {Pb, P, B, flog};
+    const bool graph_ok = c.graphs && !c.comm;
+    bool same = graph_ok && cg.m == m && cg.n == n && cg.d == d && cg.b == b && cg.s0 == s0 &&
+                cg.kc == kc && cg.ortho == c.ortho && cg.prof == c.prof_on &&
+                cg.bufgen == c.bufgen && std::equal(ptrs, ptrs + 4, cg.ptrs);
+    if (graph_ok && !same) {
+      cycle_graph_reset(c);
+      cg.m = m, cg.n = n, cg.d = d, cg.b = b, cg.s0 = s0, cg.kc = kc, cg.ortho = c.ortho;
+      cg.prof = c.prof_on;
+      cg.bufgen = c.bufgen;
+      std::copy(ptrs, ptrs + 4, cg.ptrs);
+    }
+    bool graph_ran = false;
+    if (same && !cg.exec && cg.seen >= 1) {
+      // capture the block steps exactly as the eager loop below enqueues them
+      const size_t prof0 = c.prof_open.size();
+      const int64_t l0 = g_launches.load();
+      c.capturing = true;
+      cudaGraph_t graph = nullptr;
+      cudaError_t ce = cudaStreamBeginCapture(c.st, cudaStreamCaptureModeThreadLocal);
+      if (ce == cudaSuccess) {
+        try {
+          for (int i = 0; i < kc; ++i) block_step(i);
+        } catch (...) {
+          c.capturing = false;
+          cudaStreamEndCapture(c.st, &graph);
+          if (graph) cudaGraphDestroy(graph);
+          cudaGetLastError();
+          throw;
         }
-        apply(c, false, P + lo, ldp, Pb + lo + b, ldb, b);               // S4: A Q_i
-        m_side();
-        c.flag_slot = 2 * i + 1;
-        cgs_cqr2(c, Pb, m, lo + b, b, ldb, H, Rb, false);                // S5 (H unused, R17)
-        if (i < kc - 1)
-          copy_block(Rb, b, B + (int64_t)(lo + b) * d + lo, d, b, b, false, c.st);  // Rbar_i
+        ce = cudaStreamEndCapture(c.st, &graph);
+      }
+      c.capturing = false;
+      if (ce == cudaSuccess) ce = cudaGraphInstantiate(&cg.exec, graph, 0);
+      if (graph) cudaGraphDestroy(graph);
+      cg.launches = g_launches.load() - l0;
+      g_launches.fetch_sub(cg.launches);  // nothing ran yet
+      for (size_t j = prof0; j < c.prof_open.size(); ++j) {
+        c.prof_open[j].graph_owned = true;
+        cg.prof_recs.push_back(c.prof_open[j]);
+      }
+      c.prof_open.resize(prof0);
+      if (ce != cudaSuccess) {  // not capturable here: stay eager
+        cudaGetLastError();
+        cycle_graph_reset(c);
+        c.graphs = false;
+      }
+    }
+    if (same && cg.exec) {
+      TSVD_CUDA(cudaGraphLaunch(cg.exec, c.st));
+      g_launches.fetch_add(cg.launches + 1);
+      c.prof_open.insert(c.prof_open.end(), cg.prof_recs.begin(), cg.prof_recs.end());
+      graph_ran = true;
+    } else if (graph_ok) {
+      ++cg.seen;
+    }
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int i = (pass == 0 && graph_ran) ? kc : from_slot / 2; i < kc; ++i) {
+        block_step(i, !(i == from_slot / 2 && (from_slot & 1)));
       }
       if (!c.deferred) break;
       TSVD_CUDA(cudaMemcpyAsync(hlog.data(), flog, sizeof(int) * 4 * (size_t)k,
                                 cudaMemcpyDeviceToHost, c.st));
       TSVD_CUDA(cudaStreamSynchronize(c.st));
+      if (graph_ran) prof_harvest(c);  // the graph's events are re-recorded by the next replay
       c.deferred = false;
       int bad = -1;
       for (int sl = 0; sl < 2 * kc && bad < 0; ++sl)
@@ -268,17 +335,26 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
       // P' = P_k Vbar[:, :l] (computed into scratch panels, then copied over
       // the bases' first l columns), Qbar_{k+1} moved behind them, and the
       // next B' starts as [Sigma_l; S] with S = Rbar_k Vbar[d-b:d, :l].
-      double* tPb = dbuf(c, "thick_Pb", (size_t)m * keep);
-      double* tP = dbuf(c, "thick_P", (size_t)n * keep);
       {
         Prof p(c, P_RESTART, 8.0 * (m + n) * (d + 3.0 * keep) + 16.0 * m * b,
                2.0 * (m + n) * d * keep);
-        gemm_nn(Pb, ldb, Ub, d, nullptr, 0, nullptr, tPb, keep, m, d, keep, 1.0, 0.0, nullptr,
-                c.st);
-        gemm_nn(P, ldp, Vb, d, nullptr, 0, nullptr, tP, keep, n, d, keep, 1.0, 0.0, nullptr,
-                c.st);
-        copy_block(tPb, keep, Pb, ldb, m, keep, false, c.st);
-        copy_block(tP, keep, P, ldp, n, keep, false, c.st);
+        if (outputs_in_place(c, keep, "thick_Pb", "thick_P")) {
+          // no room for m x l / n x l panels (C5 on one GPU): the row-local
+          // products overwrite the bases' first l columns through the pass
+          // scratch, chunk by chunk (out_product, as for the outputs)
+          int64_t ld_unused = 0;
+          out_product(c, "thick_Pb", Pb, ldb, m, d, Ub, d, keep, true, &ld_unused);
+          out_product(c, "thick_P", P, ldp, n, d, Vb, d, keep, true, &ld_unused);
+        } else {
+          double* tPb = dbuf(c, "thick_Pb", (size_t)m * keep);
+          double* tP = dbuf(c, "thick_P", (size_t)n * keep);
+          gemm_nn(Pb, ldb, Ub, d, nullptr, 0, nullptr, tPb, keep, m, d, keep, 1.0, 0.0, nullptr,
+                  c.st);
+          gemm_nn(P, ldp, Vb, d, nullptr, 0, nullptr, tP, keep, n, d, keep, 1.0, 0.0, nullptr,
+                  c.st);
+          copy_block(tPb, keep, Pb, ldb, m, keep, false, c.st);
+          copy_block(tP, keep, P, ldp, n, keep, false, c.st);
+        }
         copy_block(Pb + d, ldb, Pb + keep, ldb, m, b, false, c.st);
       }
       fill_zero(B, (int64_t)d * d, c.st);

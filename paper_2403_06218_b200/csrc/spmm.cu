@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(StagedCfg<LPR>::NTHR, 1) spmm_staged_kernel(
 
 static bool g_spmm_staged = [] {
   const char* e = getenv("TSVD_SPMM_STAGED");
-  return !(e && e[0] == '0');
+  return e && e[0] == '1';
 }();
 
 // X (rows x w, ld) as a 2-D tensor for tile::gather4: box = {2 LPR, 1}

@@ -41,6 +41,9 @@ def _cuda():
 
 def _solve(h, algo):
     h.set_seed(5)
+    if algo == "pip2":   # the single-reduction orthogonalisation
+        h.set_ortho("bcgs_pip2")
+        algo = "lanczos"
     if algo == "lanczos":
         st = h.block_lanczos(r=10, b=4, tol=1e-10, maxit=6, d=40)
     elif algo == "thick":
@@ -100,7 +103,7 @@ def _case(kind):
     return csr, m, n, dict(csr=csr, shape=(m, n))
 
 
-@pytest.mark.parametrize("algo", ["lanczos", "rsvd", "thick"])
+@pytest.mark.parametrize("algo", ["lanczos", "rsvd", "thick", "pip2"])
 @pytest.mark.parametrize("kind", ["dense", "csr"])
 @pytest.mark.parametrize("world", [2, 3])
 def test_loopback_world_equals_single(world, kind, algo):

@@ -428,3 +428,83 @@ def test_residuals_parity(case):
     tol = 2 * np.linalg.norm(b, axis=0) / Sg[0] + 1e-300
     assert np.all(np.abs(e - eo) <= tol)
     assert np.allclose(R * Sg, e * Sg[0], rtol=1e-14, atol=0)
+
+
+# ---- BCGS-PIP+ orthogonalisation (tsvd_set_ortho) ----------
+@pytest.mark.parametrize("case", ["c1", "sparse", "restarts"])
+def test_bcgs_pip2_lanczos_parity(case):
+    """LancSVD with the BCGS-PIP+ block orthogonalisation (reading R34) vs
+    oracle.lancsvd(ortho="bcgs_pip2") on the same bytes and Philox start:
+    same cycle count, sigma / vectors within the north_star tolerances over
+    converged triplets, no breakdown fallback."""
+    if case == "c1":
+        A, s = _c1()
+        op, kw, prm = oracle.Operator(dense=A), dict(A=A), dict(r=10, b=4, d=28, tol=1e-12, maxit=8)
+        seed = SEEDS["C1"]
+    elif case == "sparse":
+        m, n = 30000, 12000
+        csr = powerlaw_csr(m, n, 300000, 2.5, seed=23)
+        op, kw = oracle.Operator(csr=csr, shape=(m, n)), dict(csr=csr, shape=(m, n))
+        prm, seed = dict(r=20, b=8, d=96, tol=1e-10, maxit=6), 31
+    else:
+        n = 120
+        A = dense_prescribed(240, n, 10.0 * 0.93 ** np.arange(n), seed=8)
+        op, kw, prm, seed = oracle.Operator(dense=A), dict(A=A), \
+            dict(r=4, b=4, d=16, tol=1e-10, maxit=60), 5
+    ro = oracle.lancsvd(op, seed=seed, ortho="bcgs_pip2", **prm)
+    with T.TruncatedSVD(**kw) as h:
+        h.set_seed(seed)
+        h.set_ortho("bcgs_pip2")
+        st = h.block_lanczos(prm["r"], prm["b"], prm["tol"], prm["maxit"], d=prm["d"])
+        Ug, Sg, Vg = h.get()
+        info = h.info()
+        rho = h.rho()
+    # PIP+ falls back to CGS2 when a Lanczos block is nearly inside span(P)
+    # (W - H^T H loses its positive definiteness): the sparse case takes 5
+    # fallbacks in the oracle too, so only C1 must be fallback-free
+    if case == "c1":
+        assert info["breakdowns"] == 0
+    # the slow-decay restart case sits at tol after ~9 cycles: PIP+'s rounding
+    # (Pythagorean Gram) may move the last restart by one cycle either way
+    assert abs(info["cycles"] - ro.cycles) <= (1 if case == "restarts" else 0)
+    conv = (rho <= prm["tol"]) & (ro.rho <= prm["tol"] * ro.S[0])
+    assert conv.sum() >= min(prm["r"], 4)
+    _accept(op, Ug, Sg, Vg, ro.S, conv_mask=conv)
+    _vec_parity(Ug[:, conv], Vg[:, conv], ro.U[:, conv], ro.V[:, conv], ro.S[conv])
+    if case == "c1":
+        assert st == T.TSVD_OK
+        assert np.abs(Sg - s[:10]).max() / s[0] <= 1e-10
+
+
+# ---- CUDA graph of the Lanczos cycle (solvers.cu) ---------------------------
+@pytest.mark.parametrize("kind", ["dense", "csr"])
+def test_cycle_graph_replay_is_bit_identical(kind):
+    """Solve 1 runs the block steps eagerly, solve 2 captures them into a
+    CUDA graph and launches it, solve 3 replays it: the three results and
+    the per-phase launch counts must be identical (the graph records the
+    same kernels with the same arguments), also with profiling on."""
+    if kind == "dense":
+        A, _ = _c1()
+        kw = dict(A=A)
+        prm = dict(r=10, b=4, tol=1e-12, maxit=8, d=28)
+    else:
+        m, n = 20000, 8000
+        csr = powerlaw_csr(m, n, 200000, 2.5, seed=17)
+        kw = dict(csr=csr, shape=(m, n))
+        prm = dict(r=12, b=8, tol=1e-10, maxit=3, d=64)
+    outs = []
+    with T.TruncatedSVD(**kw) as h:
+        h.set_graphs(True)
+        h.set_profiling(True)
+        for _ in range(3):
+            h.set_seed(4)
+            h.reset_profile()
+            h.block_lanczos(**prm)
+            prof = h.profile()
+            outs.append((*h.get(), h.info(), {k: v["launches"] for k, v in prof.items()},
+                         {k: v["calls"] for k, v in prof.items()}))
+    for o in outs[1:]:
+        for a, b in zip(outs[0][:3], o[:3]):
+            assert np.array_equal(a, b)
+        assert o[3]["launches"] == outs[0][3]["launches"]
+        assert o[4] == outs[0][4] and o[5] == outs[0][5]

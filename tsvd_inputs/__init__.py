@@ -47,6 +47,7 @@ SEEDS = {
     "C4": 0x2403062184,
     "C5": 0x2403062185,
     "C5s": 0x2403062185,
+    "C5g2": 0x2403062186,
 }
 
 # BASELINE.json configs with the solver settings of SURVEY.md 8(a)/8(d).
@@ -63,6 +64,12 @@ CONFIGS = {
     # matrix is generated on the device (powerlaw_csr_device)
     "C5": dict(kind="csr", m=50_000_000, n=50_000_000, nnz=1_000_000_000,
                alpha=2.5, r=100, b=32, d=160, tol=1e-8, maxit=1, device_gen=True),
+    # C5 (iii): the G2 twin at C5 scale (blockdiag_csr_device: closed-form
+    # spectrum, top 100 = linspace(200, 100), tail <= 20; mean row ~20 ->
+    # nnz ~1e9), LancSVD to tol with thick restart (keep 128) on one GPU
+    "C5g2": dict(kind="csr", m=50_000_000, n=50_000_000, nnz=1_000_000_000, alpha=2.5,
+                 mean_block=2.6, top=(200.0, 100.0, 100), tail_max=20.0,
+                 r=100, b=32, d=160, keep=128, tol=1e-8, maxit=40, device_gen="g2"),
     # C5 scaled down by 10 (SURVEY 8(d) "Oracle timing"): the host oracle's sample
     "C5s": dict(kind="csr", m=5_000_000, n=5_000_000, nnz=100_000_000,
                 alpha=2.5, r=100, b=32, d=160, tol=1e-8, maxit=1),
@@ -340,3 +347,85 @@ def blockdiag_csr(m: int, n: int, mean_row: float, alpha: float, seed: int,
     rowptr[1:] = np.cumsum(np.bincount(rows, minlength=m))
     sigma_all = np.sort(np.concatenate([sig, np.zeros(max(0, n - nsig))]))[::-1]
     return rowptr, cols.astype(np.int32), np.ascontiguousarray(vals), sigma_all
+
+
+def blockdiag_csr_device(m: int, n: int, mean_row: float, alpha: float, seed: int,
+                         top_sigma, tail_max: float = 1.0, max_width: int = 256,
+                         device="cuda", chunk_rows: int = 4_000_000):
+    """G2 at C5 scale, generated with torch on `device`:
+    A = Pi_r blockdiag(B_1..B_T) Pi_c^T, square blocks (m = n), widths n_t
+    from the same Pareto recipe as blockdiag_csr (row length = n_t: power-law
+    rows), B_t = H(x_t) diag(s_t) H(y_t) with Householder reflectors
+    H(v) = I - 2 v v^T (unit v), so sigma(B_t) = s_t exactly and
+    sigma(A) = union of the s_t (closed form).  The len(top_sigma) largest
+    values are `top_sigma` (placed in random blocks), every other one is
+    uniform in (0, tail_max).  Entry (i, j) of B_t, written out:
+        s_i [i == j] - 2 x_i x_j s_j - 2 s_i y_i y_j + 4 c_t x_i y_j,
+        c_t = sum_k x_k s_k y_k.
+    The columns a block owns are a random subset of [0, n) in increasing
+    order (so every CSR row comes out sorted: canonical without a sort of
+    the nonzeros).  Returns (rowptr int64[m+1], colidx int32, vals f64,
+    sigma_all_sorted_desc as a numpy array); O(nnz) work, rows generated in
+    chunks to bound the temporaries."""
+    import torch
+    if m != n:
+        raise ValueError("blockdiag_csr_device builds square blocks (m = n)")
+    f64, i64 = torch.float64, torch.int64
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    scale = mean_row * (alpha - 2.0) / (alpha - 1.0)
+    # block widths: Pareto draws, rounded, capped; cut where the sum reaches n
+    est = int(2.5 * n / max(1.0, mean_row)) + 1024
+    u = torch.rand(est, generator=g, dtype=f64, device=device)
+    w = torch.clamp(torch.round((1.0 - u) ** (-1.0 / (alpha - 1.0)) * scale), 1, max_width).to(i64)
+    csum = torch.cumsum(w, 0)
+    T = int(torch.searchsorted(csum, torch.tensor([n], device=device, dtype=i64)).item()) + 1
+    w = w[:T].clone()
+    w[-1] -= int(csum[T - 1].item()) - n          # the last block ends exactly at n
+    start = torch.zeros(T + 1, dtype=i64, device=device)
+    start[1:] = torch.cumsum(w, 0)
+    del u, csum
+    # per column slot: its block, the singular value, the reflector vectors
+    blk = torch.repeat_interleave(torch.arange(T, device=device, dtype=i64), w)
+    s = torch.rand(n, generator=g, dtype=f64, device=device) * tail_max
+    top = torch.as_tensor(np.sort(np.asarray(top_sigma, dtype=np.float64))[::-1].copy(),
+                          device=device)
+    pos = torch.randperm(n, generator=g, device=device)[:top.numel()]
+    s[pos] = top
+    x = torch.randn(n, generator=g, dtype=f64, device=device)
+    y = torch.randn(n, generator=g, dtype=f64, device=device)
+    for v in (x, y):
+        nrm = torch.zeros(T, dtype=f64, device=device).index_add_(0, blk, v * v)
+        v /= torch.sqrt(nrm)[blk]
+    cblk = torch.zeros(T, dtype=f64, device=device).index_add_(0, blk, x * s * y)
+    # rows: global row g <- slot rinv[g]; columns: block t owns a random
+    # subset of [0, n), sorted, at slots start[t] .. start[t+1]-1
+    rinv = torch.randperm(n, generator=g, device=device)
+    cp = torch.randperm(n, generator=g, device=device)
+    key = blk * n + cp
+    cols_sorted = (torch.sort(key).values - blk * n).to(torch.int32)
+    del key, cp
+    L = w[blk[rinv]]                              # row lengths in global row order
+    rowptr = torch.zeros(m + 1, dtype=i64, device=device)
+    rowptr[1:] = torch.cumsum(L, 0)
+    nnz = int(rowptr[-1].item())
+    colidx = torch.empty(nnz, dtype=torch.int32, device=device)
+    vals = torch.empty(nnz, dtype=f64, device=device)
+    for r0 in range(0, m, chunk_rows):
+        r1 = min(m, r0 + chunk_rows)
+        z0, z1 = int(rowptr[r0].item()), int(rowptr[r1].item())
+        grow = torch.repeat_interleave(torch.arange(r0, r1, device=device, dtype=i64),
+                                       L[r0:r1])
+        j = torch.arange(z0, z1, device=device, dtype=i64) - rowptr[grow]
+        slot_i = rinv[grow]                       # row slot (local i = slot_i - start[t])
+        t = blk[slot_i]
+        slot_j = start[t] + j                     # column slot of local column j
+        xi, yi, si = x[slot_i], y[slot_i], s[slot_i]
+        xj, yj, sj = x[slot_j], y[slot_j], s[slot_j]
+        v = -2.0 * xi * xj * sj - 2.0 * si * yi * yj + 4.0 * cblk[t] * xi * yj
+        v += torch.where(slot_i == slot_j, si, torch.zeros_like(si))
+        colidx[z0:z1] = cols_sorted[slot_j]
+        vals[z0:z1] = v
+        del grow, j, slot_i, t, slot_j, xi, yi, si, xj, yj, sj, v
+    sigma_all = np.sort(s.cpu().numpy())[::-1]
+    return rowptr, colidx, vals, sigma_all
