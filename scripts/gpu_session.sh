@@ -1,10 +1,10 @@
 set -x
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
-timeout 900 python -m pytest tests/test_gpu_solvers.py tests/test_gpu_loopback.py tests/test_gpu_kernels.py tests/test_gpu_dist.py -m gpu -q -p no:cacheprovider > $O/s7_pytest.log 2>&1
-echo pytest rc $?
-SPMM_CFG=C2,C3 timeout 300 python scripts/bench_kernels.py spmm > $O/s7_spmm.log 2>&1
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $O/s7_bench.json 2> $O/s7_bench.err
-TSVD_GRAPHS=0 timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $O/s7_bench_nograph.json 2> $O/s7_bench_nograph.err
-timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --ortho bcgs_pip2 > $O/s7_bench_pip2.json 2> $O/s7_bench_pip2.err
+timeout 1200 python tests/c5g2_check.py > $O/s8_c5g2.json 2> $O/s8_c5g2.err
+echo c5g2 rc $?
+timeout 1500 python bench.py --config C5g2 --steps 1 --warmup 1 --no-cpu-baseline > $O/s8_bench_c5g2.json 2> $O/s8_bench_c5g2.err
+echo bench c5g2 rc $?
+timeout 900 python bench.py --config C5 --steps 3 --warmup 1 --no-cpu-baseline > $O/s8_bench_c5.json 2> $O/s8_bench_c5.err
+echo bench c5 rc $?
 echo done
