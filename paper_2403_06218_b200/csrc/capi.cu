@@ -1,6 +1,9 @@
 // extern "C" entry points of include/tsvd.h.  Argument validation, copies
 // across the host/device boundary, and exception -> status translation.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "ctx.h"
@@ -76,8 +79,23 @@ const char* tsvd_last_error(void) { return tsvd::g_last_error.c_str(); }
 
 // Build the CSR part of a handle whose local/global geometry is already set:
 // c->m local rows, c->ng columns.  Validates, uploads, transposes, plans.
+// TSVD_TIMING=1: create-time phases on stderr (development)
+struct PhaseClock {
+  bool on = getenv("TSVD_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(const char* what, cudaStream_t st) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[tsvd create] %-12s %8.2f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 static tsvd_status setup_csr(tsvd_ctx* c, int64_t nnz, const int64_t* rowptr,
                              const int32_t* colidx, const double* vals, int mem_kind) {
+  PhaseClock clk;
   const int64_t m = c->m, n = c->ng;
   Csr& A = c->A;
   A.rows = m;
@@ -104,17 +122,22 @@ static tsvd_status setup_csr(tsvd_ctx* c, int64_t nnz, const int64_t* rowptr,
     TSVD_CUDA(cudaMemcpyAsync(A.vals, vals, nnz * sizeof(double), kind, c->st));
   }
   TSVD_CUDA(cudaStreamSynchronize(c->st));
+  clk.lap("upload", c->st);
   const int bad = csr_validate_device(A, c->st);  // warp per row, exact
+  clk.lap("validate", c->st);
   if (bad & ~2) return TSVD_EINVAL;               // bounds / out-of-range columns
   if (bad & 2) {                                  // unsorted or duplicates: canonicalise
     csr_canonicalize(A, c->st);
     TSVD_CUDA(cudaMemcpy(hrp.data(), A.rowptr, (m + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
   }
   csr_transpose(A, c->AT, c->st);
+  clk.lap("transpose", c->st);
   csr_build_plan(A, hrp.data(), c->st);
+  clk.lap("plan A", c->st);
   std::vector<int64_t> hrpt(n + 1);
   TSVD_CUDA(cudaMemcpy(hrpt.data(), c->AT.rowptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
   csr_build_plan(c->AT, hrpt.data(), c->st);
+  clk.lap("plan A^T", c->st);
   return TSVD_OK;
 }
 

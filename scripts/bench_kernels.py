@@ -79,6 +79,28 @@ def nn_bench():
               f"{tf:.1f} TF/s ({tf / 37.1:.2f} of DMMA)", flush=True)
 
 
+def nn32_bench():
+    """the w = 32 NN pass at C3's largest s (the dominant kernel of C3 / C5)
+    and the TN pass beside it, for ncu"""
+    q, s, w = 1_000_000, 640, 32
+    X = torch.randn((q, s + w), dtype=torch.float64, device="cuda")
+    H = torch.randn((s, w), dtype=torch.float64, device="cuda")
+    Z = torch.empty((q, w), dtype=torch.float64, device="cuda")
+    C = torch.empty((s, w), dtype=torch.float64, device="cuda")
+    G = torch.empty((148, w, w), dtype=torch.float64, device="cuda")
+    L = T.lib()
+    ms = timeit(lambda: L.tsvd_dbg_gemm_nn(X.data_ptr(), s + w, H.data_ptr(), w, Z.data_ptr(), w,
+                                           q, s, w, -1.0, 1.0, None))
+    tf = 2.0 * q * (s + w) * w / (ms * 1e-3) / 1e12
+    print(f"gemm_nn q={q} s={s} w={w}: {ms:.3f} ms  {tf:.1f} TF/s ({tf / 37.1:.2f} of DMMA)",
+          flush=True)
+    ms = timeit(lambda: L.tsvd_dbg_gemm_tn(X.data_ptr(), s + w, X[:, s:].data_ptr(), s + w, q, s,
+                                           w, C.data_ptr(), None))
+    tf = 2.0 * q * s * w / (ms * 1e-3) / 1e12
+    print(f"gemm_tn q={q} s={s} w={w}: {ms:.3f} ms  {tf:.1f} TF/s ({tf / 37.1:.2f} of DMMA)",
+          flush=True)
+
+
 def sweep_bench():
     q, w = 1_000_000, 16
     X = torch.randn((q, 400), dtype=torch.float64, device="cuda")

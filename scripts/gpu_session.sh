@@ -1,10 +1,10 @@
 set -x
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
-timeout 1200 python tests/c5g2_check.py > $O/s8_c5g2.json 2> $O/s8_c5g2.err
-echo c5g2 rc $?
-timeout 1500 python bench.py --config C5g2 --steps 1 --warmup 1 --no-cpu-baseline > $O/s8_bench_c5g2.json 2> $O/s8_bench_c5g2.err
-echo bench c5g2 rc $?
-timeout 900 python bench.py --config C5 --steps 3 --warmup 1 --no-cpu-baseline > $O/s8_bench_c5.json 2> $O/s8_bench_c5.err
-echo bench c5 rc $?
+timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=30 > $O/s9_pytest.log 2>&1
+echo pytest rc $?
+timeout 1200 python scripts/equal_accuracy.py C3 C4 > $O/s9_equal_accuracy.jsonl 2> $O/s9_equal_accuracy.err
+echo eq rc $?
+timeout 600 python bench.py --config C3 --steps 3 --warmup 3 --no-cpu-baseline > $O/s9_bench_C3.json 2> $O/s9_bench_C3.err
+timeout 600 python bench.py --config C4 --steps 3 --warmup 3 --no-cpu-baseline > $O/s9_bench_C4.json 2> $O/s9_bench_C4.err
 echo done
