@@ -649,6 +649,7 @@ def main():
         m_loc = int((geo["row_end"] - geo["row_begin"]) if use_dist else cfg["m"])
         n_loc = int(-(-cfg["n"] // world) if use_dist else cfg["n"])
         Uo, So, Vo = pinned(np.empty((m_loc, r))), pinned(np.empty(r)), pinned(np.empty((n_loc, r)))
+        parts = []
         for _ in range(args.e2e_steps):
             t0 = time.perf_counter()
             dkw2 = fresh_dist_kw(geo) if use_dist else None
@@ -657,15 +658,21 @@ def main():
                       T.TruncatedSVD(csr=hin["csr"], shape=hwork["shape"]))
             else:
                 h2 = (T.TruncatedSVD(hin["A"], dist=dkw2) if dkw2 else T.TruncatedSVD(hin["A"]))
+            t1 = time.perf_counter()
             h2.set_seed(seed)
             h2.set_krylov_dim(d)
             h2.set_thick_restart(keep)
             h2.set_ortho(args.ortho)
             solve(h2)
+            torch.cuda.synchronize()
+            t2 = time.perf_counter()
             h2.get_into(Uo[:h2.m], So, Vo[:h2.n])
+            t3 = time.perf_counter()
             h2.close()
             torch.cuda.synchronize()
             times.append(time.perf_counter() - t0)
+            parts.append([round(1e3 * (t1 - t0), 1), round(1e3 * (t2 - t1), 1),
+                          round(1e3 * (t3 - t2), 1), round(1e3 * (time.perf_counter() - t3), 1)])
             d2h = Uo[:h2.m].nbytes + So.nbytes + Vo[:h2.n].nbytes
         ev = statistics.median(times)
         if dist:
@@ -673,7 +680,8 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ev = float(t.item())
         e2e = {"value": round(ev, 6), "unit": "s", "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(d2h)}
+               "d2h_bytes_per_step": int(d2h),
+               "steps_ms_create_solve_get_destroy": parts}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

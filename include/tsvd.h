@@ -214,8 +214,9 @@ tsvd_status tsvd_set_start(tsvd_t h, const double* block, int64_t rows,
  * (CGS-CQR2, Alg. 5) and the basic restart of [9], restart block
  * re-orthonormalised (reading R11).  Cycles until
  * max_{i<=r} ||Rbar_k Vbar[last b rows, i]||_2 <= tol * sigma_1 (from Eq. 10,
- * reading R12) or maxit cycles.  r >= 1 wanted triplets, b >= 1 block size,
- * tol > 0, maxit >= 1. */
+ * reading R12) or maxit cycles.  r >= 1 wanted triplets, b >= 1 block size
+ * (any width: blocks wider than 32 are orthogonalised in 32-column panels as
+ * Alg. 3 does), tol > 0, maxit >= 1. */
 tsvd_status tsvd_block_lanczos(tsvd_t h, int r, int b, double tol, int maxit);
 /* tsvd_block_lanczos_threshold (Eq. 3): the rank r
  * is set by the threshold ||A - U_r S_r V_r^T||_2 = sigma_{r+1} <= tau *

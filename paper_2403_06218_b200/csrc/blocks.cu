@@ -18,6 +18,8 @@
 #include <mutex>
 #include <unordered_map>
 
+#include <algorithm>
+
 #include "ctx.h"
 
 namespace tsvd {
@@ -492,6 +494,36 @@ void cgs2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H,
     if (s > 0 && H) copy_block(coef, 1, H + j, w, s, 1, false, c.st);
     if (j > 0) copy_block(coef + s, 1, R + j, w, j, 1, false, c.st);
   }
+}
+
+// LancSVD's block orthogonalisation for any block width b (b >= 1):
+// the columns [s, s + b) of `basis` against [0, s), R (b x b, ld b) with
+// Y = P H + Q R (H discarded, reading R17).  b <= 32: one CholQR2 (s = 0) or
+// CGS-CQR2 call.  Wider blocks go in 32-column panels exactly like Alg. 3
+// (CGS-QR): panel j against P and the earlier panels, R's column block j =
+// [the earlier panels' rows of H_j; R_jj].  The QR with positive diagonal is
+// unique, so this is the oracle's b-wide CholQR2 / CGS-CQR2 up to rounding.
+int block_orth(Ctx& c, double* basis, int64_t q, int s, int b, int64_t ld, double* R) {
+  if (b <= 32) {
+    if (s == 0) return cholqr2(c, basis, q, b, ld, R);
+    double* H = dbuf(c, "H", (size_t)s * 32);
+    return cgs_cqr2(c, basis, q, s, b, ld, H, R, false);
+  }
+  int bd = 0;
+  fill_zero(R, (int64_t)b * b, c.st);
+  double* Hj = dbuf(c, "borth_H", (size_t)(s + b) * 32);
+  double* Rj = dbuf(c, "borth_R", 32 * 32);
+  for (int j0 = 0; j0 < b; j0 += 32) {
+    const int w = std::min(32, b - j0);
+    if (s + j0 == 0) {
+      bd += cholqr2(c, basis, q, w, ld, Rj);
+    } else {
+      bd += cgs_cqr2(c, basis, q, s + j0, w, ld, Hj, Rj, true);
+      if (j0 > 0) copy_block(Hj + (size_t)s * w, w, R + j0, b, j0, w, false, c.st);
+    }
+    copy_block(Rj, w, R + (int64_t)j0 * b + j0, b, w, w, false, c.st);
+  }
+  return bd;
 }
 
 int cgs_qr(Ctx& c, double* Y, int64_t q, int l, int64_t ld, int bq, double* R) {

@@ -1,6 +1,8 @@
 // extern "C" entry points of include/tsvd.h.  Argument validation, copies
 // across the host/device boundary, and exception -> status translation.
 #include <algorithm>
+#include <mutex>
+#include <vector>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -29,6 +31,28 @@ using namespace tsvd;
     return TSVD_ECUDA;                                 \
   }
 
+// Pinned host words for the per-cycle flag / sweep read-backs, handed out
+// from a process-wide arena: cudaMallocHost / cudaFreeHost per handle
+// synchronise the device (and cost milliseconds on a busy host).
+static std::mutex g_pin_mu;
+static std::vector<int*> g_pin_free;
+static int* pinned_words() {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  if (g_pin_free.empty()) {
+    int* blk = nullptr;
+    TSVD_CUDA(cudaMallocHost(&blk, 64 * 8 * sizeof(int)));  // 64 slots of 8 ints, never freed
+    for (int i = 0; i < 64; ++i) g_pin_free.push_back(blk + 8 * i);
+  }
+  int* p = g_pin_free.back();
+  g_pin_free.pop_back();
+  return p;
+}
+static void pinned_words_free(int* p) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.push_back(p);
+}
+
 static tsvd_status init_ctx(tsvd_ctx* c) {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
@@ -37,8 +61,8 @@ static tsvd_status init_ctx(tsvd_ctx* c) {
   }
   TSVD_CUDA(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
   c->own_stream = true;
-  TSVD_CUDA(cudaMalloc(&c->dflags, 4 * sizeof(int)));
-  TSVD_CUDA(cudaMallocHost(&c->hflags, 8 * sizeof(int)));
+  c->dflags = (int*)dmalloc(4 * sizeof(int), c->st);  // stream-ordered pool, no device sync
+  c->hflags = pinned_words();
   return TSVD_OK;
 }
 
@@ -51,8 +75,8 @@ static void destroy_ctx(tsvd_ctx* c) {
   free_bufs(*c);
   prof_release(*c);
   comm_destroy(*c);
-  cudaFree(c->dflags);
-  if (c->hflags) cudaFreeHost(c->hflags);
+  if (c->dflags) dfree(c->dflags, c->st);
+  pinned_words_free(c->hflags);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
   delete c;
 }
@@ -103,15 +127,11 @@ static tsvd_status setup_csr(tsvd_ctx* c, int64_t nnz, const int64_t* rowptr,
   A.nnz = nnz;
   const cudaMemcpyKind kind = mem_kind == TSVD_DEVICE ? cudaMemcpyDeviceToDevice
                                                       : cudaMemcpyHostToDevice;
-  std::vector<int64_t> hrp(m + 1);
-  if (mem_kind == TSVD_DEVICE) {
-    TSVD_CUDA(cudaMemcpy(hrp.data(), rowptr, (m + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
-  } else {
-    std::memcpy(hrp.data(), rowptr, (m + 1) * sizeof(int64_t));
+  if (mem_kind != TSVD_DEVICE) {
     // row pointer checked here (O(m)); the column indices on the device below
-    if (hrp[0] != 0 || hrp[m] != nnz) return TSVD_EINVAL;
+    if (rowptr[0] != 0 || rowptr[m] != nnz) return TSVD_EINVAL;
     for (int64_t i = 0; i < m; ++i)
-      if (hrp[i + 1] < hrp[i]) return TSVD_EINVAL;
+      if (rowptr[i + 1] < rowptr[i]) return TSVD_EINVAL;
   }
   dmalloc_t(&A.rowptr, m + 1, c->st);
   dmalloc_t(&A.colidx, std::max<int64_t>(1, nnz), c->st);
@@ -126,17 +146,12 @@ static tsvd_status setup_csr(tsvd_ctx* c, int64_t nnz, const int64_t* rowptr,
   const int bad = csr_validate_device(A, c->st);  // warp per row, exact
   clk.lap("validate", c->st);
   if (bad & ~2) return TSVD_EINVAL;               // bounds / out-of-range columns
-  if (bad & 2) {                                  // unsorted or duplicates: canonicalise
-    csr_canonicalize(A, c->st);
-    TSVD_CUDA(cudaMemcpy(hrp.data(), A.rowptr, (m + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
-  }
+  if (bad & 2) csr_canonicalize(A, c->st);        // unsorted or duplicates: canonicalise
   csr_transpose(A, c->AT, c->st);
   clk.lap("transpose", c->st);
-  csr_build_plan(A, hrp.data(), c->st);
+  csr_plan(A, c->st);
   clk.lap("plan A", c->st);
-  std::vector<int64_t> hrpt(n + 1);
-  TSVD_CUDA(cudaMemcpy(hrpt.data(), c->AT.rowptr, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
-  csr_build_plan(c->AT, hrpt.data(), c->st);
+  csr_plan(c->AT, c->st);
   clk.lap("plan A^T", c->st);
   return TSVD_OK;
 }

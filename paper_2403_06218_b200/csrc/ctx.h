@@ -131,6 +131,8 @@ int cgs_cqr2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double*
              double* R, bool need_h = true);
 void cgs2(Ctx& c, double* basis, int64_t q, int s, int w, int64_t ld, double* H, double* R);
 int cgs_qr(Ctx& c, double* Y, int64_t q, int l, int64_t ld, int bq, double* R);
+// any-width LancSVD block orthogonalisation (32-column panels above 32)
+int block_orth(Ctx& c, double* basis, int64_t q, int s, int b, int64_t ld, double* R);
 void apply(Ctx& c, bool trans, const double* X, int64_t ldx, double* Y, int64_t ldy, int w);
 
 // collectives (comm.cu); no-ops / errors when world == 1 / NCCL missing

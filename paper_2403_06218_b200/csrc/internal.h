@@ -111,6 +111,9 @@ template <class T> inline void dmalloc_t(T** p, size_t count, cudaStream_t st) {
 }
 void csr_transpose(const Csr& A, Csr& T, cudaStream_t st);
 void csr_build_plan(Csr& A, const int64_t* host_rowptr, cudaStream_t st);
+// the plan built on the device (default; the host plan when the staged SpMM
+// needs its length bins)
+void csr_plan(Csr& A, cudaStream_t st);
 void csr_free(Csr& A, cudaStream_t st);
 // device validation of a CSR: 0 if canonical; bits: 1 bad row bounds, 2
 // unsorted or duplicate columns in a row (canonicalisable), 4 rowptr[0] != 0

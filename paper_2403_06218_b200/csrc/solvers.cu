@@ -140,7 +140,6 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   const int64_t m = c.m, n = c.n;  // this rank's rows (single GPU: all)
   DeferredGuard guard(c);
   if (r < 1 || b < 1 || !(tol > 0.0) || maxit < 1) return TSVD_EINVAL;
-  if (b > 32) return TSVD_EINVAL;  // kernel tile limit
   if (r > c.ng) return TSVD_ESHAPE;
   int d = c.krylov_d;
   if (d == 0) {
@@ -169,9 +168,10 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   double* Vb = dbuf(c, "Vb", (size_t)d * d);
   double* Sg = dbuf(c, "Sg", (size_t)d);
   double* jw = dbuf(c, "jacobi_work", small_svd_work(d));
-  double* H = dbuf(c, "H", (size_t)d * 32);
-  double* R = dbuf(c, "R", 32 * 32);
-  double* Rb = dbuf(c, "Rb", 32 * 32);
+  (void)dbuf(c, "H", (size_t)d * 32);
+  const size_t rb = (size_t)std::max(32, b);
+  double* R = dbuf(c, "R", rb * rb);
+  double* Rb = dbuf(c, "Rb", rb * rb);
   double* rho = dbuf(c, "rho", (size_t)d);
   // pre-size the pass workspaces for the largest q and s of this solve
   (void)dbuf(c, "scratch", (size_t)std::max(m, n) * 32);
@@ -187,7 +187,7 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   else
     launch_philox_normal(Pb, m, b, ldb, c.seed, 0, c.m0, c.mg, c.st);
   m_side();
-  cholqr2(c, Pb, m, b, ldb, R);
+  block_orth(c, Pb, m, 0, b, ldb, R);
 
   std::vector<double> hrho(r), hs(1);
   unsigned* hsw = reinterpret_cast<unsigned*>(c.hflags + 4);  // pinned word
@@ -208,16 +208,13 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
       apply(c, true, Pb + lo, ldb, P + lo, ldp, b);                  // S2: A^T Qbar_i
       n_side();
       c.flag_slot = 2 * i;
-      if (lo == 0)
-        cholqr2(c, P, n, b, ldp, R);                                 // S3a
-      else
-        cgs_cqr2(c, P, n, lo, b, ldp, H, R, false);                  // S3b (H unused, R17)
+      block_orth(c, P, n, lo, b, ldp, R);                            // S3a / S3b (H unused, R17)
       copy_block(R, b, B + (int64_t)lo * d + lo, d, b, b, true, c.st);  // L_i = R^T
     }
     apply(c, false, P + lo, ldp, Pb + lo + b, ldb, b);               // S4: A Q_i
     m_side();
     c.flag_slot = 2 * i + 1;
-    cgs_cqr2(c, Pb, m, lo + b, b, ldb, H, Rb, false);                // S5 (H unused, R17)
+    block_orth(c, Pb, m, lo + b, b, ldb, Rb);                        // S5 (H unused, R17)
     if (i < kc - 1)
       copy_block(Rb, b, B + (int64_t)(lo + b) * d + lo, d, b, b, false, c.st);  // Rbar_i
   };
@@ -369,7 +366,7 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
       Prof p(c, P_RESTART, 8.0 * m * (d + b), 2.0 * m * d * b);
       gemm_nn(Pb, ldb, Ub, d, nullptr, 0, nullptr, Pb + d, ldb, m, d, b, 1.0, 0.0, nullptr, c.st);
     }
-    cholqr2(c, Pb + d, m, b, ldb, R);
+    block_orth(c, Pb + d, m, 0, b, ldb, R);
     {
       Prof p(c, P_RESTART, 16.0 * m * b, 0);
       copy_block(Pb + d, ldb, Pb, ldb, m, b, false, c.st);

@@ -645,6 +645,165 @@ __global__ void csr_permute_kernel(const int64_t* __restrict__ old_rp,
 // output row of each position), and long rows are cut into segments.  A warp
 // of short rows then reads adjacent rows' nonzeros (one chain fewer than an
 // order[] -> rowptr[row] indirection) and writes Y[perm[p]].
+// ---------------------------------------------------- device-side plan ---
+// The same plan as csr_build_plan, built on the device so handle creation
+// does not walk the row pointer on the host (create time of C2: two host
+// plans were ~30 ms of ~60 ms).  Rows get a sort key encoding their class
+// and length -- short (<= kLongRow): kLongRow - len; medium: kLongRow + 1 +
+// kMedRow - len; long: one key above -- and a stable radix sort of (key, row)
+// yields exactly the host order (short / medium by decreasing length, ties
+// and long rows in row order).  Only the long rows' positions come back to
+// the host to cut them into segments.
+constexpr uint32_t kKeyLong = kLongRow + 1 + kMedRow + 1;
+
+__global__ void plan_keys_kernel(const int64_t* __restrict__ rowptr, int64_t rows,
+                                 uint32_t* __restrict__ key, int32_t* __restrict__ idx) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t len = rowptr[i + 1] - rowptr[i];
+    key[i] = len <= kLongRow ? (uint32_t)(kLongRow - len)
+                             : len <= kMedRow ? (uint32_t)(kLongRow + 1 + kMedRow - len) : kKeyLong;
+    idx[i] = (int32_t)i;
+  }
+}
+
+__global__ void plan_lens_kernel(const int64_t* __restrict__ rowptr,
+                                 const int32_t* __restrict__ perm, int64_t rows,
+                                 int64_t* __restrict__ lens) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q <= rows;
+       q += (int64_t)gridDim.x * blockDim.x)
+    lens[q] = q < rows ? rowptr[perm[q] + 1] - rowptr[perm[q]] : 0;
+}
+
+// counts[0] = #keys <= kLongRow (short), counts[1] = #keys < kKeyLong, on sorted keys
+__global__ void plan_counts_kernel(const uint32_t* __restrict__ key, int64_t rows,
+                                   int64_t* __restrict__ counts) {
+  const uint32_t bound = threadIdx.x == 0 ? (uint32_t)kLongRow + 1 : kKeyLong;
+  if (threadIdx.x > 1) return;
+  int64_t lo = 0, hi = rows;  // first position with key >= bound
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (key[mid] < bound) lo = mid + 1; else hi = mid;
+  }
+  counts[threadIdx.x] = lo;
+}
+
+static bool csr_build_plan_device(Csr& A, cudaStream_t st) {
+  const int64_t rows = A.rows;
+  if (rows <= 0 || rows >= (int64_t)INT32_MAX) return false;
+  const unsigned grid = (unsigned)std::min<int64_t>((rows + 255) / 256, 148 * 16);
+  uint32_t *k_in, *k_out;
+  int32_t *i_in, *perm;
+  int64_t *lens, *new_rp, *counts;
+  dmalloc_t(&k_in, rows, st);
+  dmalloc_t(&k_out, rows, st);
+  dmalloc_t(&i_in, rows, st);
+  dmalloc_t(&perm, rows + 4, st);  // + padding: bulk copies read whole 16-byte pieces
+  TSVD_CUDA(cudaMemsetAsync(perm + rows, 0, 4 * sizeof(int32_t), st));
+  dmalloc_t(&lens, rows + 1, st);
+  dmalloc_t(&new_rp, rows + 1, st);
+  dmalloc_t(&counts, 2, st);
+  plan_keys_kernel<<<grid, 256, 0, st>>>(A.rowptr, rows, k_in, i_in);
+  TSVD_CHECK_LAUNCH();
+  int end_bit = 1;
+  while ((1u << end_bit) <= kKeyLong) ++end_bit;
+  size_t sort_b = 0, scan_b = 0;
+  TSVD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, sort_b, k_in, k_out, i_in, perm, (int)rows,
+                                            0, end_bit, st));
+  TSVD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_b, lens, new_rp, (int)(rows + 1), st));
+  void* tmp = dmalloc(std::max(sort_b, scan_b), st);
+  TSVD_CUDA(cub::DeviceRadixSort::SortPairs(tmp, sort_b, k_in, k_out, i_in, perm, (int)rows, 0,
+                                            end_bit, st));
+  plan_lens_kernel<<<grid, 256, 0, st>>>(A.rowptr, perm, rows, lens);
+  plan_counts_kernel<<<1, 32, 0, st>>>(k_out, rows, counts);
+  TSVD_CHECK_LAUNCH();
+  TSVD_CUDA(cub::DeviceScan::ExclusiveSum(tmp, scan_b, lens, new_rp, (int)(rows + 1), st));
+  int64_t hc[2] = {0, 0};
+  TSVD_CUDA(cudaMemcpyAsync(hc, counts, sizeof(hc), cudaMemcpyDeviceToHost, st));
+  TSVD_CUDA(cudaStreamSynchronize(st));
+  const int64_t nshort = hc[0], nmed = hc[1] - hc[0], q0 = hc[1], nlong = rows - q0;
+  // long rows: their rows and new row-pointer range back to the host
+  std::vector<int32_t> lrow(nlong);
+  std::vector<int64_t> lrp(nlong + 1);
+  if (nlong > 0) {
+    TSVD_CUDA(cudaMemcpyAsync(lrow.data(), perm + q0, nlong * sizeof(int32_t),
+                              cudaMemcpyDeviceToHost, st));
+    TSVD_CUDA(cudaMemcpyAsync(lrp.data(), new_rp + q0, (nlong + 1) * sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, st));
+    TSVD_CUDA(cudaStreamSynchronize(st));
+  }
+  std::vector<int64_t> srow, sbeg, send, sprow;
+  std::vector<int32_t> sslot, spfirst, spcnt;
+  int32_t slots = 0;
+  for (int64_t j = 0; j < nlong; ++j) {
+    const int64_t i = lrow[j], b = lrp[j], len = lrp[j + 1] - lrp[j];
+    const int64_t nseg = (len + kSeg - 1) / kSeg;
+    if (nseg > 1) {
+      sprow.push_back(i);
+      spfirst.push_back(slots);
+      spcnt.push_back((int32_t)nseg);
+    }
+    for (int64_t sg = 0; sg < nseg; ++sg) {
+      srow.push_back(i);
+      sbeg.push_back(b + sg * kSeg);
+      send.push_back(std::min(b + len, b + (sg + 1) * kSeg));
+      sslot.push_back(nseg > 1 ? slots++ : -1);
+    }
+  }
+  A.nseg = (int64_t)srow.size();
+  A.nsplit = (int64_t)sprow.size();
+  A.nslots = slots;
+  A.nshort = nshort;
+  A.nmed = nmed;
+  auto up64 = [&](std::vector<int64_t>& v, int64_t** d) {
+    if (v.empty()) return;
+    dmalloc_t(d, v.size(), st);
+    TSVD_CUDA(cudaMemcpyAsync(*d, v.data(), v.size() * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  };
+  auto up32 = [&](std::vector<int32_t>& v, int32_t** d) {
+    if (v.empty()) return;
+    dmalloc_t(d, v.size(), st);
+    TSVD_CUDA(cudaMemcpyAsync(*d, v.data(), v.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  };
+  up64(srow, &A.seg_row);
+  up64(sbeg, &A.seg_beg);
+  up64(send, &A.seg_end);
+  up32(sslot, &A.seg_slot);
+  up64(sprow, &A.split_row);
+  up32(spfirst, &A.split_first);
+  up32(spcnt, &A.split_count);
+  A.perm = perm;
+  if (A.nnz > 0) {
+    int32_t* nci;
+    double* nva;
+    dmalloc_t(&nci, A.nnz + 4, st);
+    dmalloc_t(&nva, A.nnz + 2, st);
+    const unsigned pg = (unsigned)std::min<int64_t>((rows + 7) / 8, 148 * 64);
+    csr_permute_kernel<<<pg, 256, 0, st>>>(A.rowptr, A.colidx, A.vals, A.perm, new_rp, rows, nci,
+                                           nva);
+    TSVD_CHECK_LAUNCH();
+    dfree(A.colidx, st);
+    dfree(A.vals, st);
+    A.colidx = nci;
+    A.vals = nva;
+  }
+  dfree(A.rowptr, st);
+  A.rowptr = new_rp;
+  TSVD_CUDA(cudaStreamSynchronize(st));
+  for (void* q : {(void*)k_in, (void*)k_out, (void*)i_in, (void*)lens, (void*)counts, tmp})
+    dfree(q, st);
+  return true;
+}
+
+void csr_plan(Csr& A, cudaStream_t st) {
+  // the staged SpMM (TSVD_SPMM_STAGED=1) also needs the length bins: host plan
+  if (!g_spmm_staged && csr_build_plan_device(A, st)) return;
+  std::vector<int64_t> hrp(A.rows + 1);
+  TSVD_CUDA(cudaMemcpy(hrp.data(), A.rowptr, (A.rows + 1) * sizeof(int64_t),
+                       cudaMemcpyDeviceToHost));
+  csr_build_plan(A, hrp.data(), st);
+}
+
 void csr_build_plan(Csr& A, const int64_t* hrp, cudaStream_t st) {
   auto len_of = [&](int64_t i) { return hrp[i + 1] - hrp[i]; };
   // short rows, counting-sorted by decreasing length (stable in the row index)

@@ -871,7 +871,7 @@ struct NnTmaCfg {
 };
 
 template <int KC, int S, int NYB>
-__global__ void __launch_bounds__(288, NYB == 1 ? 2 : 1) gemm_nn_tma_kernel(
+__global__ void __maxnreg__(NYB == 1 ? 112 : 224) gemm_nn_tma_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
     const __grid_constant__ CUtensorMap ymap, int use_y, const double* __restrict__ T, double* Z,
     int64_t ldz, int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram,
@@ -922,12 +922,17 @@ __global__ void __launch_bounds__(288, NYB == 1 ? 2 : 1) gemm_nn_tma_kernel(
   Z += (int64_t)blockIdx.y * zsplit;
   if (warp == 8) {  // producer: X/H chunks into the ring, the tile's Y rows into Ys
     if (lane == 0) {
+      // ring slot / phase and (tile, k-chunk) kept as running counters: no
+      // 64-bit divisions by S and by the runtime nk per step
+      int st = 0, kc = 0;
+      unsigned u = 0;
+      int64_t lt = 0;
       for (int64_t j = 0; j < nsteps; ++j) {
-        const int st = (int)(j % S);
-        const unsigned u = (unsigned)(j / S);
+        if (j > 0) {
+          if (++st == S) st = 0, ++u;
+          if (++kc == nk) kc = 0, ++lt;
+        }
         if (j >= S) mbar_wait(&empty[st], (u - 1) & 1);
-        const int64_t lt = j / nk;
-        const int kc = (int)(j % nk);
         const int r0 = (int)((blockIdx.x + lt * gridDim.x) * NT_R);
         unsigned char* base = sm + (size_t)st * CF::stage;
         mbar_expect_tx(&full[st], CF::tx);
@@ -955,11 +960,14 @@ __global__ void __launch_bounds__(288, NYB == 1 ? 2 : 1) gemm_nn_tma_kernel(
   const bool zal = Z && ((((uintptr_t)Z) | (uintptr_t)(ldz * 8)) & 15) == 0;
   double* Ow = Os + warp * 16 * OP;  // this warp's rows of the out tile
   double acc[2][2][NT][2];
+  int st = 0, kc = 0;
+  unsigned u = 0;
+  int64_t lt = 0;
   for (int64_t j = 0; j < nsteps; ++j) {
-    const int st = (int)(j % S);
-    const unsigned u = (unsigned)(j / S);
-    const int kc = (int)(j % nk);
-    const int64_t lt = j / nk;
+    if (j > 0) {
+      if (++st == S) st = 0, ++u;
+      if (++kc == nk) kc = 0, ++lt;
+    }
     const int64_t r0 = (blockIdx.x + lt * gridDim.x) * NT_R;
     if (kc == 0) {
 #pragma unroll
@@ -1170,12 +1178,17 @@ __global__ void __launch_bounds__(288, 1) gemm_nn_out_tma_kernel(
   Z += (int64_t)blockIdx.y * zsplit;
   if (warp == 8) {
     if (lane == 0) {
+      // ring slot / phase and (tile, k-chunk) kept as running counters: no
+      // 64-bit divisions by S and by the runtime nk per step
+      int st = 0, kc = 0;
+      unsigned u = 0;
+      int64_t lt = 0;
       for (int64_t j = 0; j < nsteps; ++j) {
-        const int st = (int)(j % S);
-        const unsigned u = (unsigned)(j / S);
+        if (j > 0) {
+          if (++st == S) st = 0, ++u;
+          if (++kc == nk) kc = 0, ++lt;
+        }
         if (j >= S) mbar_wait(&empty[st], (u - 1) & 1);
-        const int64_t lt = j / nk;
-        const int kc = (int)(j % nk);
         const int r0 = (int)((blockIdx.x + lt * gridDim.x) * NT_R);
         unsigned char* base = sm + (size_t)st * CF::stage;
         mbar_expect_tx(&full[st], CF::tx);

@@ -1,10 +1,9 @@
 set -x
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
-timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=30 > $O/s9_pytest.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_solvers.py -m gpu -q -x -p no:cacheprovider > $O/s12_pytest.log 2>&1
 echo pytest rc $?
-timeout 1200 python scripts/equal_accuracy.py C3 C4 > $O/s9_equal_accuracy.jsonl 2> $O/s9_equal_accuracy.err
-echo eq rc $?
-timeout 600 python bench.py --config C3 --steps 3 --warmup 3 --no-cpu-baseline > $O/s9_bench_C3.json 2> $O/s9_bench_C3.err
-timeout 600 python bench.py --config C4 --steps 3 --warmup 3 --no-cpu-baseline > $O/s9_bench_C4.json 2> $O/s9_bench_C4.err
+timeout 300 python scripts/bench_kernels.py nn32 nn > $O/s12_nn.log 2>&1
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > $O/s12_bench.json 2> $O/s12_bench.err
+timeout 600 python bench.py --config C3 --steps 3 --warmup 2 --no-cpu-baseline --e2e-steps 0 > $O/s12_bench_C3.json 2> $O/s12_bench_C3.err
 echo done

@@ -508,3 +508,28 @@ def test_cycle_graph_replay_is_bit_identical(kind):
             assert np.array_equal(a, b)
         assert o[3]["launches"] == outs[0][3]["launches"]
         assert o[4] == outs[0][4] and o[5] == outs[0][5]
+
+
+@pytest.mark.parametrize("b,d,r", [(40, 120, 20), (48, 96, 30)])
+def test_wide_block_lanczos_parity(b, d, r):
+    """P:174 allows any b >= 1: blocks wider than the 32-column kernel tile
+    are orthogonalised in 32-column panels (block_orth, as Alg. 3 does for
+    RandSVD); the QR with positive diagonal is unique, so the result equals
+    the oracle's b-wide CholQR2 / CGS-CQR2 iteration to rounding."""
+    n = 200
+    s = 10.0 * 0.9 ** np.arange(n)
+    A = dense_prescribed(400, n, s, seed=b)
+    op = oracle.Operator(dense=A)
+    ro = oracle.lancsvd(op, r=r, b=b, d=d, tol=1e-10, maxit=6, seed=3)
+    with T.TruncatedSVD(A) as h:
+        h.set_seed(3)
+        st = h.block_lanczos(r=r, b=b, tol=1e-10, maxit=6, d=d)
+        Ug, Sg, Vg = h.get()
+        info = h.info()
+        rho = h.rho()
+    assert info["cycles"] == ro.cycles and info["breakdowns"] == 0
+    conv = (rho <= 1e-10) & (ro.rho <= 1e-10 * ro.S[0])
+    assert conv.sum() >= 10
+    _accept(op, Ug, Sg, Vg, ro.S, conv_mask=conv)
+    assert np.abs(Sg - s[:r])[conv].max() / s[0] <= 1e-10
+    _vec_parity(Ug[:, conv], Vg[:, conv], ro.U[:, conv], ro.V[:, conv], ro.S[conv])

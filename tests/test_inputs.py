@@ -44,3 +44,21 @@ def test_device_generator_deterministic():
     b = powerlaw_csr_device(5000, 4000, 40000, 2.5, seed=9, device="cpu")
     for x, y in zip(a, b):
         assert torch.equal(x, y)
+
+
+def test_blockdiag_device_g2_closed_form_spectrum():
+    """G2 at C5 scale is built by blockdiag_csr_device (torch); on the CPU at
+    a small size its dense SVD equals the prescribed spectrum (Householder
+    reflector blocks: sigma(B_t) = s_t exactly) and the CSR is canonical."""
+    torch = pytest.importorskip("torch")
+    import scipy.sparse as sp
+    from tsvd_inputs import blockdiag_csr_device
+    m = 2500
+    rp, ci, va, sig = blockdiag_csr_device(m, m, 3.0, 2.5, 5, np.linspace(50, 30, 10),
+                                           tail_max=5.0, device="cpu", chunk_rows=600)
+    rp, ci, va = rp.numpy(), ci.numpy(), va.numpy()
+    A = sp.csr_matrix((va, ci.astype(np.int64), rp), shape=(m, m))
+    sv = np.linalg.svd(A.toarray(), compute_uv=False)
+    assert np.abs(sv - sig).max() <= 1e-13 * sig[0]
+    assert np.allclose(sig[:10], np.linspace(50, 30, 10)) and sig[10] <= 5.0
+    assert all(np.all(np.diff(ci[rp[i]:rp[i + 1]]) > 0) for i in range(m))
