@@ -871,11 +871,10 @@ struct NnTmaCfg {
 };
 
 template <int KC, int S, int NYB>
-__global__ void __maxnreg__(NYB == 1 ? 112 : 224) gemm_nn_tma_kernel(
-    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
-    const __grid_constant__ CUtensorMap ymap, int use_y, const double* __restrict__ T, double* Z,
-    int64_t ldz, int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram,
-    int64_t zsplit) {
+__device__ __forceinline__ void nn_tma_body(
+    const CUtensorMap& xmap, const CUtensorMap& hmap, const CUtensorMap& ymap, int use_y,
+    const double* __restrict__ T, double* Z, int64_t ldz, int64_t q, int s, int w, double alpha,
+    double beta, double* __restrict__ gram, int64_t zsplit) {
   // split-K (gridDim.y > 1, plain products only: no Y / T / Gram): CTA row y
   // takes K chunks [nk_all y / Y, nk_all (y+1) / Y) and writes its partial
   // product to Z + y zsplit; the caller sums the partials in a fixed order.
@@ -1131,6 +1130,29 @@ __global__ void __maxnreg__(NYB == 1 ? 112 : 224) gemm_nn_tma_kernel(
   }
 }
 
+// Register budgets: w <= 16 (NYB = 1) runs two CTAs per SM; w <= 32
+// (NYB = 2) one CTA.  Its 9 warps put 3 warps on one SM sub-partition, whose
+// 16384-register file caps a thread at 168 registers (measured: 216 fails
+// to launch with "too many resources"), so the w = 32 kernel keeps a few
+// spilled scalars; a 2-warps-per-partition layout (producer folded into a
+// consumer warp) would lift the cap.
+template <int KC, int S, int NYB>
+__global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
+    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
+    const __grid_constant__ CUtensorMap ymap, int use_y, const double* __restrict__ T, double* Z,
+    int64_t ldz, int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram,
+    int64_t zsplit) {
+  nn_tma_body<KC, S, NYB>(xmap, hmap, ymap, use_y, T, Z, ldz, q, s, w, alpha, beta, gram, zsplit);
+}
+template <int KC, int S, int NYB>
+__global__ void __launch_bounds__(288, 1) gemm_nn_tma_kernel_w32(
+    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
+    const __grid_constant__ CUtensorMap ymap, int use_y, const double* __restrict__ T, double* Z,
+    int64_t ldz, int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram,
+    int64_t zsplit) {
+  nn_tma_body<KC, S, NYB>(xmap, hmap, ymap, use_y, T, Z, ldz, q, s, w, alpha, beta, gram, zsplit);
+}
+
 // Output products Z = X H with w up to 64 (Alg. 2 S8/S9: V = P Vbar_r,
 // U = Pbar Ubar_r; Alg. 1 S6/S7), beta = 0 and no Gram: the same TMA ring
 // as gemm_nn_tma_kernel with 4 H boxes (64 columns) per stage, one
@@ -1306,20 +1328,20 @@ static bool nn_tma_launch(const double* X, int64_t ldx, const double* H, int64_t
     using CF2 = NnTmaCfg<NNT_KC, 3, 2>;
     static bool attr2 = false;
     if (!attr2) {
-      TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_tma_kernel<NNT_KC, 3, 2>,
+      TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_tma_kernel_w32<NNT_KC, 3, 2>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF2::bytes));
       attr2 = true;
     }
     const int ctas = nn_ctas(q, 32);
     const int ks = (use_y || T || gram) ? 1 : pick_split(q, s, w, ctas, part_cap);
     if (ks > 1) {
-      gemm_nn_tma_kernel<NNT_KC, 3, 2><<<dim3(ctas / ks, ks), 288, CF2::bytes, st>>>(
+      gemm_nn_tma_kernel_w32<NNT_KC, 3, 2><<<dim3(ctas / ks, ks), 288, CF2::bytes, st>>>(
           xm, hm, ym, 0, nullptr, part, w, q, s, w, alpha, 0.0, nullptr, q * w);
       TSVD_CHECK_LAUNCH();
       reduce_launch(part, ks, q * w, Z, w, ldz == w ? 0 : ldz, st);
       return true;
     }
-    gemm_nn_tma_kernel<NNT_KC, 3, 2><<<ctas, 288, CF2::bytes, st>>>(
+    gemm_nn_tma_kernel_w32<NNT_KC, 3, 2><<<ctas, 288, CF2::bytes, st>>>(
         xm, hm, ym, use_y, T, Z, ldz, q, s, w, alpha, beta, gram, 0);
     TSVD_CHECK_LAUNCH();
     return true;
