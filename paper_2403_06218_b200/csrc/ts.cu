@@ -870,7 +870,7 @@ struct NnTmaCfg {
   static constexpr unsigned tx = (unsigned)stage;
 };
 
-template <int KC, int S, int NYB>
+template <int KC, int S, int NYB, bool FOLD>
 __device__ __forceinline__ void nn_tma_body(
     const CUtensorMap& xmap, const CUtensorMap& hmap, const CUtensorMap& ymap, int use_y,
     const double* __restrict__ T, double* Z, int64_t ldz, int64_t q, int s, int w, double alpha,
@@ -897,7 +897,7 @@ __device__ __forceinline__ void nn_tma_body(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gid = lane >> 2, tig = lane & 3;
   const int prow = ((gid & 1) << 2) | (gid >> 1);
-  for (int i = tid; i < WP * WP; i += 288) {
+  for (int i = tid; i < WP * WP; i += blockDim.x) {
     const int r = i / WP, c = i % WP;
     Ts[r * TP + c] = (r < w && c < w) ? (T ? T[r * w + c] : (r == c ? 1.0 : 0.0)) : 0.0;
   }
@@ -919,39 +919,50 @@ __device__ __forceinline__ void nn_tma_body(
   const int nk = (int)((int64_t)nk_all * (blockIdx.y + 1) / gridDim.y) - kb;
   const int64_t nsteps = my_tiles * nk;
   Z += (int64_t)blockIdx.y * zsplit;
-  if (warp == 8) {  // producer: X/H chunks into the ring, the tile's Y rows into Ys
-    if (lane == 0) {
-      // ring slot / phase and (tile, k-chunk) kept as running counters: no
-      // 64-bit divisions by S and by the runtime nk per step
-      int st = 0, kc = 0;
-      unsigned u = 0;
-      int64_t lt = 0;
-      for (int64_t j = 0; j < nsteps; ++j) {
-        if (j > 0) {
-          if (++st == S) st = 0, ++u;
-          if (++kc == nk) kc = 0, ++lt;
-        }
-        if (j >= S) mbar_wait(&empty[st], (u - 1) & 1);
-        const int r0 = (int)((blockIdx.x + lt * gridDim.x) * NT_R);
-        unsigned char* base = sm + (size_t)st * CF::stage;
-        mbar_expect_tx(&full[st], CF::tx);
-#pragma unroll
-        for (int b = 0; b < CF::NB; ++b)
-          tma_load_2d(base + b * CF::xbox, &xmap, (kb + kc) * KC + b * 16, r0, &full[st]);
-#pragma unroll
-        for (int b = 0; b < NYB; ++b)
-          tma_load_2d(base + CF::NB * CF::xbox + b * CF::hbox, &hmap, b * 16, (kb + kc) * KC,
-                      &full[st]);
-        if (use_y && kc == nk - 1) {  // with the tile's last chunk: never stalls the X ring
-          if (lt > 0) mbar_wait(yempty, (unsigned)(lt - 1) & 1);
-          mbar_expect_tx(yfull, (unsigned)(NYB * CF::xbox));
-#pragma unroll
-          for (int b = 0; b < NYB; ++b)
-            tma_load_2d(sm + CF::y_off + b * CF::xbox, &ymap, b * 16, r0, yfull);
-        }
-      }
+  // producer: X/H chunks into the ring, the tile's Y rows into Ys.  Its ring
+  // slot / phase and (tile, k-chunk) are running counters (no 64-bit
+  // divisions by S and by the runtime nk per step).  FOLD = false: a 9th
+  // warp; FOLD = true (w = 32): lane 0 of consumer warp 0 issues step
+  // j + S - 1 at the top of its step j, so the CTA has 8 warps = 2 per SM
+  // sub-partition and a thread may hold up to 255 registers (with 9 warps
+  // one sub-partition hosts 3 and the cap is 168).
+  int pst = 0, pkc = 0;
+  unsigned pu = 0;
+  int64_t plt = 0, pj = 0;
+  auto produce = [&]() {  // issue step pj (lane 0 of the producing warp)
+    if (pj > 0) {
+      if (++pst == S) pst = 0, ++pu;
+      if (++pkc == nk) pkc = 0, ++plt;
     }
-    return;
+    if (pj >= S) mbar_wait(&empty[pst], (pu - 1) & 1);
+    const int r0 = (int)((blockIdx.x + plt * gridDim.x) * NT_R);
+    unsigned char* base = sm + (size_t)pst * CF::stage;
+    mbar_expect_tx(&full[pst], CF::tx);
+#pragma unroll
+    for (int b = 0; b < CF::NB; ++b)
+      tma_load_2d(base + b * CF::xbox, &xmap, (kb + pkc) * KC + b * 16, r0, &full[pst]);
+#pragma unroll
+    for (int b = 0; b < NYB; ++b)
+      tma_load_2d(base + CF::NB * CF::xbox + b * CF::hbox, &hmap, b * 16, (kb + pkc) * KC,
+                  &full[pst]);
+    if (!FOLD && use_y && pkc == nk - 1) {  // with the tile's last chunk: never stalls the X ring
+      if (plt > 0) mbar_wait(yempty, (unsigned)(plt - 1) & 1);
+      mbar_expect_tx(yfull, (unsigned)(NYB * CF::xbox));
+#pragma unroll
+      for (int b = 0; b < NYB; ++b)
+        tma_load_2d(sm + CF::y_off + b * CF::xbox, &ymap, b * 16, r0, yfull);
+    }
+    ++pj;
+  };
+  if constexpr (!FOLD) {
+    if (warp == 8) {
+      if (lane == 0)
+        while (pj < nsteps) produce();
+      return;
+    }
+  } else {
+    if (warp == 0 && lane == 0)
+      while (pj < nsteps && pj < S - 1) produce();
   }
   double gw[NGP][2];
 #pragma unroll
@@ -963,11 +974,26 @@ __device__ __forceinline__ void nn_tma_body(
   unsigned u = 0;
   int64_t lt = 0;
   for (int64_t j = 0; j < nsteps; ++j) {
+    if constexpr (FOLD) {
+      if (warp == 0 && lane == 0 && pj < nsteps) produce();  // step j + S - 1
+    }
     if (j > 0) {
       if (++st == S) st = 0, ++u;
       if (++kc == nk) kc = 0, ++lt;
     }
     const int64_t r0 = (blockIdx.x + lt * gridDim.x) * NT_R;
+    if constexpr (FOLD) {
+      // the tile's Y rows, issued when the tile starts: warp 0 has finished
+      // the previous tile's epilogue itself (a wait inside produce() could
+      // wait for warp 0's own arrival when a tile has fewer than S chunks)
+      if (use_y && kc == 0 && warp == 0 && lane == 0) {
+        if (lt > 0) mbar_wait(yempty, (unsigned)(lt - 1) & 1);
+        mbar_expect_tx(yfull, (unsigned)(NYB * CF::xbox));
+#pragma unroll
+        for (int b = 0; b < NYB; ++b)
+          tma_load_2d(sm + CF::y_off + b * CF::xbox, &ymap, b * 16, (int)r0, yfull);
+      }
+    }
     if (kc == 0) {
 #pragma unroll
       for (int h = 0; h < 2; ++h)
@@ -1142,15 +1168,17 @@ __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
     const __grid_constant__ CUtensorMap ymap, int use_y, const double* __restrict__ T, double* Z,
     int64_t ldz, int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram,
     int64_t zsplit) {
-  nn_tma_body<KC, S, NYB>(xmap, hmap, ymap, use_y, T, Z, ldz, q, s, w, alpha, beta, gram, zsplit);
+  nn_tma_body<KC, S, NYB, false>(xmap, hmap, ymap, use_y, T, Z, ldz, q, s, w, alpha, beta, gram,
+                                 zsplit);
 }
 template <int KC, int S, int NYB>
-__global__ void __launch_bounds__(288, 1) gemm_nn_tma_kernel_w32(
+__global__ void __launch_bounds__(256, 1) gemm_nn_tma_kernel_w32(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
     const __grid_constant__ CUtensorMap ymap, int use_y, const double* __restrict__ T, double* Z,
     int64_t ldz, int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram,
     int64_t zsplit) {
-  nn_tma_body<KC, S, NYB>(xmap, hmap, ymap, use_y, T, Z, ldz, q, s, w, alpha, beta, gram, zsplit);
+  nn_tma_body<KC, S, NYB, true>(xmap, hmap, ymap, use_y, T, Z, ldz, q, s, w, alpha, beta, gram,
+                                zsplit);
 }
 
 // Output products Z = X H with w up to 64 (Alg. 2 S8/S9: V = P Vbar_r,
@@ -1227,17 +1255,22 @@ __global__ void __launch_bounds__(288, 1) gemm_nn_out_tma_kernel(
   }
   const bool vec = ((ldz & 1) == 0) && ((((uintptr_t)Z) & 15) == 0);
   double acc[2][NT][2];
+  int st = 0, kc = 0;
+  unsigned u = 0;
+  int64_t lt = 0;
   for (int64_t j = 0; j < nsteps; ++j) {
-    const int st = (int)(j % S);
-    const int kc = (int)(j % nk);
-    const int64_t r0 = (blockIdx.x + (j / nk) * gridDim.x) * NT_R;
+    if (j > 0) {  // running counters, as in the producer
+      if (++st == S) st = 0, ++u;
+      if (++kc == nk) kc = 0, ++lt;
+    }
+    const int64_t r0 = (blockIdx.x + lt * gridDim.x) * NT_R;
     if (kc == 0) {
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
         for (int ni = 0; ni < NT; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
     }
-    mbar_wait(&full[st], (unsigned)(j / S) & 1);
+    mbar_wait(&full[st], u & 1);
     {
       const unsigned char* base = sm + (size_t)st * CF::stage;
       const unsigned char* hb0 = base + CF::NB * CF::xbox;
@@ -1335,13 +1368,13 @@ static bool nn_tma_launch(const double* X, int64_t ldx, const double* H, int64_t
     const int ctas = nn_ctas(q, 32);
     const int ks = (use_y || T || gram) ? 1 : pick_split(q, s, w, ctas, part_cap);
     if (ks > 1) {
-      gemm_nn_tma_kernel_w32<NNT_KC, 3, 2><<<dim3(ctas / ks, ks), 288, CF2::bytes, st>>>(
+      gemm_nn_tma_kernel_w32<NNT_KC, 3, 2><<<dim3(ctas / ks, ks), 256, CF2::bytes, st>>>(
           xm, hm, ym, 0, nullptr, part, w, q, s, w, alpha, 0.0, nullptr, q * w);
       TSVD_CHECK_LAUNCH();
       reduce_launch(part, ks, q * w, Z, w, ldz == w ? 0 : ldz, st);
       return true;
     }
-    gemm_nn_tma_kernel_w32<NNT_KC, 3, 2><<<ctas, 288, CF2::bytes, st>>>(
+    gemm_nn_tma_kernel_w32<NNT_KC, 3, 2><<<ctas, 256, CF2::bytes, st>>>(
         xm, hm, ym, use_y, T, Z, ldz, q, s, w, alpha, beta, gram, 0);
     TSVD_CHECK_LAUNCH();
     return true;
