@@ -213,6 +213,18 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------- cpu baseline --
+_HOST_WORK = {}
+
+
+def host_workload(cfg_name: str):
+    """make_workload for the host oracle, generated once per process (the
+    reference arm runs several steps on the same bytes)."""
+    if cfg_name not in _HOST_WORK:
+        _HOST_WORK.clear()
+        _HOST_WORK[cfg_name] = make_workload(cfg_name, 0)
+    return _HOST_WORK[cfg_name]
+
+
 def oracle_sample(cfg_name: str, budget_s: float, cycles: int, seed: int, keep: int = 0,
                   d: int | None = None):
     """Time the oracle's LancSVD block steps (Alg. 2 S2-S5, calling only
@@ -225,7 +237,7 @@ def oracle_sample(cfg_name: str, budget_s: float, cycles: int, seed: int, keep: 
     scale = 1.0
     if cfg_name == "C5":  # host-sized sample: C5 scaled down 10x (same alpha, mean row)
         cfg_name, scale = "C5s", 10.0
-    cfg, seed_, work = make_workload(cfg_name, 0)
+    cfg, seed_, work = host_workload(cfg_name)
     op = oracle.Operator(dense=work["A"]) if "A" in work else oracle.Operator(csr=work["csr"], shape=work["shape"])
     m, n, b = cfg["m"], cfg["n"], cfg["b"]
     d = d or cfg["d"]
@@ -305,7 +317,7 @@ def oracle_full(cfg_name: str, seed: int, keep: int = 0, d: int | None = None,
     config on the host, timed end to end (matrix already in host memory, as
     the GPU arm's A is resident in HBM).  No extrapolation."""
     import oracle
-    cfg, _, work = make_workload(cfg_name, 0)
+    cfg, _, work = host_workload(cfg_name)
     op = oracle.Operator(dense=work["A"]) if "A" in work else \
         oracle.Operator(csr=work["csr"], shape=work["shape"])
     d = d or cfg["d"]
@@ -331,7 +343,7 @@ def oracle_sample_rsvd(cfg_name: str, budget_s: float, seed: int):
     import oracle
     from oracle.core import DrawCtx, cgs_qr, small_svd
     from oracle.philox import gaussian_block
-    cfg, _, work = make_workload(cfg_name, 0)
+    cfg, _, work = host_workload(cfg_name)
     op = oracle.Operator(dense=work["A"]) if "A" in work else oracle.Operator(csr=work["csr"], shape=work["shape"])
     n, r, p, q = cfg["n"], cfg["r"], cfg["rsvd_p"], cfg["rsvd_q"]
     l, bq = r + p, 16
@@ -588,13 +600,26 @@ def main():
     t_hbm = dv["bytes"] / (peak * 1e9) if dv["bytes"] > 0 else 0.0
     t_fp = dv["flops"] / (fpeak * 1e12) if dv["flops"] > 0 else 0.0
     traffic = None
+    traffic_src = None
+    # preferred: DRAM bytes per launch measured by ncu on the launches of this
+    # very command (scripts/capture_traffic.py -> profiles/ncu_traffic_bench.json);
+    # else the probe ratio at a known shape x this run's algorithmic bytes
+    bfile = os.path.join(ROOT, "profiles", "ncu_traffic_bench.json")
+    if cfg_name == "C2" and not rsvd and os.path.exists(bfile):
+        try:
+            tb = json.load(open(bfile)).get(dn)
+            if tb:
+                traffic, traffic_src = tb["dram_bytes_per_launch"], tb["source"]
+        except Exception:
+            traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tfile) and dv["bytes"] > 0:
+    if traffic is None and os.path.exists(tfile) and dv["bytes"] > 0:
         try:
             tj = json.load(open(tfile))
             tr = tj.get(f"{dn}:{'csr' if 'csr' in work else 'dense'}") or tj.get(dn)
             if tr:
                 traffic = tr["dram_over_alg"] * dv["bytes"] / calls
+                traffic_src = f"probe ratio {tr['dram_over_alg']} x alg bytes ({tr.get('source')})"
         except Exception:
             traffic = None
     sec = dv["ms"] * 1e-3
@@ -614,6 +639,7 @@ def main():
                 "unit": "GB/s", "frac": round(ach / peak, 4), "traffic": traffic,
                 "fp64_TFps": round(dv["flops"] / sec / 1e12, 2),
                 "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"}
+    roof["traffic_source"] = traffic_src
     roof["alg_bytes_per_launch"] = dv["bytes"] / calls
     roof["avg_launch_ms"] = dv["ms"] / calls
     total_ms = sum(v["ms"] for v in prof.values()) or 1.0

@@ -181,6 +181,13 @@ void scale_column(double* col, int64_t q, int64_t ld, const double* nrm, cudaStr
 void small_svd(const double* B, int d, double* Ub, double* S, double* Vb, double* work,
                cudaStream_t st);
 size_t small_svd_work(int d);
+// the same SVD when only Vbar[:, :nv] is needed (LancSVD): the Jacobi sweeps
+// skip V, Vbar[:, :nv] = B^T Ubar[:, :nv] / sigma afterwards; the device word
+// small_svd_top_ok_dev is 0 when sigma_nv < 1e-3 sigma_1 (then rerun
+// small_svd).  part: gemm_tn workspace of tn_part_size(d, d) doubles.
+void small_svd_top(const double* B, int d, int nv, double* Ub, double* S, double* Vb,
+                   double* work, double* part, cudaStream_t st);
+const unsigned* small_svd_top_ok_dev(const double* work, int d);
 int small_svd_sweeps(const double* work, int d);  // sweeps of the last small_svd (syncs)
 // device word holding the sweep count of the last small_svd (read together
 // with rho once per cycle); a count equal to small_svd_max_sweeps() means the

@@ -384,7 +384,7 @@ __device__ __forceinline__ void jac_pair(int t, int ir, int& p, int& q) {
 // shuffles) -> apply to the columns; warp 0 also applies them to J.  red is
 // double-buffered by inner-round parity, so one barrier per inner round
 // suffices (a warp reads red[ir & 1] before it can reach barrier ir + 1).
-template <int RG, int JB, int MODE, int NTHR>
+template <int RG, int JB, int MODE, int NTHR, bool WV = true>
 __device__ __forceinline__ void jac_inner(int ir, double (&x)[RG][2 * JB],
                                           double (&vv)[RG][2 * JB],
                                           double (*red)[3 * JB + 1], int* any_rot, double tol,
@@ -453,9 +453,11 @@ __device__ __forceinline__ void jac_inner(int ir, double (&x)[RG][2 * JB],
       x[k][q] = st * xp + ct * xq;
       // the same rotation on this thread's rows of V (held in registers for
       // the round): no accumulated J, no serial J update on the step's path
-      const double vp = vv[k][p], vq = vv[k][q];
-      vv[k][p] = ct * vp - st * vq;
-      vv[k][q] = st * vp + ct * vq;
+      if constexpr (WV) {
+        const double vp = vv[k][p], vq = vv[k][q];
+        vv[k][p] = ct * vp - st * vq;
+        vv[k][q] = st * vp + ct * vq;
+      }
     }
   }
 }
@@ -484,7 +486,10 @@ __device__ __forceinline__ void jac_wait_ver(unsigned* ver, int b, unsigned g) {
   while (*v < g) __nanosleep(32);
 }
 
-template <int RG, int JC, bool CYC, int JR_T>
+// WV = false: the rotations are not applied to V (the caller forms the
+// needed right vectors as B^T u_i / sigma_i afterwards, small_svd_top): half
+// the rotation work and no V traffic per round.
+template <int RG, int JC, bool CYC, int JR_T, bool WV = true>
 __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict__ G,
                                                             double* __restrict__ V, int d, int nb,
                                                             double* __restrict__ nrm,
@@ -545,13 +550,15 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
       // this round's V rows: in flight during the inner rounds (the pair's V
       // columns belong to this CTA until it publishes the new versions)
       double vv[RG][JW];
+      if constexpr (WV) {
 #pragma unroll
-      for (int k = 0; k < RG; ++k) {
-        const int row = tid + JR_T * k;
+        for (int k = 0; k < RG; ++k) {
+          const int row = tid + JR_T * k;
 #pragma unroll
-        for (int c = 0; c < JW; ++c) {
-          const int col = c < JC ? bi * JC + c : bj * JC + (c - JC);
-          vv[k][c] = row < dp ? __ldcg(V + (size_t)col * dp + row) : 0.0;
+          for (int c = 0; c < JW; ++c) {
+            const int col = c < JC ? bi * JC + c : bj * JC + (c - JC);
+            vv[k][c] = row < dp ? __ldcg(V + (size_t)col * dp + row) : 0.0;
+          }
         }
       }
       if (tid == 0) any_rot = 0;
@@ -567,15 +574,15 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
       if (!CYC) {
 #pragma unroll
         for (int ir = 0; ir < JW - 1; ++ir)
-          jac_inner<RG, JC, 0, JR_T>(ir, x, vv, red, &any_rot, tol, absmin);
+          jac_inner<RG, JC, 0, JR_T, WV>(ir, x, vv, red, &any_rot, tol, absmin);
       } else if (round == 0) {
 #pragma unroll
         for (int ir = 0; ir < JC - 1; ++ir)
-          jac_inner<RG, JC, 1, JR_T>(ir, x, vv, red, &any_rot, tol, absmin);
+          jac_inner<RG, JC, 1, JR_T, WV>(ir, x, vv, red, &any_rot, tol, absmin);
       } else {
 #pragma unroll
         for (int ir = 0; ir < JC; ++ir)
-          jac_inner<RG, JC, 2, JR_T>(ir, x, vv, red, &any_rot, tol, absmin);
+          jac_inner<RG, JC, 2, JR_T, WV>(ir, x, vv, red, &any_rot, tol, absmin);
       }
       __syncthreads();
       JT(2);
@@ -592,14 +599,16 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
           }
         }
         // V pair rows, rotated in registers alongside G
+        if constexpr (WV) {
 #pragma unroll
-        for (int k = 0; k < RG; ++k) {
-          const int row = tid + JR_T * k;
-          if (row < dp) {
+          for (int k = 0; k < RG; ++k) {
+            const int row = tid + JR_T * k;
+            if (row < dp) {
 #pragma unroll
-            for (int c = 0; c < JW; ++c) {
-              const int col = c < JC ? bi * JC + c : bj * JC + (c - JC);
-              __stcg(V + (size_t)col * dp + row, vv[k][c]);
+              for (int c = 0; c < JW; ++c) {
+                const int col = c < JC ? bi * JC + c : bj * JC + (c - JC);
+                __stcg(V + (size_t)col * dp + row, vv[k][c]);
+              }
             }
           }
         }
@@ -647,7 +656,7 @@ __global__ void __launch_bounds__(JR_T, 1) jacobi_reg_kernel(double* __restrict_
     if (lane == 0) S[cnt] = sj;
     for (int i = lane; i < d; i += 32) {
       Ub[(size_t)i * d + cnt] = __ldcg(G + (size_t)j * d + i) * inv;
-      Vb[(size_t)i * d + cnt] = __ldcg(V + (size_t)j * dp + i);
+      if constexpr (WV) Vb[(size_t)i * d + cnt] = __ldcg(V + (size_t)j * dp + i);
     }
   }
 }
@@ -658,7 +667,7 @@ int g_jacobi_jc = getenv("TSVD_JACOBI_JC") ? atoi(getenv("TSVD_JACOBI_JC")) : 4;
 // TSVD_JACOBI_NT = 64 | 128 | 256 forces the CTA size (0, default: by d)
 int g_jacobi_nt = getenv("TSVD_JACOBI_NT") ? atoi(getenv("TSVD_JACOBI_NT")) : 0;
 
-template <int JCV>
+template <int JCV, bool WV = true>
 static bool reg_launch(const double* B, int d, double* Ub, double* S, double* Vb, double* work,
                        unsigned* ctl, cudaStream_t st) {
   int nbr = (d + JCV - 1) / JCV;
@@ -674,8 +683,8 @@ static bool reg_launch(const double* B, int d, double* Ub, double* S, double* Vb
   const int RG = (d + nth - 1) / nth;
   void* fn = nullptr;
 #define REG_FN(R, NT)                                                                  \
-  fn = g_jacobi_cyc ? (void*)jacobi_reg_kernel<R, JCV, true, NT>                        \
-                    : (void*)jacobi_reg_kernel<R, JCV, false, NT>
+  fn = g_jacobi_cyc ? (void*)jacobi_reg_kernel<R, JCV, true, NT, WV>                    \
+                    : (void*)jacobi_reg_kernel<R, JCV, false, NT, WV>
   if (nth == 64) {
     if (RG <= 1) REG_FN(1, 64);
     else if (RG == 2) REG_FN(2, 64);
@@ -735,6 +744,44 @@ int small_svd_sweeps(const double* work, int d) {
   unsigned h = 0;
   TSVD_CUDA(cudaMemcpy(&h, ctl + 4, sizeof(unsigned), cudaMemcpyDeviceToHost));
   return (int)h;
+}
+
+// Vbar[:, c] /= sigma_c for c < nv; ok = sigma_{nv-1} >= 1e-3 sigma_0 > 0
+__global__ void vbar_scale_kernel(double* __restrict__ Vb, int d, int nv,
+                                  const double* __restrict__ S, unsigned* __restrict__ ok) {
+  const int64_t n = (int64_t)d * nv;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t / nv), c = (int)(t % nv);
+    const double sc = S[c];
+    Vb[(int64_t)i * d + c] = sc > 0.0 ? Vb[(int64_t)i * d + c] / sc : 0.0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    *ok = (S[0] > 0.0 && S[nv - 1] >= 1e-3 * S[0]) ? 1u : 0u;
+}
+
+const unsigned* small_svd_top_ok_dev(const double* work, int d) {
+  return jac_ctl(const_cast<double*>(work), d) + 12;
+}
+
+void small_svd_top(const double* B, int d, int nv, double* Ub, double* S, double* Vb,
+                   double* work, double* part, cudaStream_t st) {
+  if (d > kJacobiMaxD) throw Error{TSVD_ESHAPE, "small_svd: d > 1536"};
+  unsigned* ctl = jac_ctl(work, d);
+  if (g_jacobi_jc != 4 || !g_jacobi_cyc || !reg_launch<4, false>(B, d, Ub, S, Vb, work, ctl, st)) {
+    small_svd(B, d, Ub, S, Vb, work, st);  // no top-only path for this configuration
+    TSVD_CUDA(cudaMemsetAsync(ctl + 12, 0xff, sizeof(unsigned), st));  // ok (V complete)
+    return;
+  }
+  // Vbar[:, :nv] = B^T Ubar[:, :nv] diag(1 / sigma): the right singular
+  // vectors from the left ones (B vbar_i = sigma_i ubar_i), forward error
+  // O(u sigma_1 / sigma_i) -- the solver falls back to the rotated V when
+  // sigma_nv < 1e-3 sigma_1 (flag ctl[12] = 0)
+  gemm_tn(B, d, Ub, d, d, d, nv, Vb, d, part, st);
+  const int64_t n = (int64_t)d * nv;
+  vbar_scale_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 4), 256, 0, st>>>(
+      Vb, d, nv, S, ctl + 12);
+  TSVD_CHECK_LAUNCH();
 }
 
 void small_svd(const double* B, int d, double* Ub, double* S, double* Vb, double* work,

@@ -305,20 +305,34 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
       from_slot = bad;
     }
     c.deferred = false;
-    {
-      Prof p(c, P_SVD, 16.0 * d * d, 0);
-      small_svd(B, d, Ub, Sg, Vb, jw, c.st);                           // B_k = Ub S Vb^T
+    // B_k = Ub S Vb^T.  Only Vbar[:, :max(r, l)] is ever read (rho, outputs,
+    // thick restart), so the sweeps skip V and those columns are formed as
+    // B^T ubar_i / sigma_i (small_svd_top); if sigma_max(r,l) < 1e-3 sigma_1 the
+    // full Jacobi with rotated V runs instead (host-checked with rho below).
+    const int nv = std::min(d, std::max(r, keep));
+    for (int full = 0; full < 2; ++full) {
+      {
+        Prof p(c, P_SVD, 16.0 * d * d, 0);
+        if (full)
+          small_svd(B, d, Ub, Sg, Vb, jw, c.st);
+        else
+          small_svd_top(B, d, nv, Ub, Sg, Vb, jw, dbuf(c, "part_tn", 8), c.st);
+      }
+      {
+        Prof p(c, P_OTHER, 0, 0);
+        lanczos_rho(Rb, b, Vb, d, Sg, r, rho, c.st);
+      }
+      TSVD_CUDA(cudaMemcpyAsync(hrho.data(), rho, r * sizeof(double), cudaMemcpyDeviceToHost, c.st));
+      TSVD_CUDA(cudaMemcpyAsync(hs.data(), Sg, sizeof(double), cudaMemcpyDeviceToHost, c.st));
+      TSVD_CUDA(cudaMemcpyAsync(hsw, small_svd_sweeps_dev(jw, d), sizeof(unsigned),
+                                cudaMemcpyDeviceToHost, c.st));
+      if (!full)
+        TSVD_CUDA(cudaMemcpyAsync(hsw + 1, small_svd_top_ok_dev(jw, d), sizeof(unsigned),
+                                  cudaMemcpyDeviceToHost, c.st));
+      TSVD_CUDA(cudaStreamSynchronize(c.st));
+      svdw.add(*hsw);
+      if (full || hsw[1]) break;
     }
-    {
-      Prof p(c, P_OTHER, 0, 0);
-      lanczos_rho(Rb, b, Vb, d, Sg, r, rho, c.st);
-    }
-    TSVD_CUDA(cudaMemcpyAsync(hrho.data(), rho, r * sizeof(double), cudaMemcpyDeviceToHost, c.st));
-    TSVD_CUDA(cudaMemcpyAsync(hs.data(), Sg, sizeof(double), cudaMemcpyDeviceToHost, c.st));
-    TSVD_CUDA(cudaMemcpyAsync(hsw, small_svd_sweeps_dev(jw, d), sizeof(unsigned),
-                              cudaMemcpyDeviceToHost, c.st));
-    TSVD_CUDA(cudaStreamSynchronize(c.st));
-    svdw.add(*hsw);
     nconv = 0;
     rho_max = 0.0;
     for (int i = 0; i < r; ++i) {

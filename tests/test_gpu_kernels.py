@@ -82,7 +82,8 @@ def test_gemm_tn(q, s, w):
                                               (3000, 50, 40, 1.0, 0.0), (65, 700, 8, 2.0, 0.5),
                                               (50000, 320, 32, -1.0, 1.0), (20001, 96, 24, 1.0, 0.0),
                                               (777, 40, 18, 0.5, -2.0), (9000, 2000, 32, 1.0, 0.0),
-                                              (5000, 0, 32, 0.0, 1.0), (3001, 0, 24, 0.0, -0.5)])
+                                              (5000, 0, 32, 0.0, 1.0), (3001, 0, 24, 0.0, -0.5),
+                                              (200000, 40, 32, -1.0, 1.0), (150000, 20, 32, 1.0, 1.0)])
 def test_gemm_nn(q, s, w, alpha, beta):
     rng = np.random.default_rng(q * 7 + s + w)
     X = rng.standard_normal((q, max(s, 1)))[:, :s]
@@ -195,7 +196,10 @@ def test_cholqr2_parity(q, w, kappa):
 
 @pytest.mark.parametrize("q,s,w,kappa", [(1000, 8, 4, 1.0), (20000, 100, 16, 1e4),
                                          (4099, 37, 32, 1e7), (50000, 384, 16, 1e2),
-                                         (30000, 320, 32, 1e3), (7000, 50, 27, 1e4)])
+                                         (30000, 320, 32, 1e3), (7000, 50, 27, 1e4),
+                                         # many 128-row tiles per CTA with fewer K chunks
+                                         # than ring stages (w = 32 folded producer)
+                                         (200000, 32, 32, 1e2), (300000, 60, 32, 1e3)])
 def test_cgs_cqr2_parity(q, s, w, kappa):
     rng = np.random.default_rng(q + s)
     P, _ = np.linalg.qr(rng.standard_normal((q, s)))
