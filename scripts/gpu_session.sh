@@ -1,11 +1,14 @@
+# round-2 evidence: C2 launch list, full capture of the top kernels, traffic of the benched launches
 set -x
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
-nvidia-smi --query-gpu=index,name,memory.used,utilization.gpu --format=csv > $O/s16_smi.txt
-timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_solvers.py tests/test_gpu_loopback.py -m gpu -q -x -p no:cacheprovider --timeout 120 > $O/s16_pytest.log 2>&1
-echo pytest rc $?
-timeout 120 python scripts/bench_kernels.py nn32 nn > $O/s16_nn.log 2>&1
-timeout 300 python bench.py --config C3 --steps 3 --warmup 2 --no-cpu-baseline --e2e-steps 0 > $O/s16_bench_C3.json 2> $O/s16_bench_C3.err
-timeout 300 python bench.py --config C4 --steps 3 --warmup 2 --no-cpu-baseline --e2e-steps 0 > $O/s16_bench_C4.json 2> $O/s16_bench_C4.err
-timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > $O/s16_bench.json 2> $O/s16_bench.err
+B="python bench.py --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 0"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file $O/r02_C2_launches.csv $B > /dev/null 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:gemm_nn_tma_kernel --csv --log-file $O/r02_traffic_ortho_nn.csv $B > /dev/null 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:gemm_tn_tma_kernel --csv --log-file $O/r02_traffic_ortho_tn.csv $B > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:gemm_nn_tma_kernel -s 60 -c 2 -o $O/r02_full_nn $B > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:gemm_tn_tma_kernel -s 60 -c 1 -o $O/r02_full_tn $B > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:spmm_kernel -s 20 -c 1 -o $O/r02_full_spmm $B > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:jacobi_reg_kernel -c 1 -o $O/r02_full_jacobi $B > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:rowT_kernel -s 40 -c 1 -o $O/r02_full_rowt $B > /dev/null 2>&1
 echo done
