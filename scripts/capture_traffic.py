@@ -37,7 +37,7 @@ def main(phase, kernel, path):
         val = float(rec["Metric Value"].replace(",", ""))
         unit = rec.get("Metric Unit", "")
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9,
-                 "usecond": 1e-6, "msecond": 1e-3}.get(unit, 1.0)
+                 "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3}.get(unit, 1.0)
         per.setdefault(key, {})[rec["Metric Name"]] = val * scale
     launches = [v for v in per.values() if "dram__bytes_read.sum" in v]
     if not launches:
