@@ -592,6 +592,35 @@ void apply(Ctx& c, bool trans, const double* X, int64_t ldx, double* Y, int64_t 
       all_gather(c, shard, full, (size_t)c.nsh * w);
     }
     apply_local(c, false, full, w, Y, ldy, w);
+  } else if (!c.ATp.empty() && !c.dense) {
+    // pipelined reduce-scatter: the partial A_g^T X is formed
+    // one n-shard at a time from the row pieces of CSR(A_g^T); as soon as
+    // shard p is written, its reduction to rank p (ncclReduce, in shard
+    // order on every rank) starts on the communication stream while the
+    // compute stream multiplies shard p + 1
+    if (!c.comm_st) {
+      TSVD_CUDA(cudaStreamCreateWithFlags(&c.comm_st, cudaStreamNonBlocking));
+      c.comm_ev.resize(c.world + 1);
+      for (auto& e : c.comm_ev) TSVD_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int64_t tail = npad - c.ng;  // padding rows of the last shard stay zero
+    if (tail > 0) fill_zero(full + (size_t)c.ng * w, tail * w, c.st);
+    Prof p(c, P_APPLY_AT, 12.0 * c.AT.nnz + 8.0 * (c.ng + 1) + 8.0 * w * (c.ng + c.m),
+           2.0 * c.AT.nnz * w);
+    int64_t slots = std::max<int64_t>(1, c.AT.nslots);
+    for (const Csr& P : c.ATp) slots = std::max(slots, P.nslots);
+    double* part = dbuf(c, "spmm_part_t", (size_t)slots * 64);
+    for (int g = 0; g < c.world; ++g) {
+      const Csr& P = c.ATp[g];
+      double* out = full + (size_t)g * c.nsh * w;
+      if (P.rows > 0) launch_spmm_wide(P, X, ldx, out, w, w, part, c.st);
+      TSVD_CUDA(cudaEventRecord(c.comm_ev[g], c.st));
+      TSVD_CUDA(cudaStreamWaitEvent(c.comm_st, c.comm_ev[g], 0));
+      reduce_sum_to(c, out, shard, (size_t)c.nsh * w, g, c.comm_st);
+    }
+    TSVD_CUDA(cudaEventRecord(c.comm_ev[c.world], c.comm_st));
+    TSVD_CUDA(cudaStreamWaitEvent(c.st, c.comm_ev[c.world], 0));
+    copy_block(shard, w, Y, ldy, c.n, w, false, c.st);
   } else {
     fill_zero(full, npad * w, c.st);
     apply_local(c, true, X, ldx, full, w, w);

@@ -71,6 +71,9 @@ static void destroy_ctx(tsvd_ctx* c) {
   if (c->st) cudaStreamSynchronize(c->st);
   csr_free(c->A, c->st);
   csr_free(c->AT, c->st);
+  for (auto& P : c->ATp) csr_free(P, c->st);
+  for (auto e : c->comm_ev) cudaEventDestroy(e);
+  if (c->comm_st) cudaStreamDestroy(c->comm_st);
   dfree(c->Ad, c->st);
   free_bufs(*c);
   prof_release(*c);
@@ -149,6 +152,14 @@ static tsvd_status setup_csr(tsvd_ctx* c, int64_t nnz, const int64_t* rowptr,
   if (bad & 2) csr_canonicalize(A, c->st);        // unsorted or duplicates: canonicalise
   csr_transpose(A, c->AT, c->st);
   clk.lap("transpose", c->st);
+  if (c->world > 1) {  // n-shard pieces of CSR(A_g^T) for the pipelined reduce-scatter
+    c->ATp.resize(c->world);
+    for (int g = 0; g < c->world; ++g) {
+      const int64_t r0 = std::min<int64_t>(n, (int64_t)g * c->nsh);
+      const int64_t r1 = std::min<int64_t>(n, r0 + c->nsh);
+      csr_slice_rows(c->AT, r0, r1, c->ATp[g], c->st);
+    }
+  }
   csr_plan(A, c->st);
   clk.lap("plan A", c->st);
   csr_plan(c->AT, c->st);

@@ -34,6 +34,8 @@ struct NcclApi {
                                 ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int,
+                         ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -52,9 +54,10 @@ NcclApi& api() {
   a.AllReduce = (decltype(a.AllReduce))dlsym(h, "ncclAllReduce");
   a.ReduceScatter = (decltype(a.ReduceScatter))dlsym(h, "ncclReduceScatter");
   a.AllGather = (decltype(a.AllGather))dlsym(h, "ncclAllGather");
+  a.Reduce = (decltype(a.Reduce))dlsym(h, "ncclReduce");
   a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
   a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllReduce && a.ReduceScatter &&
-         a.AllGather;
+         a.AllGather && a.Reduce;
   return a;
 }
 
@@ -172,21 +175,22 @@ __global__ void loop_gather_kernel(LoopPtrs src, int world, size_t count, double
 }
 
 template <class F>
-static void loop_collective(Ctx& c, const double* send, F&& body) {
+static void loop_collective(Ctx& c, const double* send, F&& body, cudaStream_t st = nullptr) {
   LoopGroup& g = *c.loop;
   const int r = c.rank;
+  if (!st) st = c.st;
   g.send[r] = send;
-  TSVD_CUDA(cudaEventRecord(g.ready[r], c.st));
+  TSVD_CUDA(cudaEventRecord(g.ready[r], st));
   loop_barrier(g);
   for (int k = 0; k < g.world; ++k)
-    if (k != r) TSVD_CUDA(cudaStreamWaitEvent(c.st, g.ready[k], 0));
+    if (k != r) TSVD_CUDA(cudaStreamWaitEvent(st, g.ready[k], 0));
   LoopPtrs ptrs{};
   for (int k = 0; k < g.world; ++k) ptrs.p[k] = g.send[k];
   body(ptrs);
-  TSVD_CUDA(cudaEventRecord(g.done[r], c.st));
+  TSVD_CUDA(cudaEventRecord(g.done[r], st));
   loop_barrier(g);  // every rank has read every send buffer (on its stream)
   for (int k = 0; k < g.world; ++k)
-    if (k != r) TSVD_CUDA(cudaStreamWaitEvent(c.st, g.done[k], 0));
+    if (k != r) TSVD_CUDA(cudaStreamWaitEvent(st, g.done[k], 0));
 }
 
 static unsigned loop_grid(size_t n) {
@@ -229,6 +233,22 @@ void reduce_scatter_sum(Ctx& c, const double* send, double* recv, size_t recv_co
   check(api().ReduceScatter(send, recv, recv_count, ncclFloat64, ncclSum, (ncclComm_t)c.comm,
                             c.st),
         "ncclReduceScatter");
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+void reduce_sum_to(Ctx& c, const double* send, double* recv, size_t count, int root,
+                   cudaStream_t st) {
+  if (c.loop) {
+    loop_collective(c, send, [&](const LoopPtrs& p) {
+      if (c.rank == root) {
+        loop_sum_kernel<<<loop_grid(count), 256, 0, st>>>(p, c.loop->world, 0, count, recv);
+        TSVD_CHECK_LAUNCH();
+      }
+    }, st);
+    return;
+  }
+  check(api().Reduce(send, recv, count, ncclFloat64, ncclSum, root, (ncclComm_t)c.comm, st),
+        "ncclReduce");
   g_launches.fetch_add(1, std::memory_order_relaxed);
 }
 

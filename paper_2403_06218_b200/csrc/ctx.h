@@ -50,6 +50,12 @@ struct tsvd_ctx {
   int64_t cur_row0 = 0, cur_qtot = 0;  // rows of the block being orthogonalised (Philox)
   bool dense = false;
   tsvd::Csr A, AT;           // CSR(A), CSR(A^T)
+  // multi-GPU (world > 1): CSR(A_g^T) cut at the n-shard boundaries, so
+  // A_g^T X is produced one shard at a time and each shard's reduction to its
+  // owner (ncclReduce) overlaps the next shard's SpMM (comm_st, events)
+  std::vector<tsvd::Csr> ATp;
+  cudaStream_t comm_st = nullptr;
+  std::vector<cudaEvent_t> comm_ev;
   double* Ad = nullptr;      // dense A, row-major m x n
   int64_t lda = 0;
   cudaStream_t st = nullptr;
@@ -143,6 +149,9 @@ void comm_destroy(Ctx& c);
 void allreduce_sum(Ctx& c, double* buf, size_t count);
 void reduce_scatter_sum(Ctx& c, const double* send, double* recv, size_t recv_count);
 void all_gather(Ctx& c, const double* send, double* recv, size_t send_count);
+// sum of every rank's send (count) into recv on rank `root`, ordered on `st`
+void reduce_sum_to(Ctx& c, const double* send, double* recv, size_t count, int root,
+                   cudaStream_t st);
 LoopGroup* loop_group_create(int world);
 void loop_group_destroy(LoopGroup* g);
 void loop_join(Ctx& c, LoopGroup* g, int rank);

@@ -115,6 +115,8 @@ void csr_build_plan(Csr& A, const int64_t* host_rowptr, cudaStream_t st);
 // needs its length bins)
 void csr_plan(Csr& A, cudaStream_t st);
 void csr_free(Csr& A, cudaStream_t st);
+// rows [r0, r1) of a canonical, unplanned CSR as their own planned CSR
+void csr_slice_rows(const Csr& A, int64_t r0, int64_t r1, Csr& P, cudaStream_t st);
 // device validation of a CSR: 0 if canonical; bits: 1 bad row bounds, 2
 // unsorted or duplicate columns in a row (canonicalisable), 4 rowptr[0] != 0
 // or rowptr[rows] != nnz, 8 column index out of range

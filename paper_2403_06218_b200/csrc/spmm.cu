@@ -931,6 +931,41 @@ void csr_build_plan(Csr& A, const int64_t* hrp, cudaStream_t st) {
   TSVD_CUDA(cudaStreamSynchronize(st));
 }
 
+__global__ void rebase_rowptr_kernel(const int64_t* __restrict__ src, int64_t n,
+                                     int64_t* __restrict__ dst) {
+  const int64_t base = src[0];
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i] - base;
+}
+
+// Rows [r0, r1) of a canonical (not yet planned) CSR as a CSR of their own,
+// with its own load-balancing plan (the row-range pieces of CSR(A_g^T) the
+// pipelined reduce-scatter multiplies one n-shard at a time).
+void csr_slice_rows(const Csr& A, int64_t r0, int64_t r1, Csr& P, cudaStream_t st) {
+  P = Csr{};
+  P.rows = r1 - r0;
+  P.cols = A.cols;
+  int64_t b[2] = {0, 0};
+  TSVD_CUDA(cudaMemcpyAsync(&b[0], A.rowptr + r0, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  TSVD_CUDA(cudaMemcpyAsync(&b[1], A.rowptr + r1, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  TSVD_CUDA(cudaStreamSynchronize(st));
+  P.nnz = b[1] - b[0];
+  dmalloc_t(&P.rowptr, P.rows + 1, st);
+  dmalloc_t(&P.colidx, std::max<int64_t>(1, P.nnz), st);
+  dmalloc_t(&P.vals, std::max<int64_t>(1, P.nnz), st);
+  rebase_rowptr_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((P.rows + 256) / 256, 148 * 8)),
+                         256, 0, st>>>(A.rowptr + r0, P.rows, P.rowptr);
+  TSVD_CHECK_LAUNCH();
+  if (P.nnz > 0) {
+    TSVD_CUDA(cudaMemcpyAsync(P.colidx, A.colidx + b[0], P.nnz * sizeof(int32_t),
+                              cudaMemcpyDeviceToDevice, st));
+    TSVD_CUDA(cudaMemcpyAsync(P.vals, A.vals + b[0], P.nnz * sizeof(double),
+                              cudaMemcpyDeviceToDevice, st));
+  }
+  csr_plan(P, st);
+}
+
 void csr_free(Csr& A, cudaStream_t st) {
   dfree(A.rowptr, st);
   dfree(A.colidx, st);
