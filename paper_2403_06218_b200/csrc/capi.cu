@@ -655,7 +655,13 @@ tsvd_status tsvd_dbg_small_svd(const double* B, int d, double* Ub, double* S, do
   TSVD_API_BEGIN
   tsvd_ctx* c = dbg_ctx(stream);
   double* work = dbuf(*c, "jacobi_work", small_svd_work(d));
-  small_svd(B, d, Ub, S, Vb, work, c->st);
+  // development A/B: TSVD_DBG_SVD_TOP = nv runs the Lanczos driver's
+  // top-nv path (no rotated V; Vbar[:, :nv] = B^T Ubar / sigma)
+  static const int top_nv = getenv("TSVD_DBG_SVD_TOP") ? atoi(getenv("TSVD_DBG_SVD_TOP")) : 0;
+  if (top_nv > 0)
+    small_svd_top(B, d, std::min(top_nv, d), Ub, S, Vb, work, dbuf(*c, "part_tn", tn_part_size(d, d)), c->st);
+  else
+    small_svd(B, d, Ub, S, Vb, work, c->st);
   TSVD_CUDA(cudaStreamSynchronize(c->st));
   const int sw = small_svd_sweeps(work, d);
   if (sweeps) *sweeps = sw;

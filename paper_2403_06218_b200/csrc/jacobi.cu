@@ -768,7 +768,12 @@ void small_svd_top(const double* B, int d, int nv, double* Ub, double* S, double
                    double* work, double* part, cudaStream_t st) {
   if (d > kJacobiMaxD) throw Error{TSVD_ESHAPE, "small_svd: d > 1536"};
   unsigned* ctl = jac_ctl(work, d);
-  if (g_jacobi_jc != 4 || !g_jacobi_cyc || !reg_launch<4, false>(B, d, Ub, S, Vb, work, ctl, st)) {
+  bool ok = false;
+  if (g_jacobi_cyc) {
+    if (g_jacobi_jc == 4) ok = reg_launch<4, false>(B, d, Ub, S, Vb, work, ctl, st);
+    else if (g_jacobi_jc == 8) ok = reg_launch<8, false>(B, d, Ub, S, Vb, work, ctl, st);
+  }
+  if (!ok) {
     small_svd(B, d, Ub, S, Vb, work, st);  // no top-only path for this configuration
     TSVD_CUDA(cudaMemsetAsync(ctl + 12, 0xff, sizeof(unsigned), st));  // ok (V complete)
     return;

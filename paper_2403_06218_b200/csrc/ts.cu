@@ -853,6 +853,8 @@ __global__ void __launch_bounds__(256) rowT_kernel(const double* Y, int64_t ldy,
 // conflict-free as well.  Output rows follow the same permutation.
 constexpr int NT_R = 128;
 bool g_nn_tma = getenv("TSVD_NN_TMA") ? atoi(getenv("TSVD_NN_TMA")) != 0 : true;
+// w <= 16 with the producer folded into warp 0 (8 warps, 2 CTAs/SM): A/B knob
+bool g_nn_fold16 = getenv("TSVD_NN_FOLD16") ? atoi(getenv("TSVD_NN_FOLD16")) != 0 : true;
 
 template <int KC, int S, int NYB = 1>  // NYB = 16-column boxes of H / Y (w <= 16 NYB)
 struct NnTmaCfg {
@@ -1172,6 +1174,15 @@ __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
                                  zsplit);
 }
 template <int KC, int S, int NYB>
+__global__ void __launch_bounds__(256, 2) gemm_nn_tma_kernel_fold16(
+    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
+    const __grid_constant__ CUtensorMap ymap, int use_y, const double* __restrict__ T, double* Z,
+    int64_t ldz, int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram,
+    int64_t zsplit) {
+  nn_tma_body<KC, S, NYB, true>(xmap, hmap, ymap, use_y, T, Z, ldz, q, s, w, alpha, beta, gram,
+                                zsplit);
+}
+template <int KC, int S, int NYB>
 __global__ void __launch_bounds__(256, 1) gemm_nn_tma_kernel_w32(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
     const __grid_constant__ CUtensorMap ymap, int use_y, const double* __restrict__ T, double* Z,
@@ -1384,19 +1395,23 @@ static bool nn_tma_launch(const double* X, int64_t ldx, const double* H, int64_t
   if (!attr) {
     TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_tma_kernel<NNT_KC, NNT_S, 1>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
+    TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_tma_kernel_fold16<NNT_KC, NNT_S, 1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
     attr = true;
   }
   const int ctas = nn_ctas(q, 16);
   const int ks = (use_y || T || gram) ? 1 : pick_split(q, s, w, ctas, part_cap);
+  auto kern = g_nn_fold16 ? gemm_nn_tma_kernel_fold16<NNT_KC, NNT_S, 1>
+                          : gemm_nn_tma_kernel<NNT_KC, NNT_S, 1>;
+  const int nthr = g_nn_fold16 ? 256 : 288;
   if (ks > 1) {
-    gemm_nn_tma_kernel<NNT_KC, NNT_S, 1><<<dim3(ctas / ks, ks), 288, CF::bytes, st>>>(
-        xm, hm, ym, 0, nullptr, part, w, q, s, w, alpha, 0.0, nullptr, q * w);
+    kern<<<dim3(ctas / ks, ks), nthr, CF::bytes, st>>>(xm, hm, ym, 0, nullptr, part, w, q, s, w,
+                                                      alpha, 0.0, nullptr, q * w);
     TSVD_CHECK_LAUNCH();
     reduce_launch(part, ks, q * w, Z, w, ldz == w ? 0 : ldz, st);
     return true;
   }
-  gemm_nn_tma_kernel<NNT_KC, NNT_S, 1><<<ctas, 288, CF::bytes, st>>>(
-      xm, hm, ym, use_y, T, Z, ldz, q, s, w, alpha, beta, gram, 0);
+  kern<<<ctas, nthr, CF::bytes, st>>>(xm, hm, ym, use_y, T, Z, ldz, q, s, w, alpha, beta, gram, 0);
   TSVD_CHECK_LAUNCH();
   return true;
 }

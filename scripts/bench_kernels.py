@@ -33,6 +33,16 @@ def svd_bench():
     for d in [int(x) for x in os.environ.get("SVD_D", "28,128,200,384,450,704").split(",")]:
         rng = np.random.default_rng(d)
         B = torch.from_numpy(np.tril(rng.standard_normal((d, d))) * (0.97 ** np.arange(d))).cuda()
+        if os.environ.get("SVD_LANCZOS") and d != 384:
+            # Lanczos-shaped lower block-bidiagonal B (b = 32), as tests/test_gpu_kernels.py
+            bb, B0 = 32, np.zeros((d, d))
+            for i in range(d // bb):
+                sc = 100.0 * 0.97 ** i
+                B0[i * bb:(i + 1) * bb, i * bb:(i + 1) * bb] = sc * np.tril(rng.standard_normal((bb, bb)))
+                if (i + 2) * bb <= d:
+                    B0[(i + 1) * bb:(i + 2) * bb, i * bb:(i + 1) * bb] = 0.3 * sc * np.triu(
+                        rng.standard_normal((bb, bb)))
+            B = torch.from_numpy(B0).cuda()
         if d == 384 and os.path.exists(os.path.join(os.path.dirname(__file__), "B384_lanczos.npy")):
             B = torch.from_numpy(np.load(os.path.join(os.path.dirname(__file__), "B384_lanczos.npy"))).cuda()
         Ub = torch.empty((d, d), dtype=torch.float64, device="cuda")
