@@ -1164,6 +1164,194 @@ __device__ __forceinline__ void nn_tma_body(
 // to launch with "too many resources"), so the w = 32 kernel keeps a few
 // spilled scalars; a 2-warps-per-partition layout (producer folded into a
 // consumer warp) would lift the cap.
+// s = 0 passes fed by TMA (round 2): the streaming row pass Z = beta Y T
+// (+ per-CTA Gram Z^T Z) with Y tiles of 128 rows x 16 NYB columns loaded
+// by cp.async.bulk.tensor into an S-stage full/empty mbarrier ring (lane 0 of
+// warp 0 is the producer, folded as in nn_tma_body), so S tiles per CTA are
+// in flight without holding registers; the 8 warps (16 rows each) take the Y
+// A-fragments from the swizzled tile (paired-k, permuted rows, conflict-free
+// as in nn_tma_body), multiply by T with DMMA, store Z from the fragments and
+// add their own rows to the Gram.  The register-ring rowT_kernel reached 0.66
+// of HBM in the C2 solve (ncu: latency-bound, 48 % DRAM).
+template <int NYB, int S>
+struct RowtTmaCfg {
+  static constexpr int WP = 16 * NYB, OP = WP + 4, TP = WP + 4;
+  static constexpr size_t box = (size_t)NT_R * 16 * 8;  // 16 KB
+  static constexpr size_t stage = NYB * box;
+  static constexpr size_t os_off = S * stage;
+  static constexpr size_t ts_off = os_off + (size_t)NT_R * OP * 8;
+  static constexpr size_t bar_off = ts_off + (size_t)WP * TP * 8;
+  static constexpr size_t bytes = bar_off + 2 * S * 8 + 1024;
+};
+
+template <int NYB, int S>
+__global__ void __launch_bounds__(256, NYB == 1 ? 2 : 1) rowT_tma_kernel(
+    const __grid_constant__ CUtensorMap ymap, const double* __restrict__ T, double* Z,
+    int64_t ldz, int64_t q, int w, double beta, double* __restrict__ gram) {
+  using CF = RowtTmaCfg<NYB, S>;
+  constexpr int WP = CF::WP, NT = 2 * NYB, OP = CF::OP, TP = CF::TP;
+  constexpr int NGP = NT * (NT + 1) / 2;
+  extern __shared__ unsigned char smraw[];
+  unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  double* Os = (double*)(sm + CF::os_off);
+  double* Ts = (double*)(sm + CF::ts_off);
+  uint64_t* full = (uint64_t*)(sm + CF::bar_off);
+  uint64_t* empty = full + S;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gid = lane >> 2, tig = lane & 3;
+  const int prow = ((gid & 1) << 2) | (gid >> 1);
+  for (int i = tid; i < WP * WP; i += blockDim.x) {
+    const int r = i / WP, c = i % WP;
+    Ts[r * TP + c] = (r < w && c < w) ? (T ? T[r * w + c] : (r == c ? 1.0 : 0.0)) : 0.0;
+  }
+  if (tid == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t ntiles = (q + NT_R - 1) / NT_R;
+  const int64_t my_tiles =
+      (ntiles > (int64_t)blockIdx.x) ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  int pst = 0;
+  unsigned pu = 0;
+  int64_t pj = 0;
+  auto produce = [&]() {  // tile pj of this CTA into slot pst
+    if (pj > 0 && ++pst == S) pst = 0, ++pu;
+    if (pj >= S) mbar_wait(&empty[pst], (pu - 1) & 1);
+    const int r0 = (int)((blockIdx.x + pj * gridDim.x) * NT_R);
+    mbar_expect_tx(&full[pst], (unsigned)CF::stage);
+#pragma unroll
+    for (int b = 0; b < NYB; ++b)
+      tma_load_2d(sm + (size_t)pst * CF::stage + b * CF::box, &ymap, b * 16, r0, &full[pst]);
+    ++pj;
+  };
+  if (warp == 0 && lane == 0)
+    while (pj < my_tiles && pj < S - 1) produce();
+  double gw[NGP][2];
+#pragma unroll
+  for (int p = 0; p < NGP; ++p) gw[p][0] = gw[p][1] = 0.0;
+  const bool zal = Z && ((((uintptr_t)Z) | (uintptr_t)(ldz * 8)) & 15) == 0;
+  double* Ow = Os + warp * 16 * OP;
+  int st = 0;
+  unsigned u = 0;
+  for (int64_t j = 0; j < my_tiles; ++j) {
+    if (warp == 0 && lane == 0 && pj < my_tiles) produce();  // tile j + S - 1
+    if (j > 0 && ++st == S) st = 0, ++u;
+    const int64_t r0 = (blockIdx.x + j * gridDim.x) * NT_R;
+    mbar_wait(&full[st], u & 1);
+    const double* Ys = (const double*)(sm + (size_t)st * CF::stage);
+    double yt[2][NT][2];
+    if (T) {
+      double2 ya[2][2 * NYB];
+#pragma unroll
+      for (int kk2 = 0; kk2 < 2 * NYB; ++kk2) {
+        const double* yb = Ys + (kk2 >> 1) * (CF::box / 8);
+        const int chunk = (((kk2 & 1) << 2) | tig) ^ prow;
+        ya[0][kk2] = *reinterpret_cast<const double2*>(yb + (warp * 16 + prow) * 16 + chunk * 2);
+        ya[1][kk2] =
+            *reinterpret_cast<const double2*>(yb + (warp * 16 + 8 + prow) * 16 + chunk * 2);
+      }
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni) yt[mi][ni][0] = yt[mi][ni][1] = 0.0;
+#pragma unroll
+      for (int kk2 = 0; kk2 < 2 * NYB; ++kk2)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int ni = 0; ni < NT; ++ni) {
+            const double b = Ts[(kk2 * 8 + 2 * tig + h) * TP + ni * 8 + gid];
+            dmma884(yt[0][ni][0], yt[0][ni][1], h ? ya[0][kk2].y : ya[0][kk2].x, b);
+            dmma884(yt[1][ni][0], yt[1][ni][1], h ? ya[1][kk2].y : ya[1][kk2].x, b);
+          }
+    } else {  // T = I: the values themselves, in accumulator layout
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < NT; ++ni) {
+          const double2 yv = *reinterpret_cast<const double2*>(
+              Ys + (ni >> 1) * (CF::box / 8) + (warp * 16 + mi * 8 + prow) * 16 +
+              ((((ni & 1) << 2) | tig) ^ prow) * 2);
+          yt[mi][ni][0] = yv.x;
+          yt[mi][ni][1] = yv.y;
+        }
+    }
+    // release the slot once the loaded values were consumed (the DMMAs /
+    // moves above complete before the arrive is issued in program order for
+    // every lane; __syncwarp orders the warp's lanes)
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < NT; ++ni) {
+        const int rl = mi * 8 + prow, c = ni * 8 + 2 * tig;
+        const int64_t row = r0 + warp * 16 + rl;
+        const bool rv = row < q;
+        const double z0 = (c < w && rv) ? beta * yt[mi][ni][0] : 0.0;
+        const double z1 = (c + 1 < w && rv) ? beta * yt[mi][ni][1] : 0.0;
+        if (gram) {
+          Ow[rl * OP + c] = z0;
+          Ow[rl * OP + c + 1] = z1;
+        }
+        if (Z && rv) {
+          double* zp = Z + row * ldz + c;
+          if (zal && c + 1 < w) {
+            *reinterpret_cast<double2*>(zp) = make_double2(z0, z1);
+          } else {
+            if (c < w) zp[0] = z0;
+            if (c + 1 < w) zp[1] = z1;
+          }
+        }
+      }
+    if (gram) {
+      __syncwarp();
+#pragma unroll
+      for (int mi = 0, p = 0; mi < NT; ++mi)
+#pragma unroll
+        for (int ni = mi; ni < NT; ++ni, ++p)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const int kr = kk * 4 + tig;
+            dmma884(gw[p][0], gw[p][1], Ow[kr * OP + mi * 8 + gid], Ow[kr * OP + ni * 8 + gid]);
+          }
+      __syncwarp();
+    }
+  }
+  if (gram) {
+    // the ring is idle (every issued tile was consumed): per-warp partials
+    // there, summed over the warps in a fixed order and mirrored
+    double* red = (double*)sm;
+    __syncthreads();
+#pragma unroll
+    for (int p = 0; p < NGP; ++p)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) red[(warp * NGP + p) * 64 + gid * 8 + 2 * tig + e] = gw[p][e];
+    __syncthreads();
+    for (int idx = tid; idx < NGP * 64; idx += 256) {
+      const int p = idx / 64, ii = (idx % 64) / 8, jj = idx % 8;
+      int mi = 0, base = 0;
+      while (p >= base + (NT - mi)) {
+        base += NT - mi;
+        ++mi;
+      }
+      const int ni = mi + (p - base);
+      double sum = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum += red[(k * NGP + p) * 64 + ii * 8 + jj];
+      const int i = mi * 8 + ii, jc = ni * 8 + jj;
+      if (i < w && jc < w) {
+        gram[(int64_t)blockIdx.x * w * w + i * w + jc] = sum;
+        gram[(int64_t)blockIdx.x * w * w + jc * w + i] = sum;
+      }
+    }
+  }
+}
+
 template <int KC, int S, int NYB>
 __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap,
@@ -1454,6 +1642,39 @@ static bool nn_out_tma_launch(const double* X, int64_t ldx, const double* H, int
   return true;
 }
 
+bool g_rowt_tma = getenv("TSVD_ROWT_TMA") ? atoi(getenv("TSVD_ROWT_TMA")) != 0 : true;
+constexpr int ROWT_S16 = 4, ROWT_S32 = 4;  // ring stages (w <= 16: 2 CTAs / SM)
+
+static bool rowt_tma_launch(const double* Y, int64_t ldy, const double* T, double* Z,
+                            int64_t ldz, int64_t q, int w, double beta, double* gram,
+                            cudaStream_t st) {
+  if (q >= (int64_t)1 << 31) return false;
+  CUtensorMap ym;
+  if (!make_map(&ym, Y, q, w, ldy, NT_R)) return false;
+  const int ctas = nn_ctas(q, w);  // the callers finalise that many Gram partials
+  if (w <= 16) {
+    using CF = RowtTmaCfg<1, ROWT_S16>;
+    static bool attr = false;
+    if (!attr) {
+      TSVD_CUDA(cudaFuncSetAttribute(rowT_tma_kernel<1, ROWT_S16>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
+      attr = true;
+    }
+    rowT_tma_kernel<1, ROWT_S16><<<ctas, 256, CF::bytes, st>>>(ym, T, Z, ldz, q, w, beta, gram);
+  } else {
+    using CF = RowtTmaCfg<2, ROWT_S32>;
+    static bool attr = false;
+    if (!attr) {
+      TSVD_CUDA(cudaFuncSetAttribute(rowT_tma_kernel<2, ROWT_S32>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
+      attr = true;
+    }
+    rowT_tma_kernel<2, ROWT_S32><<<ctas, 256, CF::bytes, st>>>(ym, T, Z, ldz, q, w, beta, gram);
+  }
+  TSVD_CHECK_LAUNCH();
+  return true;
+}
+
 template <int WP, int VEC>
 static void nn_launch(const double* X, int64_t ldx, const double* H, int64_t ldh,
                       const double* Y, int64_t ldy, const double* T, double* Z, int64_t ldz,
@@ -1506,6 +1727,9 @@ void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const d
       return;
     }
   }
+  if (s == 0 && w <= 32 && g_rowt_tma && Y && aligned16(Y, ldy) &&
+      rowt_tma_launch(Y, ldy, T, Z, ldz, q, w, beta, gram, st))
+    return;
   if (s == 0 && w <= 32 && g_rowt32 | (w <= 16)) {  // streaming row pass
     if (w <= 8)
       rowT_kernel<8><<<nn_ctas(q, w), 256, 0, st>>>(Y, ldy, T, Z, ldz, q, w, beta, gram);
