@@ -294,6 +294,12 @@ typedef struct {
 } tsvd_prof_entry;
 enum { TSVD_NPROF = 9 };
 tsvd_status tsvd_set_profiling(tsvd_t h, int on);
+/* Record only the phases whose bit (1 << phase index above) is set in
+ * `mask` (0 = off; tsvd_set_profiling(h, 1) = all phases).  Each recorded
+ * phase call adds two event records to the stream; bench.py times its
+ * solves with only the dominant phase recorded (the roofline needs that
+ * phase's event time) and takes the full breakdown from a separate solve. */
+tsvd_status tsvd_set_profiling_mask(tsvd_t h, unsigned mask);
 tsvd_status tsvd_get_profile(tsvd_t h, tsvd_prof_entry* out /* TSVD_NPROF */);
 tsvd_status tsvd_reset_profile(tsvd_t h);
 

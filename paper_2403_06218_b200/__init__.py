@@ -36,7 +36,7 @@ EXPORTS = [
     "tsvd_strerror", "tsvd_last_error", "tsvd_dbg_philox", "tsvd_dbg_philox_words",
     "tsvd_dbg_apply", "tsvd_dbg_cholqr2", "tsvd_dbg_cgs_cqr2", "tsvd_dbg_cgs_qr",
     "tsvd_dbg_small_svd", "tsvd_dbg_gemm_tn", "tsvd_dbg_gemm_nn",
-    "tsvd_set_profiling", "tsvd_get_profile", "tsvd_reset_profile",
+    "tsvd_set_profiling", "tsvd_set_profiling_mask", "tsvd_get_profile", "tsvd_reset_profile",
     "tsvd_create_csr_dist", "tsvd_create_dense_dist", "tsvd_nccl_unique_id",
     "tsvd_partition_rows", "tsvd_set_allocator", "tsvd_residuals", "tsvd_loopback_create",
     "tsvd_loopback_destroy", "tsvd_set_ortho", "tsvd_set_graphs",
@@ -62,6 +62,10 @@ class TsvdProfEntry(C.Structure):
 
 
 NPROF = 9
+# phase index order of tsvd_get_profile (include/tsvd.h): bit i of
+# tsvd_set_profiling_mask records phase i
+PROF_PHASES = ("apply_A", "apply_AT", "ortho_tn", "ortho_nn", "ortho_small", "small_svd",
+               "restart_out", "other", "ortho_rowT")
 
 
 class TsvdError(RuntimeError):
@@ -103,6 +107,7 @@ _SIGS = {
     "tsvd_dbg_gemm_tn": [vp, i64, vp, i64, i64, i32, i32, vp, vp],
     "tsvd_dbg_gemm_nn": [vp, i64, vp, i64, vp, i64, i64, i32, i32, dbl, dbl, vp],
     "tsvd_set_profiling": [vp, i32],
+    "tsvd_set_profiling_mask": [vp, C.c_uint32],
     "tsvd_get_profile": [vp, C.POINTER(TsvdProfEntry)],
     "tsvd_reset_profile": [vp],
     "tsvd_create_csr_dist": [C.POINTER(vp), C.POINTER(TsvdDist), i64, vp, vp, vp, i32],
@@ -385,6 +390,10 @@ class TruncatedSVD:
 
     def set_profiling(self, on: bool = True):
         _check(lib().tsvd_set_profiling(self._h, int(bool(on))), "tsvd_set_profiling")
+
+    def set_profiling_mask(self, mask: int):
+        """record only the phases whose bit is set (PROF_PHASES order)"""
+        _check(lib().tsvd_set_profiling_mask(self._h, int(mask)), "tsvd_set_profiling_mask")
 
     def profile(self) -> dict:
         """Per-phase event time and algorithmic bytes/flops (tsvd_get_profile)."""

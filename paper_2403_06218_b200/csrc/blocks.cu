@@ -149,7 +149,7 @@ static cudaError_t record(Ctx& c, cudaEvent_t e) {
 
 Prof::Prof(Ctx& c_, int cat_, double bytes_, double flops_)
     : c(c_), cat(cat_), bytes(bytes_), flops(flops_) {
-  if (!c.prof_on) return;
+  if (!c.prof_on || !((c.prof_mask >> cat) & 1u)) return;
   a = pool_get(c);
   TSVD_CUDA(record(c, a));
   l0 = g_launches.load();

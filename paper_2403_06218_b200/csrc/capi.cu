@@ -532,7 +532,15 @@ tsvd_status tsvd_get_rho(tsvd_t h, double* rho) {
 
 tsvd_status tsvd_set_profiling(tsvd_t h, int on) {
   if (!h) return TSVD_EINVAL;
-  h->prof_on = on != 0;
+  h->prof_mask = on != 0 ? (1u << TSVD_NPROF) - 1u : 0u;
+  h->prof_on = h->prof_mask != 0;
+  return TSVD_OK;
+}
+
+tsvd_status tsvd_set_profiling_mask(tsvd_t h, unsigned mask) {
+  if (!h) return TSVD_EINVAL;
+  h->prof_mask = mask & ((1u << TSVD_NPROF) - 1u);
+  h->prof_on = h->prof_mask != 0;
   return TSVD_OK;
 }
 

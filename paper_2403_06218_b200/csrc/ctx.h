@@ -26,7 +26,7 @@ struct ProfRec {
 struct CycleGraph {
   int64_t m = -1, n = -1;
   int d = 0, b = 0, s0 = 0, kc = 0, ortho = -1;
-  bool prof = false;
+  unsigned prof = 0;   // profiling phase mask the graph was captured with
   const void* ptrs[4] = {nullptr, nullptr, nullptr, nullptr};
   uint64_t bufgen = 0;
   int seen = 0;                   // eager runs with this key (capture on the second)
@@ -91,6 +91,7 @@ struct tsvd_ctx {
   int replaced = 0;           // dependent columns replaced by Philox draws
   // instrumentation (tsvd_set_profiling)
   bool prof_on = false;
+  unsigned prof_mask = 0;                 // phases recorded (bit = phase index)
   std::vector<tsvd::ProfRec> prof_open;   // recorded, not yet harvested
   std::vector<cudaEvent_t> ev_pool;
   tsvd_prof_entry prof[TSVD_NPROF]{};

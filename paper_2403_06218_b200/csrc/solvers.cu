@@ -235,12 +235,12 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
     const void* ptrs[4] = {Pb, P, B, flog};
     const bool graph_ok = c.graphs && !c.comm;
     bool same = graph_ok && cg.m == m && cg.n == n && cg.d == d && cg.b == b && cg.s0 == s0 &&
-                cg.kc == kc && cg.ortho == c.ortho && cg.prof == c.prof_on &&
+                cg.kc == kc && cg.ortho == c.ortho && cg.prof == c.prof_mask &&
                 cg.bufgen == c.bufgen && std::equal(ptrs, ptrs + 4, cg.ptrs);
     if (graph_ok && !same) {
       cycle_graph_reset(c);
       cg.m = m, cg.n = n, cg.d = d, cg.b = b, cg.s0 = s0, cg.kc = kc, cg.ortho = c.ortho;
-      cg.prof = c.prof_on;
+      cg.prof = c.prof_mask;
       cg.bufgen = c.bufgen;
       std::copy(ptrs, ptrs + 4, cg.ptrs);
     }
