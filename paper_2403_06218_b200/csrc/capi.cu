@@ -12,6 +12,7 @@
 
 namespace tsvd {
 std::atomic<int64_t> g_launches{0};
+bool g_pdl = getenv("TSVD_PDL") ? atoi(getenv("TSVD_PDL")) != 0 : false;  // measured: no gain (DESIGN 6)
 static thread_local std::string g_last_error;
 }  // namespace tsvd
 

@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -36,6 +37,33 @@ extern std::atomic<int64_t> g_launches;
     ::tsvd::g_launches.fetch_add(1, std::memory_order_relaxed);             \
     TSVD_CUDA(cudaGetLastError());                                          \
   } while (0)
+
+// Programmatic dependent launch (Hopper+; TSVD_PDL=0 turns it off): the
+// hot-path kernels of a solve are launched with programmatic stream
+// serialisation, so a kernel's launch and CTA dispatch overlap the tail of
+// its predecessor.  Every kernel launched this way starts with pdl_enter():
+// griddepcontrol.wait (returns once the predecessor grid has completed and
+// its memory is visible -- nothing of the kernel's inputs is read before
+// it) and griddepcontrol.launch_dependents (lets the NEXT kernel be launched
+// once every CTA of this one has started; its own wait still orders it
+// after this grid's completion).  Without the attribute both are no-ops.
+extern bool g_pdl;
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  TSVD_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+  // (the launch site's TSVD_CHECK_LAUNCH() counts it)
+}
 
 // ------------------------------------------------------------ data views --
 // Row-major view: element (i, j) at p[i*ld + j].  Row offsets are 64-bit.
@@ -139,6 +167,11 @@ void gemm_tn(const double* X, int64_t ldx, const double* Y, int64_t ldy, int64_t
 int nn_ctas(int64_t q, int w);
 // part/part_cap (doubles): optional scratch for split-K partials of plain
 // products (beta = 0, no T/gram) with few row tiles; nullptr disables the split.
+// X[:, :w] <- X[:, :s] H (s x w, w <= min(s, 128)) in place, one pass over
+// X (row-local product; ts.cu).  Returns false when the shape / alignment
+// is not supported (the caller stages through scratch instead).
+bool gemm_nn_out_inplace(double* X, int64_t ldx, const double* H, int64_t ldh, int64_t q, int s,
+                         int w, cudaStream_t st);
 void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const double* Y,
              int64_t ldy, const double* T, double* Z, int64_t ldz, int64_t q, int s, int w,
              double alpha, double beta, double* gram, cudaStream_t st, double* part = nullptr,

@@ -4,6 +4,7 @@
 // H += Hbar L^T (reading R5), block copies, CGS2 column bookkeeping, the
 // Lanczos rho test and sign normalisation.
 #include "internal.h"
+#include "ptx.cuh"
 
 namespace tsvd {
 
@@ -85,6 +86,7 @@ __global__ void __launch_bounds__(fin_threads(WT)) finalize_kernel(
     const double* __restrict__ Lprev, double* __restrict__ L, double* __restrict__ T,
     double* __restrict__ R, double* __restrict__ H, const double* __restrict__ Hbar, int s,
     int* __restrict__ flag) {
+  pdl_enter();
   constexpr int NTH = fin_threads(WT);
   __shared__ double red[NTH];
   __shared__ double Ws[32 * 33];
@@ -285,6 +287,7 @@ __global__ void __launch_bounds__(fin_threads(WT)) finalize_kernel(
 // entries).  The single-CTA finaliser then runs with np = 1.
 __global__ void __launch_bounds__(256) gram_prereduce_kernel(double* __restrict__ gram, int np,
                                                              int C) {
+  pdl_enter();
   __shared__ double red[8][33];
   const int lane = threadIdx.x & 31, g = threadIdx.x >> 5;
   const int e = blockIdx.x * 32 + lane;
@@ -307,7 +310,7 @@ static void fin_launch(const double* gram, int np, int w, int mode, double* Wout
                        const double* Lprev, double* L, double* T, double* R, double* H,
                        const double* Hbar, int s, int* flag, cudaStream_t st) {
   if (np > 1 && w * w > fin_threads(w == 32 ? 32 : 0)) {
-    gram_prereduce_kernel<<<(w * w + 31) / 32, 256, 0, st>>>(const_cast<double*>(gram), np,
+    launch_pdl(gram_prereduce_kernel, (w * w + 31) / 32, 256, 0, st, const_cast<double*>(gram), np,
                                                              w * w);
     TSVD_CHECK_LAUNCH();
     np = 1;
@@ -328,7 +331,7 @@ static void fin_launch(const double* gram, int np, int w, int mode, double* Wout
     attr = true;
   }
 #define FIN_GO(WTV)                                                                           \
-  finalize_kernel<WTV><<<1, fin_threads(WTV), dyn, st>>>(gram, np, w, mode, Wout, Lprev, L, T, R, H, Hbar, \
+  launch_pdl(finalize_kernel<WTV>, 1, fin_threads(WTV), dyn, st, gram, np, w, mode, Wout, Lprev, L, T, R, H, Hbar, \
                                               s, flag)
   if (w == 32) FIN_GO(32);
   else if (w == 16) FIN_GO(16);
@@ -482,6 +485,7 @@ __global__ void small_gemm_kernel(const double* __restrict__ A, int lda, int ta,
                                   const double* __restrict__ B, int ldb, int tb,
                                   double* __restrict__ Cm, int ldc, int m, int n, int k,
                                   double alpha, double beta) {
+  pdl_enter();
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t >= (int64_t)m * n) return;
   const int i = (int)(t / n), j = (int)(t % n);
@@ -508,7 +512,7 @@ void small_gemm(const double* A, int lda, bool ta, const double* B, int ldb, boo
                 int ldc, int m, int n, int k, double alpha, double beta, cudaStream_t st) {
   const int64_t e = (int64_t)m * n;
   if (e <= 0) return;
-  small_gemm_kernel<<<(unsigned)((e + 127) / 128), 128, 0, st>>>(A, lda, ta ? 1 : 0, B, ldb,
+  launch_pdl(small_gemm_kernel, (unsigned)((e + 127) / 128), 128, 0, st, A, lda, ta ? 1 : 0, B, ldb,
                                                                   tb ? 1 : 0, C, ldc, m, n, k,
                                                                   alpha, beta);
   TSVD_CHECK_LAUNCH();
@@ -518,6 +522,7 @@ void small_gemm(const double* A, int lda, bool ta, const double* B, int ldb, boo
 __global__ void copy_block_kernel(const double* __restrict__ src, int64_t lds,
                                   double* __restrict__ dst, int64_t ldd, int64_t rows, int cols,
                                   int transpose) {
+  pdl_enter();
   const int64_t n = rows * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
@@ -533,7 +538,7 @@ void copy_block(const double* src, int64_t lds, double* dst, int64_t ldd, int64_
   if (n <= 0) return;
   int64_t blocks = (n + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  copy_block_kernel<<<(unsigned)blocks, 256, 0, st>>>(src, lds, dst, ldd, rows, cols,
+  launch_pdl(copy_block_kernel, (unsigned)blocks, 256, 0, st, src, lds, dst, ldd, rows, cols,
                                                        transpose ? 1 : 0);
   TSVD_CHECK_LAUNCH();
 }
@@ -581,6 +586,7 @@ __global__ void lanczos_rho_kernel(const double* __restrict__ Rbar, int b,
                                    const double* __restrict__ Vb, int d,
                                    const double* __restrict__ S, int cnt,
                                    double* __restrict__ rho) {
+  pdl_enter();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= cnt) return;
   double ss = 0.0;
@@ -594,7 +600,7 @@ __global__ void lanczos_rho_kernel(const double* __restrict__ Rbar, int b,
 
 void lanczos_rho(const double* Rbar, int b, const double* Vb, int d, const double* S, int cnt,
                  double* rho, cudaStream_t st) {
-  lanczos_rho_kernel<<<(cnt + 127) / 128, 128, 0, st>>>(Rbar, b, Vb, d, S, cnt, rho);
+  launch_pdl(lanczos_rho_kernel, (cnt + 127) / 128, 128, 0, st, Rbar, b, Vb, d, S, cnt, rho);
   TSVD_CHECK_LAUNCH();
 }
 

@@ -78,6 +78,10 @@ static double* out_product(Ctx& c, const char* name, double* X, int64_t ldx, int
     *ld = r;
     return Z;
   }
+  if (gemm_nn_out_inplace(X, ldx, H, ldh, rows, s, r, c.st)) {  // one pass, no scratch
+    *ld = ldx;
+    return X;
+  }
   const size_t cap = (size_t)std::max(c.m, c.n) * 32;  // pre-sized by the solvers
   double* stage = dbuf(c, "scratch", cap);
   const int64_t chunk = std::max<int64_t>(1, (int64_t)(cap / r));

@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(256) spmm_kernel(Csr A, const double* __restri
                                                    int64_t ldy, int w, double* __restrict__ part,
                                                    int64_t nb_long, int64_t nb_med,
                                                    int64_t nmed_run, int64_t nshort_run) {
+  pdl_enter();
   const int64_t b = blockIdx.x;
   if (b < nb_long) {
     spmm_long_dev<L, VEC>(A.seg_row, A.seg_beg, A.seg_end, A.seg_slot, A.colidx, A.vals, X, ldx,
@@ -253,6 +254,7 @@ __global__ void spmm_fixup_kernel(const int64_t* __restrict__ split_row,
                                   const int32_t* __restrict__ split_count,
                                   const double* __restrict__ part, double* __restrict__ Y,
                                   int64_t ldy, int w, int64_t nsplit) {
+  pdl_enter();
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t r = t / kPartW;
   const int c = (int)(t % kPartW);
@@ -279,14 +281,13 @@ static void spmm_dispatch(const Csr& A, const double* X, int64_t ldx, double* Y,
   const int64_t nb_long = A.nseg;
   const int64_t blocks = nb_short + nb_med + nb_long;
   if (blocks > 0) {
-    spmm_kernel<L, VEC><<<(unsigned)blocks, 256, 0, st>>>(A, X, ldx, Y, ldy, w, part, nb_long,
+    launch_pdl(spmm_kernel<L, VEC>, (unsigned)blocks, 256, 0, st, A, X, ldx, Y, ldy, w, part, nb_long,
                                                            nb_med, nmed_run, nshort_run);
     TSVD_CHECK_LAUNCH();
   }
   if (fixup && A.nsplit > 0) {
     const int64_t thr = A.nsplit * kPartW;
-    spmm_fixup_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(
-        A.split_row, A.split_first, A.split_count, part, Y, ldy, w, A.nsplit);
+    launch_pdl(spmm_fixup_kernel, (unsigned)((thr + 255) / 256), 256, 0, st, A.split_row, A.split_first, A.split_count, part, Y, ldy, w, A.nsplit);
     TSVD_CHECK_LAUNCH();
   }
 }
@@ -562,8 +563,7 @@ static bool staged_launch(const Csr& A, const double* X, int64_t ldx, double* Y,
   }
   if (A.nsplit > 0) {
     const int64_t thr = A.nsplit * kPartW;
-    spmm_fixup_kernel<<<(unsigned)((thr + 255) / 256), 256, 0, st>>>(
-        A.split_row, A.split_first, A.split_count, part, Y, ldy, w, A.nsplit);
+    launch_pdl(spmm_fixup_kernel, (unsigned)((thr + 255) / 256), 256, 0, st, A.split_row, A.split_first, A.split_count, part, Y, ldy, w, A.nsplit);
     TSVD_CHECK_LAUNCH();
   }
   return true;

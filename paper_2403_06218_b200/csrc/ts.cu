@@ -109,6 +109,7 @@ __global__ void __launch_bounds__(256, (WP == 32) ? 1 : 2) gemm_tn_kernel(const 
                                                          int64_t q, int s, int w,
                                                          double* __restrict__ C, int64_t ldc,
                                                          double* __restrict__ part) {
+  pdl_enter();
   using CF = TnCfg<WP>;
   constexpr int XP = CF::XP, YP = CF::YP, NT = CF::NT, MT = CF::MT;
   extern __shared__ __align__(16) double sm[];
@@ -211,6 +212,7 @@ template <int ST, int NYB>
 __global__ void __launch_bounds__(288, 2) gemm_tn_tma_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap ymap,
     int64_t q, int s, int w, double* __restrict__ C, int64_t ldc, double* __restrict__ part) {
+  pdl_enter();
   using CF = TnTmaCfg<ST, NYB>;
   constexpr int S = CF::S, MT = CF::MT, NT = 2 * NYB, WP = 16 * NYB;
   static_assert((size_t)ST * WP * 8 <= CF::stage * CF::S, "reduction tile must fit the ring");
@@ -324,6 +326,7 @@ __global__ void __launch_bounds__(288, 2) gemm_tn_tma_kernel(
 __global__ void reduce_partials_kernel(const double* __restrict__ part, int nparts,
                                        int64_t count, double* __restrict__ out, int w,
                                        int64_t ldc) {
+  pdl_enter();
   __shared__ double red[8][33];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int64_t base = (int64_t)blockIdx.x * 32; base < count; base += (int64_t)gridDim.x * 32) {
@@ -357,7 +360,7 @@ static void reduce_launch(const double* part, int nparts, int64_t count, double*
   if (count <= 0) return;
   int64_t blocks = (count + 31) / 32;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  reduce_partials_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, nparts, count, out, w, ldc);
+  launch_pdl(reduce_partials_kernel, (unsigned)blocks, 256, 0, st, part, nparts, count, out, w, ldc);
   TSVD_CHECK_LAUNCH();
 }
 
@@ -381,7 +384,7 @@ static void tn_launch(dim3 grid, const double* X, int64_t ldx, const double* Y, 
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     attr = true;
   }
-  gemm_tn_kernel<WP, VEC><<<grid, 256, bytes, st>>>(X, ldx, Y, ldy, q, s, w, C, ldc, part);
+  launch_pdl(gemm_tn_kernel<WP, VEC>, grid, 256, bytes, st, X, ldx, Y, ldy, q, s, w, C, ldc, part);
   TSVD_CHECK_LAUNCH();
 }
 
@@ -402,8 +405,7 @@ static void tn_tma_go(const CUtensorMap& xm, const CUtensorMap& ym, int64_t q, i
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
     attr = true;
   }
-  gemm_tn_tma_kernel<ST, NYB><<<dim3(s_tiles, (unsigned)splits), 288, CF::bytes, st>>>(
-      xm, ym, q, s, w, C, ldc, part);
+  launch_pdl(gemm_tn_tma_kernel<ST, NYB>, dim3(s_tiles, (unsigned)splits), 288, CF::bytes, st, xm, ym, q, s, w, C, ldc, part);
   TSVD_CHECK_LAUNCH();
   if (splits > 1) reduce_launch(part, (int)splits, (int64_t)s * w, C, w, ldc == w ? 0 : ldc, st);
 }
@@ -503,6 +505,7 @@ __global__ void __launch_bounds__(256, NnCfg<WP>::PER_SM) gemm_nn_kernel(
     const double* __restrict__ X, int64_t ldx, const double* __restrict__ H, int64_t ldh,
     const double* Y, int64_t ldy, const double* __restrict__ T, double* Z, int64_t ldz,
     int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram) {
+  pdl_enter();
   using CF = NnCfg<WP>;
   constexpr int S = CF::S, XP = CF::XP, HP = CF::HP, OP = CF::OP, NT = CF::NT;
   constexpr int NPAIR = NT * NT, PPW = (NPAIR + 7) / 8, KY = WP / 4, NACC = CF::NACC;
@@ -719,6 +722,7 @@ __global__ void __launch_bounds__(256) rowT_kernel(const double* Y, int64_t ldy,
                                                    const double* __restrict__ T, double* Z,
                                                    int64_t ldz, int64_t q, int w, double beta,
                                                    double* __restrict__ gram) {
+  pdl_enter();
   // Gram: only the NPAIR upper-triangular 8 x 8 tile pairs (mi <= ni) are
   // accumulated (W is symmetric; mirrored when written)
   constexpr int NT = WP / 8, KY = WP / 4, NPAIR = NT * (NT + 1) / 2, ZP = WP + 4;
@@ -1185,9 +1189,10 @@ struct RowtTmaCfg {
 };
 
 template <int NYB, int S>
-__global__ void __launch_bounds__(256, NYB == 1 ? 2 : 1) rowT_tma_kernel(
+__global__ void __launch_bounds__(256, 2) rowT_tma_kernel(
     const __grid_constant__ CUtensorMap ymap, const double* __restrict__ T, double* Z,
     int64_t ldz, int64_t q, int w, double beta, double* __restrict__ gram) {
+  pdl_enter();
   using CF = RowtTmaCfg<NYB, S>;
   constexpr int WP = CF::WP, NT = 2 * NYB, OP = CF::OP, TP = CF::TP;
   constexpr int NGP = NT * (NT + 1) / 2;
@@ -1358,6 +1363,7 @@ __global__ void __launch_bounds__(288, 2) gemm_nn_tma_kernel(
     const __grid_constant__ CUtensorMap ymap, int use_y, const double* __restrict__ T, double* Z,
     int64_t ldz, int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram,
     int64_t zsplit) {
+  pdl_enter();
   nn_tma_body<KC, S, NYB, false>(xmap, hmap, ymap, use_y, T, Z, ldz, q, s, w, alpha, beta, gram,
                                  zsplit);
 }
@@ -1367,6 +1373,7 @@ __global__ void __launch_bounds__(256, 2) gemm_nn_tma_kernel_fold16(
     const __grid_constant__ CUtensorMap ymap, int use_y, const double* __restrict__ T, double* Z,
     int64_t ldz, int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram,
     int64_t zsplit) {
+  pdl_enter();
   nn_tma_body<KC, S, NYB, true>(xmap, hmap, ymap, use_y, T, Z, ldz, q, s, w, alpha, beta, gram,
                                 zsplit);
 }
@@ -1376,6 +1383,7 @@ __global__ void __launch_bounds__(256, 1) gemm_nn_tma_kernel_w32(
     const __grid_constant__ CUtensorMap ymap, int use_y, const double* __restrict__ T, double* Z,
     int64_t ldz, int64_t q, int s, int w, double alpha, double beta, double* __restrict__ gram,
     int64_t zsplit) {
+  pdl_enter();
   nn_tma_body<KC, S, NYB, true>(xmap, hmap, ymap, use_y, T, Z, ldz, q, s, w, alpha, beta, gram,
                                 zsplit);
 }
@@ -1386,22 +1394,31 @@ __global__ void __launch_bounds__(256, 1) gemm_nn_tma_kernel_w32(
 // accumulator set of 2 x 8 DMMA tiles per warp, and Z stored straight from
 // the accumulator fragments (no shared out tile).  These products are
 // DMMA-bound (2 s w flops per 8 s bytes).
-template <int KC, int S>
+template <int KC, int S, int NH = 4>  // NH = 16-column H boxes per stage (w <= 16 NH)
 struct NnOutCfg {
   static constexpr int NB = KC / 16;
   static constexpr size_t xbox = (size_t)NT_R * 16 * 8;
   static constexpr size_t hbox = (size_t)KC * 16 * 8;
-  static constexpr size_t stage = NB * xbox + 4 * hbox;
+  static constexpr size_t stage = NB * xbox + NH * hbox;
   static constexpr size_t bar_off = S * stage;
   static constexpr size_t bytes = bar_off + 2 * S * 8 + 1024;
   static constexpr unsigned tx = (unsigned)stage;
 };
 
-template <int KC, int S, int NT>  // NT = 8-column tiles computed (w <= 8 NT <= 64)
+// NT = 8-column tiles computed (w <= 8 NT <= 128).  In place (Z = X, ldz =
+// ldx, one launch for all w columns, no split-K): a tile's output rows are
+// written only after every K chunk of that tile has landed in shared memory
+// (the epilogue follows the tile's last full-barrier wait), and no other CTA
+// reads those rows, so Z may overwrite X's first w columns -- the outputs
+// and the thick-restart panels of C5, which have no room for separate
+// m x r / n x r buffers, without a scratch round trip.
+template <int KC, int S, int NT>
 __global__ void __launch_bounds__(288, 1) gemm_nn_out_tma_kernel(
     const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap, double* Z,
     int64_t ldz, int64_t q, int s, int w, double alpha, int64_t zsplit) {
-  using CF = NnOutCfg<KC, S>;  // split-K over blockIdx.y as in gemm_nn_tma_kernel
+  pdl_enter();
+  constexpr int NH = (NT + 1) / 2;
+  using CF = NnOutCfg<KC, S, NH>;  // split-K over blockIdx.y as in gemm_nn_tma_kernel
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = (uint64_t*)(sm + CF::bar_off);
@@ -1445,7 +1462,7 @@ __global__ void __launch_bounds__(288, 1) gemm_nn_out_tma_kernel(
         for (int b = 0; b < CF::NB; ++b)
           tma_load_2d(base + b * CF::xbox, &xmap, (kb + kc) * KC + b * 16, r0, &full[st]);
 #pragma unroll
-        for (int b = 0; b < 4; ++b)
+        for (int b = 0; b < NH; ++b)
           tma_load_2d(base + CF::NB * CF::xbox + b * CF::hbox, &hmap, b * 16, (kb + kc) * KC,
                       &full[st]);
       }
@@ -1567,14 +1584,12 @@ static bool nn_tma_launch(const double* X, int64_t ldx, const double* H, int64_t
     const int ctas = nn_ctas(q, 32);
     const int ks = (use_y || T || gram) ? 1 : pick_split(q, s, w, ctas, part_cap);
     if (ks > 1) {
-      gemm_nn_tma_kernel_w32<NNT_KC, 3, 2><<<dim3(ctas / ks, ks), 256, CF2::bytes, st>>>(
-          xm, hm, ym, 0, nullptr, part, w, q, s, w, alpha, 0.0, nullptr, q * w);
+      launch_pdl(gemm_nn_tma_kernel_w32<NNT_KC, 3, 2>, dim3(ctas / ks, ks), 256, CF2::bytes, st, xm, hm, ym, 0, nullptr, part, w, q, s, w, alpha, 0.0, nullptr, q * w);
       TSVD_CHECK_LAUNCH();
       reduce_launch(part, ks, q * w, Z, w, ldz == w ? 0 : ldz, st);
       return true;
     }
-    gemm_nn_tma_kernel_w32<NNT_KC, 3, 2><<<ctas, 256, CF2::bytes, st>>>(
-        xm, hm, ym, use_y, T, Z, ldz, q, s, w, alpha, beta, gram, 0);
+    launch_pdl(gemm_nn_tma_kernel_w32<NNT_KC, 3, 2>, ctas, 256, CF2::bytes, st, xm, hm, ym, use_y, T, Z, ldz, q, s, w, alpha, beta, gram, 0);
     TSVD_CHECK_LAUNCH();
     return true;
   }
@@ -1593,13 +1608,13 @@ static bool nn_tma_launch(const double* X, int64_t ldx, const double* H, int64_t
                           : gemm_nn_tma_kernel<NNT_KC, NNT_S, 1>;
   const int nthr = g_nn_fold16 ? 256 : 288;
   if (ks > 1) {
-    kern<<<dim3(ctas / ks, ks), nthr, CF::bytes, st>>>(xm, hm, ym, 0, nullptr, part, w, q, s, w,
+    launch_pdl(kern, dim3(ctas / ks, ks), nthr, CF::bytes, st, xm, hm, ym, 0, nullptr, part, w, q, s, w,
                                                       alpha, 0.0, nullptr, q * w);
     TSVD_CHECK_LAUNCH();
     reduce_launch(part, ks, q * w, Z, w, ldz == w ? 0 : ldz, st);
     return true;
   }
-  kern<<<ctas, nthr, CF::bytes, st>>>(xm, hm, ym, use_y, T, Z, ldz, q, s, w, alpha, beta, gram, 0);
+  launch_pdl(kern, ctas, nthr, CF::bytes, st, xm, hm, ym, use_y, T, Z, ldz, q, s, w, alpha, beta, gram, 0);
   TSVD_CHECK_LAUNCH();
   return true;
 }
@@ -1630,7 +1645,7 @@ static bool nn_out_tma_launch(const double* X, int64_t ldx, const double* H, int
   double* zo = ks > 1 ? part : Z;
   const int64_t ldo = ks > 1 ? w : ldz;
 #define OUT_GO(NTV)                                                                       \
-  gemm_nn_out_tma_kernel<NNT_KC, OS, NTV><<<dim3(ctas / ks, ks), 288, CF::bytes, st>>>(    \
+  launch_pdl(gemm_nn_out_tma_kernel<NNT_KC, OS, NTV>, dim3(ctas / ks, ks), 288, CF::bytes, st, \
       xm, hm, zo, ldo, q, s, w, alpha, ks > 1 ? q * w : 0)
   if (nt <= 5) OUT_GO(5);
   else if (nt == 6) OUT_GO(6);
@@ -1642,8 +1657,51 @@ static bool nn_out_tma_launch(const double* X, int64_t ldx, const double* H, int
   return true;
 }
 
+// 64 < w <= 128: all w columns from ONE read of X (13 or 16 accumulator
+// tiles of 8 columns per warp, NH = 8 H boxes per stage, 3 stages =
+// 192 KB), no split-K.  Z may alias X's first w
+// columns (ldz = ldx): see gemm_nn_out_tma_kernel.
+static bool nn_out_wide_launch(const double* X, int64_t ldx, const double* H, int64_t ldh,
+                               double* Z, int64_t ldz, int64_t q, int s, int w, double alpha,
+                               cudaStream_t st) {
+  if (q >= (int64_t)1 << 31 || s >= (1 << 30) || w > 128) return false;
+  CUtensorMap xm, hm;
+  if (!make_map(&xm, X, q, s, ldx, NT_R) || !make_map(&hm, H, s, w, ldh, NNT_KC)) return false;
+  constexpr int WS = 3;
+  using CF = NnOutCfg<NNT_KC, WS, 8>;
+  static bool attr = false;
+  if (!attr) {
+    TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_out_tma_kernel<NNT_KC, WS, 13>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
+    TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_out_tma_kernel<NNT_KC, WS, 16>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
+    attr = true;
+  }
+  const int nt = (w + 7) / 8;
+  const int ctas = nn_ctas(q, 32);
+  if (nt <= 13)
+    launch_pdl(gemm_nn_out_tma_kernel<NNT_KC, WS, 13>, ctas, 288, CF::bytes, st, xm, hm, Z, ldz,
+               q, s, w, alpha, (int64_t)0);
+  else
+    launch_pdl(gemm_nn_out_tma_kernel<NNT_KC, WS, 16>, ctas, 288, CF::bytes, st, xm, hm, Z, ldz,
+               q, s, w, alpha, (int64_t)0);
+  TSVD_CHECK_LAUNCH();
+  return true;
+}
+
+bool g_out_wide = getenv("TSVD_OUT_WIDE") ? atoi(getenv("TSVD_OUT_WIDE")) != 0 : true;
+
+bool gemm_nn_out_inplace(double* X, int64_t ldx, const double* H, int64_t ldh, int64_t q, int s,
+                         int w, cudaStream_t st) {
+  if (!g_out_wide || w > 128 || w > s || q <= 0 || !aligned16(X, ldx) || !aligned16(H, ldh))
+    return false;
+  if (w <= 64)  // the 4-stage kernel (4 H boxes), no split-K (part_cap = 0)
+    return nn_out_tma_launch(X, ldx, H, ldh, X, ldx, q, s, w, 1.0, st, nullptr, 0);
+  return nn_out_wide_launch(X, ldx, H, ldh, X, ldx, q, s, w, 1.0, st);
+}
+
 bool g_rowt_tma = getenv("TSVD_ROWT_TMA") ? atoi(getenv("TSVD_ROWT_TMA")) != 0 : true;
-constexpr int ROWT_S16 = 4, ROWT_S32 = 4;  // ring stages (w <= 16: 2 CTAs / SM)
+constexpr int ROWT_S16 = 4, ROWT_S32 = 2;  // ring stages (2 CTAs / SM)
 
 static bool rowt_tma_launch(const double* Y, int64_t ldy, const double* T, double* Z,
                             int64_t ldz, int64_t q, int w, double beta, double* gram,
@@ -1660,7 +1718,7 @@ static bool rowt_tma_launch(const double* Y, int64_t ldy, const double* T, doubl
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
       attr = true;
     }
-    rowT_tma_kernel<1, ROWT_S16><<<ctas, 256, CF::bytes, st>>>(ym, T, Z, ldz, q, w, beta, gram);
+    launch_pdl(rowT_tma_kernel<1, ROWT_S16>, ctas, 256, CF::bytes, st, ym, T, Z, ldz, q, w, beta, gram);
   } else {
     using CF = RowtTmaCfg<2, ROWT_S32>;
     static bool attr = false;
@@ -1669,7 +1727,12 @@ static bool rowt_tma_launch(const double* Y, int64_t ldy, const double* T, doubl
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
       attr = true;
     }
-    rowT_tma_kernel<2, ROWT_S32><<<ctas, 256, CF::bytes, st>>>(ym, T, Z, ldz, q, w, beta, gram);
+    // two CTAs per SM (128 registers, 2 x 110 KB) when no Gram partials are
+    // written; with a Gram the grid must be the nn_ctas(q, w) partials the
+    // caller finalises (one CTA per SM at w > 16)
+    const int g32 = gram ? ctas : (int)std::min<int64_t>((q + NT_R - 1) / NT_R, 2 * 148);
+    launch_pdl(rowT_tma_kernel<2, ROWT_S32>, std::max(1, g32), 256, CF::bytes, st, ym, T, Z, ldz,
+               q, w, beta, gram);
   }
   TSVD_CHECK_LAUNCH();
   return true;
@@ -1687,7 +1750,7 @@ static void nn_launch(const double* X, int64_t ldx, const double* H, int64_t ldh
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
     attr = true;
   }
-  gemm_nn_kernel<WP, VEC><<<nn_ctas(q, WP), 256, bytes, st>>>(X, ldx, H, ldh, Y, ldy, T, Z,
+  launch_pdl(gemm_nn_kernel<WP, VEC>, nn_ctas(q, WP), 256, bytes, st, X, ldx, H, ldh, Y, ldy, T, Z,
                                                                ldz, q, s, w, alpha, beta, gram);
   TSVD_CHECK_LAUNCH();
 }
@@ -1707,6 +1770,11 @@ void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const d
   if (w > 32) {
     if (T || gram) throw Error{TSVD_EINVAL, "gemm_nn: T/gram need w <= 32"};
     if (beta == 0.0 && s > 0 && g_nn_tma && aligned16(X, ldx) && aligned16(H, ldh)) {
+      // one read of X for all w <= 128 columns when the rows give enough
+      // tiles for the grid (no split-K needed)
+      if (g_out_wide && w > 64 && w <= 128 && (q + NT_R - 1) / NT_R >= 8 * 148 &&
+          nn_out_wide_launch(X, ldx, H, ldh, Z, ldz, q, s, w, alpha, st))
+        return;
       bool done = true;
       for (int c0 = 0; c0 < w && done; c0 += 64)
         done = nn_out_tma_launch(X, ldx, H + c0, ldh, Z + c0, ldz, q, s, std::min(64, w - c0),
@@ -1732,11 +1800,11 @@ void gemm_nn(const double* X, int64_t ldx, const double* H, int64_t ldh, const d
     return;
   if (s == 0 && w <= 32 && g_rowt32 | (w <= 16)) {  // streaming row pass
     if (w <= 8)
-      rowT_kernel<8><<<nn_ctas(q, w), 256, 0, st>>>(Y, ldy, T, Z, ldz, q, w, beta, gram);
+      launch_pdl(rowT_kernel<8>, nn_ctas(q, w), 256, 0, st, Y, ldy, T, Z, ldz, q, w, beta, gram);
     else if (w <= 16)
-      rowT_kernel<16><<<nn_ctas(q, w), 256, 0, st>>>(Y, ldy, T, Z, ldz, q, w, beta, gram);
+      launch_pdl(rowT_kernel<16>, nn_ctas(q, w), 256, 0, st, Y, ldy, T, Z, ldz, q, w, beta, gram);
     else  // nn_ctas(q, w) CTAs: the callers finalise that many Gram partials
-      rowT_kernel<32><<<nn_ctas(q, w), 256, 0, st>>>(Y, ldy, T, Z, ldz, q, w, beta, gram);
+      launch_pdl(rowT_kernel<32>, nn_ctas(q, w), 256, 0, st, Y, ldy, T, Z, ldz, q, w, beta, gram);
     TSVD_CHECK_LAUNCH();
     return;
   }

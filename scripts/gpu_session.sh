@@ -1,8 +1,7 @@
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
-for M in all dominant none; do
-timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 0 --prof-mode $M > $O/s6_bench_C2_$M.json 2> $O/s6_bench_C2_$M.err
-done
-timeout 600 python bench.py --config C4 --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 --prof-mode all > $O/s6_bench_C4_all.json 2> $O/s6_bench_C4_all.err
-timeout 600 python bench.py --config C4 --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $O/s6_bench_C4_dominant.json 2> $O/s6_bench_C4_dominant.err
+timeout 1200 python -m pytest tests/test_gpu_solvers.py tests/test_gpu_loopback.py -x -q -p no:cacheprovider > $O/s12_pytest.log 2>&1
+echo "pytest rc $?" >> $O/s12_pytest.log
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $O/s12_bench_C2.json 2> $O/s12_bench_C2.err
+timeout 600 python bench.py --config C4 --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 > $O/s12_bench_C4.json 2> $O/s12_bench_C4.err
 echo done
