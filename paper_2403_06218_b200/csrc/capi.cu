@@ -75,6 +75,8 @@ static void destroy_ctx(tsvd_ctx* c) {
   for (auto& P : c->ATp) csr_free(P, c->st);
   for (auto e : c->comm_ev) cudaEventDestroy(e);
   if (c->comm_st) cudaStreamDestroy(c->comm_st);
+  if (c->copy_st) cudaStreamDestroy(c->copy_st);
+  if (c->copy_ev) cudaEventDestroy(c->copy_ev);
   dfree(c->Ad, c->st);
   free_bufs(*c);
   prof_release(*c);
@@ -497,13 +499,26 @@ tsvd_status tsvd_get(tsvd_t h, double* U, int64_t ldu, double* S, double* V, int
   TSVD_API_BEGIN
   const cudaMemcpyKind k = mem_kind == TSVD_DEVICE ? cudaMemcpyDeviceToDevice
                                                    : cudaMemcpyDeviceToHost;
+  // to the host with both U and V wanted: V on a second stream (after the
+  // solve's work on h->st), so the two copies use two copy engines
+  cudaStream_t vst = h->st;
+  if (U && V && k == cudaMemcpyDeviceToHost) {
+    if (!h->copy_st) {
+      TSVD_CUDA(cudaStreamCreateWithFlags(&h->copy_st, cudaStreamNonBlocking));
+      TSVD_CUDA(cudaEventCreateWithFlags(&h->copy_ev, cudaEventDisableTiming));
+    }
+    TSVD_CUDA(cudaEventRecord(h->copy_ev, h->st));
+    TSVD_CUDA(cudaStreamWaitEvent(h->copy_st, h->copy_ev, 0));
+    vst = h->copy_st;
+  }
+  if (V)
+    TSVD_CUDA(cudaMemcpy2DAsync(V, ldv * sizeof(double), h->V, h->ldV * sizeof(double),
+                                r * sizeof(double), h->n, k, vst));
   if (U)
     TSVD_CUDA(cudaMemcpy2DAsync(U, ldu * sizeof(double), h->U, h->ldU * sizeof(double),
                                 r * sizeof(double), h->m, k, h->st));
-  if (V)
-    TSVD_CUDA(cudaMemcpy2DAsync(V, ldv * sizeof(double), h->V, h->ldV * sizeof(double),
-                                r * sizeof(double), h->n, k, h->st));
   if (S) TSVD_CUDA(cudaMemcpyAsync(S, h->S, r * sizeof(double), k, h->st));
+  if (vst != h->st) TSVD_CUDA(cudaStreamSynchronize(vst));
   TSVD_CUDA(cudaStreamSynchronize(h->st));
   return TSVD_OK;
   TSVD_API_END

@@ -55,6 +55,10 @@ struct tsvd_ctx {
   // owner (ncclReduce) overlaps the next shard's SpMM (comm_st, events)
   std::vector<tsvd::Csr> ATp;
   cudaStream_t comm_st = nullptr;
+  // tsvd_get: V's device->host copy runs on copy_st beside U's (two copy
+  // engines on the PCIe link instead of one)
+  cudaStream_t copy_st = nullptr;
+  cudaEvent_t copy_ev = nullptr;
   std::vector<cudaEvent_t> comm_ev;
   double* Ad = nullptr;      // dense A, row-major m x n
   int64_t lda = 0;
