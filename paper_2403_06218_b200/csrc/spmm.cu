@@ -621,21 +621,73 @@ void launch_spmm_wide(const Csr& A, const double* X, int64_t ldx, double* Y, int
 // ------------------------------------------------------- plan / transpose --
 // Copies the nonzeros of the rows in permuted order: position p of the new
 // layout holds row perm[p] (one warp per row, lane-strided).
+constexpr int64_t kPermWarpMax = 4096;  // > kMedRow: only long rows exceed it
 __global__ void csr_permute_kernel(const int64_t* __restrict__ old_rp,
                                    const int32_t* __restrict__ old_ci,
                                    const double* __restrict__ old_va,
                                    const int32_t* __restrict__ perm,
                                    const int64_t* __restrict__ new_rp, int64_t rows,
-                                   int32_t* __restrict__ new_ci, double* __restrict__ new_va) {
+                                   int32_t* __restrict__ new_ci, double* __restrict__ new_va,
+                                   int64_t* __restrict__ long_rows, int* __restrict__ nlong) {
   const int lane = threadIdx.x & 31;
   for (int64_t p = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; p < rows;
        p += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int64_t ob = old_rp[perm[p]], nb = new_rp[p], len = new_rp[p + 1] - nb;
+    if (len > kPermWarpMax) {  // listed for csr_permute_long_kernel
+      if (lane == 0) long_rows[atomicAdd(nlong, 1)] = p;
+      continue;
+    }
     for (int64_t k = lane; k < len; k += 32) {
       new_ci[nb + k] = old_ci[ob + k];
       new_va[nb + k] = old_va[ob + k];
     }
   }
+}
+
+// the rows with more than kPermWarpMax nonzeros (listed by
+// csr_permute_kernel, in any order -- each is a plain copy): every row's
+// nonzeros spread over the whole grid instead of one warp (C2's
+// 140 000-nonzero row took 0.75 ms per CSR)
+__global__ void csr_permute_long_kernel(const int64_t* __restrict__ old_rp,
+                                        const int32_t* __restrict__ old_ci,
+                                        const double* __restrict__ old_va,
+                                        const int32_t* __restrict__ perm,
+                                        const int64_t* __restrict__ new_rp,
+                                        const int64_t* __restrict__ long_rows,
+                                        const int* __restrict__ nlong,
+                                        int32_t* __restrict__ new_ci,
+                                        double* __restrict__ new_va) {
+  const int n = *nlong;
+  for (int i = 0; i < n; ++i) {
+    const int64_t p = long_rows[i];
+    const int64_t nb = new_rp[p], len = new_rp[p + 1] - nb;
+    const int64_t ob = old_rp[perm[p]];
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < len;
+         k += (int64_t)gridDim.x * blockDim.x) {
+      new_ci[nb + k] = old_ci[ob + k];
+      new_va[nb + k] = old_va[ob + k];
+    }
+  }
+}
+
+// moves the nonzeros of A into the permuted row order (new_rp, A.perm)
+static void csr_permute(const Csr& A, const int64_t* new_rp, int32_t* nci, double* nva,
+                        cudaStream_t st) {
+  int* nlong;
+  int64_t* lrows;
+  dmalloc_t(&nlong, 1, st);
+  dmalloc_t(&lrows, A.nnz / kPermWarpMax + 2, st);
+  TSVD_CUDA(cudaMemsetAsync(nlong, 0, sizeof(int), st));
+  // one warp per row, up to 64 CTAs per SM in flight (latency-bound)
+  const unsigned pg = (unsigned)std::min<int64_t>((A.rows + 7) / 8, 148 * 64);
+  csr_permute_kernel<<<pg, 256, 0, st>>>(A.rowptr, A.colidx, A.vals, A.perm, new_rp, A.rows, nci,
+                                         nva, lrows, nlong);
+  TSVD_CHECK_LAUNCH();
+  csr_permute_long_kernel<<<148 * 2, 256, 0, st>>>(A.rowptr, A.colidx, A.vals, A.perm, new_rp,
+                                                   lrows, nlong, nci, nva);
+  TSVD_CHECK_LAUNCH();
+  dfree(lrows, st);
+  dfree(nlong, st);
 }
 
 // Row-sorted layout + load-balancing plan (called once per CSR, after the
@@ -778,10 +830,7 @@ static bool csr_build_plan_device(Csr& A, cudaStream_t st) {
     double* nva;
     dmalloc_t(&nci, A.nnz + 4, st);
     dmalloc_t(&nva, A.nnz + 2, st);
-    const unsigned pg = (unsigned)std::min<int64_t>((rows + 7) / 8, 148 * 64);
-    csr_permute_kernel<<<pg, 256, 0, st>>>(A.rowptr, A.colidx, A.vals, A.perm, new_rp, rows, nci,
-                                           nva);
-    TSVD_CHECK_LAUNCH();
+    csr_permute(A, new_rp, nci, nva, st);
     dfree(A.colidx, st);
     dfree(A.vals, st);
     A.colidx = nci;
@@ -916,11 +965,7 @@ void csr_build_plan(Csr& A, const int64_t* hrp, cudaStream_t st) {
     double* nva;
     dmalloc_t(&nci, A.nnz + 4, st);  // +padding: bulk copies read whole 16-byte pieces
     dmalloc_t(&nva, A.nnz + 2, st);
-    // one warp per row, up to 64 CTAs per SM in flight (latency-bound)
-    const unsigned pg = (unsigned)std::min<int64_t>((A.rows + 7) / 8, 148 * 64);
-    csr_permute_kernel<<<pg, 256, 0, st>>>(A.rowptr, A.colidx, A.vals, A.perm, new_rp,
-                                                A.rows, nci, nva);
-    TSVD_CHECK_LAUNCH();
+    csr_permute(A, new_rp, nci, nva, st);
     dfree(A.colidx, st);
     dfree(A.vals, st);
     A.colidx = nci;
@@ -1070,31 +1115,43 @@ void csr_transpose(const Csr& A, Csr& T, cudaStream_t st) {
   dfree(keys_out, st);
 }
 
-// one warp per row: bounds, monotone row pointer, strictly increasing
-// in-range column indices (canonical CSR, include/tsvd.h)
-__global__ void csr_validate_kernel(const int64_t* __restrict__ rowptr,
-                                    const int32_t* __restrict__ colidx, int64_t rows,
-                                    int64_t cols, int64_t nnz, int* __restrict__ bad) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < rows;
-       i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+// Canonical-CSR check (include/tsvd.h) in two element-parallel passes, so a
+// 140 000-nonzero row is not walked by one warp (that took 2.2 ms of C2's
+// handle creation): (1) one thread per row checks the row pointer (bounds,
+// monotone) and marks the first position of every nonempty row in a bitmap;
+// (2) one thread per nonzero checks its column is in range and, unless it
+// starts a row, larger than its predecessor's.  If (1) flags the row
+// pointer, (2)'s row starts are meaningless, but the handle is rejected
+// anyway.
+__global__ void csr_validate_rows_kernel(const int64_t* __restrict__ rowptr, int64_t rows,
+                                         int64_t nnz, unsigned* __restrict__ start_bits,
+                                         int* __restrict__ bad) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t b = rowptr[i], e = rowptr[i + 1];
     if (b > e || b < 0 || e > nnz) {
-      if (lane == 0) atomicOr(bad, 1);
+      atomicOr(bad, 1);
       continue;
     }
-    bool ok = true, inrange = true;
-    for (int64_t k = b + lane; k < e; k += 32) {
-      const int64_t c = colidx[k];
-      if (c < 0 || c >= cols) inrange = false;
-      else if (k > b && colidx[k - 1] >= c) ok = false;
-    }
-    if (!__all_sync(0xffffffffu, inrange) && lane == 0) atomicOr(bad, 8);
-    if (!__all_sync(0xffffffffu, ok) && lane == 0) atomicOr(bad, 2);
+    if (b < e) atomicOr(start_bits + (b >> 5), 1u << (b & 31));
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     if (rowptr[0] != 0 || rowptr[rows] != nnz) atomicOr(bad, 4);
   }
+}
+
+__global__ void csr_validate_cols_kernel(const int32_t* __restrict__ colidx, int64_t cols,
+                                         int64_t nnz, const unsigned* __restrict__ start_bits,
+                                         int* __restrict__ bad) {
+  int flags = 0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = colidx[k];
+    if (c < 0 || c >= cols) flags |= 8;
+    else if (k > 0 && !((start_bits[k >> 5] >> (k & 31)) & 1u) && colidx[k - 1] >= c) flags |= 2;
+  }
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if (flags && (threadIdx.x & 31) == 0) atomicOr(bad, flags);
 }
 
 // ---------------------------------------------------------- canonicalise --
@@ -1197,14 +1254,24 @@ void csr_canonicalize(Csr& A, cudaStream_t st) {
 
 int csr_validate_device(const Csr& A, cudaStream_t st) {
   int* d;
+  unsigned* bits;
+  const int64_t nw = A.nnz / 32 + 1;
   dmalloc_t(&d, 1, st);
+  dmalloc_t(&bits, nw, st);
   TSVD_CUDA(cudaMemsetAsync(d, 0, sizeof(int), st));
-  const unsigned vg = (unsigned)std::max<int64_t>(1, std::min<int64_t>((A.rows + 7) / 8, 148 * 64));
-  csr_validate_kernel<<<vg, 256, 0, st>>>(A.rowptr, A.colidx, A.rows, A.cols, A.nnz, d);
+  TSVD_CUDA(cudaMemsetAsync(bits, 0, sizeof(unsigned) * nw, st));
+  const unsigned rg = (unsigned)std::max<int64_t>(1, std::min<int64_t>((A.rows + 255) / 256, 148 * 16));
+  csr_validate_rows_kernel<<<rg, 256, 0, st>>>(A.rowptr, A.rows, A.nnz, bits, d);
   TSVD_CHECK_LAUNCH();
+  if (A.nnz > 0) {
+    const unsigned cg = (unsigned)std::max<int64_t>(1, std::min<int64_t>((A.nnz + 255) / 256, 148 * 16));
+    csr_validate_cols_kernel<<<cg, 256, 0, st>>>(A.colidx, A.cols, A.nnz, bits, d);
+    TSVD_CHECK_LAUNCH();
+  }
   int h = 0;
   TSVD_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, st));
   TSVD_CUDA(cudaStreamSynchronize(st));
+  dfree(bits, st);
   dfree(d, st);
   return h;
 }
