@@ -98,9 +98,11 @@ static TnGeom tn_geom(int64_t q, int s, int w) {
   return g;
 }
 
+constexpr int kTnMaxWaveSplit = 8;  // row splits of a many-s-tile product (tn_tma_go)
+
 size_t tn_part_size(int64_t q, int s) {
   const TnGeom g = tn_geom(q, s, 1);  // the most splits any width uses
-  return (size_t)(g.splits + 1) * (size_t)std::max(s, 1) * 32;
+  return (size_t)(std::max(g.splits, kTnMaxWaveSplit) + 1) * (size_t)std::max(s, 1) * 32;
 }
 
 template <int WP, int VEC>
@@ -399,6 +401,21 @@ static void tn_tma_go(const CUtensorMap& xm, const CUtensorMap& ym, int64_t q, i
   int64_t splits = (int64_t)(2 * 148) / s_tiles;
   if (splits > chunks / 4) splits = chunks / 4;
   if (splits < 1) splits = 1;
+  if (splits == 1 && s_tiles > 148) {
+    // many s-tiles (dense A^T X, s = n): 625 tiles on 296 resident CTAs ran
+    // 3 waves, the last 11 % full (0.70 of the DMMA peak at C4); a row split
+    // ks makes the last wave nearly full -- the smallest ks reaching 95 %
+    // (partials ks s w, within tn_part_size) -- summed by reduce_partials
+    constexpr int R = 2 * 148;
+    auto eff = [&](int64_t ks) {
+      const int64_t u = (int64_t)s_tiles * ks;
+      return (double)u / (double)(((u + R - 1) / R) * R);
+    };
+    for (int64_t ks = 2; ks <= kTnMaxWaveSplit && eff(splits) < 0.95; ++ks) {
+      if (chunks / ks < 16) break;
+      if (eff(ks) > eff(splits) + 0.02) splits = ks;
+    }
+  }
   static bool attr = false;
   if (!attr) {
     TSVD_CUDA(cudaFuncSetAttribute(gemm_tn_tma_kernel<ST, NYB>,
@@ -1412,11 +1429,13 @@ struct NnOutCfg {
 // reads those rows, so Z may overwrite X's first w columns -- the outputs
 // and the thick-restart panels of C5, which have no room for separate
 // m x r / n x r buffers, without a scratch round trip.
-template <int KC, int S, int NT>
-__global__ void __launch_bounds__(288, 1) gemm_nn_out_tma_kernel(
-    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap, double* Z,
-    int64_t ldz, int64_t q, int s, int w, double alpha, int64_t zsplit) {
-  pdl_enter();
+// FOLD (the 13 / 16-tile kernels): the producer is lane 0 of consumer warp 0
+// (8 warps, up to 255 registers) instead of a 9th warp (168-register cap:
+// 36 / 104 bytes of spills), as in nn_tma_body.
+template <int KC, int S, int NT, bool FOLD>
+__device__ __forceinline__ void nn_out_body(const CUtensorMap& xmap, const CUtensorMap& hmap,
+                                            double* Z, int64_t ldz, int64_t q, int s, int w,
+                                            double alpha, int64_t zsplit) {
   constexpr int NH = (NT + 1) / 2;
   using CF = NnOutCfg<KC, S, NH>;  // split-K over blockIdx.y as in gemm_nn_tma_kernel
   extern __shared__ unsigned char smraw[];
@@ -1442,32 +1461,38 @@ __global__ void __launch_bounds__(288, 1) gemm_nn_out_tma_kernel(
   const int nk = (int)((int64_t)nk_all * (blockIdx.y + 1) / gridDim.y) - kb;
   const int64_t nsteps = my_tiles * nk;
   Z += (int64_t)blockIdx.y * zsplit;
-  if (warp == 8) {
-    if (lane == 0) {
-      // ring slot / phase and (tile, k-chunk) kept as running counters: no
-      // 64-bit divisions by S and by the runtime nk per step
-      int st = 0, kc = 0;
-      unsigned u = 0;
-      int64_t lt = 0;
-      for (int64_t j = 0; j < nsteps; ++j) {
-        if (j > 0) {
-          if (++st == S) st = 0, ++u;
-          if (++kc == nk) kc = 0, ++lt;
-        }
-        if (j >= S) mbar_wait(&empty[st], (u - 1) & 1);
-        const int r0 = (int)((blockIdx.x + lt * gridDim.x) * NT_R);
-        unsigned char* base = sm + (size_t)st * CF::stage;
-        mbar_expect_tx(&full[st], CF::tx);
-#pragma unroll
-        for (int b = 0; b < CF::NB; ++b)
-          tma_load_2d(base + b * CF::xbox, &xmap, (kb + kc) * KC + b * 16, r0, &full[st]);
-#pragma unroll
-        for (int b = 0; b < NH; ++b)
-          tma_load_2d(base + CF::NB * CF::xbox + b * CF::hbox, &hmap, b * 16, (kb + kc) * KC,
-                      &full[st]);
-      }
+  // producer: ring slot / phase and (tile, k-chunk) kept as running
+  // counters (no 64-bit divisions by S and by the runtime nk per step)
+  int pst = 0, pkc = 0;
+  unsigned pu = 0;
+  int64_t plt = 0, pj = 0;
+  auto produce = [&]() {  // issue step pj
+    if (pj > 0) {
+      if (++pst == S) pst = 0, ++pu;
+      if (++pkc == nk) pkc = 0, ++plt;
     }
-    return;
+    if (pj >= S) mbar_wait(&empty[pst], (pu - 1) & 1);
+    const int r0 = (int)((blockIdx.x + plt * gridDim.x) * NT_R);
+    unsigned char* base = sm + (size_t)pst * CF::stage;
+    mbar_expect_tx(&full[pst], CF::tx);
+#pragma unroll
+    for (int b = 0; b < CF::NB; ++b)
+      tma_load_2d(base + b * CF::xbox, &xmap, (kb + pkc) * KC + b * 16, r0, &full[pst]);
+#pragma unroll
+    for (int b = 0; b < NH; ++b)
+      tma_load_2d(base + CF::NB * CF::xbox + b * CF::hbox, &hmap, b * 16, (kb + pkc) * KC,
+                  &full[pst]);
+    ++pj;
+  };
+  if constexpr (!FOLD) {
+    if (warp == 8) {
+      if (lane == 0)
+        while (pj < nsteps) produce();
+      return;
+    }
+  } else {
+    if (warp == 0 && lane == 0)
+      while (pj < nsteps && pj < S - 1) produce();
   }
   const bool vec = ((ldz & 1) == 0) && ((((uintptr_t)Z) & 15) == 0);
   double acc[2][NT][2];
@@ -1475,6 +1500,9 @@ __global__ void __launch_bounds__(288, 1) gemm_nn_out_tma_kernel(
   unsigned u = 0;
   int64_t lt = 0;
   for (int64_t j = 0; j < nsteps; ++j) {
+    if constexpr (FOLD) {
+      if (warp == 0 && lane == 0 && pj < nsteps) produce();  // step j + S - 1
+    }
     if (j > 0) {  // running counters, as in the producer
       if (++st == S) st = 0, ++u;
       if (++kc == nk) kc = 0, ++lt;
@@ -1535,6 +1563,21 @@ __global__ void __launch_bounds__(288, 1) gemm_nn_out_tma_kernel(
       }
     }
   }
+}
+
+template <int KC, int S, int NT>
+__global__ void __launch_bounds__(288, 1) gemm_nn_out_tma_kernel(
+    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap, double* Z,
+    int64_t ldz, int64_t q, int s, int w, double alpha, int64_t zsplit) {
+  pdl_enter();
+  nn_out_body<KC, S, NT, false>(xmap, hmap, Z, ldz, q, s, w, alpha, zsplit);
+}
+template <int KC, int S, int NT>
+__global__ void __launch_bounds__(256, 1) gemm_nn_out_tma_kernel_fold(
+    const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap hmap, double* Z,
+    int64_t ldz, int64_t q, int s, int w, double alpha, int64_t zsplit) {
+  pdl_enter();
+  nn_out_body<KC, S, NT, true>(xmap, hmap, Z, ldz, q, s, w, alpha, zsplit);
 }
 
 constexpr int NNT_KC = 32, NNT_S = 2;
@@ -1671,19 +1714,19 @@ static bool nn_out_wide_launch(const double* X, int64_t ldx, const double* H, in
   using CF = NnOutCfg<NNT_KC, WS, 8>;
   static bool attr = false;
   if (!attr) {
-    TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_out_tma_kernel<NNT_KC, WS, 13>,
+    TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_out_tma_kernel_fold<NNT_KC, WS, 13>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
-    TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_out_tma_kernel<NNT_KC, WS, 16>,
+    TSVD_CUDA(cudaFuncSetAttribute(gemm_nn_out_tma_kernel_fold<NNT_KC, WS, 16>,
                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::bytes));
     attr = true;
   }
   const int nt = (w + 7) / 8;
   const int ctas = nn_ctas(q, 32);
   if (nt <= 13)
-    launch_pdl(gemm_nn_out_tma_kernel<NNT_KC, WS, 13>, ctas, 288, CF::bytes, st, xm, hm, Z, ldz,
+    launch_pdl(gemm_nn_out_tma_kernel_fold<NNT_KC, WS, 13>, ctas, 256, CF::bytes, st, xm, hm, Z, ldz,
                q, s, w, alpha, (int64_t)0);
   else
-    launch_pdl(gemm_nn_out_tma_kernel<NNT_KC, WS, 16>, ctas, 288, CF::bytes, st, xm, hm, Z, ldz,
+    launch_pdl(gemm_nn_out_tma_kernel_fold<NNT_KC, WS, 16>, ctas, 256, CF::bytes, st, xm, hm, Z, ldz,
                q, s, w, alpha, (int64_t)0);
   TSVD_CHECK_LAUNCH();
   return true;
