@@ -390,6 +390,24 @@ def residual_check(h, U=None, V=None):
 
 
 # ------------------------------------------------------------------- main --
+def same_workload_n1(cfg_name, world):
+    """At N > 1 the default workload is C5 while the N = 1 default (the BENCH
+    line) is C2; the one-GPU time of the SAME workload, from the committed
+    profile written by `bench.py --config C5` (builder-measured, not this
+    run), so a scaling series can be read against it."""
+    if world <= 1:
+        return None
+    f = os.path.join(ROOT, "profiles", "r02s", f"bench_{cfg_name}_fixed_work.json")
+    if not os.path.exists(f):
+        return None
+    try:
+        d = json.load(open(f))
+        return {"value": d["value"], "unit": d["unit"], "source": os.path.relpath(f, ROOT),
+                "note": "one B200, measured by the builder with bench.py --config " + cfg_name}
+    except Exception:
+        return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -779,6 +797,7 @@ def main():
                         "solves record only the dominant phase" if prof is full_prof else
                         "the timed solves, every phase recorded"),
         "cpu_baseline": cpu,
+        "same_workload_n1": same_workload_n1(cfg_name, world),
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk,
