@@ -15,6 +15,7 @@
 // reduced in a fixed order by a separate kernel; no floating-point atomics.
 #include <cuda.h>
 
+#include <climits>
 #include <cstdlib>
 
 #include "internal.h"
@@ -436,9 +437,20 @@ static bool tn_tma_launch(const double* X, int64_t ldx, const double* Y, int64_t
     else tn_tma_go<32, 2>(xm, ym, q, s, w, C, ldc, part, st);
     return true;
   }
-  if (s <= 16) tn_tma_go<16, 1>(xm, ym, q, s, w, C, ldc, part, st);
-  else if (s <= 32) tn_tma_go<32, 1>(xm, ym, q, s, w, C, ldc, part, st);
-  else if (s <= 48) tn_tma_go<48, 1>(xm, ym, q, s, w, C, ldc, part, st);
+  // s-tile width: every s-tile gets the same rows, so a pass takes as long as
+  // its widest tile; ST minimises s_tiles x (ST + w) -- each tile streams its
+  // ST columns of X and all w of Y -- preferring the wider tile on ties (s =
+  // 80: 48 + 32 instead of 64 + 16, which left half the CTAs idle for 60 %
+  // of the pass)
+  int best = 16;
+  int64_t cost = INT64_MAX;
+  for (int stv : {64, 48, 32, 16}) {
+    const int64_t c = (int64_t)((s + stv - 1) / stv) * (stv + w);
+    if (c < cost) cost = c, best = stv;
+  }
+  if (best == 16) tn_tma_go<16, 1>(xm, ym, q, s, w, C, ldc, part, st);
+  else if (best == 32) tn_tma_go<32, 1>(xm, ym, q, s, w, C, ldc, part, st);
+  else if (best == 48) tn_tma_go<48, 1>(xm, ym, q, s, w, C, ldc, part, st);
   else tn_tma_go<64, 1>(xm, ym, q, s, w, C, ldc, part, st);
   return true;
 }
