@@ -76,6 +76,9 @@ static void destroy_ctx(tsvd_ctx* c) {
   for (auto e : c->comm_ev) cudaEventDestroy(e);
   if (c->comm_st) cudaStreamDestroy(c->comm_st);
   if (c->copy_st) cudaStreamDestroy(c->copy_st);
+  if (c->svd_st) cudaStreamDestroy(c->svd_st);
+  if (c->svd_fork) cudaEventDestroy(c->svd_fork);
+  if (c->svd_join) cudaEventDestroy(c->svd_join);
   if (c->copy_ev) cudaEventDestroy(c->copy_ev);
   dfree(c->Ad, c->st);
   free_bufs(*c);

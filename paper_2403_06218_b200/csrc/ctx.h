@@ -59,6 +59,9 @@ struct tsvd_ctx {
   // engines on the PCIe link instead of one)
   cudaStream_t copy_st = nullptr;
   cudaEvent_t copy_ev = nullptr;
+  // the Jacobi SVD of B_k beside the last m-side orthogonalisation (solvers.cu)
+  cudaStream_t svd_st = nullptr;
+  cudaEvent_t svd_fork = nullptr, svd_join = nullptr;
   std::vector<cudaEvent_t> comm_ev;
   double* Ad = nullptr;      // dense A, row-major m x n
   int64_t lda = 0;

@@ -220,8 +220,11 @@ size_t small_svd_work(int d);
 // skip V, Vbar[:, :nv] = B^T Ubar[:, :nv] / sigma afterwards; the device word
 // small_svd_top_ok_dev is 0 when sigma_nv < 1e-3 sigma_1 (then rerun
 // small_svd).  part: gemm_tn workspace of tn_part_size(d, d) doubles.
+// hog_smem > 0: the Jacobi CTAs request that many bytes of (unused) dynamic
+// shared memory, so no streaming-pass CTA shares their SMs while the SVD
+// runs beside other work (solvers.cu).
 void small_svd_top(const double* B, int d, int nv, double* Ub, double* S, double* Vb,
-                   double* work, double* part, cudaStream_t st);
+                   double* work, double* part, cudaStream_t st, int hog_smem = 0);
 const unsigned* small_svd_top_ok_dev(const double* work, int d);
 int small_svd_sweeps(const double* work, int d);  // sweeps of the last small_svd (syncs)
 // device word holding the sweep count of the last small_svd (read together

@@ -698,7 +698,7 @@ int g_jacobi_opt = getenv("TSVD_JACOBI_ACQREL") ? atoi(getenv("TSVD_JACOBI_ACQRE
 
 template <int JCV, bool WV = true>
 static bool reg_launch(const double* B, int d, double* Ub, double* S, double* Vb, double* work,
-                       unsigned* ctl, cudaStream_t st) {
+                       unsigned* ctl, cudaStream_t st, int hog_smem = 0) {
   int nbr = (d + JCV - 1) / JCV;
   if (nbr < 2) nbr = 2;
   if (nbr & 1) ++nbr;
@@ -744,7 +744,17 @@ static bool reg_launch(const double* B, int d, double* Ub, double* S, double* Vb
   int nblocks = nbr / 2, nbv = nbr;
   int opt = g_jacobi_opt;
   void* args[] = {&G, &V, &d, &nbv, &nrm, &Ub, &S, &Vb, &ctl, &flags, &opt};
-  TSVD_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(nth), args, 0, st));
+  if (hog_smem > 0) {
+    // one attribute per instantiation (fn), set the first time it is hogged
+    static void* hogged[64];
+    static int nhog = 0;
+    if (std::find(hogged, hogged + nhog, fn) == hogged + nhog) {
+      TSVD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, hog_smem));
+      if (nhog < 64) hogged[nhog++] = fn;
+    }
+  }
+  TSVD_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(nth), args,
+                                        (size_t)std::max(0, hog_smem), st));
   TSVD_CHECK_LAUNCH();
   return true;
 }
@@ -790,13 +800,13 @@ const unsigned* small_svd_top_ok_dev(const double* work, int d) {
 }
 
 void small_svd_top(const double* B, int d, int nv, double* Ub, double* S, double* Vb,
-                   double* work, double* part, cudaStream_t st) {
+                   double* work, double* part, cudaStream_t st, int hog_smem) {
   if (d > kJacobiMaxD) throw Error{TSVD_ESHAPE, "small_svd: d > 1536"};
   unsigned* ctl = jac_ctl(work, d);
   bool ok = false;
   if (g_jacobi_cyc) {
-    if (g_jacobi_jc == 4) ok = reg_launch<4, false>(B, d, Ub, S, Vb, work, ctl, st);
-    else if (g_jacobi_jc == 8) ok = reg_launch<8, false>(B, d, Ub, S, Vb, work, ctl, st);
+    if (g_jacobi_jc == 4) ok = reg_launch<4, false>(B, d, Ub, S, Vb, work, ctl, st, hog_smem);
+    else if (g_jacobi_jc == 8) ok = reg_launch<8, false>(B, d, Ub, S, Vb, work, ctl, st, hog_smem);
   }
   if (!ok) {
     small_svd(B, d, Ub, S, Vb, work, st);  // no top-only path for this configuration

@@ -16,6 +16,10 @@
 
 namespace tsvd {
 
+bool g_svd_overlap = getenv("TSVD_SVD_OVERLAP") ? atoi(getenv("TSVD_SVD_OVERLAP")) != 0 : true;
+constexpr int kSvdHogSmem = 160 * 1024;
+constexpr int kSvdOverlapRows = 4000;
+
 static void upload_start(Ctx& c, double* dst, int64_t rows, int cols, int64_t ld) {
   TSVD_CUDA(cudaMemcpy2DAsync(dst, ld * sizeof(double), c.start.data(), cols * sizeof(double),
                               cols * sizeof(double), rows, cudaMemcpyHostToDevice, c.st));
@@ -172,6 +176,9 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   double* Vb = dbuf(c, "Vb", (size_t)d * d);
   double* Sg = dbuf(c, "Sg", (size_t)d);
   double* jw = dbuf(c, "jacobi_work", small_svd_work(d));
+  // the SVD's own TN scratch: with the overlap below it runs beside the last
+  // m-side orthogonalisation, which uses part_tn
+  double* part_svd = dbuf(c, "part_svd", tn_part_size(d, d));
   (void)dbuf(c, "H", (size_t)d * 32);
   const size_t rb = (size_t)std::max(32, b);
   double* R = dbuf(c, "R", rb * rb);
@@ -292,9 +299,61 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
     } else if (graph_ok) {
       ++cg.seen;
     }
+    // B_k is complete once the n side of the last block step has written
+    // L_k (the m side only adds Rbar_k, which goes to Rb for rho, not into
+    // B), so on one GPU the Jacobi SVD of B_k -- latency-bound on a few
+    // dozen SMs -- runs on a side stream beside that last m-side product and
+    // orthogonalisation (TSVD_SVD_OVERLAP=0: after them).  A breakdown replay
+    // rewrites B, so it waits for the early SVD and the SVD runs again.
+    const int nv = std::min(d, std::max(r, keep));
+    bool svd_early = false;
+    auto fork_svd = [&]() {
+      if (!c.svd_st) {
+        TSVD_CUDA(cudaStreamCreateWithFlags(&c.svd_st, cudaStreamNonBlocking));
+        TSVD_CUDA(cudaEventCreateWithFlags(&c.svd_fork, cudaEventDisableTiming));
+        TSVD_CUDA(cudaEventCreateWithFlags(&c.svd_join, cudaEventDisableTiming));
+      }
+      TSVD_CUDA(cudaEventRecord(c.svd_fork, c.st));
+      TSVD_CUDA(cudaStreamWaitEvent(c.svd_st, c.svd_fork, 0));
+      cudaStream_t main_st = c.st;
+      c.st = c.svd_st;  // the phase events of this SVD go on its stream
+      try {
+        Prof p(c, P_SVD, 16.0 * d * d, 0);
+        small_svd_top(B, d, nv, Ub, Sg, Vb, jw, part_svd, c.svd_st, kSvdHogSmem);
+      } catch (...) {
+        c.st = main_st;
+        throw;
+      }
+      c.st = main_st;
+      TSVD_CUDA(cudaEventRecord(c.svd_join, c.svd_st));
+      svd_early = true;
+    };
+    // only where the SVD outlasts that m-side step: the streaming passes then
+    // run on the SMs the Jacobi leaves free (its CTAs reserve shared memory,
+    // kSvdHogSmem, so no pass CTA shares an SM with them: sharing slowed the
+    // latency-bound Jacobi 1.3-2.5x).  m < kSvdOverlapRows d: C2 (m/d = 2604)
+    // and the dense C4 (57) overlap, C3 (6250) and C5 do not -- there the
+    // m-side orthogonalisation on the remaining SMs would outlast the SVD.
+    const bool overlap_ok = g_svd_overlap && !c.comm && !graph_ran &&
+                            (c.dense || m < (int64_t)kSvdOverlapRows * d);
     for (int pass = 0; pass < 2; ++pass) {
       for (int i = (pass == 0 && graph_ran) ? kc : from_slot / 2; i < kc; ++i) {
-        block_step(i, !(i == from_slot / 2 && (from_slot & 1)));
+        const bool n_part = !(i == from_slot / 2 && (from_slot & 1));
+        if (pass == 0 && overlap_ok && i == kc - 1 && n_part) {
+          const int lo = s0 + i * b;
+          apply(c, true, Pb + lo, ldb, P + lo, ldp, b);
+          n_side();
+          c.flag_slot = 2 * i;
+          block_orth(c, P, n, lo, b, ldp, R);
+          copy_block(R, b, B + (int64_t)lo * d + lo, d, b, b, true, c.st);
+          fork_svd();
+          block_step(i, false);
+        } else {
+          block_step(i, n_part);
+        }
+      }
+      if (svd_early) {  // joined before anything else reads or rewrites B, Ub, Sg, Vb
+        TSVD_CUDA(cudaStreamWaitEvent(c.st, c.svd_join, 0));
       }
       if (!c.deferred) break;
       TSVD_CUDA(cudaMemcpyAsync(hlog.data(), flog, sizeof(int) * 4 * (size_t)k,
@@ -307,20 +366,20 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
         if (hlog[2 * sl] || hlog[2 * sl + 1]) bad = sl;
       if (bad < 0) break;
       from_slot = bad;
+      svd_early = false;  // the replay changes B: the SVD runs again below
     }
     c.deferred = false;
     // B_k = Ub S Vb^T.  Only Vbar[:, :max(r, l)] is ever read (rho, outputs,
     // thick restart), so the sweeps skip V and those columns are formed as
     // B^T ubar_i / sigma_i (small_svd_top); if sigma_max(r,l) < 1e-3 sigma_1 the
     // full Jacobi with rotated V runs instead (host-checked with rho below).
-    const int nv = std::min(d, std::max(r, keep));
     for (int full = 0; full < 2; ++full) {
-      {
+      if (!(full == 0 && svd_early)) {
         Prof p(c, P_SVD, 16.0 * d * d, 0);
         if (full)
           small_svd(B, d, Ub, Sg, Vb, jw, c.st);
         else
-          small_svd_top(B, d, nv, Ub, Sg, Vb, jw, dbuf(c, "part_tn", 8), c.st);
+          small_svd_top(B, d, nv, Ub, Sg, Vb, jw, part_svd, c.st);
       }
       {
         Prof p(c, P_OTHER, 0, 0);
