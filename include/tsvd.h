@@ -281,7 +281,11 @@ tsvd_status tsvd_get_rho(tsvd_t h, double* rho);
  * of Alg. 4/5), 3 ortho_nn (gemm_nn passes of Alg. 4/5 against the basis),
  * 4 ortho_small (b x b Cholesky / reductions), 5 small_svd, 6 restart_out
  * (restart product, outputs, sign), 7 other, 8 ortho_rowT (the basis-free
- * passes: Gram of Y and the TRSM-as-multiply S L^{-T}).  bytes/flops are
+ * passes: Gram of Y and the TRSM-as-multiply S L^{-T}), 9 beside_svd (the
+ * last block step's m-side product and orthogonalisation when they run
+ * beside the Jacobi SVD of B_k on the SMs it leaves free -- kept apart so
+ * the other phases measure kernels that have the GPU to themselves).
+ * bytes/flops are
  * ALGORITHMIC (compulsory) counts per DESIGN.md "Roofline", not measured
  * traffic.  Aggregates accumulate over solves until reset. */
 typedef struct {
@@ -292,7 +296,7 @@ typedef struct {
   double bytes;       /* summed algorithmic bytes */
   double flops;       /* summed algorithmic flops */
 } tsvd_prof_entry;
-enum { TSVD_NPROF = 9 };
+enum { TSVD_NPROF = 10 };
 tsvd_status tsvd_set_profiling(tsvd_t h, int on);
 /* Record only the phases whose bit (1 << phase index above) is set in
  * `mask` (0 = off; tsvd_set_profiling(h, 1) = all phases).  Each recorded

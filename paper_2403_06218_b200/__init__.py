@@ -61,11 +61,11 @@ class TsvdProfEntry(C.Structure):
                 ("ms", C.c_double), ("bytes", C.c_double), ("flops", C.c_double)]
 
 
-NPROF = 9
+NPROF = 10
 # phase index order of tsvd_get_profile (include/tsvd.h): bit i of
 # tsvd_set_profiling_mask records phase i
 PROF_PHASES = ("apply_A", "apply_AT", "ortho_tn", "ortho_nn", "ortho_small", "small_svd",
-               "restart_out", "other", "ortho_rowT")
+               "restart_out", "other", "ortho_rowT", "beside_svd")
 
 
 class TsvdError(RuntimeError):

@@ -127,7 +127,8 @@ void free_bufs(Ctx& c) {
 
 static const char* kProfNames[TSVD_NPROF] = {"apply_A",     "apply_AT",  "ortho_tn",
                                              "ortho_nn",    "ortho_small", "small_svd",
-                                             "restart_out", "other",     "ortho_rowT"};
+                                             "restart_out", "other",     "ortho_rowT",
+                                             "beside_svd"};
 
 static cudaEvent_t pool_get(Ctx& c) {
   if (!c.ev_pool.empty()) {
@@ -148,7 +149,7 @@ static cudaError_t record(Ctx& c, cudaEvent_t e) {
 }
 
 Prof::Prof(Ctx& c_, int cat_, double bytes_, double flops_)
-    : c(c_), cat(cat_), bytes(bytes_), flops(flops_) {
+    : c(c_), cat(c_.prof_override >= 0 ? c_.prof_override : cat_), bytes(bytes_), flops(flops_) {
   if (!c.prof_on || !((c.prof_mask >> cat) & 1u)) return;
   a = pool_get(c);
   TSVD_CUDA(record(c, a));

@@ -12,7 +12,8 @@ namespace tsvd {
 struct LoopGroup;
 constexpr int kLoopMaxWorld = 8;
 // P_ROWT: the s = 0 passes (Gram of Y, TRSM-as-multiply S T) - rowT_kernel
-enum ProfCat { P_APPLY_A = 0, P_APPLY_AT, P_TN, P_NN, P_SMALL, P_SVD, P_RESTART, P_OTHER, P_ROWT };
+enum ProfCat { P_APPLY_A = 0, P_APPLY_AT, P_TN, P_NN, P_SMALL, P_SVD, P_RESTART, P_OTHER, P_ROWT,
+               P_BESIDE_SVD };
 struct ProfRec {
   int cat;
   cudaEvent_t a, b;
@@ -99,6 +100,7 @@ struct tsvd_ctx {
   // instrumentation (tsvd_set_profiling)
   bool prof_on = false;
   unsigned prof_mask = 0;                 // phases recorded (bit = phase index)
+  int prof_override = -1;                 // >= 0: every phase call counts as this one
   std::vector<tsvd::ProfRec> prof_open;   // recorded, not yet harvested
   std::vector<cudaEvent_t> ev_pool;
   tsvd_prof_entry prof[TSVD_NPROF]{};

@@ -347,7 +347,14 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
           block_orth(c, P, n, lo, b, ldp, R);
           copy_block(R, b, B + (int64_t)lo * d + lo, d, b, b, true, c.st);
           fork_svd();
-          block_step(i, false);
+          c.prof_override = P_BESIDE_SVD;
+          try {
+            block_step(i, false);
+          } catch (...) {
+            c.prof_override = -1;
+            throw;
+          }
+          c.prof_override = -1;
         } else {
           block_step(i, n_part);
         }
