@@ -744,15 +744,8 @@ static bool reg_launch(const double* B, int d, double* Ub, double* S, double* Vb
   int nblocks = nbr / 2, nbv = nbr;
   int opt = g_jacobi_opt;
   void* args[] = {&G, &V, &d, &nbv, &nrm, &Ub, &S, &Vb, &ctl, &flags, &opt};
-  if (hog_smem > 0) {
-    // one attribute per instantiation (fn), set the first time it is hogged
-    static void* hogged[64];
-    static int nhog = 0;
-    if (std::find(hogged, hogged + nhog, fn) == hogged + nhog) {
-      TSVD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, hog_smem));
-      if (nhog < 64) hogged[nhog++] = fn;
-    }
-  }
+  if (hog_smem > 0)  // idempotent host call, no shared state between handles / threads
+    TSVD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, hog_smem));
   TSVD_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(nth), args,
                                         (size_t)std::max(0, hog_smem), st));
   TSVD_CHECK_LAUNCH();
