@@ -69,6 +69,11 @@ static tsvd_status init_ctx(tsvd_ctx* c) {
 
 static void destroy_ctx(tsvd_ctx* c) {
   if (!c) return;
+  // side streams first: after an error inside a solve the forked SVD or a
+  // reduction may still be running on buffers freed below
+  if (c->svd_st) cudaStreamSynchronize(c->svd_st);
+  if (c->comm_st) cudaStreamSynchronize(c->comm_st);
+  if (c->copy_st) cudaStreamSynchronize(c->copy_st);
   if (c->st) cudaStreamSynchronize(c->st);
   csr_free(c->A, c->st);
   csr_free(c->AT, c->st);

@@ -175,6 +175,9 @@ tsvd_status lanczos_solve(Ctx& c, int r, int b, double tol, int maxit) {
   double* Ub = dbuf(c, "Ub", (size_t)d * d);
   double* Vb = dbuf(c, "Vb", (size_t)d * d);
   double* Sg = dbuf(c, "Sg", (size_t)d);
+  // a previous solve that ended in an error may have left its forked SVD
+  // running on buffers this one reuses (normally the side stream is idle)
+  if (c.svd_st) TSVD_CUDA(cudaStreamSynchronize(c.svd_st));
   double* jw = dbuf(c, "jacobi_work", small_svd_work(d));
   // the SVD's own TN scratch: with the overlap below it runs beside the last
   // m-side orthogonalisation, which uses part_tn
