@@ -744,8 +744,20 @@ static bool reg_launch(const double* B, int d, double* Ub, double* S, double* Vb
   int nblocks = nbr / 2, nbv = nbr;
   int opt = g_jacobi_opt;
   void* args[] = {&G, &V, &d, &nbv, &nrm, &Ub, &S, &Vb, &ctl, &flags, &opt};
-  if (hog_smem > 0)  // idempotent host call, no shared state between handles / threads
-    TSVD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, hog_smem));
+  if (hog_smem > 0) {
+    // never more than the device grants a block beside the kernel's static
+    // shared memory (B200: 227 KB); the reservation is only a placement hint
+    int dev = 0, optin = 0;
+    cudaFuncAttributes fa{};
+    TSVD_CUDA(cudaGetDevice(&dev));
+    TSVD_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    TSVD_CUDA(cudaFuncGetAttributes(&fa, fn));
+    hog_smem = std::min(hog_smem, optin - (int)fa.sharedSizeBytes - 1024);
+    if (hog_smem > 0)  // idempotent host call, no shared state between handles / threads
+      TSVD_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, hog_smem));
+    else
+      hog_smem = 0;
+  }
   TSVD_CUDA(cudaLaunchCooperativeKernel(fn, dim3(nblocks), dim3(nth), args,
                                         (size_t)std::max(0, hog_smem), st));
   TSVD_CHECK_LAUNCH();
