@@ -510,7 +510,9 @@ tsvd_status tsvd_get(tsvd_t h, double* U, int64_t ldu, double* S, double* V, int
   // to the host with both U and V wanted: V on a second stream (after the
   // solve's work on h->st), so the two copies use two copy engines
   cudaStream_t vst = h->st;
-  if (U && V && k == cudaMemcpyDeviceToHost) {
+  static const bool two_streams =
+      getenv("TSVD_GET_2STREAM") ? atoi(getenv("TSVD_GET_2STREAM")) != 0 : true;
+  if (two_streams && U && V && k == cudaMemcpyDeviceToHost) {
     if (!h->copy_st) {
       TSVD_CUDA(cudaStreamCreateWithFlags(&h->copy_st, cudaStreamNonBlocking));
       TSVD_CUDA(cudaEventCreateWithFlags(&h->copy_ev, cudaEventDisableTiming));
