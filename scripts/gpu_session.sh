@@ -1,7 +1,5 @@
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
-timeout 2400 python -m pytest tests -m gpu -x -q -p no:cacheprovider --timeout 900 > $O/s31_pytest.log 2>&1
-echo "pytest rc $?" >> $O/s31_pytest.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/s31_smoke.log 2>&1
-timeout 900 python bench.py > $O/s31_bench_default.json 2> $O/s31_bench_default.err
+timeout 900 python -m pytest tests/test_gpu_solvers.py -x -q -p no:cacheprovider > $O/s33_pytest.log 2>&1
+echo "pytest rc $?" >> $O/s33_pytest.log
 echo done

@@ -108,6 +108,11 @@ def test_lanczos_restarts_parity():
 
 
 def test_rank_deficient_breakdown():
+    """A breakdown in the deferred pass replays the cycle from the flagged
+    block step; the Jacobi SVD already forked beside the last m-side step
+    (solvers.cu; dense A takes that path) must be joined before the replay
+    rewrites B, and rerun.  (Exactly-zero pivots need the dense path's
+    arithmetic: the same matrix in CSR ends with tiny positive pivots.)"""
     rng = np.random.default_rng(6)
     m, n, k = 80, 40, 5
     X, _ = np.linalg.qr(rng.standard_normal((m, k)))
