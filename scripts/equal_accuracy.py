@@ -55,6 +55,28 @@ def main():
         t_r, e_r = rsvd_run(cfg["rsvd_q"])
         print(json.dumps({"config": name, "method": "rsvd", "q": cfg["rsvd_q"], "l": r + p,
                           "tts_s": round(t_r, 4), "e_max": e_r}), flush=True)
+        if os.environ.get("EQ_DSWEEP"):
+            # smaller Krylov dimensions at the crude tolerance: LancSVD's
+            # minimum work is one cycle of d, so the equal-accuracy time
+            # depends on d; thick restart (keep = r rounded up to b) so a
+            # small d can still hold the r wanted Ritz pairs across cycles
+            keep = -(-r // b) * b
+            for dd in (keep + b, keep + 2 * b, keep + 4 * b, 2 * keep, d):
+                for kp in (0, keep):
+                    if kp and kp >= dd:
+                        continue
+                    h.set_thick_restart(kp)
+                    t_l = timed(h, lambda: h.block_lanczos(r, b, max(e_r, 1e-12), 40, d=dd))
+                    e, _ = h.residuals()
+                    inf = h.info()
+                    print(json.dumps({"config": name, "method": "lanczos", "tol": e_r,
+                                      "what": "equal accuracy, d sweep", "d": dd, "keep": kp,
+                                      "b": b, "tts_s": round(t_l, 4), "e_max": float(e.max()),
+                                      "cycles": inf["cycles"], "nconv": inf["nconv"]}),
+                          flush=True)
+            h.set_thick_restart(0)
+            h.close()
+            continue
         for tol, label in ((max(e_r, 1e-12), "equal accuracy (tol = rSVD e_max)"),
                            (1e-8, "north_star tol 1e-8")):
             t_l = timed(h, lambda: h.block_lanczos(r, b, tol, 12, d=d))

@@ -1,5 +1,4 @@
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
-timeout 900 python -m pytest tests/test_gpu_solvers.py -x -q -p no:cacheprovider > $O/s33_pytest.log 2>&1
-echo "pytest rc $?" >> $O/s33_pytest.log
+EQ_DSWEEP=1 timeout 1500 python scripts/equal_accuracy.py C3 C4 > $O/s34_dsweep.jsonl 2> $O/s34_dsweep.err
 echo done
