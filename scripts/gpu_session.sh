@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
-EQ_DSWEEP=1 timeout 1500 python scripts/equal_accuracy.py C3 C4 > $O/s34_dsweep.jsonl 2> $O/s34_dsweep.err
+timeout 1800 python scripts/fig4_dense.py > $O/s35_fig4.jsonl 2> $O/s35_fig4.err
 echo done
