@@ -1,9 +1,9 @@
 cd $GRAFT_REPO_ROOT
 O=gpurun_out
-for DK in "704 0" "448 224" "512 224" "576 256"; do
-set -- $DK
-timeout 900 python bench.py --config C4 --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 0 --d $1 --keep $2 --maxit 20 > $O/s38_c4_d$1_k$2.json 2> $O/s38_c4_d$1_k$2.err
-python -c "
-import json; d=json.load(open('$O/s38_c4_d$1_k$2.json')); print('d=$1 keep=$2', d['value'], d['solver']['cycles'], d['solver']['nconv'], d['accuracy']['e_max'], d['clocks']['sm_mhz'])" >> $O/s38_sweep.log
+for OR in cgs_cqr2 bcgs_pip2; do
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 0 --ortho $OR > $O/s39_c2_$OR.json 2> $O/s39_c2_$OR.err
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 0 --ortho $OR --d 256 --keep 128 --maxit 12 > $O/s39_c2_thick_$OR.json 2> $O/s39_c2_thick_$OR.err
 done
+for f in $O/s39_*.json; do python -c "
+import json; d=json.load(open('$f')); print('$f', d['value'], d['solver']['cycles'], d['solver']['nconv'], d['solver']['breakdowns'], d['accuracy']['e_max'], d['clocks']['sm_mhz'])" >> $O/s39.log; done
 echo done
