@@ -568,3 +568,24 @@ def test_wide_block_lanczos_parity(b, d, r):
     _accept(op, Ug, Sg, Vg, ro.S, conv_mask=conv)
     assert np.abs(Sg - s[:r])[conv].max() / s[0] <= 1e-10
     _vec_parity(Ug[:, conv], Vg[:, conv], ro.U[:, conv], ro.V[:, conv], ro.S[conv])
+
+
+def test_profiling_mask_and_beside_svd_phase():
+    """tsvd_set_profiling_mask records only the selected phases; on one GPU
+    the last m-side block step runs beside the Jacobi SVD (solvers.cu) and is
+    profiled as its own phase, so ortho_nn / ortho_tn time only kernels that
+    have the GPU to themselves."""
+    A, _ = _c1()
+    with T.TruncatedSVD(A) as h:
+        h.set_seed(3)
+        h.set_profiling(True)
+        h.block_lanczos(r=10, b=4, tol=1e-12, maxit=8, d=28)
+        full = h.profile()
+        h.reset_profile()
+        h.set_profiling_mask(1 << T.PROF_PHASES.index("ortho_nn"))
+        h.block_lanczos(r=10, b=4, tol=1e-12, maxit=8, d=28)
+        only_nn = h.profile()
+        h.set_profiling(False)
+    assert full["beside_svd"]["calls"] > 0 and full["small_svd"]["calls"] > 0
+    assert only_nn["ortho_nn"]["calls"] == full["ortho_nn"]["calls"]
+    assert all(v["calls"] == 0 for k, v in only_nn.items() if k != "ortho_nn")
